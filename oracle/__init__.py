@@ -1,0 +1,211 @@
+"""ORACLE — test infrastructure only (see oracle/oracle.c header).
+
+ctypes wrapper over liboracle.so, the plain fp64 C implementation of the
+EXACT hot path.  Only tests/, __graft_entry__.smoke() and bench.py's
+cpu_baseline / --impl reference leg may import this package.  Nothing here
+imports or links the CUDA path.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SRC = os.path.join(_HERE, "oracle.c")
+_LIB = os.path.join(_HERE, "liboracle.so")
+
+SET_NONE, SET_BALL, SET_NONNEG, SET_NONNEG_BALL = 0, 1, 2, 3
+
+
+def build(force: bool = False) -> str:
+    """Compile liboracle.so with gcc (fp64, no contraction, OpenMP)."""
+    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
+        cmd = ["gcc", "-O2", "-fopenmp", "-ffp-contract=off", "-fno-fast-math", "-std=c11",
+               "-shared", "-fPIC", _SRC, "-o", _LIB + ".tmp", "-lm"]
+        subprocess.check_call(cmd)
+        os.replace(_LIB + ".tmp", _LIB)
+    return _LIB
+
+
+class _Problem(C.Structure):
+    _fields_ = [
+        ("n", C.c_int64), ("d", C.c_int64), ("n_norm", C.c_int64),
+        ("csr", C.c_int), ("A", C.c_void_p), ("a_f32", C.c_int), ("lda", C.c_int64),
+        ("row_ptr", C.c_void_p), ("col", C.c_void_p), ("val", C.c_void_p),
+        ("y", C.c_void_p), ("W", C.c_int), ("s", C.c_void_p), ("mu", C.c_void_p),
+        ("I_bar", C.c_double), ("s_row", C.c_void_p), ("I_row", C.c_void_p),
+        ("relu", C.c_int), ("set", C.c_int), ("R", C.c_double), ("center", C.c_void_p),
+    ]
+
+
+_lib = None
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        _lib = C.CDLL(build())
+        P = C.POINTER(_Problem)
+        dp = C.POINTER(C.c_double)
+        _lib.oracle_h.restype = C.c_double
+        _lib.oracle_h.argtypes = [C.c_int, dp, dp, C.c_double, C.c_int]
+        _lib.oracle_H.restype = C.c_double
+        _lib.oracle_H.argtypes = [C.c_int, dp, dp, C.c_double, C.c_int]
+        _lib.oracle_hprime_abs.restype = C.c_double
+        _lib.oracle_hprime_abs.argtypes = [C.c_int, dp, dp, C.c_double]
+        _lib.oracle_F.argtypes = [P, dp, dp, dp]
+        _lib.oracle_forward.argtypes = [P, dp, dp]
+        _lib.oracle_mean.argtypes = [P, dp, dp]
+        _lib.oracle_project.argtypes = [C.c_int, C.c_int64, C.c_double, dp, dp, dp]
+        _lib.oracle_solve.restype = C.c_int
+        _lib.oracle_solve.argtypes = [P, C.c_int, C.c_double, dp, dp]
+        _lib.oracle_lambda_max.restype = C.c_double
+        _lib.oracle_lambda_max.argtypes = [P, C.c_int, C.c_double, C.POINTER(C.c_int)]
+        _lib.oracle_reparam.argtypes = [C.c_int, dp, dp, C.c_double, C.c_int64, dp, C.c_int,
+                                        dp, dp]
+        _lib.oracle_set_threads.argtypes = [C.c_int]
+        _lib.oracle_max_threads.restype = C.c_int
+    return _lib
+
+
+def _dp(a):
+    if a is None:
+        return None
+    return a.ctypes.data_as(C.POINTER(C.c_double))
+
+
+def _f64(a):
+    return None if a is None else np.ascontiguousarray(a, dtype=np.float64)
+
+
+def set_threads(t: int) -> None:
+    lib().oracle_set_threads(int(t))
+
+
+def max_threads() -> int:
+    return int(lib().oracle_max_threads())
+
+
+class Problem:
+    """Holds the arrays (keeps them alive) and the C struct view of them."""
+
+    def __init__(self, *, y, s, mu, I_bar, d, A=None, row_ptr=None, col=None, val=None,
+                 s_row=None, I_row=None, relu=1, set=SET_BALL, R=1.0, center=None,
+                 n_norm=None):
+        self.csr = A is None
+        if self.csr:
+            self.row_ptr = np.ascontiguousarray(row_ptr, dtype=np.int64)
+            self.col = np.ascontiguousarray(col, dtype=np.int32)
+            v = np.asarray(val)
+            self.val = np.ascontiguousarray(v, dtype=np.float32 if v.dtype == np.float32 else np.float64)
+            self.a_f32 = int(self.val.dtype == np.float32)
+            self.n = self.row_ptr.shape[0] - 1
+            self.A = None
+            self.lda = 0
+        else:
+            a = np.asarray(A)
+            if a.dtype not in (np.float32, np.float64):
+                a = a.astype(np.float64)
+            self.A = np.ascontiguousarray(a)
+            self.a_f32 = int(self.A.dtype == np.float32)
+            self.n = self.A.shape[0]
+            self.lda = self.A.shape[1]
+        self.d = int(d)
+        self.y = _f64(y)
+        self.s, self.mu = _f64(s), _f64(mu)
+        self.W = self.s.shape[0]
+        self.I_bar = float(I_bar)
+        self.s_row, self.I_row = _f64(s_row), _f64(I_row)
+        self.relu, self.set, self.R = int(relu), int(set), float(R)
+        self.center = _f64(center)
+        self.n_norm = int(self.n if n_norm is None else n_norm)
+        assert self.y.shape[0] == self.n
+        st = _Problem()
+        st.n, st.d, st.n_norm = self.n, self.d, self.n_norm
+        st.csr = int(self.csr)
+        st.A = None if self.A is None else self.A.ctypes.data
+        st.a_f32, st.lda = self.a_f32, self.lda
+        if self.csr:
+            st.row_ptr, st.col, st.val = (self.row_ptr.ctypes.data, self.col.ctypes.data,
+                                          self.val.ctypes.data)
+        st.y = self.y.ctypes.data
+        st.W = self.W
+        st.s, st.mu = self.s.ctypes.data, self.mu.ctypes.data
+        st.I_bar = self.I_bar
+        st.s_row = None if self.s_row is None else self.s_row.ctypes.data
+        st.I_row = None if self.I_row is None else self.I_row.ctypes.data
+        st.relu, st.set, st.R = self.relu, self.set, self.R
+        st.center = None if self.center is None else self.center.ctypes.data
+        self._st = st
+
+    @property
+    def ptr(self):
+        return C.byref(self._st)
+
+    def F(self, x):
+        x = _f64(x)
+        g = np.zeros(self.d)
+        loss = C.c_double()
+        lib().oracle_F(self.ptr, _dp(x), _dp(g), C.byref(loss))
+        return g, loss.value
+
+    def forward(self, x):
+        x = _f64(x)
+        z = np.zeros(self.n)
+        lib().oracle_forward(self.ptr, _dp(x), _dp(z))
+        return z
+
+    def mean(self, x):
+        x = _f64(x)
+        lam = np.zeros(self.n)
+        lib().oracle_mean(self.ptr, _dp(x), _dp(lam))
+        return lam
+
+    def project(self, v):
+        return project(self.set, self.R, self.center, v)
+
+    def solve(self, T, gamma, x1=None, trace=False):
+        x = np.zeros(self.d) if x1 is None else np.array(x1, dtype=np.float64)
+        tr = np.zeros(2 * T) if trace else None
+        bad = lib().oracle_solve(self.ptr, int(T), float(gamma), _dp(x), _dp(tr))
+        return x, tr, int(bad)
+
+    def lambda_max(self, max_it=1000, tol=1e-8):
+        it = C.c_int()
+        lam = lib().oracle_lambda_max(self.ptr, int(max_it), float(tol), C.byref(it))
+        return lam, it.value
+
+
+def h(s, mu, t, relu=1):
+    s, mu = _f64(s), _f64(mu)
+    return lib().oracle_h(s.shape[0], _dp(s), _dp(mu), float(t), int(relu))
+
+
+def H(s, mu, t, relu=1):
+    s, mu = _f64(s), _f64(mu)
+    return lib().oracle_H(s.shape[0], _dp(s), _dp(mu), float(t), int(relu))
+
+
+def hprime_abs(s, mu, t):
+    s, mu = _f64(s), _f64(mu)
+    return lib().oracle_hprime_abs(s.shape[0], _dp(s), _dp(mu), float(t))
+
+
+def project(set, R, center, v):
+    v = _f64(v)
+    out = np.empty_like(v)
+    lib().oracle_project(int(set), v.shape[0], float(R), _dp(_f64(center)), _dp(v), _dp(out))
+    return out
+
+
+def reparam(s, mu, I_bar, b, clamp=1):
+    s, mu, b = _f64(s), _f64(mu), _f64(b)
+    n, W = b.shape[0], s.shape[0]
+    s_row = np.zeros((n, W))
+    I_row = np.zeros(n)
+    lib().oracle_reparam(W, _dp(s), _dp(mu), float(I_bar), n, _dp(b), int(clamp),
+                         _dp(s_row), _dp(I_row))
+    return s_row, I_row

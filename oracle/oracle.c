@@ -1,0 +1,308 @@
+/*
+ * ORACLE — test infrastructure only.
+ *
+ * A plain, slow, obviously-correct fp64 CPU implementation of what the EXACT
+ * hot path computes (arXiv 2503.19925, PAPER.md).  Only tests/,
+ * __graft_entry__.smoke() and bench.py's cpu_baseline / --impl reference leg
+ * may load this library.  It shares no code, header, table or constant with
+ * the CUDA path (paper_2503_19925_b200/csrc) and never imports it.
+ *
+ * Every function cites the passage it follows.  Loops run in the order the
+ * definition is written (rows i ascending, columns k ascending, bins j
+ * ascending); the only parallelism is OpenMP over fixed 4096-row chunks whose
+ * partial sums are combined in chunk order, so results do not depend on the
+ * thread count.
+ *
+ * Pins: see tests/test_oracle_pins.py (P1..P13 of SURVEY.md §8(c)).  Parity
+ * of the ℓ(x) value is pinned only through finite differences (reading R2).
+ */
+#include <math.h>
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+#ifdef _OPENMP
+#include <omp.h>
+#endif
+
+#define ORACLE_CHUNK 4096
+
+enum { OR_SET_NONE = 0, OR_SET_BALL = 1, OR_SET_NONNEG = 2, OR_SET_NONNEG_BALL = 3 };
+
+typedef struct {
+  int64_t n, d;             /* rows held here, columns                        */
+  int64_t n_norm;           /* the n of the 1/n in Eq.(operator)              */
+  int csr;                  /* 0: dense row-major A, 1: CSR (row_ptr,col,val)  */
+  const void *A;            /* dense values, float or double, row pitch lda    */
+  int a_f32;                /* 1: values (A or val) are float, 0: double       */
+  int64_t lda;
+  const int64_t *row_ptr;   /* CSR [n+1]                                      */
+  const int32_t *col;       /* CSR [nnz]                                      */
+  const void *val;          /* CSR [nnz]                                      */
+  const double *y;          /* [n] counts / measurements                      */
+  int W;
+  const double *s, *mu;     /* [W] spectrum, Eq.(model)       */
+  double I_bar;
+  const double *s_row;      /* optional [n*W] per-row spectrum (A.1)          */
+  const double *I_row;      /* optional [n] per-row intensity (A.1)           */
+  int relu;                 /* 1: h uses t_+ (Eq. function-h-plus)            */
+  int set;                  /* constraint set X                               */
+  double R;                 /* radius of the ball part of X                   */
+  const double *center;     /* [d] or NULL (= 0)                              */
+} oracle_problem;
+
+void oracle_set_threads(int t) {
+#ifdef _OPENMP
+  if (t > 0) omp_set_num_threads(t);
+#else
+  (void)t;
+#endif
+}
+
+int oracle_max_threads(void) {
+#ifdef _OPENMP
+  return omp_get_max_threads();
+#else
+  return 1;
+#endif
+}
+
+/* h(t) = Σ_j s_j exp(-μ_j t_+)  — Eq.(function-h-plus).
+ * relu = 0 drops the (.)_+ (Eq. eq:model-orig). */
+double oracle_h(int W, const double *s, const double *mu, double t, int relu) {
+  double tc = (relu && t < 0.0) ? 0.0 : t;
+  double h = 0.0;
+  for (int j = 0; j < W; ++j) h += s[j] * exp(-mu[j] * tc);
+  return h;
+}
+
+/* |h'(t)| = Σ_j s_j μ_j exp(-μ_j t) for t > 0 — PAPER.md:1490 (§4.2 proof of
+ * Theorem 2).  Returns NaN for t <= 0. */
+double oracle_hprime_abs(int W, const double *s, const double *mu, double t) {
+  if (!(t > 0.0)) return NAN;
+  double v = 0.0;
+  for (int j = 0; j < W; ++j) v += s[j] * mu[j] * exp(-mu[j] * t);
+  return v;
+}
+
+/* H(t) = ∫_0^t h(u) du, the primitive whose derivative is h (reading R2 of
+ * ℓ(x) = (1/n) Σ_i [y_i z_i - Ī H(z_i)] has gradient F(x)).
+ *   t >= 0 (or relu = 0):  Σ_j (s_j/μ_j) (1 - exp(-μ_j t))
+ *   t <  0 and relu = 1:   t Σ_j s_j           (h ≡ Σ s_j on t < 0)        */
+double oracle_H(int W, const double *s, const double *mu, double t, int relu) {
+  double v = 0.0;
+  if (relu && t < 0.0) {
+    for (int j = 0; j < W; ++j) v += s[j];
+    return t * v;
+  }
+  for (int j = 0; j < W; ++j) v += (s[j] / mu[j]) * (1.0 - exp(-mu[j] * t));
+  return v;
+}
+
+static double a_at(const oracle_problem *p, int64_t i, int64_t k) {
+  if (p->a_f32) return (double)((const float *)p->A)[i * p->lda + k];
+  return ((const double *)p->A)[i * p->lda + k];
+}
+
+static double v_at(const oracle_problem *p, int64_t e) {
+  if (p->a_f32) return (double)((const float *)p->val)[e];
+  return ((const double *)p->val)[e];
+}
+
+/* z_i = <a_i, x>, k ascending (dense) or in stored order (CSR). */
+static double row_dot(const oracle_problem *p, int64_t i, const double *x) {
+  double z = 0.0;
+  if (!p->csr) {
+    for (int64_t k = 0; k < p->d; ++k) z += a_at(p, i, k) * x[k];
+  } else {
+    for (int64_t e = p->row_ptr[i]; e < p->row_ptr[i + 1]; ++e) z += v_at(p, e) * x[p->col[e]];
+  }
+  return z;
+}
+
+static const double *row_s(const oracle_problem *p, int64_t i) {
+  return p->s_row ? p->s_row + i * p->W : p->s;
+}
+static double row_I(const oracle_problem *p, int64_t i) {
+  return p->I_row ? p->I_row[i] : p->I_bar;
+}
+
+/* z_i = <a_i, x> for every row (forward projection A x). */
+void oracle_forward(const oracle_problem *p, const double *x, double *z) {
+#pragma omp parallel for schedule(static)
+  for (int64_t i = 0; i < p->n; ++i) z[i] = row_dot(p, i, x);
+}
+
+/* Expected counts E[y_i | a_i] = Ī_i h_i(<a_i, x>) — Eq.(model),
+ * PAPER.md:867-869 (per-row Ī', s' of Appendix A.1 when given). */
+void oracle_mean(const oracle_problem *p, const double *x, double *lam) {
+#pragma omp parallel for schedule(static)
+  for (int64_t i = 0; i < p->n; ++i)
+    lam[i] = row_I(p, i) * oracle_h(p->W, row_s(p, i), p->mu, row_dot(p, i, x), p->relu);
+}
+
+/* F(x) = (1/n) Σ_i [y_i - Ī h(<a_i,x>)] a_i — Eq.(operator), PAPER.md:893-896,
+ * with n = p->n_norm (reading R4), and the scalar
+ * ℓ(x) = (1/n) Σ_i [y_i z_i - Ī H(z_i)] (reading R2).  g or loss may be NULL. */
+void oracle_F(const oracle_problem *p, const double *x, double *g, double *loss) {
+  const int64_t n = p->n, d = p->d;
+  const int64_t nch = (n + ORACLE_CHUNK - 1) / ORACLE_CHUNK;
+  double *part = (double *)calloc((size_t)(nch > 0 ? nch : 1) * (size_t)d, sizeof(double));
+  double *lpart = (double *)calloc((size_t)(nch > 0 ? nch : 1), sizeof(double));
+#pragma omp parallel for schedule(static)
+  for (int64_t c = 0; c < nch; ++c) {
+    double *gc = part + c * d;
+    const int64_t i1 = (c + 1) * ORACLE_CHUNK < n ? (c + 1) * ORACLE_CHUNK : n;
+    for (int64_t i = c * ORACLE_CHUNK; i < i1; ++i) {
+      const double z = row_dot(p, i, x);
+      const double *si = row_s(p, i);
+      const double Ii = row_I(p, i);
+      const double r = p->y[i] - Ii * oracle_h(p->W, si, p->mu, z, p->relu);
+      lpart[c] += p->y[i] * z - Ii * oracle_H(p->W, si, p->mu, z, p->relu);
+      if (!p->csr) {
+        for (int64_t k = 0; k < d; ++k) gc[k] += r * a_at(p, i, k);
+      } else {
+        for (int64_t e = p->row_ptr[i]; e < p->row_ptr[i + 1]; ++e) gc[p->col[e]] += r * v_at(p, e);
+      }
+    }
+  }
+  if (g) {
+    for (int64_t k = 0; k < d; ++k) g[k] = 0.0;
+    for (int64_t c = 0; c < nch; ++c)
+      for (int64_t k = 0; k < d; ++k) g[k] += part[c * d + k];
+    for (int64_t k = 0; k < d; ++k) g[k] /= (double)p->n_norm;
+  }
+  if (loss) {
+    double l = 0.0;
+    for (int64_t c = 0; c < nch; ++c) l += lpart[c];
+    *loss = l / (double)p->n_norm;
+  }
+  free(part);
+  free(lpart);
+}
+
+/* P_X(v): ℓ2 projection onto X.
+ *  BALL        B(R; c): c + (v - c) min(1, R / ||v - c||)  — PAPER.md:946,1025;
+ *                        SPEC.md:249-257
+ *  NONNEG      max(v, 0)                                   — PAPER.md:1252,1263;
+ *                                                            SPEC.md:240-248
+ *  NONNEG_BALL R_+^d ∩ B(R) centred at 0: P_B(P_+(v))      — reading R14
+ *  out may alias v. */
+void oracle_project(int set, int64_t d, double R, const double *c, const double *v, double *out) {
+  if (set == OR_SET_NONE) {
+    if (out != v) memcpy(out, v, (size_t)d * sizeof(double));
+    return;
+  }
+  if (set == OR_SET_NONNEG || set == OR_SET_NONNEG_BALL) {
+    for (int64_t k = 0; k < d; ++k) out[k] = v[k] > 0.0 ? v[k] : 0.0;
+    if (set == OR_SET_NONNEG) return;
+    double nrm2 = 0.0;
+    for (int64_t k = 0; k < d; ++k) nrm2 += out[k] * out[k];
+    const double nrm = sqrt(nrm2);
+    if (nrm > R) for (int64_t k = 0; k < d; ++k) out[k] = out[k] * (R / nrm);
+    return;
+  }
+  /* ball */
+  double nrm2 = 0.0;
+  for (int64_t k = 0; k < d; ++k) {
+    const double df = v[k] - (c ? c[k] : 0.0);
+    nrm2 += df * df;
+  }
+  const double nrm = sqrt(nrm2);
+  if (nrm <= R) {
+    if (out != v) memcpy(out, v, (size_t)d * sizeof(double));
+    return;
+  }
+  for (int64_t k = 0; k < d; ++k) {
+    const double ck = c ? c[k] : 0.0;
+    out[k] = ck + (v[k] - ck) * (R / nrm);
+  }
+}
+
+/* EXACT, Eq.(extragrad-method), constant step γ:
+ *   x_1 = P_X(x_in)                       (x_1 ∈ X)
+ *   x_{t+1/2} = P_X(x_t - γ F(x_t))
+ *   x_{t+1}   = P_X(x_t - γ F(x_{t+1/2}))   (both steps anchored at x_t)
+ * Returns x_{T+1} in x.  trace (may be NULL) gets [2T] losses ℓ at the points
+ * where F was evaluated.  Returns 0, or t (1-based) of the first non-finite
+ * iterate. */
+int oracle_solve(const oracle_problem *p, int T, double gamma, double *x, double *trace) {
+  const int64_t d = p->d;
+  double *g = (double *)malloc((size_t)d * sizeof(double));
+  double *xh = (double *)malloc((size_t)d * sizeof(double));
+  double *v = (double *)malloc((size_t)d * sizeof(double));
+  int bad = 0;
+  oracle_project(p->set, d, p->R, p->center, x, x);
+  for (int t = 1; t <= T && !bad; ++t) {
+    double l;
+    oracle_F(p, x, g, &l);
+    if (trace) trace[2 * (t - 1)] = l;
+    for (int64_t k = 0; k < d; ++k) v[k] = x[k] - gamma * g[k];
+    oracle_project(p->set, d, p->R, p->center, v, xh);
+    oracle_F(p, xh, g, &l);
+    if (trace) trace[2 * (t - 1) + 1] = l;
+    for (int64_t k = 0; k < d; ++k) v[k] = x[k] - gamma * g[k];
+    oracle_project(p->set, d, p->R, p->center, v, x);
+    for (int64_t k = 0; k < d; ++k)
+      if (!isfinite(x[k]) || !isfinite(xh[k])) { bad = t; break; }
+  }
+  free(g);
+  free(xh);
+  free(v);
+  return bad;
+}
+
+/* λ_max(Σ), Σ = (1/n_norm) A^T A, by power iteration
+ * v <- Σ v / ||Σ v|| from v_0 = 1/sqrt(d), stopping when the Rayleigh
+ * estimate changes by <= tol relatively or after max_it. */
+double oracle_lambda_max(const oracle_problem *p, int max_it, double tol, int *iters) {
+  const int64_t n = p->n, d = p->d;
+  double *v = (double *)malloc((size_t)d * sizeof(double));
+  double *w = (double *)malloc((size_t)d * sizeof(double));
+  double *z = (double *)malloc((size_t)(n > 0 ? n : 1) * sizeof(double));
+  for (int64_t k = 0; k < d; ++k) v[k] = 1.0 / sqrt((double)d);
+  double lam = 0.0;
+  int it = 0;
+  for (it = 1; it <= max_it; ++it) {
+    oracle_forward(p, v, z);
+    for (int64_t k = 0; k < d; ++k) w[k] = 0.0;
+    for (int64_t i = 0; i < n; ++i) {
+      if (!p->csr) {
+        for (int64_t k = 0; k < d; ++k) w[k] += z[i] * a_at(p, i, k);
+      } else {
+        for (int64_t e = p->row_ptr[i]; e < p->row_ptr[i + 1]; ++e) w[p->col[e]] += z[i] * v_at(p, e);
+      }
+    }
+    double nrm2 = 0.0;
+    for (int64_t k = 0; k < d; ++k) {
+      w[k] /= (double)p->n_norm;
+      nrm2 += w[k] * w[k];
+    }
+    const double nrm = sqrt(nrm2);
+    const double prev = lam;
+    lam = nrm; /* ||Σ v|| with ||v|| = 1 */
+    for (int64_t k = 0; k < d; ++k) v[k] = w[k] / nrm;
+    if (it > 1 && fabs(lam - prev) <= tol * lam) break;
+  }
+  if (iters) *iters = it;
+  free(v);
+  free(w);
+  free(z);
+  return lam;
+}
+
+/* Known-materials reparameterisation, Appendix A.1:
+ *   Ī'_i  = Ī Σ_j s_j exp(-μ_j b_i)
+ *   s'_ij = s_j exp(-μ_j b_i) / Σ_k s_k exp(-μ_k b_i)
+ * with b_i = <a_i^1, x^1> + <a_i^2, x^2> the known-material line integral,
+ * clamped to b_i+ when clamp = 1 (reading R7; SPEC.md:88-90 requires e_j >= 0). */
+void oracle_reparam(int W, const double *s, const double *mu, double I_bar, int64_t n,
+                    const double *b, int clamp, double *s_row, double *I_row) {
+#pragma omp parallel for schedule(static)
+  for (int64_t i = 0; i < n; ++i) {
+    const double bi = (clamp && b[i] < 0.0) ? 0.0 : b[i];
+    double tot = 0.0;
+    for (int j = 0; j < W; ++j) tot += s[j] * exp(-mu[j] * bi);
+    for (int j = 0; j < W; ++j) s_row[i * W + j] = s[j] * exp(-mu[j] * bi) / tot;
+    I_row[i] = I_bar * tot;
+  }
+}
