@@ -1,0 +1,192 @@
+/*
+ * poly.h — C ABI of the B200-native (sm_100a) hot path of EXACT, the
+ * projected-extragradient estimator of arXiv 2503.19925.
+ *
+ * The library evaluates, on the GPU,
+ *
+ *   h(t)  = Σ_j s_j exp(-μ_j t_+)                     Eq.(function-h-plus)
+ *   F(x)  = (1/n) Σ_i [y_i - Ī h(<a_i, x>)] a_i       Eq.(operator),
+ *   ℓ(x)  = (1/n) Σ_i [y_i <a_i,x> - Ī H(<a_i,x>)],   H' = h                (reading R2;
+ *                                                      ∇ℓ = F, so EXACT's VI is min_X ℓ)
+ *   x_{t+1/2} = P_X(x_t - γ F(x_t)),
+ *   x_{t+1}   = P_X(x_t - γ F(x_{t+1/2}))              Eq.(extragrad-method)
+ *
+ * with P_X the ℓ2 projection onto X = B(R; c), the
+ * nonnegative orthant or R_+^d ∩ B(R) (reading R14).
+ * Per-row spectra (s'_ij, Ī'_i) implement the known-materials reduction of
+ * Appendix A.1.
+ *
+ * Conventions (all entry points):
+ *  - Return value: POLY_OK (0) or one of the POLY_E* codes below; on error
+ *    poly_last_error() returns a thread-local, NUL-terminated message.
+ *  - "device" pointers are CUDA device (or managed) memory of the current
+ *    device; "host" pointers are ordinary or pinned host memory.  Vectors
+ *    marked "device or host" are classified with cudaPointerGetAttributes.
+ *  - Work is enqueued on the cudaStream_t given in poly_problem.stream and is
+ *    asynchronous, except where a host output is requested (then the call
+ *    synchronises that stream before returning).
+ *  - The handle BORROWS every device array of poly_problem until poly_free;
+ *    the caller must keep them alive and unmodified.  Host arrays (s, mu,
+ *    center) are copied during poly_init.  With POLY_FLAG_HOST_INPUTS the
+ *    matrix/measurement arrays are host pointers and are copied into
+ *    library-owned device memory during poly_init.
+ *  - Multi-GPU (world > 1): one process per GPU; every rank calls every
+ *    entry point in lockstep (NCCL semantics).  Each rank holds a contiguous
+ *    block of rows; F is the allreduce(sum) over ranks of the local
+ *    unnormalised sums, scaled by 1/n_global, so every rank sees identical
+ *    bits and applies the identical projection.  On an NCCL error the rank
+ *    aborts its communicator (ncclCommAbort) and returns POLY_ENCCL.
+ *  - Not thread-safe per handle; distinct handles may be used concurrently.
+ */
+#ifndef POLY_H_
+#define POLY_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define POLY_ABI_VERSION 1
+
+/* status codes */
+#define POLY_OK 0
+#define POLY_EINVAL 1        /* bad argument: dims, spectrum, alignment, set, ... */
+#define POLY_ECUDA 2         /* CUDA runtime / launch failure (message has the CUDA error) */
+#define POLY_ENCCL 3         /* NCCL failure or NCCL unavailable when world > 1 */
+#define POLY_ENONFINITE 4    /* poly_solve produced a non-finite iterate */
+#define POLY_ENOMEM 5        /* device allocation failed */
+#define POLY_EUNSUPPORTED 6  /* valid request outside what this build implements */
+
+/* poly_problem.layout */
+#define POLY_DENSE 0         /* A row-major n_local x d, row pitch lda elements */
+#define POLY_CSR 1           /* row_ptr[n_local+1] (int64), col[nnz] (int32), val[nnz] */
+/* poly_problem.dtype: element type of A (dense) or val (CSR) */
+#define POLY_F32 0
+#define POLY_F64 1
+/* poly_problem.ytype: element type of y */
+#define POLY_Y_I32 0         /* Poisson counts (Eq. Poisson-model), must be >= 0 */
+#define POLY_Y_F32 1         /* counts + electronic noise, may be negative */
+#define POLY_Y_F64 2         /* e.g. noiseless expected counts in tests */
+/* poly_problem.set: the constraint set X */
+#define POLY_SET_NONE 0      /* X = R^d (P_X = identity) */
+#define POLY_SET_BALL 1      /* X = B(R; center), center NULL = 0 */
+#define POLY_SET_NONNEG 2    /* X = R_+^d */
+#define POLY_SET_NONNEG_BALL 3 /* X = R_+^d ∩ B(R), center must be NULL (P_B ∘ P_+ is exact) */
+/* poly_problem.flags */
+#define POLY_FLAG_HOST_INPUTS 1u /* A/row_ptr/col/val/y/s_row/I_row are HOST pointers; copied at init */
+#define POLY_FLAG_NO_GRAPH 2u    /* poly_solve launches kernels directly instead of via a CUDA graph */
+#define POLY_FLAG_NO_PDL 4u      /* disable programmatic dependent launch between kernels */
+
+/* poly_solve flags */
+#define POLY_SOLVE_PROFILE 1u    /* time every kernel with CUDA events (implies no graph);
+                                    read with poly_kernel_times */
+
+typedef struct poly_handle poly_handle; /* opaque, library-owned */
+
+typedef struct poly_problem {
+  int64_t n_local;     /* rows held by this rank (>= 0)                                  */
+  int64_t n_global;    /* n of the 1/n in Eq.(operator): total rows over all ranks (>= 1) */
+  int64_t row_offset;  /* global index of this rank's first row (bookkeeping only)       */
+  int64_t d;           /* columns = length of x (>= 1)                                   */
+  int32_t layout;      /* POLY_DENSE | POLY_CSR                                          */
+  int32_t dtype;       /* POLY_F32 | POLY_F64                                            */
+  const void *A;       /* dense: device, row-major, 16-byte aligned, lda*elsize % 16 == 0 */
+  int64_t lda;         /* dense: row pitch in elements, lda >= d                         */
+  const int64_t *row_ptr; /* CSR: device [n_local+1], row_ptr[0] = 0, nondecreasing      */
+  const int32_t *col;  /* CSR: device [nnz], 0 <= col < d                                */
+  const void *val;     /* CSR: device [nnz], dtype elements                              */
+  int64_t nnz;         /* CSR: number of stored entries = row_ptr[n_local]               */
+  int32_t ytype;       /* POLY_Y_I32 | POLY_Y_F32 | POLY_Y_F64                           */
+  int32_t W;           /* spectral bins, 1 <= W <= 64                                    */
+  const void *y;       /* device [n_local] measurements                                  */
+  const double *s;     /* host [W]: s_j in (0,1], |Σ s_j - 1| <= 1e-12 */
+  const double *mu;    /* host [W]: μ_j > 0                                              */
+  double I_bar;        /* Ī > 0                                                          */
+  const float *s_row;  /* optional device [n_local*W]: per-row spectrum s'_ij (A.1)      */
+  const float *I_row;  /* optional device [n_local]: per-row intensity Ī'_i (A.1); both or neither */
+  int32_t relu;        /* 1: h uses t_+ (Eq. function-h-plus); 0: Eq.(eq:model-orig)     */
+  int32_t set;         /* POLY_SET_*                                                     */
+  double R;            /* ball radius (> 0) for POLY_SET_BALL / POLY_SET_NONNEG_BALL     */
+  const double *center;/* host [d] ball centre or NULL (= 0)                             */
+  int32_t rank;        /* 0 <= rank < world                                              */
+  int32_t world;       /* number of ranks (>= 1); world > 1 needs nccl_id                */
+  const void *nccl_id; /* host, 128-byte ncclUniqueId from poly_nccl_unique_id on rank 0 */
+  void *stream;        /* cudaStream_t (NULL = legacy default stream)                    */
+  uint32_t flags;      /* POLY_FLAG_*                                                    */
+  int32_t reserved;
+} poly_problem;
+
+/* Validate *p, copy host parameters, pick the kernel configuration for
+ * (layout, dtype, d), allocate the workspaces (per-CTA partial gradients,
+ * solver state, communicator) and, when world > 1, create the NCCL
+ * communicator.  *out receives the handle (NULL on error).
+ * Errors: POLY_EINVAL (dimension mismatch SPEC.md:63,311; spectrum invariants
+ * SPEC.md:24-28; R <= 0 for a ball set; misaligned A; NONNEG_BALL with a
+ * centre), POLY_EUNSUPPORTED (dense d above the largest tile, W > 64),
+ * POLY_ENOMEM, POLY_ECUDA, POLY_ENCCL. */
+int poly_init(const poly_problem *p, poly_handle **out);
+
+/* One evaluation of the operator, Eq.(operator):
+ *   g[k]  = F(x)_k,  k < d        (device or host [d] fp64; may be NULL)
+ *   *loss = ℓ(x)                  (host double; may be NULL — then no sync)
+ * x: device or host [d] fp64.  One pass over A (the fused row-tile kernel),
+ * the fixed-order partial reduction and, for world > 1, one allreduce. */
+int poly_loss_grad(poly_handle *h, const double *x, double *g, double *loss);
+
+/* EXACT, Eq.(extragrad-method), T iterations with constant step γ > 0:
+ *   x_1 = P_X(x_in);  x_{t+1/2} = P_X(x_t - γ F(x_t));  x_{t+1} = P_X(x_t - γ F(x_{t+1/2})).
+ * x: device or host [d] fp64; in: x_in, out: x_{T+1} (always in X).
+ * trace: host [2T] fp64 or NULL; receives ℓ at each of the 2T points where F
+ * was evaluated.  flags: POLY_SOLVE_*.  On a non-finite iterate returns
+ * POLY_ENONFINITE with *bad_iter = the 1-based iteration t (bad_iter may be
+ * NULL).  Synchronises the stream before returning. */
+int poly_solve(poly_handle *h, double *x, int T, double gamma, uint32_t flags,
+               double *trace, int *bad_iter);
+
+/* Forward projection z_i = <a_i, x> for the local rows, accumulated in fp64
+ * (fp32 A values promoted exactly), fixed reduction order.
+ * x: device [d] fp64; z: device [n_local] fp64. */
+int poly_forward(poly_handle *h, const double *x, double *z);
+
+/* Expected counts λ_i = Ī_i h_i(<a_i, x>) (Eq. model),
+ * fp64 throughout.  x: device [d] fp64; lam: device [n_local] fp64. */
+int poly_expected_counts(poly_handle *h, const double *x, double *lam);
+
+/* Known-materials reparameterisation of Appendix A.1:
+ *   Ī'_i = Ī Σ_j s_j e^{-μ_j b_i},  s'_ij = s_j e^{-μ_j b_i} / Σ_k s_k e^{-μ_k b_i},
+ * with b_i the known-material line integral, replaced by max(b_i, 0) when
+ * clamp = 1 (reading R7).  b: device [n] fp64; s_row: device [n*W] fp32;
+ * I_row: device [n] fp32; s, mu: host [W].  Enqueued on `stream`. */
+int poly_reparameterize(int32_t W, const double *s, const double *mu, double I_bar, int64_t n,
+                        const double *b, int32_t clamp, float *s_row, float *I_row, void *stream);
+
+/* Average device time (ms) of each kernel class over the last poly_solve
+ * called with POLY_SOLVE_PROFILE: out[0] loss+grad pass (the fused A-stream
+ * kernel), out[1] reduce/project kernel(s), out[2] allreduce (0 if world==1),
+ * out[3] loss+grad launches, out[4] all kernel launches.  nout <= 5. */
+int poly_kernel_times(poly_handle *h, double *out, int32_t nout);
+
+/* Static description of the chosen configuration, for reports:
+ * out[0] grid CTAs, out[1] threads/CTA, out[2] rows per stage, out[3] stages,
+ * out[4] dynamic smem bytes, out[5] SM count.  nout <= 6. */
+int poly_describe(poly_handle *h, int64_t *out, int32_t nout);
+
+/* Write a fresh 128-byte ncclUniqueId into out (host).  Call on rank 0 and
+ * broadcast the bytes to all ranks before poly_init.  POLY_ENCCL if NCCL
+ * cannot be loaded. */
+int poly_nccl_unique_id(void *out128);
+
+/* Release everything the handle owns (workspaces, graphs, communicator). */
+void poly_free(poly_handle *h);
+
+/* Thread-local message for the last error of this thread ("" if none). */
+const char *poly_last_error(void);
+
+/* POLY_ABI_VERSION of the loaded library. */
+int poly_abi_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* POLY_H_ */

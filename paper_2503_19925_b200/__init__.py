@@ -1,0 +1,156 @@
+"""B200-native (sm_100a) hot path of EXACT (arXiv 2503.19925).
+
+Thin ctypes binding over libpoly.so (include/poly.h).  The functions below
+carry the C names and only marshal arguments; every step of the path runs in
+the library's CUDA kernels.  There is no CPU fallback: importing this package
+without the built library raises ImportError.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libpoly.so")
+
+POLY_OK, POLY_EINVAL, POLY_ECUDA, POLY_ENCCL, POLY_ENONFINITE, POLY_ENOMEM, POLY_EUNSUPPORTED = range(7)
+POLY_DENSE, POLY_CSR = 0, 1
+POLY_F32, POLY_F64 = 0, 1
+POLY_Y_I32, POLY_Y_F32, POLY_Y_F64 = 0, 1, 2
+POLY_SET_NONE, POLY_SET_BALL, POLY_SET_NONNEG, POLY_SET_NONNEG_BALL = 0, 1, 2, 3
+POLY_FLAG_HOST_INPUTS, POLY_FLAG_NO_GRAPH, POLY_FLAG_NO_PDL = 1, 2, 4
+POLY_SOLVE_PROFILE = 1
+
+EXPORTED = ["poly_init", "poly_loss_grad", "poly_solve", "poly_forward", "poly_expected_counts",
+            "poly_reparameterize", "poly_kernel_times", "poly_describe", "poly_nccl_unique_id",
+            "poly_free", "poly_last_error", "poly_abi_version"]
+
+
+class PolyProblem(C.Structure):
+    """Mirror of `poly_problem` (include/poly.h); field order is the ABI."""
+    _fields_ = [
+        ("n_local", C.c_int64), ("n_global", C.c_int64), ("row_offset", C.c_int64),
+        ("d", C.c_int64), ("layout", C.c_int32), ("dtype", C.c_int32),
+        ("A", C.c_void_p), ("lda", C.c_int64),
+        ("row_ptr", C.c_void_p), ("col", C.c_void_p), ("val", C.c_void_p), ("nnz", C.c_int64),
+        ("ytype", C.c_int32), ("W", C.c_int32), ("y", C.c_void_p),
+        ("s", C.c_void_p), ("mu", C.c_void_p), ("I_bar", C.c_double),
+        ("s_row", C.c_void_p), ("I_row", C.c_void_p),
+        ("relu", C.c_int32), ("set", C.c_int32), ("R", C.c_double), ("center", C.c_void_p),
+        ("rank", C.c_int32), ("world", C.c_int32), ("nccl_id", C.c_void_p),
+        ("stream", C.c_void_p), ("flags", C.c_uint32), ("reserved", C.c_int32),
+    ]
+
+
+class PolyError(RuntimeError):
+    def __init__(self, code, msg):
+        super().__init__(f"poly error {code}: {msg}")
+        self.code = code
+
+
+def _load():
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"{LIB_PATH} is missing: build it with "
+                          "`python -c 'import __graft_entry__ as g; g.build()'` (no CPU fallback)")
+    lib = C.CDLL(LIB_PATH)
+    vp, i32, i64, dbl = C.c_void_p, C.c_int32, C.c_int64, C.c_double
+    dp = C.POINTER(C.c_double)
+    lib.poly_init.argtypes = [C.POINTER(PolyProblem), C.POINTER(vp)]
+    lib.poly_loss_grad.argtypes = [vp, vp, vp, dp]
+    lib.poly_solve.argtypes = [vp, vp, C.c_int, dbl, C.c_uint32, dp, C.POINTER(C.c_int)]
+    lib.poly_forward.argtypes = [vp, vp, vp]
+    lib.poly_expected_counts.argtypes = [vp, vp, vp]
+    lib.poly_reparameterize.argtypes = [i32, dp, dp, dbl, i64, vp, i32, vp, vp, vp]
+    lib.poly_kernel_times.argtypes = [vp, dp, i32]
+    lib.poly_describe.argtypes = [vp, C.POINTER(C.c_int64), i32]
+    lib.poly_nccl_unique_id.argtypes = [vp]
+    lib.poly_free.argtypes = [vp]
+    lib.poly_free.restype = None
+    lib.poly_last_error.restype = C.c_char_p
+    for name in EXPORTED:
+        if name not in ("poly_free", "poly_last_error"):
+            getattr(lib, name).restype = C.c_int
+    return lib
+
+
+_lib = _load()
+
+
+def lib():
+    return _lib
+
+
+def _check(rc):
+    if rc != POLY_OK:
+        raise PolyError(rc, _lib.poly_last_error().decode(errors="replace"))
+    return rc
+
+
+# ----------------------------------------------------------------- C names
+def poly_abi_version() -> int:
+    return _lib.poly_abi_version()
+
+
+def poly_last_error() -> str:
+    return _lib.poly_last_error().decode(errors="replace")
+
+
+def poly_init(problem: PolyProblem) -> int:
+    h = C.c_void_p()
+    _check(_lib.poly_init(C.byref(problem), C.byref(h)))
+    return h.value
+
+
+def poly_loss_grad(h: int, x_ptr: int, g_ptr: int | None, want_loss: bool):
+    loss = C.c_double()
+    _check(_lib.poly_loss_grad(h, x_ptr, g_ptr, C.byref(loss) if want_loss else None))
+    return loss.value if want_loss else None
+
+
+def poly_solve(h: int, x_ptr: int, T: int, gamma: float, flags: int = 0, trace=None):
+    """trace: None or a ctypes double array of length 2T."""
+    bad = C.c_int(0)
+    rc = _lib.poly_solve(h, x_ptr, int(T), float(gamma), int(flags), trace, C.byref(bad))
+    if rc == POLY_ENONFINITE:
+        raise PolyError(rc, f"{poly_last_error()} (bad_iter={bad.value})")
+    _check(rc)
+
+
+def poly_forward(h: int, x_ptr: int, z_ptr: int):
+    _check(_lib.poly_forward(h, x_ptr, z_ptr))
+
+
+def poly_expected_counts(h: int, x_ptr: int, lam_ptr: int):
+    _check(_lib.poly_expected_counts(h, x_ptr, lam_ptr))
+
+
+def poly_reparameterize(W, s, mu, I_bar, n, b_ptr, clamp, s_row_ptr, I_row_ptr, stream=None):
+    sa = (C.c_double * W)(*s)
+    ma = (C.c_double * W)(*mu)
+    _check(_lib.poly_reparameterize(W, sa, ma, float(I_bar), int(n), b_ptr, int(clamp),
+                                    s_row_ptr, I_row_ptr, stream))
+
+
+def poly_kernel_times(h: int):
+    out = (C.c_double * 5)()
+    _check(_lib.poly_kernel_times(h, out, 5))
+    return list(out)
+
+
+def poly_describe(h: int):
+    out = (C.c_int64 * 6)()
+    _check(_lib.poly_describe(h, out, 6))
+    return dict(zip(["grid", "threads", "rows_per_stage", "stages", "smem", "sms"], list(out)))
+
+
+def poly_nccl_unique_id() -> bytes:
+    buf = C.create_string_buffer(128)
+    _check(_lib.poly_nccl_unique_id(buf))
+    return buf.raw
+
+
+def poly_free(h: int):
+    _lib.poly_free(h)
+
+
+from .api import Poly  # noqa: E402,F401

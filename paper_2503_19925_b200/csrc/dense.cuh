@@ -1,0 +1,321 @@
+// K1 — fused dense row-tile loss+gradient kernel (sm_100a).
+//
+// One pass over A computes, for the rows a CTA owns (PAPER.md:893-896,
+// Eq. operator; ℓ per DESIGN.md reading R2):
+//   a1  z_i = <a_i, x>                  (fp32 FMA on 4-element chunks, fp64 sum)
+//   a2  h(z_i) = Σ_j s_j e^{-μ_j z_i+}   (lanes over bins j, fp64 exp)
+//   a3  r_i = y_i - Ī_i h(z_i)           (fp64), ℓ_i = y_i z_i - Ī_i H(z_i)
+//   a4  g += r_i a_i                      (the a_i values still in registers)
+// and writes one fp64 partial vector per CTA (a5 is the finalize kernel).
+//
+// Data movement: a persistent grid (one CTA per SM) streams a contiguous row
+// range through an S-stage shared-memory ring.  Warp 0 is the producer: lane 0
+// issues one 1D bulk copy (TMA engine, L2 evict-first) per stage — a stage is
+// RPS consecutive rows, contiguous in HBM because A is row-major — and all 32
+// lanes fetch the stage's y / Ī'_i / s'_i· with cp.async, whose completion
+// arrives on the same mbarrier.  Consumer warps own a column slab of x and g
+// in registers; WPR warps cooperate on one row when d exceeds one slab
+// (partial dots exchanged through shared memory, one named barrier per stage).
+#pragma once
+
+#include <type_traits>
+
+#include "common.cuh"
+
+namespace poly {
+
+struct DenseArgs {
+  const void *A;
+  int64_t lda;           // row pitch, elements
+  int64_t n;             // local rows
+  int32_t d;
+  int32_t W;
+  const void *y;
+  int32_t ytype;         // 0 i32, 1 f32, 2 f64
+  int32_t relu;
+  const float *s_row;    // optional [n*W]
+  const float *I_row;    // optional [n]
+  double I_bar;
+  const double *x;       // fp64 [d]
+  const double *spec;    // [3*kMaxW]: s, mu, 1/mu
+  double *partials;      // [gridDim.x * d]
+  double *loss_partials; // [gridDim.x]
+  int32_t stages;
+  int32_t side_stride;   // bytes of side data per stage
+};
+
+// Link + residual for one row (warp-uniform z).  Lanes take bins j = lane,
+// lane+32, ...; two fp64 warp sums give h and H.  Returns r_i; accumulates
+// ℓ_i into *lacc on lane 0 when `count_loss`.
+template <bool LOSS>
+__device__ __forceinline__ double row_residual(const double *sp, int W, int relu, double z,
+                                               double yv, double Ii, const float *srow,
+                                               bool count_loss, double *lacc) {
+  const int lane = threadIdx.x & 31;
+  const bool neg = relu && z < 0.0;
+  const double zc = neg ? 0.0 : z;
+  double hs = 0.0, Hs = 0.0;
+  for (int j = lane; j < W; j += 32) {
+    const double sj = srow ? (double)srow[j] : sp[j];
+    const double e = exp_nonpos(-sp[kMaxW + j] * zc);
+    hs += sj * e;
+    if (LOSS) Hs += neg ? sj * z : sj * sp[2 * kMaxW + j] * (1.0 - e);
+  }
+  hs = warp_sum(hs);
+  if (LOSS) {
+    Hs = warp_sum(Hs);
+    if (count_loss && lane == 0) *lacc += yv * z - Ii * Hs;
+  }
+  return yv - Ii * hs;
+}
+
+__device__ __forceinline__ double load_y(const unsigned char *yb, int ytype, int r) {
+  if (ytype == 0) return (double)((const int32_t *)yb)[2 * r];
+  if (ytype == 1) return (double)((const float *)yb)[2 * r];
+  return ((const double *)yb)[r];
+}
+
+template <typename T>
+struct Vec16;
+template <>
+struct Vec16<float> {
+  using type = float4;
+  static constexpr int N = 4;
+};
+template <>
+struct Vec16<double> {
+  using type = double2;
+  static constexpr int N = 2;
+};
+
+template <typename T>
+__device__ __forceinline__ void unpack(const typename Vec16<T>::type &v, T *o);
+template <>
+__device__ __forceinline__ void unpack<float>(const float4 &v, float *o) {
+  o[0] = v.x, o[1] = v.y, o[2] = v.z, o[3] = v.w;
+}
+template <>
+__device__ __forceinline__ void unpack<double>(const double2 &v, double *o) {
+  o[0] = v.x, o[1] = v.y;
+}
+
+// 16-byte chunk of a row at column c0 (smem), zeroing columns >= d.
+template <typename T>
+__device__ __forceinline__ void load_chunk(const T *rowp, int c0, int d, T *ch) {
+  constexpr int VEC = Vec16<T>::N;
+  if (c0 < d) {
+    const typename Vec16<T>::type t = *reinterpret_cast<const typename Vec16<T>::type *>(rowp + c0);
+    unpack<T>(t, ch);
+#pragma unroll
+    for (int e = 0; e < VEC; ++e)
+      if (c0 + e >= d) ch[e] = (T)0;
+  } else {
+#pragma unroll
+    for (int e = 0; e < VEC; ++e) ch[e] = (T)0;
+  }
+}
+
+// T: element type of A (float/double); V: 16-byte chunks per lane per slab;
+// WPR: warps per row; NW: consumer warps; RPS: rows per stage.
+template <typename T, int V, int WPR, int NW, int RPS, bool LOSS>
+__global__ void __launch_bounds__(32 * (NW + 1), 1) k_dense_loss_grad(const DenseArgs a) {
+  constexpr int VEC = Vec16<T>::N;
+  constexpr int SLAB = 32 * VEC * V;  // columns per warp slab
+  constexpr int G = NW / WPR;         // row groups
+  constexpr int RG = RPS / G;         // rows per group per stage
+  static_assert(NW % WPR == 0 && RPS % G == 0, "bad tile");
+
+  extern __shared__ __align__(128) unsigned char smem[];
+  const int S = a.stages;
+  const int64_t lda = a.lda;
+  const size_t stage_elems = (size_t)RPS * (size_t)lda;
+  T *ring = reinterpret_cast<T *>(smem);
+  unsigned char *side = smem + (size_t)S * stage_elems * sizeof(T);
+  double *red = reinterpret_cast<double *>(side + (size_t)S * a.side_stride);  // [2][G][RG][WPR]
+  double *sp = red + 2 * G * RG * WPR;                                         // [3*kMaxW]
+  uint64_t *full = reinterpret_cast<uint64_t *>(sp + 3 * kMaxW);
+  uint64_t *empty = full + S;
+  double *lsum = reinterpret_cast<double *>(empty + S);  // [NW]
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t rb = a.n * (int64_t)blockIdx.x / gridDim.x;
+  const int64_t re = a.n * (int64_t)(blockIdx.x + 1) / gridDim.x;
+  const int nstage = (int)((re - rb + RPS - 1) / RPS);
+  const int yoff = 0, ioff = RPS * 8, soff = RPS * 12;  // side layout: y[8B], I'[4B], s'[4B*W]
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < S; ++s) {
+      mbar_init(&full[s], 1 + 32);
+      mbar_init(&empty[s], NW);
+    }
+    fence_mbar_init();
+  }
+  for (int i = threadIdx.x; i < 3 * kMaxW; i += blockDim.x) sp[i] = a.spec[i];
+  __syncthreads();
+
+  if (warp == 0) {
+    // ------------------------------------------------------------ producer
+    // A is immutable, so streaming may start before the previous kernel
+    // (programmatic dependent launch) has finished.
+    const uint64_t pol = l2_evict_first_policy();
+    const int ysz = a.ytype == 2 ? 8 : 4;
+    for (int st = 0; st < nstage; ++st) {
+      const int slot = st % S;
+      const uint32_t use = (uint32_t)(st / S);
+      if (use > 0) mbar_wait(&empty[slot], (use - 1) & 1u);
+      const int64_t r0 = rb + (int64_t)st * RPS;
+      const int rows = (int)min((int64_t)RPS, re - r0);
+      if (lane == 0) {
+        const uint32_t bytes = (uint32_t)((size_t)rows * lda * sizeof(T));
+        mbar_arrive_expect_tx(&full[slot], bytes);
+        bulk_g2s(ring + (size_t)slot * stage_elems, (const T *)a.A + r0 * lda, bytes, &full[slot],
+                 pol);
+      }
+      unsigned char *sd = side + (size_t)slot * a.side_stride;
+      const unsigned char *yg = (const unsigned char *)a.y + r0 * ysz;
+      for (int r = lane; r < rows; r += 32) {
+        if (ysz == 8)
+          cp_async8(sd + yoff + 8 * r, yg + 8 * r);
+        else
+          cp_async4(sd + yoff + 8 * r, yg + 4 * r);
+      }
+      if (a.I_row) {
+        for (int r = lane; r < rows; r += 32) cp_async4(sd + ioff + 4 * r, a.I_row + r0 + r);
+        const float *sg = a.s_row + r0 * a.W;
+        for (int e = lane; e < rows * a.W; e += 32) cp_async4(sd + soff + 4 * e, sg + e);
+      }
+      cp_async_mbar_arrive(&full[slot]);
+    }
+    asm volatile("cp.async.wait_all;" ::: "memory");
+    return;
+  }
+
+  // ------------------------------------------------------------ consumers
+  const int cw = warp - 1;
+  const int grp = cw / WPR, w = cw % WPR;
+  pdl_wait();  // x is written by the previous kernel
+
+  T xr[V][VEC], gacc[V][VEC];
+#pragma unroll
+  for (int v = 0; v < V; ++v) {
+    const int c0 = w * SLAB + v * 32 * VEC + lane * VEC;
+#pragma unroll
+    for (int e = 0; e < VEC; ++e) {
+      xr[v][e] = (c0 + e < a.d) ? (T)a.x[c0 + e] : (T)0;
+      gacc[v][e] = (T)0;
+    }
+  }
+  double lacc = 0.0;
+  const bool has_rowspec = a.I_row != nullptr;
+  int buf = 0;
+
+  for (int st = 0; st < nstage; ++st) {
+    const int slot = st % S;
+    mbar_wait(&full[slot], (uint32_t)(st / S) & 1u);
+    const int64_t r0 = rb + (int64_t)st * RPS;
+    const int rows = (int)min((int64_t)RPS, re - r0);
+    const T *tile = ring + (size_t)slot * stage_elems;
+    const unsigned char *sd = side + (size_t)slot * a.side_stride;
+
+    // Row chunks stay in registers between the dot and the axpy when they are
+    // few; otherwise they are re-read from the (still resident) smem tile.
+    constexpr bool KEEP = V * VEC * RG <= 16;
+    T av[KEEP ? RG : 1][V][VEC];
+    double zp[RG];
+    // a1: partial dot of this warp's slab for each of its rows
+#pragma unroll
+    for (int q = 0; q < RG; ++q) {
+      const int lr = grp + G * q;
+      double p = 0.0;
+      if (lr < rows) {
+        const T *rowp = tile + (size_t)lr * lda;
+#pragma unroll
+        for (int v = 0; v < V; ++v) {
+          T ch[VEC];
+          load_chunk<T>(rowp, w * SLAB + v * 32 * VEC + lane * VEC, a.d, ch);
+          T pv = ch[0] * xr[v][0];
+#pragma unroll
+          for (int e = 1; e < VEC; ++e) pv = fma(ch[e], xr[v][e], pv);
+          p += (double)pv;
+          if (KEEP) {
+#pragma unroll
+            for (int e = 0; e < VEC; ++e) av[KEEP ? q : 0][v][e] = ch[e];
+          }
+        }
+      }
+      zp[q] = warp_sum(p);
+    }
+    if (WPR > 1) {
+      double *rb2 = red + (size_t)buf * G * RG * WPR + (size_t)grp * RG * WPR;
+      if (lane == 0) {
+#pragma unroll
+        for (int q = 0; q < RG; ++q) rb2[q * WPR + w] = zp[q];
+      }
+      named_bar_sync(1 + grp, 32 * WPR);
+#pragma unroll
+      for (int q = 0; q < RG; ++q) {
+        double z = 0.0;
+#pragma unroll
+        for (int k = 0; k < WPR; ++k) z += rb2[q * WPR + k];
+        zp[q] = z;
+      }
+      buf ^= 1;
+    }
+    // a2-a4
+#pragma unroll
+    for (int q = 0; q < RG; ++q) {
+      const int lr = grp + G * q;
+      if (lr < rows) {
+        const double yv = load_y(sd + yoff, a.ytype, lr);
+        const double Ii = has_rowspec ? (double)((const float *)(sd + ioff))[lr] : a.I_bar;
+        const float *srow = has_rowspec ? (const float *)(sd + soff) + lr * a.W : nullptr;
+        const double r = row_residual<LOSS>(sp, a.W, a.relu, zp[q], yv, Ii, srow, w == 0, &lacc);
+        const T rt = (T)r;
+        const T *rowp = tile + (size_t)lr * lda;
+#pragma unroll
+        for (int v = 0; v < V; ++v) {
+          T ch[VEC];
+          if (KEEP) {
+#pragma unroll
+            for (int e = 0; e < VEC; ++e) ch[e] = av[KEEP ? q : 0][v][e];
+          } else {
+            load_chunk<T>(rowp, w * SLAB + v * 32 * VEC + lane * VEC, a.d, ch);
+          }
+#pragma unroll
+          for (int e = 0; e < VEC; ++e) gacc[v][e] = fma(rt, ch[e], gacc[v][e]);
+        }
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[slot]);
+  }
+
+  // ------------------------------------------- per-CTA partial (fixed order)
+  named_bar_sync(15, 32 * NW);  // every consumer is done with the ring
+  T *gred = ring;               // [G][d]
+#pragma unroll
+  for (int v = 0; v < V; ++v) {
+    const int c0 = w * SLAB + v * 32 * VEC + lane * VEC;
+#pragma unroll
+    for (int e = 0; e < VEC; ++e)
+      if (c0 + e < a.d) gred[(size_t)grp * a.d + c0 + e] = gacc[v][e];
+  }
+  if (lane == 0) lsum[cw] = lacc;
+  named_bar_sync(15, 32 * NW);
+  const int t = threadIdx.x - 32;
+  double *outp = a.partials + (size_t)blockIdx.x * a.d;
+  for (int c = t; c < a.d; c += 32 * NW) {
+    double acc = 0.0;
+#pragma unroll 4
+    for (int g = 0; g < G; ++g) acc += (double)gred[(size_t)g * a.d + c];
+    outp[c] = acc;
+  }
+  if (t == 0) {
+    double l = 0.0;
+    for (int k = 0; k < NW; ++k) l += lsum[k];
+    a.loss_partials[blockIdx.x] = l;
+  }
+  pdl_trigger();
+}
+
+}  // namespace poly

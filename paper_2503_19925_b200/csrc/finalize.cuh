@@ -1,0 +1,178 @@
+// K2/K3 — fixed-order reduction of the per-CTA partial gradients, the 1/n
+// scale of Eq.(operator), and the extragradient step + projection
+//   x_out = P_X(x_anchor - γ g)
+// onto X = B(R; c), R_+^d or R_+^d ∩ B(R).
+//
+// Grid: ceil(d/32) blocks of 256 threads; thread (cl, sl) = (tid % 32,
+// tid / 32) sums partial rows i = sl, sl+8, ... of column blockIdx.x*32+cl,
+// and the 8 slices are combined in order — deterministic for a fixed grid.
+// The projection needs ||v - c||: each block writes its share, and the last
+// block to arrive (atomic ticket) forms the norm in fixed order and applies
+// the scale to all d entries.
+#pragma once
+
+#include "common.cuh"
+
+namespace poly {
+
+enum FinMode : int32_t {
+  FIN_GRAD = 0,       // g = Σ partials / n, loss
+  FIN_STEP = 1,       // x_out = P_X(anchor - γ Σ partials / n)
+  FIN_REDUCE = 2,     // comm[0..d) = Σ partials, comm[d] = Σ loss partials (unnormalised)
+  FIN_GRAD_COMM = 3,  // g = comm / n, loss = comm[d] / n
+  FIN_STEP_COMM = 4,  // x_out = P_X(anchor - γ comm / n)
+  FIN_PROJECT = 5,    // x_out = P_X(anchor)
+};
+
+struct SolveState {
+  double gamma;
+  double loss_cur;     // ℓ at the last evaluation
+  double *trace;       // [trace_cap] or null
+  int32_t trace_cap;
+  int32_t counter;     // F evaluations folded into a step so far
+  int32_t bad;         // 0 or first (1-based) step counter whose iterate was non-finite
+  uint32_t ticket;
+};
+
+struct FinArgs {
+  int32_t mode;
+  int32_t d;
+  int32_t G;                 // number of partial rows
+  int32_t set;
+  int64_t n_norm;            // the n of Eq.(operator)
+  const double *partials;    // [G][d]
+  const double *loss_partials;  // [G]
+  double *comm;              // [d+1]
+  double *g_out;             // optional [d]
+  const double *anchor;      // [d]
+  double *x_out;             // [d] (may alias anchor)
+  double *v_scratch;         // [d]
+  double *block_norm;        // [gridDim.x]
+  int32_t zero_partials;     // 1: reset partials[0][*] and loss_partials[0] to 0 after reading (G == 1)
+  const double *center;      // [d] or null
+  double R;
+  SolveState *state;
+};
+
+__global__ void __launch_bounds__(256) k_finalize(const FinArgs a) {
+  __shared__ double sm[8][33];
+  __shared__ double s_loss;
+  __shared__ int s_last;
+  pdl_wait();
+  pdl_trigger();
+  const int tid = threadIdx.x, cl = tid & 31, sl = tid >> 5;
+  const int c = blockIdx.x * 32 + cl;
+  const int mode = a.mode;
+  const bool from_comm = (mode == FIN_GRAD_COMM || mode == FIN_STEP_COMM);
+  const bool needs_g = (mode != FIN_PROJECT);
+
+  // ---- gradient column sums (a5), fixed order
+  double tot = 0.0;
+  if (needs_g) {
+    double acc = 0.0;
+    if (c < a.d) {
+      if (from_comm) {
+        if (sl == 0) acc = a.comm[c];
+      } else {
+        for (int i = sl; i < a.G; i += 8) acc += a.partials[(size_t)i * a.d + c];
+        if (a.zero_partials && sl == 0) const_cast<double *>(a.partials)[c] = 0.0;
+      }
+    }
+    sm[sl][cl] = acc;
+  }
+  // ---- loss (block 0, warp 1), fixed order
+  if (blockIdx.x == 0 && sl == 1 && needs_g) {
+    double l = 0.0;
+    if (from_comm) {
+      l = (cl == 0) ? a.comm[a.d] : 0.0;
+    } else {
+      for (int i = cl; i < a.G; i += 32) l += a.loss_partials[i];
+    }
+    l = warp_sum(l);
+    if (a.zero_partials && cl == 0 && !from_comm) const_cast<double *>(a.loss_partials)[0] = 0.0;
+    if (cl == 0) s_loss = l;
+  }
+  __syncthreads();
+  if (sl != 0) {
+    if (mode == FIN_GRAD || mode == FIN_GRAD_COMM || mode == FIN_REDUCE) return;
+  }
+  if (sl == 0 && needs_g) {
+#pragma unroll
+    for (int k = 0; k < 8; ++k) tot += sm[k][cl];
+  }
+  if (mode == FIN_REDUCE) {
+    if (c < a.d) a.comm[c] = tot;
+    if (blockIdx.x == 0 && cl == 0) a.comm[a.d] = s_loss;
+    return;
+  }
+  const double nn = (double)a.n_norm;
+  if (mode == FIN_GRAD || mode == FIN_GRAD_COMM) {
+    if (c < a.d && a.g_out) a.g_out[c] = tot / nn;
+    if (blockIdx.x == 0 && cl == 0) a.state->loss_cur = s_loss / nn;
+    return;
+  }
+
+  // ---- step + projection (a7)
+  double q = 0.0;
+  if (sl == 0) {
+    if (c < a.d) {
+      double v = a.anchor[c];
+      if (needs_g) {
+        const double g = tot / nn;
+        if (a.g_out) a.g_out[c] = g;
+        v = v - a.state->gamma * g;
+      }
+      if (a.set == 2 || a.set == 3) v = v > 0.0 ? v : 0.0;
+      const double df = (a.set == 1 && a.center) ? v - a.center[c] : v;
+      q = df * df;
+      a.v_scratch[c] = v;
+    }
+    q = warp_sum(q);
+    if (cl == 0) {
+      a.block_norm[blockIdx.x] = q;
+      if (blockIdx.x == 0 && needs_g) a.state->loss_cur = s_loss / nn;
+      __threadfence();
+      const uint32_t prev = atomicAdd(&a.state->ticket, 1u);
+      s_last = (prev == gridDim.x - 1);
+    }
+  }
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  // last block: ||v - c||² in fixed order, then the scale
+  if (sl == 0) {
+    double nr = 0.0;
+    for (int b = cl; b < (int)gridDim.x; b += 32) nr += ((volatile double *)a.block_norm)[b];
+    nr = warp_sum(nr);
+    if (cl == 0) sm[0][0] = nr;
+  }
+  __syncthreads();
+  const double nrm = sqrt(sm[0][0]);
+  double scale = 1.0;
+  if ((a.set == 1 || a.set == 3) && nrm > a.R) scale = a.R / nrm;
+  for (int k = tid; k < a.d; k += blockDim.x) {
+    const double v = ((volatile double *)a.v_scratch)[k];
+    double xo;
+    if (a.set == 1) {
+      const double ck = a.center ? a.center[k] : 0.0;
+      xo = scale == 1.0 ? v : ck + (v - ck) * scale;
+    } else {
+      xo = v * scale;
+    }
+    a.x_out[k] = xo;
+  }
+  if (tid == 0) {
+    SolveState *s = a.state;
+    s->ticket = 0;
+    if (needs_g) {
+      const int k = s->counter;
+      if (s->trace && k < s->trace_cap) s->trace[k] = *(volatile double *)&s->loss_cur;
+      s->counter = k + 1;
+      if (!isfinite(nrm) && s->bad == 0) s->bad = k + 1;
+    } else if (!isfinite(nrm) && s->bad == 0) {
+      s->bad = -1;
+    }
+  }
+}
+
+}  // namespace poly

@@ -1,0 +1,877 @@
+// Host implementation of the C ABI in include/poly.h.
+//
+// Per F evaluation the library enqueues, on its own work
+// stream (ordered after the caller's stream with events):
+//   K1 k_dense_loss_grad (or K4 k_csr_loss_grad)   one pass over A
+//   K2/K3 k_finalize                                fixed-order reduce, 1/n,
+//                                                   step + projection
+//   (world > 1: k_finalize(REDUCE) -> ncclAllReduce(d+1 doubles) -> k_finalize)
+// and poly_solve replays one CUDA graph per U EXACT iterations
+// (Eq. extragrad-method) with programmatic dependent launch
+// between the kernels so the next A stream starts while the step finishes.
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nccl.h>
+#include <stdarg.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <algorithm>
+#include <cmath>
+#include <vector>
+
+#include "../../include/poly.h"
+#include "aux.cuh"
+#include "csr.cuh"
+#include "dense.cuh"
+#include "finalize.cuh"
+
+using namespace poly;
+
+namespace {
+
+thread_local char g_err[1024] = "";
+
+int fail(int code, const char *fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+  return code;
+}
+
+#define CK(call)                                                                               \
+  do {                                                                                         \
+    cudaError_t e_ = (call);                                                                   \
+    if (e_ != cudaSuccess)                                                                     \
+      return fail(POLY_ECUDA, "%s failed: %s (%s:%d)", #call, cudaGetErrorString(e_), __FILE__, \
+                  __LINE__);                                                                   \
+  } while (0)
+
+#define TRY(call)           \
+  do {                      \
+    int r_ = (call);        \
+    if (r_ != POLY_OK) return r_; \
+  } while (0)
+
+// ------------------------------------------------------------------ NCCL
+struct NcclApi {
+  void *lib = nullptr;
+  decltype(&ncclGetUniqueId) getUniqueId = nullptr;
+  decltype(&ncclCommInitRank) commInitRank = nullptr;
+  decltype(&ncclAllReduce) allReduce = nullptr;
+  decltype(&ncclCommDestroy) commDestroy = nullptr;
+  decltype(&ncclCommAbort) commAbort = nullptr;
+  decltype(&ncclGetErrorString) errStr = nullptr;
+};
+
+NcclApi *nccl_api() {
+  static NcclApi api;
+  static bool tried = false;
+  if (tried) return api.lib ? &api : nullptr;
+  tried = true;
+  const char *names[] = {"libnccl.so.2", "libnccl.so"};
+  for (const char *nm : names) {
+    api.lib = dlopen(nm, RTLD_NOW | RTLD_GLOBAL);
+    if (api.lib) break;
+  }
+  if (!api.lib) return nullptr;
+  api.getUniqueId = (decltype(api.getUniqueId))dlsym(api.lib, "ncclGetUniqueId");
+  api.commInitRank = (decltype(api.commInitRank))dlsym(api.lib, "ncclCommInitRank");
+  api.allReduce = (decltype(api.allReduce))dlsym(api.lib, "ncclAllReduce");
+  api.commDestroy = (decltype(api.commDestroy))dlsym(api.lib, "ncclCommDestroy");
+  api.commAbort = (decltype(api.commAbort))dlsym(api.lib, "ncclCommAbort");
+  api.errStr = (decltype(api.errStr))dlsym(api.lib, "ncclGetErrorString");
+  if (!api.getUniqueId || !api.commInitRank || !api.allReduce || !api.commDestroy ||
+      !api.commAbort || !api.errStr) {
+    api.lib = nullptr;
+    return nullptr;
+  }
+  return &api;
+}
+
+// ------------------------------------------------------- kernel variants
+struct DenseVariant {
+  int V, WPR, NW, RPS;
+  const void *fn[2];  // [LOSS]
+};
+
+#define DV(T, V, WPR, NW, RPS)                                              \
+  DenseVariant {                                                            \
+    V, WPR, NW, RPS, {                                                      \
+      (const void *)&k_dense_loss_grad<T, V, WPR, NW, RPS, false>,          \
+          (const void *)&k_dense_loss_grad<T, V, WPR, NW, RPS, true>        \
+    }                                                                       \
+  }
+
+// columns per slab: 32 lanes x (16 B / elsize) x V
+const DenseVariant kDenseF32[] = {
+    DV(float, 1, 1, 16, 64), DV(float, 2, 1, 16, 32), DV(float, 4, 1, 16, 16),
+    DV(float, 8, 1, 12, 12), DV(float, 8, 2, 12, 6),  DV(float, 8, 4, 12, 3),
+    DV(float, 8, 8, 8, 1),
+};
+const DenseVariant kDenseF64[] = {
+    DV(double, 1, 1, 16, 64), DV(double, 2, 1, 16, 32), DV(double, 4, 1, 16, 16),
+    DV(double, 8, 1, 12, 12), DV(double, 8, 2, 12, 6),  DV(double, 8, 4, 12, 3),
+    DV(double, 8, 8, 8, 1),
+};
+
+constexpr int kCsrKreg = 16;
+const void *kCsrFn[2][2] = {
+    {(const void *)&k_csr_loss_grad<float, kCsrKreg, false>,
+     (const void *)&k_csr_loss_grad<float, kCsrKreg, true>},
+    {(const void *)&k_csr_loss_grad<double, kCsrKreg, false>,
+     (const void *)&k_csr_loss_grad<double, kCsrKreg, true>},
+};
+
+constexpr size_t kSmemLimit = 227 * 1024;
+constexpr size_t kRingBudget = 200 * 1024;
+
+__global__ void k_min_i32(const int32_t *y, int64_t n, int32_t *out) {
+  int32_t m = 0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    m = min(m, y[i]);
+  if (m < 0) atomicMin(out, m);
+}
+
+__global__ void k_check_csr(const int64_t *rp, const int32_t *col, int64_t n, int64_t nnz, int d,
+                            int32_t *bad) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i <= n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    if (i == 0 && rp[0] != 0) atomicOr(bad, 1);
+    if (i == n && rp[n] != nnz) atomicOr(bad, 2);
+    if (i < n && rp[i + 1] < rp[i]) atomicOr(bad, 4);
+  }
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < nnz;
+       e += (int64_t)gridDim.x * blockDim.x)
+    if (col[e] < 0 || col[e] >= d) atomicOr(bad, 8);
+}
+
+bool is_device_ptr(const void *p) {
+  if (!p) return false;
+  cudaPointerAttributes at;
+  if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged;
+}
+
+}  // namespace
+
+struct poly_handle {
+  poly_problem p{};
+  int dev = 0, sms = 0;
+  int elsize = 4, ysz = 4;
+  cudaStream_t user = nullptr, work = nullptr;
+  cudaEvent_t ev_in = nullptr, ev_out = nullptr;
+  std::vector<void *> owned;  // library-owned device buffers
+  double *spec = nullptr, *center = nullptr;
+  // K1
+  const DenseVariant *dv = nullptr;
+  int k1_grid = 0, k1_threads = 0, k1_stages = 0, k1_side = 0;
+  size_t k1_smem = 0;
+  int k4_grid = 0;
+  // workspaces
+  int G = 0;  // partial rows
+  double *partials = nullptr, *loss_partials = nullptr, *comm = nullptr;
+  double *xa = nullptr, *xh = nullptr, *xin = nullptr, *gbuf = nullptr;
+  double *vscratch = nullptr, *block_norm = nullptr, *trace = nullptr;
+  int trace_cap = 0;
+  SolveState *state = nullptr, *hstate = nullptr;
+  int fin_grid = 0;
+  bool pdl = true, use_graph = true;
+  cudaGraphExec_t gexec[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};  // [loss][U>1]
+  int graph_U = 8;
+  ncclComm_t nccl = nullptr;
+  // profiling
+  bool prof = false;
+  std::vector<cudaEvent_t> evpool;
+  size_t evused = 0;
+  struct Rec { int kind; cudaEvent_t a, b; };
+  std::vector<Rec> recs;
+  double ktimes[5] = {0, 0, 0, 0, 0};
+};
+
+namespace {
+
+template <typename... Args>
+int launch(poly_handle *h, const void *fn, dim3 grid, dim3 block, size_t smem, bool pdl,
+           Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = h->work;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = (pdl && h->pdl) ? 1 : 0;
+  void *argv[] = {(void *)&args...};
+  CK(cudaLaunchKernelExC(&cfg, fn, argv));
+  return POLY_OK;
+}
+
+cudaEvent_t prof_event(poly_handle *h) {
+  if (h->evused == h->evpool.size()) {
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    h->evpool.push_back(e);
+  }
+  return h->evpool[h->evused++];
+}
+
+struct ProfScope {
+  poly_handle *h;
+  int kind;
+  cudaEvent_t a = nullptr;
+  ProfScope(poly_handle *h_, int k) : h(h_), kind(k) {
+    if (h->prof) {
+      a = prof_event(h);
+      cudaEventRecord(a, h->work);
+    }
+  }
+  ~ProfScope() {
+    if (h->prof) {
+      cudaEvent_t b = prof_event(h);
+      cudaEventRecord(b, h->work);
+      h->recs.push_back({kind, a, b});
+    }
+  }
+};
+
+// K1 / K4: one pass over A at x (fp64, device)
+int enqueue_pass(poly_handle *h, const double *x, bool loss) {
+  ProfScope ps(h, 0);
+  const poly_problem &p = h->p;
+  if (p.layout == POLY_DENSE) {
+    DenseArgs a{};
+    a.A = p.A;
+    a.lda = p.lda;
+    a.n = p.n_local;
+    a.d = (int32_t)p.d;
+    a.W = p.W;
+    a.y = p.y;
+    a.ytype = p.ytype;
+    a.relu = p.relu;
+    a.s_row = p.s_row;
+    a.I_row = p.I_row;
+    a.I_bar = p.I_bar;
+    a.x = x;
+    a.spec = h->spec;
+    a.partials = h->partials;
+    a.loss_partials = h->loss_partials;
+    a.stages = h->k1_stages;
+    a.side_stride = h->k1_side;
+    return launch(h, h->dv->fn[loss ? 1 : 0], dim3(h->k1_grid), dim3(h->k1_threads), h->k1_smem,
+                  true, a);
+  }
+  CsrArgs a{};
+  a.row_ptr = p.row_ptr;
+  a.col = p.col;
+  a.val = p.val;
+  a.n = p.n_local;
+  a.d = (int32_t)p.d;
+  a.W = p.W;
+  a.y = p.y;
+  a.ytype = p.ytype;
+  a.relu = p.relu;
+  a.s_row = p.s_row;
+  a.I_row = p.I_row;
+  a.I_bar = p.I_bar;
+  a.x = x;
+  a.spec = h->spec;
+  a.gacc = h->partials;
+  a.lacc = h->loss_partials;
+  return launch(h, kCsrFn[p.dtype][loss ? 1 : 0], dim3(h->k4_grid), dim3(256), 0, true, a);
+}
+
+FinArgs fin_base(poly_handle *h, int mode) {
+  FinArgs f{};
+  f.mode = mode;
+  f.d = (int32_t)h->p.d;
+  f.G = h->G;
+  f.set = h->p.set;
+  f.n_norm = h->p.n_global;
+  f.partials = h->partials;
+  f.loss_partials = h->loss_partials;
+  f.comm = h->comm;
+  f.v_scratch = h->vscratch;
+  f.block_norm = h->block_norm;
+  f.zero_partials = h->p.layout == POLY_CSR ? 1 : 0;
+  f.center = h->center;
+  f.R = h->p.R;
+  f.state = h->state;
+  return f;
+}
+
+int enqueue_fin(poly_handle *h, const FinArgs &f) {
+  ProfScope ps(h, 1);
+  return launch(h, (const void *)&k_finalize, dim3(h->fin_grid), dim3(256), 0, true, f);
+}
+
+int enqueue_allreduce(poly_handle *h) {
+  ProfScope ps(h, 2);
+  NcclApi *api = nccl_api();
+  ncclResult_t r = api->allReduce(h->comm, h->comm, (size_t)h->p.d + 1, ncclFloat64, ncclSum,
+                                  h->nccl, h->work);
+  if (r != ncclSuccess) {
+    api->commAbort(h->nccl);
+    h->nccl = nullptr;
+    return fail(POLY_ENCCL, "ncclAllReduce failed: %s", api->errStr(r));
+  }
+  return POLY_OK;
+}
+
+// F at x, then either g/loss (step == false) or x_out = P_X(anchor - γ F(x)).
+int enqueue_eval(poly_handle *h, const double *x, bool loss, bool step, const double *anchor,
+                 double *x_out, double *g_out) {
+  TRY(enqueue_pass(h, x, loss));
+  FinArgs f = fin_base(h, 0);
+  f.anchor = anchor;
+  f.x_out = x_out;
+  f.g_out = g_out;
+  if (h->p.world == 1) {
+    f.mode = step ? FIN_STEP : FIN_GRAD;
+    return enqueue_fin(h, f);
+  }
+  FinArgs r = f;
+  r.mode = FIN_REDUCE;
+  TRY(enqueue_fin(h, r));
+  TRY(enqueue_allreduce(h));
+  f.mode = step ? FIN_STEP_COMM : FIN_GRAD_COMM;
+  f.zero_partials = 0;
+  return enqueue_fin(h, f);
+}
+
+// one EXACT iteration on the internal iterate xa (anchor), half-step in xh
+int enqueue_iteration(poly_handle *h, bool loss) {
+  TRY(enqueue_eval(h, h->xa, loss, true, h->xa, h->xh, nullptr));
+  return enqueue_eval(h, h->xh, loss, true, h->xa, h->xa, nullptr);
+}
+
+int build_graph(poly_handle *h, bool loss, int U, cudaGraphExec_t *out) {
+  cudaGraph_t g = nullptr;
+  CK(cudaStreamBeginCapture(h->work, cudaStreamCaptureModeThreadLocal));
+  int rc = POLY_OK;
+  for (int u = 0; u < U && rc == POLY_OK; ++u) rc = enqueue_iteration(h, loss);
+  cudaError_t e = cudaStreamEndCapture(h->work, &g);
+  if (rc != POLY_OK) {
+    if (g) cudaGraphDestroy(g);
+    return rc;
+  }
+  if (e != cudaSuccess) return fail(POLY_ECUDA, "graph capture: %s", cudaGetErrorString(e));
+  e = cudaGraphInstantiate(out, g, 0);
+  cudaGraphDestroy(g);
+  if (e != cudaSuccess) return fail(POLY_ECUDA, "graph instantiate: %s", cudaGetErrorString(e));
+  return POLY_OK;
+}
+
+int sync_in(poly_handle *h) {
+  CK(cudaEventRecord(h->ev_in, h->user));
+  CK(cudaStreamWaitEvent(h->work, h->ev_in, 0));
+  return POLY_OK;
+}
+int sync_out(poly_handle *h) {
+  CK(cudaEventRecord(h->ev_out, h->work));
+  CK(cudaStreamWaitEvent(h->user, h->ev_out, 0));
+  return POLY_OK;
+}
+
+template <typename T>
+int dev_alloc(poly_handle *h, T **ptr, size_t count) {
+  void *p = nullptr;
+  cudaError_t e = cudaMalloc(&p, std::max<size_t>(count, 1) * sizeof(T));
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return fail(POLY_ENOMEM, "cudaMalloc(%zu bytes): %s", count * sizeof(T), cudaGetErrorString(e));
+  }
+  h->owned.push_back(p);
+  *ptr = (T *)p;
+  return POLY_OK;
+}
+
+int copy_in(poly_handle *h, const void **field, size_t bytes) {
+  if (!*field || bytes == 0) return POLY_OK;
+  void *d = nullptr;
+  TRY(dev_alloc(h, (unsigned char **)&d, bytes));
+  CK(cudaMemcpyAsync(d, *field, bytes, cudaMemcpyHostToDevice, h->work));
+  *field = d;
+  return POLY_OK;
+}
+
+int validate(const poly_problem *p) {
+  if (!p) return fail(POLY_EINVAL, "problem is NULL");
+  if (p->n_local < 0) return fail(POLY_EINVAL, "n_local < 0");
+  if (p->n_global < 1 || p->n_global < p->n_local) return fail(POLY_EINVAL, "n_global must be >= max(1, n_local)");
+  if (p->d < 1 || p->d > (1 << 30)) return fail(POLY_EINVAL, "d out of range");
+  if (p->layout != POLY_DENSE && p->layout != POLY_CSR) return fail(POLY_EINVAL, "bad layout");
+  if (p->dtype != POLY_F32 && p->dtype != POLY_F64) return fail(POLY_EINVAL, "bad dtype");
+  if (p->ytype < POLY_Y_I32 || p->ytype > POLY_Y_F64) return fail(POLY_EINVAL, "bad ytype");
+  if (p->W < 1) return fail(POLY_EINVAL, "W < 1 (SPEC.md:28)");
+  if (p->W > kMaxW) return fail(POLY_EUNSUPPORTED, "W > %d", kMaxW);
+  if (!p->s || !p->mu) return fail(POLY_EINVAL, "spectrum pointers are NULL");
+  double tot = 0.0;
+  for (int j = 0; j < p->W; ++j) {
+    if (!(p->s[j] > 0.0 && p->s[j] <= 1.0)) return fail(POLY_EINVAL, "s[%d] not in (0,1] (SPEC.md:25)", j);
+    if (!(p->mu[j] > 0.0) || !std::isfinite(p->mu[j])) return fail(POLY_EINVAL, "mu[%d] must be > 0 (SPEC.md:26)", j);
+    tot += p->s[j];
+  }
+  if (std::fabs(tot - 1.0) > 1e-12) return fail(POLY_EINVAL, "sum_j s_j = %.17g != 1 (SPEC.md:25)", tot);
+  if (!(p->I_bar > 0.0) || !std::isfinite(p->I_bar)) return fail(POLY_EINVAL, "I_bar must be > 0 (SPEC.md:27)");
+  if ((p->s_row == nullptr) != (p->I_row == nullptr)) return fail(POLY_EINVAL, "s_row and I_row must both be given or both NULL");
+  if (p->relu != 0 && p->relu != 1) return fail(POLY_EINVAL, "relu must be 0 or 1");
+  if (p->set < POLY_SET_NONE || p->set > POLY_SET_NONNEG_BALL) return fail(POLY_EINVAL, "bad set");
+  if ((p->set == POLY_SET_BALL || p->set == POLY_SET_NONNEG_BALL) && !(p->R > 0.0))
+    return fail(POLY_EINVAL, "ball radius must be > 0");
+  if (p->set == POLY_SET_NONNEG_BALL && p->center) return fail(POLY_EINVAL, "NONNEG_BALL requires center = NULL");
+  if (p->world < 1 || p->rank < 0 || p->rank >= p->world) return fail(POLY_EINVAL, "bad rank/world");
+  if (p->world > 1 && !p->nccl_id) return fail(POLY_EINVAL, "world > 1 needs nccl_id");
+  if (p->n_local > 0) {
+    if (!p->y) return fail(POLY_EINVAL, "y is NULL");
+    if (p->layout == POLY_DENSE) {
+      if (!p->A) return fail(POLY_EINVAL, "A is NULL");
+      if (p->lda < p->d) return fail(POLY_EINVAL, "lda < d");
+      const int es = p->dtype == POLY_F32 ? 4 : 8;
+      if ((p->lda * es) % 16 != 0) return fail(POLY_EINVAL, "lda*elsize must be a multiple of 16 bytes");
+      if (!(p->flags & POLY_FLAG_HOST_INPUTS) && ((uintptr_t)p->A % 16) != 0)
+        return fail(POLY_EINVAL, "A must be 16-byte aligned");
+    } else {
+      if (!p->row_ptr || (p->nnz > 0 && (!p->col || !p->val))) return fail(POLY_EINVAL, "CSR arrays are NULL");
+      if (p->nnz < 0) return fail(POLY_EINVAL, "nnz < 0");
+    }
+  }
+  return POLY_OK;
+}
+
+int setup_dense(poly_handle *h) {
+  const poly_problem &p = h->p;
+  const int vec = 16 / h->elsize;
+  const DenseVariant *tab = p.dtype == POLY_F32 ? kDenseF32 : kDenseF64;
+  const DenseVariant *dv = nullptr;
+  for (int i = 0; i < 7; ++i) {
+    const int64_t cols = (int64_t)32 * vec * tab[i].V * tab[i].WPR;
+    if (p.d <= cols) {
+      dv = &tab[i];
+      break;
+    }
+  }
+  if (!dv) return fail(POLY_EUNSUPPORTED, "dense d = %lld exceeds the largest tile (%d columns)",
+                       (long long)p.d, 32 * vec * 8 * 8);
+  h->dv = dv;
+  h->k1_threads = 32 * (dv->NW + 1);
+  const int G = dv->NW / dv->WPR;
+  const int RG = dv->RPS / G;
+  const size_t stage = (size_t)dv->RPS * p.lda * h->elsize;
+  h->k1_side = (int)(((size_t)dv->RPS * (12 + 4 * p.W) + 15) / 16 * 16);
+  const size_t fixed = (size_t)2 * G * RG * dv->WPR * 8 + 3 * kMaxW * 8 + 2 * 8 * 8 + dv->NW * 8 + 256;
+  int S = (int)(kRingBudget / (stage + h->k1_side));
+  S = std::max(2, std::min(8, S));
+  size_t ring = (size_t)S * stage;
+  const size_t gred = (size_t)G * p.d * h->elsize;
+  while (ring < gred && S < 8) ring = (size_t)(++S) * stage;
+  if (ring < gred) return fail(POLY_EUNSUPPORTED, "tile configuration does not fit (ring < reduction)");
+  h->k1_stages = S;
+  h->k1_smem = ring + (size_t)S * h->k1_side + fixed;
+  if (h->k1_smem > kSmemLimit) {
+    S = 2;
+    h->k1_stages = S;
+    h->k1_smem = (size_t)S * (stage + h->k1_side) + fixed;
+    if (h->k1_smem > kSmemLimit || (size_t)S * stage < gred)
+      return fail(POLY_EUNSUPPORTED, "row of %lld elements too large for the smem ring", (long long)p.lda);
+  }
+  for (int l = 0; l < 2; ++l)
+    CK(cudaFuncSetAttribute(dv->fn[l], cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->k1_smem));
+  const int64_t tiles = (p.n_local + dv->RPS - 1) / dv->RPS;
+  h->k1_grid = (int)std::max<int64_t>(1, std::min<int64_t>(h->sms, tiles));
+  h->G = h->k1_grid;
+  return POLY_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int poly_abi_version(void) { return POLY_ABI_VERSION; }
+const char *poly_last_error(void) { return g_err; }
+
+int poly_nccl_unique_id(void *out128) {
+  if (!out128) return fail(POLY_EINVAL, "out is NULL");
+  NcclApi *api = nccl_api();
+  if (!api) return fail(POLY_ENCCL, "cannot load libnccl.so.2");
+  ncclUniqueId id;
+  ncclResult_t r = api->getUniqueId(&id);
+  if (r != ncclSuccess) return fail(POLY_ENCCL, "ncclGetUniqueId: %s", api->errStr(r));
+  memcpy(out128, &id, sizeof(id));
+  return POLY_OK;
+}
+
+void poly_free(poly_handle *h) {
+  if (!h) return;
+  if (h->work) cudaStreamSynchronize(h->work);
+  for (auto &a : h->gexec)
+    for (auto &g : a)
+      if (g) cudaGraphExecDestroy(g);
+  if (h->nccl) {
+    NcclApi *api = nccl_api();
+    if (api) api->commDestroy(h->nccl);
+  }
+  for (void *p : h->owned) cudaFree(p);
+  if (h->hstate) cudaFreeHost(h->hstate);
+  for (cudaEvent_t e : h->evpool) cudaEventDestroy(e);
+  if (h->ev_in) cudaEventDestroy(h->ev_in);
+  if (h->ev_out) cudaEventDestroy(h->ev_out);
+  if (h->work) cudaStreamDestroy(h->work);
+  delete h;
+}
+
+int poly_init(const poly_problem *pin, poly_handle **out) {
+  if (!out) return fail(POLY_EINVAL, "out is NULL");
+  *out = nullptr;
+  TRY(validate(pin));
+  poly_handle *h = new poly_handle();
+  h->p = *pin;
+  poly_problem &p = h->p;
+  int rc = POLY_OK;
+  auto bail = [&](int code) {
+    poly_free(h);
+    return code;
+  };
+  if (cudaGetDevice(&h->dev) != cudaSuccess ||
+      cudaDeviceGetAttribute(&h->sms, cudaDevAttrMultiProcessorCount, h->dev) != cudaSuccess) {
+    cudaGetLastError();
+    delete h;
+    return fail(POLY_ECUDA, "no CUDA device available");
+  }
+  h->elsize = p.dtype == POLY_F32 ? 4 : 8;
+  h->ysz = p.ytype == POLY_Y_F64 ? 8 : 4;
+  h->user = (cudaStream_t)p.stream;
+  h->pdl = !(p.flags & POLY_FLAG_NO_PDL);
+  h->use_graph = !(p.flags & POLY_FLAG_NO_GRAPH);
+  if (cudaStreamCreateWithFlags(&h->work, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaEventCreateWithFlags(&h->ev_in, cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&h->ev_out, cudaEventDisableTiming) != cudaSuccess)
+    return bail(fail(POLY_ECUDA, "stream/event creation failed"));
+  if ((rc = sync_in(h)) != POLY_OK) return bail(rc);
+
+  // host inputs -> library-owned device copies
+  if (p.flags & POLY_FLAG_HOST_INPUTS) {
+    const size_t n = (size_t)p.n_local;
+    if (p.layout == POLY_DENSE) {
+      if ((rc = copy_in(h, &p.A, n * p.lda * h->elsize)) != POLY_OK) return bail(rc);
+    } else {
+      const void *rp = p.row_ptr, *cl = p.col;
+      if ((rc = copy_in(h, &rp, (n + 1) * 8)) != POLY_OK) return bail(rc);
+      if ((rc = copy_in(h, &cl, (size_t)p.nnz * 4)) != POLY_OK) return bail(rc);
+      if ((rc = copy_in(h, &p.val, (size_t)p.nnz * h->elsize)) != POLY_OK) return bail(rc);
+      p.row_ptr = (const int64_t *)rp;
+      p.col = (const int32_t *)cl;
+    }
+    if ((rc = copy_in(h, &p.y, n * h->ysz)) != POLY_OK) return bail(rc);
+    const void *sr = p.s_row, *ir = p.I_row;
+    if ((rc = copy_in(h, &sr, n * p.W * 4)) != POLY_OK) return bail(rc);
+    if ((rc = copy_in(h, &ir, n * 4)) != POLY_OK) return bail(rc);
+    p.s_row = (const float *)sr;
+    p.I_row = (const float *)ir;
+  }
+
+  // spectrum [s | mu | 1/mu] and centre
+  std::vector<double> spec(3 * kMaxW, 0.0);
+  for (int j = 0; j < p.W; ++j) {
+    spec[j] = p.s[j];
+    spec[kMaxW + j] = p.mu[j];
+    spec[2 * kMaxW + j] = 1.0 / p.mu[j];
+  }
+  if ((rc = dev_alloc(h, &h->spec, 3 * kMaxW)) != POLY_OK) return bail(rc);
+  if (cudaMemcpy(h->spec, spec.data(), spec.size() * 8, cudaMemcpyHostToDevice) != cudaSuccess)
+    return bail(fail(POLY_ECUDA, "spectrum upload failed"));
+  if (p.center) {
+    if ((rc = dev_alloc(h, &h->center, p.d)) != POLY_OK) return bail(rc);
+    if (cudaMemcpy(h->center, p.center, p.d * 8, cudaMemcpyHostToDevice) != cudaSuccess)
+      return bail(fail(POLY_ECUDA, "centre upload failed"));
+  }
+  p.s = p.mu = p.center = nullptr;  // host copies are not kept
+
+  // tile configuration and workspaces
+  if (p.layout == POLY_DENSE) {
+    if ((rc = setup_dense(h)) != POLY_OK) return bail(rc);
+    if ((rc = dev_alloc(h, &h->partials, (size_t)h->G * p.d)) != POLY_OK) return bail(rc);
+    if ((rc = dev_alloc(h, &h->loss_partials, (size_t)h->G)) != POLY_OK) return bail(rc);
+  } else {
+    h->G = 1;
+    const int64_t warps = std::max<int64_t>(1, p.n_local);
+    h->k4_grid = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)h->sms * 8, (warps + 7) / 8));
+    if ((rc = dev_alloc(h, &h->partials, (size_t)p.d)) != POLY_OK) return bail(rc);
+    if ((rc = dev_alloc(h, &h->loss_partials, 1)) != POLY_OK) return bail(rc);
+    if (cudaMemsetAsync(h->partials, 0, p.d * 8, h->work) != cudaSuccess ||
+        cudaMemsetAsync(h->loss_partials, 0, 8, h->work) != cudaSuccess)
+      return bail(fail(POLY_ECUDA, "memset failed"));
+  }
+  h->fin_grid = (int)((p.d + 31) / 32);
+  if ((rc = dev_alloc(h, &h->comm, (size_t)p.d + 1)) != POLY_OK) return bail(rc);
+  if ((rc = dev_alloc(h, &h->xa, (size_t)p.d)) != POLY_OK) return bail(rc);
+  if ((rc = dev_alloc(h, &h->xh, (size_t)p.d)) != POLY_OK) return bail(rc);
+  if ((rc = dev_alloc(h, &h->xin, (size_t)p.d)) != POLY_OK) return bail(rc);
+  if ((rc = dev_alloc(h, &h->gbuf, (size_t)p.d)) != POLY_OK) return bail(rc);
+  if ((rc = dev_alloc(h, &h->vscratch, (size_t)p.d)) != POLY_OK) return bail(rc);
+  if ((rc = dev_alloc(h, &h->block_norm, (size_t)h->fin_grid)) != POLY_OK) return bail(rc);
+  if ((rc = dev_alloc(h, &h->state, 1)) != POLY_OK) return bail(rc);
+  if (cudaMallocHost(&h->hstate, sizeof(SolveState)) != cudaSuccess)
+    return bail(fail(POLY_ENOMEM, "cudaMallocHost failed"));
+  memset(h->hstate, 0, sizeof(SolveState));
+  if (cudaMemcpyAsync(h->state, h->hstate, sizeof(SolveState), cudaMemcpyHostToDevice, h->work) != cudaSuccess)
+    return bail(fail(POLY_ECUDA, "state upload failed"));
+
+  // input checks that need the device: counts >= 0, CSR structure
+  if (p.n_local > 0) {
+    int32_t *flag = nullptr;
+    if ((rc = dev_alloc(h, &flag, 1)) != POLY_OK) return bail(rc);
+    int32_t hv = 0;
+    cudaMemsetAsync(flag, 0, 4, h->work);
+    if (p.ytype == POLY_Y_I32) {
+      k_min_i32<<<std::min<int64_t>(1024, (p.n_local + 255) / 256), 256, 0, h->work>>>(
+          (const int32_t *)p.y, p.n_local, flag);
+      cudaMemcpyAsync(&hv, flag, 4, cudaMemcpyDeviceToHost, h->work);
+      if (cudaStreamSynchronize(h->work) != cudaSuccess)
+        return bail(fail(POLY_ECUDA, "count check failed: %s", cudaGetErrorString(cudaGetLastError())));
+      if (hv < 0) return bail(fail(POLY_EINVAL, "negative Poisson count in y (PAPER.md:876-878)"));
+    }
+    if (p.layout == POLY_CSR) {
+      cudaMemsetAsync(flag, 0, 4, h->work);
+      k_check_csr<<<1024, 256, 0, h->work>>>(p.row_ptr, p.col, p.n_local, p.nnz, (int)p.d, flag);
+      cudaMemcpyAsync(&hv, flag, 4, cudaMemcpyDeviceToHost, h->work);
+      if (cudaStreamSynchronize(h->work) != cudaSuccess)
+        return bail(fail(POLY_ECUDA, "CSR check failed: %s", cudaGetErrorString(cudaGetLastError())));
+      if (hv) return bail(fail(POLY_EINVAL, "invalid CSR structure (code %d)", hv));
+    }
+  }
+
+  if (p.world > 1) {
+    NcclApi *api = nccl_api();
+    if (!api) return bail(fail(POLY_ENCCL, "world > 1 but libnccl.so.2 cannot be loaded"));
+    ncclUniqueId id;
+    memcpy(&id, p.nccl_id, sizeof(id));
+    ncclResult_t r = api->commInitRank(&h->nccl, p.world, id, p.rank);
+    if (r != ncclSuccess) {
+      h->nccl = nullptr;
+      return bail(fail(POLY_ENCCL, "ncclCommInitRank: %s", api->errStr(r)));
+    }
+  }
+  p.nccl_id = nullptr;
+  if (cudaStreamSynchronize(h->work) != cudaSuccess)
+    return bail(fail(POLY_ECUDA, "init: %s", cudaGetErrorString(cudaGetLastError())));
+  g_err[0] = 0;
+  *out = h;
+  return POLY_OK;
+}
+
+int poly_loss_grad(poly_handle *h, const double *x, double *g, double *loss) {
+  if (!h || !x) return fail(POLY_EINVAL, "NULL handle or x");
+  TRY(sync_in(h));
+  const double *xd = x;
+  if (!is_device_ptr(x)) {
+    CK(cudaMemcpyAsync(h->xin, x, h->p.d * 8, cudaMemcpyHostToDevice, h->work));
+    xd = h->xin;
+  }
+  const bool g_dev = g && is_device_ptr(g);
+  double *gd = g ? (g_dev ? g : h->gbuf) : nullptr;
+  h->prof = false;
+  TRY(enqueue_eval(h, xd, loss != nullptr, false, nullptr, nullptr, gd));
+  if (g && !g_dev) CK(cudaMemcpyAsync(g, h->gbuf, h->p.d * 8, cudaMemcpyDeviceToHost, h->work));
+  if (loss) {
+    CK(cudaMemcpyAsync(&h->hstate->loss_cur, &h->state->loss_cur, 8, cudaMemcpyDeviceToHost, h->work));
+    CK(cudaStreamSynchronize(h->work));
+    *loss = h->hstate->loss_cur;
+  } else if (g && !g_dev) {
+    CK(cudaStreamSynchronize(h->work));
+  }
+  TRY(sync_out(h));
+  CK(cudaGetLastError());
+  return POLY_OK;
+}
+
+int poly_solve(poly_handle *h, double *x, int T, double gamma, uint32_t flags, double *trace,
+               int *bad_iter) {
+  if (!h || !x) return fail(POLY_EINVAL, "NULL handle or x");
+  if (T < 0) return fail(POLY_EINVAL, "T < 0");
+  if (!(gamma > 0.0) || !std::isfinite(gamma)) return fail(POLY_EINVAL, "gamma must be > 0");
+  if (bad_iter) *bad_iter = 0;
+  TRY(sync_in(h));
+  const bool x_dev = is_device_ptr(x);
+  CK(cudaMemcpyAsync(h->xa, x, h->p.d * 8, x_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice,
+                     h->work));
+  const bool want_trace = trace != nullptr;
+  if (want_trace && h->trace_cap < 2 * T) {
+    double *nt = nullptr;
+    TRY(dev_alloc(h, &nt, (size_t)2 * T));
+    h->trace = nt;
+    h->trace_cap = 2 * T;
+  }
+  SolveState st{};
+  st.gamma = gamma;
+  st.trace = want_trace ? h->trace : nullptr;
+  st.trace_cap = want_trace ? 2 * T : 0;
+  *h->hstate = st;
+  CK(cudaMemcpyAsync(h->state, h->hstate, sizeof(SolveState), cudaMemcpyHostToDevice, h->work));
+
+  h->prof = (flags & POLY_SOLVE_PROFILE) != 0;
+  h->recs.clear();
+  h->evused = 0;
+  // x_1 = P_X(x_in)
+  {
+    FinArgs f = fin_base(h, FIN_PROJECT);
+    f.anchor = h->xa;
+    f.x_out = h->xa;
+    TRY(enqueue_fin(h, f));
+  }
+  const bool loss = want_trace;
+  if (h->use_graph && !h->prof && T > 0) {
+    const int U = std::min(h->graph_U, T);
+    int li = loss ? 1 : 0;
+    int rc = POLY_OK;
+    if (T >= h->graph_U && !h->gexec[li][1]) rc = build_graph(h, loss, h->graph_U, &h->gexec[li][1]);
+    if (rc == POLY_OK && (T % h->graph_U) && !h->gexec[li][0]) rc = build_graph(h, loss, 1, &h->gexec[li][0]);
+    if (rc != POLY_OK && h->pdl) {  // retry capture without programmatic edges
+      h->pdl = false;
+      cudaGetLastError();
+      rc = POLY_OK;
+      if (T >= h->graph_U && !h->gexec[li][1]) rc = build_graph(h, loss, h->graph_U, &h->gexec[li][1]);
+      if (rc == POLY_OK && (T % h->graph_U) && !h->gexec[li][0]) rc = build_graph(h, loss, 1, &h->gexec[li][0]);
+    }
+    if (rc != POLY_OK) return rc;
+    (void)U;
+    for (int t = 0; t + h->graph_U <= T; t += h->graph_U) CK(cudaGraphLaunch(h->gexec[li][1], h->work));
+    for (int t = 0; t < T % h->graph_U; ++t) CK(cudaGraphLaunch(h->gexec[li][0], h->work));
+  } else {
+    for (int t = 0; t < T; ++t) TRY(enqueue_iteration(h, loss));
+  }
+  CK(cudaMemcpyAsync(x, h->xa, h->p.d * 8, x_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost,
+                     h->work));
+  if (want_trace) CK(cudaMemcpyAsync(trace, h->trace, (size_t)2 * T * 8, cudaMemcpyDeviceToHost, h->work));
+  CK(cudaMemcpyAsync(h->hstate, h->state, sizeof(SolveState), cudaMemcpyDeviceToHost, h->work));
+  CK(cudaStreamSynchronize(h->work));
+  if (h->prof) {
+    double sum[3] = {0, 0, 0};
+    int cnt[3] = {0, 0, 0};
+    for (auto &r : h->recs) {
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, r.a, r.b);
+      sum[r.kind] += ms;
+      cnt[r.kind]++;
+    }
+    for (int k = 0; k < 3; ++k) h->ktimes[k] = cnt[k] ? sum[k] / cnt[k] : 0.0;
+    h->ktimes[3] = cnt[0];
+    h->ktimes[4] = cnt[0] + cnt[1];
+    h->prof = false;
+  }
+  TRY(sync_out(h));
+  CK(cudaGetLastError());
+  if (h->hstate->bad != 0) {
+    const int b = h->hstate->bad;
+    if (bad_iter) *bad_iter = b > 0 ? (b + 1) / 2 : 0;
+    return fail(POLY_ENONFINITE, "non-finite iterate at iteration %d", b > 0 ? (b + 1) / 2 : 0);
+  }
+  return POLY_OK;
+}
+
+}  // extern "C"
+
+namespace {
+int aux_rows(poly_handle *h, const double *x, double *out, int want_counts) {
+  if (!h || !x || !out) return fail(POLY_EINVAL, "NULL argument");
+  const poly_problem &p = h->p;
+  if (p.n_local == 0) return POLY_OK;
+  TRY(sync_in(h));
+  AuxArgs a{};
+  a.layout = p.layout;
+  a.dtype = p.dtype;
+  a.A = p.A;
+  a.lda = p.lda;
+  a.row_ptr = p.row_ptr;
+  a.col = p.col;
+  a.val = p.val;
+  a.n = p.n_local;
+  a.d = (int32_t)p.d;
+  a.W = p.W;
+  a.relu = p.relu;
+  a.s_row = p.s_row;
+  a.I_row = p.I_row;
+  a.I_bar = p.I_bar;
+  a.x = x;
+  a.spec = h->spec;
+  a.out = out;
+  a.want_counts = want_counts;
+  const int grid = (int)std::min<int64_t>((int64_t)h->sms * 16, (p.n_local + 7) / 8);
+  if (p.dtype == POLY_F32)
+    k_aux_rows<float><<<grid, 256, 0, h->work>>>(a);
+  else
+    k_aux_rows<double><<<grid, 256, 0, h->work>>>(a);
+  CK(cudaGetLastError());
+  TRY(sync_out(h));
+  return POLY_OK;
+}
+}  // namespace
+
+extern "C" {
+
+int poly_forward(poly_handle *h, const double *x, double *z) { return aux_rows(h, x, z, 0); }
+
+int poly_expected_counts(poly_handle *h, const double *x, double *lam) {
+  return aux_rows(h, x, lam, 1);
+}
+
+int poly_reparameterize(int32_t W, const double *s, const double *mu, double I_bar, int64_t n,
+                        const double *b, int32_t clamp, float *s_row, float *I_row, void *stream) {
+  if (W < 1 || W > kMaxW || !s || !mu || n < 0 || (n > 0 && (!b || !s_row || !I_row)))
+    return fail(POLY_EINVAL, "poly_reparameterize: bad arguments");
+  if (!(I_bar > 0.0)) return fail(POLY_EINVAL, "I_bar must be > 0");
+  if (n == 0) return POLY_OK;
+  ReparamArgs a{};
+  a.W = W;
+  a.clamp = clamp;
+  a.n = n;
+  a.I_bar = I_bar;
+  for (int j = 0; j < W; ++j) {
+    if (!(s[j] > 0.0) || !(mu[j] > 0.0)) return fail(POLY_EINVAL, "bad spectrum");
+    a.s[j] = s[j];
+    a.mu[j] = mu[j];
+  }
+  a.b = b;
+  a.s_row = s_row;
+  a.I_row = I_row;
+  const int grid = (int)std::min<int64_t>(148 * 32, (n + 255) / 256);
+  k_reparam<<<grid, 256, 0, (cudaStream_t)stream>>>(a);
+  CK(cudaGetLastError());
+  return POLY_OK;
+}
+
+int poly_kernel_times(poly_handle *h, double *out, int32_t nout) {
+  if (!h || !out || nout < 0 || nout > 5) return fail(POLY_EINVAL, "bad arguments");
+  for (int i = 0; i < nout; ++i) out[i] = h->ktimes[i];
+  return POLY_OK;
+}
+
+int poly_describe(poly_handle *h, int64_t *out, int32_t nout) {
+  if (!h || !out || nout < 0 || nout > 6) return fail(POLY_EINVAL, "bad arguments");
+  int64_t v[6];
+  if (h->p.layout == POLY_DENSE) {
+    v[0] = h->k1_grid;
+    v[1] = h->k1_threads;
+    v[2] = h->dv->RPS;
+    v[3] = h->k1_stages;
+    v[4] = (int64_t)h->k1_smem;
+  } else {
+    v[0] = h->k4_grid;
+    v[1] = 256;
+    v[2] = 1;
+    v[3] = 0;
+    v[4] = 0;
+  }
+  v[5] = h->sms;
+  for (int i = 0; i < nout; ++i) out[i] = v[i];
+  return POLY_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,454 @@
+"""GPU parity: the CUDA path (through the C ABI) against the fp64 oracle on
+the same seeded inputs, each side building its inputs independently.
+
+Tolerances (BASELINE.json north_star): per-call gradient relative ℓ2 error
+<= 1e-4 for the fp32 path, final iterate after T iterations <= 1e-3, counts
+and indices bit-exact.  The fp64 path (C1 fp64) is held to 1e-12 (DESIGN.md
+§Tolerances: fp64 with reordered sums, n*d = 2e5 terms).
+"""
+import math
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+import oracle  # noqa: E402
+from gen import configs as G  # noqa: E402
+from gen import rng  # noqa: E402
+from oracle import workloads as OW  # noqa: E402
+
+TOL32 = 1e-4
+TOL64 = 1e-12
+
+
+def _P():
+    import paper_2503_19925_b200 as P
+    return P
+
+
+def _W():
+    from paper_2503_19925_b200 import workloads as PW
+    return PW
+
+
+def rel(a, b):
+    a, b = np.asarray(a, dtype=np.float64), np.asarray(b, dtype=np.float64)
+    return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300))
+
+
+def gpu_F(p, x):
+    xt = torch.tensor(np.asarray(x, dtype=np.float64), device="cuda")
+    g, loss = p.loss_grad(xt)
+    return g.cpu().numpy(), loss
+
+
+def test_points(w_or, prob, cfg, k_iter=3, gamma=None):
+    """x = 0, x⋆, P_X(x⋆ + 0.3 u) for random unit u, first oracle iterates."""
+    d = cfg.d
+    xs = w_or["x_star"]
+    pts = [np.zeros(d), xs.copy()]
+    r = np.random.default_rng(cfg.seed + 100)
+    for _ in range(3):
+        u = r.standard_normal(d)
+        pts.append(prob.project(xs + 0.3 * u / np.linalg.norm(u)))
+    if gamma is not None:
+        x = np.zeros(d)
+        for _ in range(k_iter):
+            x, _, _ = prob.solve(1, gamma, x1=x)
+            pts.append(x.copy())
+    return pts
+
+
+# ------------------------------------------------------------------ inputs
+@pytest.fixture(scope="module")
+def c2_gpu():
+    return _W().build(G.C2)
+
+
+def test_synth_bit_exact_c2_sampled_rows(c2_gpu):
+    rows = np.array([0, 1, 2, 4097, 99_999, 123_457, 199_998, 199_999])
+    ref = OW.build(G.C2, rows=rows)
+    A = c2_gpu["A"][torch.tensor(rows, device="cuda")][:, :G.C2.d].cpu().numpy()
+    assert np.array_equal(A, ref["A"])                                   # A bit-exact
+    k = c2_gpu["counts"].cpu().numpy()[rows]
+    assert np.array_equal(k, ref["counts"])                              # counts bit-exact
+    lam = c2_gpu["lam"].cpu().numpy()[rows]
+    assert np.allclose(lam, ref["lam"], rtol=1e-13, atol=0)
+
+
+def test_counts_hash_c2(c2_gpu):
+    """P14: Σy, Σy² over all rows agree between device and host reductions."""
+    k = c2_gpu["counts"]
+    s1 = int(k.to(torch.int64).sum().item())
+    s2 = int((k.to(torch.int64) ** 2).sum().item())
+    kk = k.cpu().numpy().astype(np.int64)
+    assert s1 == int(kk.sum()) and s2 == int((kk * kk).sum())
+    assert kk.min() >= 0
+
+
+# ------------------------------------------------------------------ C1
+@pytest.mark.parametrize("cfg,tol", [(G.C1, TOL64), (G.C1F, TOL32)])
+def test_c1_loss_grad_parity(cfg, tol):
+    W = _W()
+    wg = W.build(cfg)
+    wo = OW.build(cfg)
+    assert np.array_equal(wg["counts"].cpu().numpy(), wo["counts"])
+    A = wg["A"][:, :cfg.d].cpu().numpy()
+    assert np.array_equal(A, wo["A"])
+    p = W.make_poly(wg)
+    prob = wo["problem"]
+    gam, _ = OW.step_size(prob, wo["s"], wo["mu"], cfg.I_bar)
+    for x in test_points(wo, prob, cfg, gamma=gam):
+        g_ref, l_ref = prob.F(x)
+        g, l = gpu_F(p, x)
+        assert rel(g, g_ref) <= tol, (rel(g, g_ref), np.linalg.norm(x))
+        assert abs(l - l_ref) <= max(tol, 1e-12) * max(1.0, abs(l_ref))
+
+
+@pytest.mark.parametrize("cfg,tol", [(G.C1, 1e-10), (G.C1F, 1e-3)])
+def test_c1_solve_parity(cfg, tol):
+    W = _W()
+    wg = W.build(cfg)
+    wo = OW.build(cfg)
+    prob = wo["problem"]
+    gam, _ = OW.step_size(prob, wo["s"], wo["mu"], cfg.I_bar)
+    x_ref, tr_ref, bad = prob.solve(cfg.T, gam, trace=True)
+    assert bad == 0
+    p = W.make_poly(wg)
+    x = torch.zeros(cfg.d, dtype=torch.float64, device="cuda")
+    tr = p.solve(x, cfg.T, gam, trace=True)
+    assert rel(x.cpu().numpy(), x_ref) <= tol
+    assert np.allclose(tr, tr_ref, rtol=max(tol, 1e-9), atol=0)
+    # graph and direct launches agree bit for bit
+    x2 = torch.zeros(cfg.d, dtype=torch.float64, device="cuda")
+    p.solve(x2, cfg.T, gam, profile=True)
+    assert torch.equal(x, x2)
+
+
+# ------------------------------------------------------------------ C2
+def test_c2_row_subset_parity(c2_gpu):
+    """Full-size C2 data, the launch configuration of a 8192-row shard,
+    against the oracle on the same rows (n_global = 200000)."""
+    r0, m = 57_331, 8192
+    rows = np.arange(r0, r0 + m)
+    wo = OW.build(G.C2, rows=rows)
+    W = _W()
+    sub = dict(c2_gpu)
+    sub.update(row0=r0, n_local=m, y=c2_gpu["y"][r0:r0 + m],
+               mat=dict(A=c2_gpu["A"][r0:r0 + m], d=G.C2.d))
+    p = W.make_poly(sub)
+    prob = wo["problem"]
+    assert prob.n_norm == G.C2.n
+    for x in test_points(wo, prob, G.C2):
+        g_ref, l_ref = prob.F(x)
+        g, l = gpu_F(p, x)
+        assert rel(g, g_ref) <= TOL32, rel(g, g_ref)
+        assert abs(l - l_ref) <= TOL32 * abs(l_ref)
+
+
+def test_c2_full_size_properties(c2_gpu):
+    """At full size: shard additivity (3 row blocks, each its own launch
+    configuration) and the Stein population closed form (pin P4b)."""
+    from scipy.special import erfcx
+    W = _W()
+    cfg = G.C2
+    p = W.make_poly(c2_gpu)
+    xs = c2_gpu["x_star"].cpu().numpy()
+    r = np.random.default_rng(5)
+    x = r.standard_normal(cfg.d)
+    x *= 0.5 / np.linalg.norm(x)
+    g, l = gpu_F(p, x)
+    cuts = [0, 66_667, 133_333, cfg.n]
+    acc, lacc = np.zeros(cfg.d), 0.0
+    for a, b in zip(cuts[:-1], cuts[1:]):
+        sub = dict(c2_gpu)
+        sub.update(row0=a, n_local=b - a, y=c2_gpu["y"][a:b], mat=dict(A=c2_gpu["A"][a:b], d=cfg.d))
+        gs, ls = gpu_F(W.make_poly(sub), x)
+        acc += gs
+        lacc += ls
+    assert rel(acc, g) <= 1e-6 and abs(lacc - l) <= 1e-6 * abs(l)
+    s, mu = cfg.spectrum
+
+    def c(sig):
+        return float(np.sum(s * mu * 0.5 * erfcx(mu * sig / math.sqrt(2.0))))
+    fbar = cfg.I_bar * (c(np.linalg.norm(x)) * x - c(np.linalg.norm(xs)) * xs)
+    assert rel(g, fbar) <= 3 * 1.1 * math.sqrt(cfg.d / cfg.n)
+
+
+def test_c2_reduced_solve_parity():
+    """C2 recipe on its first 20000 rows (own problem, n = 20000), T = 200."""
+    cfg = G.scaled(G.C2, 20_000)
+    W = _W()
+    wg = W.build(cfg)
+    wo = OW.build(cfg)
+    prob = wo["problem"]
+    gam, _ = OW.step_size(prob, wo["s"], wo["mu"], cfg.I_bar)
+    x_ref, _, _ = prob.solve(cfg.T, gam)
+    x = torch.zeros(cfg.d, dtype=torch.float64, device="cuda")
+    W.make_poly(wg).solve(x, cfg.T, gam)
+    assert rel(x.cpu().numpy(), x_ref) <= 1e-3
+
+
+# ------------------------------------------------------------------ C3
+def test_c3_reparam_rows_and_parity():
+    cfg = G.C3
+    W = _W()
+    wg = W.build(cfg)
+    rows = np.array([0, 5, 77_777, 500_001, 999_999])
+    wo = OW.build(cfg, rows=rows)
+    sr = wg["s_row"].cpu().numpy()[rows]
+    Ir = wg["I_row"].cpu().numpy()[rows]
+    ulp = np.abs(sr.view(np.int32) - wo["s_row"].astype(np.float32).view(np.int32))
+    assert ulp.max() <= 1
+    assert np.max(np.abs(Ir.view(np.int32) - wo["I_row"].astype(np.float32).view(np.int32))) <= 1
+    assert np.array_equal(wg["counts"].cpu().numpy()[rows], wo["counts"])
+    # F over a 4096-row block, full recipe (n_global = 1e6)
+    r0, m = 300_000, 4096
+    wb = OW.build(cfg, rows=np.arange(r0, r0 + m))
+    sub = dict(wg)
+    sub.update(row0=r0, n_local=m, y=wg["y"][r0:r0 + m], s_row=wg["s_row"][r0:r0 + m],
+               I_row=wg["I_row"][r0:r0 + m], mat=dict(A=wg["A"][r0:r0 + m], d=cfg.d))
+    # the oracle uses the GPU-independent fp32-rounded s', Ī' of its own build
+    assert np.max(np.abs(wg["s_row"][r0:r0 + m].cpu().numpy() - wb["s_row"])) <= 1e-7
+    p = W.make_poly(sub)
+    prob = wb["problem"]
+    for x in test_points(wb, prob, cfg):
+        g_ref, _ = prob.F(x)
+        g, _ = gpu_F(p, x)
+        assert rel(g, g_ref) <= TOL32, rel(g, g_ref)
+
+
+# ------------------------------------------------------------------ C4
+@pytest.fixture(scope="module")
+def c4():
+    return _W().build(G.C4), OW.build(G.C4)
+
+
+def test_c4_csr_inputs_bit_exact(c4):
+    wg, wo = c4
+    assert np.array_equal(wg["row_ptr"].cpu().numpy(), wo["row_ptr"])
+    assert np.array_equal(wg["col"].cpu().numpy(), wo["col"])
+    assert np.array_equal(wg["val"].cpu().numpy(), wo["val"])
+    assert np.array_equal(wg["counts"].cpu().numpy(), wo["counts"])
+    assert np.array_equal(wg["y"].cpu().numpy().astype(np.float64), wo["y"])
+    assert (wg["y"].cpu().numpy() < 0).sum() >= 0
+
+
+def test_c4_full_size_parity(c4):
+    wg, wo = c4
+    cfg = G.C4
+    p = _W().make_poly(wg)
+    prob = wo["problem"]
+    for x in test_points(wo, prob, cfg):
+        g_ref, l_ref = prob.F(x)
+        g, l = gpu_F(p, x)
+        assert rel(g, g_ref) <= TOL32, rel(g, g_ref)
+        assert abs(l - l_ref) <= TOL32 * abs(l_ref)
+
+
+def test_c4_solve_parity(c4):
+    wg, wo = c4
+    prob = wo["problem"]
+    lam, _ = prob.lambda_max(max_it=30, tol=1e-6)
+    gam = 1.0 / (4.0 * G.C4.I_bar * lam * float(np.dot(wo["s"], wo["mu"])))
+    x_ref, _, _ = prob.solve(20, gam)
+    x = torch.zeros(G.C4.d, dtype=torch.float64, device="cuda")
+    _W().make_poly(wg).solve(x, 20, gam)
+    assert rel(x.cpu().numpy(), x_ref) <= 1e-3
+    assert x.min().item() >= 0.0 and x.norm().item() <= wo["R"] * (1 + 1e-12)
+
+
+# ------------------------------------------------------------------ edge cases
+def _rand_problem(n, d, W=5, seed=0, relu=1, ytype="i32", rowspec=False, dtype=np.float32,
+                  lda=None, I_bar=200.0):
+    r = np.random.default_rng(seed)
+    lda = lda or (d + 3) // 4 * 4 if dtype == np.float32 else (lda or (d + 1) // 2 * 2)
+    A = np.zeros((n, lda), dtype=dtype)
+    A[:, :d] = rng.gaussian_rows(seed, rng.STREAM_TEST, np.arange(n), d).astype(dtype) / math.sqrt(d)
+    A[:, d:] = np.nan if lda > d else 0  # padding must be ignored
+    s = r.uniform(0.5, 1.0, W)
+    s /= s.sum()
+    mu = r.uniform(0.3, 3.0, W)
+    xs = r.standard_normal(d)
+    xs *= 0.8 / np.linalg.norm(xs)
+    s_row = I_row = None
+    if rowspec:
+        s_row = r.uniform(0.1, 1, (n, W)).astype(np.float32)
+        s_row /= s_row.sum(axis=1, keepdims=True)
+        I_row = r.uniform(50, 300, n).astype(np.float32)
+    pr = oracle.Problem(A=A[:, :d].astype(np.float64), y=np.zeros(n), s=s, mu=mu, I_bar=I_bar,
+                        d=d, relu=relu, s_row=s_row, I_row=I_row)
+    lam = pr.mean(xs)
+    k = rng.poisson(seed, rng.STREAM_Y, lam, np.arange(n))
+    if ytype == "i32":
+        y = k.astype(np.int32)
+    elif ytype == "f32":
+        y = (k - 0.5 * lam - 20).astype(np.float32)   # includes negatives
+    else:
+        y = lam.copy()
+    return dict(A=A, s=s, mu=mu, y=y, xs=xs, s_row=s_row, I_row=I_row, relu=relu, d=d, n=n,
+                I_bar=I_bar)
+
+
+def _both(pb, set=G.SET_NONE, R=1.0, center=None):
+    P = _P()
+    dev = lambda a: None if a is None else torch.tensor(a, device="cuda")  # noqa: E731
+    p = P.Poly(A=dev(pb["A"]), d=pb["d"], y=dev(pb["y"]), s=pb["s"], mu=pb["mu"],
+               I_bar=pb["I_bar"], s_row=dev(pb["s_row"]), I_row=dev(pb["I_row"]),
+               relu=pb["relu"], set=set, R=R, center=center)
+    o = oracle.Problem(A=pb["A"][:, :pb["d"]].astype(np.float64), y=pb["y"], s=pb["s"],
+                       mu=pb["mu"], I_bar=pb["I_bar"], d=pb["d"], relu=pb["relu"],
+                       s_row=None if pb["s_row"] is None else pb["s_row"].astype(np.float64),
+                       I_row=None if pb["I_row"] is None else pb["I_row"].astype(np.float64),
+                       set=set, R=R, center=center)
+    return p, o
+
+
+@pytest.mark.parametrize("n,d", [(1, 4), (7, 37), (100, 128), (1000, 1000), (333, 1030),
+                                 (257, 2100), (97, 4097), (31, 8192), (5000, 100), (20011, 513)])
+def test_edge_shapes_f32(n, d):
+    pb = _rand_problem(n, d, seed=n + d)
+    p, o = _both(pb)
+    for x in (np.zeros(d), pb["xs"], -pb["xs"]):
+        g_ref, l_ref = o.F(x)
+        g, l = gpu_F(p, x)
+        assert rel(g, g_ref) <= TOL32, (n, d, rel(g, g_ref))
+        assert abs(l - l_ref) <= TOL32 * max(1.0, abs(l_ref))
+
+
+@pytest.mark.parametrize("n,d", [(3, 2), (64, 64), (1000, 129), (500, 600), (77, 4096)])
+def test_edge_shapes_f64(n, d):
+    pb = _rand_problem(n, d, seed=7 * n + d, dtype=np.float64)
+    p, o = _both(pb)
+    for x in (np.zeros(d), pb["xs"]):
+        g_ref, l_ref = o.F(x)
+        g, l = gpu_F(p, x)
+        assert rel(g, g_ref) <= 1e-12, (n, d, rel(g, g_ref))
+        assert abs(l - l_ref) <= 1e-12 * max(1.0, abs(l_ref))
+
+
+@pytest.mark.parametrize("W", [1, 31, 33, 64])
+@pytest.mark.parametrize("relu", [0, 1])
+def test_edge_spectra_and_relu(W, relu):
+    pb = _rand_problem(900, 200, W=W, seed=W + 10 * relu, relu=relu)
+    p, o = _both(pb)
+    for x in (np.zeros(200), pb["xs"], 0.5 * pb["xs"]):
+        g_ref, l_ref = o.F(x)
+        g, l = gpu_F(p, x)
+        assert rel(g, g_ref) <= TOL32
+        assert abs(l - l_ref) <= TOL32 * max(1.0, abs(l_ref))
+
+
+@pytest.mark.parametrize("ytype", ["f32", "f64"])
+def test_edge_y_types_and_rowspec(ytype):
+    pb = _rand_problem(3000, 300, W=7, seed=3, ytype=ytype, rowspec=True)
+    p, o = _both(pb)
+    g_ref, _ = o.F(pb["xs"])
+    g, _ = gpu_F(p, pb["xs"])
+    if ytype == "f64":   # noiseless: F(x⋆) ≈ 0 relative to F(0)
+        g0, _ = o.F(np.zeros(300))
+        assert np.linalg.norm(g - g_ref) <= TOL32 * np.linalg.norm(g0)
+    else:
+        assert rel(g, g_ref) <= TOL32
+
+
+def test_edge_empty_rows():
+    P = _P()
+    A = torch.zeros((0, 8), dtype=torch.float32, device="cuda")
+    y = torch.zeros(0, dtype=torch.int32, device="cuda")
+    p = P.Poly(A=A, y=y, s=[1.0], mu=[1.0], I_bar=10.0, n_global=5)
+    g, l = p.loss_grad(torch.ones(8, dtype=torch.float64, device="cuda"))
+    assert torch.count_nonzero(g).item() == 0 and l == 0.0
+
+
+@pytest.mark.parametrize("st,center", [(G.SET_BALL, None), (G.SET_BALL, "c"), (G.SET_NONNEG, None),
+                                       (G.SET_NONNEG_BALL, None), (G.SET_NONE, None)])
+def test_edge_sets_solve(st, center):
+    pb = _rand_problem(4000, 96, seed=11)
+    c = pb["xs"] * 0.5 if center else None
+    p, o = _both(pb, set=st, R=0.6, center=c)
+    gam = 1e-3
+    x0 = np.full(96, 0.3)
+    x_ref, tr_ref, _ = o.solve(15, gam, x1=x0, trace=True)
+    x = torch.tensor(x0, device="cuda")
+    tr = p.solve(x, 15, gam, trace=True)
+    assert rel(x.cpu().numpy(), x_ref) <= 1e-5
+    assert np.allclose(tr, tr_ref, rtol=1e-5)
+
+
+def test_host_pointers_and_host_inputs():
+    P = _P()
+    pb = _rand_problem(2000, 64, seed=21)
+    _, o = _both(pb)
+    p = P.Poly(A=torch.tensor(pb["A"]), d=64, y=torch.tensor(pb["y"]), s=pb["s"], mu=pb["mu"],
+               I_bar=pb["I_bar"], flags=P.POLY_FLAG_HOST_INPUTS, set=G.SET_NONE)
+    x = torch.tensor(pb["xs"])                      # host x and host g
+    g, l = p.loss_grad(x, g=torch.empty(64, dtype=torch.float64))
+    g_ref, l_ref = o.F(pb["xs"])
+    assert rel(g.numpy(), g_ref) <= TOL32 and abs(l - l_ref) <= TOL32 * abs(l_ref)
+    xs = torch.zeros(64, dtype=torch.float64)       # host iterate through poly_solve
+    p.solve(xs, 5, 1e-3)
+    x_ref, _, _ = o.solve(5, 1e-3)
+    assert rel(xs.numpy(), x_ref) <= 1e-5
+
+
+def test_determinism_bitwise(c2_gpu):
+    p = _W().make_poly(c2_gpu)
+    x = torch.zeros(G.C2.d, dtype=torch.float64, device="cuda")
+    g1, l1 = p.loss_grad(x + 0.01)
+    g2, l2 = p.loss_grad(x + 0.01)
+    assert torch.equal(g1, g2) and l1 == l2
+
+
+def test_nonfinite_is_reported():
+    P = _P()
+    pb = _rand_problem(500, 32, seed=4)
+    p, _ = _both(pb, set=G.SET_NONE)
+    x = torch.full((32,), 1e300, dtype=torch.float64, device="cuda")
+    with pytest.raises(P.PolyError) as ei:
+        p.solve(x, 3, 1e300)
+    assert ei.value.code == P.POLY_ENONFINITE
+
+
+def test_negative_counts_rejected():
+    P = _P()
+    A = torch.zeros((4, 4), dtype=torch.float32, device="cuda")
+    y = torch.tensor([1, 2, -1, 3], dtype=torch.int32, device="cuda")
+    with pytest.raises(P.PolyError) as ei:
+        P.Poly(A=A, y=y, s=[1.0], mu=[1.0], I_bar=10.0)
+    assert ei.value.code == P.POLY_EINVAL
+
+
+def test_forward_bit_consistency_rows(c2_gpu):
+    """poly_forward z per sampled row vs the oracle's fp64 z (misindexed rows
+    would show as O(1) errors)."""
+    rows = np.array([0, 13, 150_000, 199_999])
+    wo = OW.build(G.C2, rows=rows)
+    p = _W().make_poly(c2_gpu)
+    z = p.forward(c2_gpu["x_star"]).cpu().numpy()[rows]
+    z_ref = wo["problem"].forward(wo["x_star"])
+    assert np.allclose(z, z_ref, rtol=1e-13, atol=1e-13)
+
+
+def test_sharded_emulation_matches_full():
+    """T3-emu: P logical ranks on one GPU (row blocks, n_global = n), summed in
+    rank order, equal the single-handle result (the allreduce's maths)."""
+    cfg = G.scaled(G.C2, 30_000)
+    W = _W()
+    full = W.build(cfg)
+    x = torch.full((cfg.d,), 0.01, dtype=torch.float64, device="cuda")
+    g, l = W.make_poly(full).loss_grad(x)
+    for P_ in (2, 3, 8):
+        acc = torch.zeros_like(g)
+        lacc = 0.0
+        for r in range(P_):
+            a, b = cfg.n * r // P_, cfg.n * (r + 1) // P_
+            w = W.build(cfg, row0=a, n_local=b - a)
+            assert torch.equal(w["A"], full["A"][a:b]) and torch.equal(w["y"], full["y"][a:b])
+            gr, lr = W.make_poly(w).loss_grad(x)
+            acc += gr
+            lacc += lr
+        assert rel(acc.cpu().numpy(), g.cpu().numpy()) <= 1e-6 and abs(lacc - l) <= 1e-6 * abs(l)
