@@ -117,13 +117,15 @@ __device__ __forceinline__ void load_chunk(const T *rowp, int c0, int d, T *ch) 
 
 // T: element type of A (float/double); V: 16-byte chunks per lane per slab;
 // WPR: warps per row; NW: consumer warps; RPS: rows per stage.
-template <typename T, int V, int WPR, int NW, int RPS, bool LOSS>
+// FULL: d == 32*VEC*V*WPR exactly, so no column masking is needed.
+template <typename T, int V, int WPR, int NW, int RPS, bool LOSS, bool FULL>
 __global__ void __launch_bounds__(32 * (NW + 1), 1) k_dense_loss_grad(const DenseArgs a) {
   constexpr int VEC = Vec16<T>::N;
   constexpr int SLAB = 32 * VEC * V;  // columns per warp slab
   constexpr int G = NW / WPR;         // row groups
   constexpr int RG = RPS / G;         // rows per group per stage
   static_assert(NW % WPR == 0 && RPS % G == 0, "bad tile");
+  using VT = typename Vec16<T>::type;
 
   extern __shared__ __align__(128) unsigned char smem[];
   const int S = a.stages;
@@ -159,10 +161,10 @@ __global__ void __launch_bounds__(32 * (NW + 1), 1) k_dense_loss_grad(const Dens
     // (programmatic dependent launch) has finished.
     const uint64_t pol = l2_evict_first_policy();
     const int ysz = a.ytype == 2 ? 8 : 4;
+    int slot = 0;
+    uint32_t eph = 1;  // toggled to 0 when the ring first wraps: wait for phase 0
     for (int st = 0; st < nstage; ++st) {
-      const int slot = st % S;
-      const uint32_t use = (uint32_t)(st / S);
-      if (use > 0) mbar_wait(&empty[slot], (use - 1) & 1u);
+      if (st >= S) mbar_wait(&empty[slot], eph);
       const int64_t r0 = rb + (int64_t)st * RPS;
       const int rows = (int)min((int64_t)RPS, re - r0);
       if (lane == 0) {
@@ -185,6 +187,10 @@ __global__ void __launch_bounds__(32 * (NW + 1), 1) k_dense_loss_grad(const Dens
         for (int e = lane; e < rows * a.W; e += 32) cp_async4(sd + soff + 4 * e, sg + e);
       }
       cp_async_mbar_arrive(&full[slot]);
+      if (++slot == S) {
+        slot = 0;
+        eph ^= 1u;
+      }
     }
     asm volatile("cp.async.wait_all;" ::: "memory");
     return;
@@ -209,9 +215,11 @@ __global__ void __launch_bounds__(32 * (NW + 1), 1) k_dense_loss_grad(const Dens
   const bool has_rowspec = a.I_row != nullptr;
   int buf = 0;
 
+  const int lane_off = w * SLAB + lane * VEC;  // + v * 32 * VEC
+  int slot = 0;
+  uint32_t fph = 0;
   for (int st = 0; st < nstage; ++st) {
-    const int slot = st % S;
-    mbar_wait(&full[slot], (uint32_t)(st / S) & 1u);
+    mbar_wait(&full[slot], fph);
     const int64_t r0 = rb + (int64_t)st * RPS;
     const int rows = (int)min((int64_t)RPS, re - r0);
     const T *tile = ring + (size_t)slot * stage_elems;
@@ -222,26 +230,40 @@ __global__ void __launch_bounds__(32 * (NW + 1), 1) k_dense_loss_grad(const Dens
     constexpr bool KEEP = V * VEC * RG <= 16;
     T av[KEEP ? RG : 1][V][VEC];
     double zp[RG];
-    // a1: partial dot of this warp's slab for each of its rows
+    (void)av;
+    // a1: partial dot of this warp's slab for each of its rows: fp32 FMA over
+    // pairs of 16-byte chunks, fp64 tree over the pairs, fp64 warp sum.
 #pragma unroll
     for (int q = 0; q < RG; ++q) {
       const int lr = grp + G * q;
       double p = 0.0;
       if (lr < rows) {
-        const T *rowp = tile + (size_t)lr * lda;
+        const T *rowp = tile + (size_t)lr * lda + lane_off;
+        T pp[(V + 1) / 2];
 #pragma unroll
         for (int v = 0; v < V; ++v) {
           T ch[VEC];
-          load_chunk<T>(rowp, w * SLAB + v * 32 * VEC + lane * VEC, a.d, ch);
-          T pv = ch[0] * xr[v][0];
+          if (FULL)
+            unpack<T>(*reinterpret_cast<const VT *>(rowp + v * 32 * VEC), ch);
+          else
+            load_chunk<T>(rowp - lane_off, lane_off + v * 32 * VEC, a.d, ch);
+          T pv = (v & 1) ? pp[v >> 1] : (T)0;
 #pragma unroll
-          for (int e = 1; e < VEC; ++e) pv = fma(ch[e], xr[v][e], pv);
-          p += (double)pv;
+          for (int e = 0; e < VEC; ++e) pv = fma(ch[e], xr[v][e], pv);
+          pp[v >> 1] = pv;
           if (KEEP) {
 #pragma unroll
             for (int e = 0; e < VEC; ++e) av[KEEP ? q : 0][v][e] = ch[e];
           }
         }
+        double t[(V + 1) / 2];
+#pragma unroll
+        for (int k = 0; k < (V + 1) / 2; ++k) t[k] = (double)pp[k];
+#pragma unroll
+        for (int w2 = 1; w2 < (V + 1) / 2; w2 <<= 1)
+#pragma unroll
+          for (int k = 0; k + w2 < (V + 1) / 2; k += 2 * w2) t[k] += t[k + w2];
+        p = t[0];
       }
       zp[q] = warp_sum(p);
     }
@@ -271,15 +293,17 @@ __global__ void __launch_bounds__(32 * (NW + 1), 1) k_dense_loss_grad(const Dens
         const float *srow = has_rowspec ? (const float *)(sd + soff) + lr * a.W : nullptr;
         const double r = row_residual<LOSS>(sp, a.W, a.relu, zp[q], yv, Ii, srow, w == 0, &lacc);
         const T rt = (T)r;
-        const T *rowp = tile + (size_t)lr * lda;
+        const T *rowp = tile + (size_t)lr * lda + lane_off;
 #pragma unroll
         for (int v = 0; v < V; ++v) {
           T ch[VEC];
           if (KEEP) {
 #pragma unroll
             for (int e = 0; e < VEC; ++e) ch[e] = av[KEEP ? q : 0][v][e];
+          } else if (FULL) {
+            unpack<T>(*reinterpret_cast<const VT *>(rowp + v * 32 * VEC), ch);
           } else {
-            load_chunk<T>(rowp, w * SLAB + v * 32 * VEC + lane * VEC, a.d, ch);
+            load_chunk<T>(rowp - lane_off, lane_off + v * 32 * VEC, a.d, ch);
           }
 #pragma unroll
           for (int e = 0; e < VEC; ++e) gacc[v][e] = fma(rt, ch[e], gacc[v][e]);
@@ -288,6 +312,10 @@ __global__ void __launch_bounds__(32 * (NW + 1), 1) k_dense_loss_grad(const Dens
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[slot]);
+    if (++slot == S) {
+      slot = 0;
+      fph ^= 1u;
+    }
   }
 
   // ------------------------------------------- per-CTA partial (fixed order)

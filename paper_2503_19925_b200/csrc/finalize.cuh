@@ -74,7 +74,20 @@ __global__ void __launch_bounds__(256) k_finalize(const FinArgs a) {
       if (from_comm) {
         if (sl == 0) acc = a.comm[c];
       } else {
-        for (int i = sl; i < a.G; i += 8) acc += a.partials[(size_t)i * a.d + c];
+        // four independent accumulators (loads in flight together), combined
+        // in a fixed order: deterministic for a fixed G
+        double q0 = 0.0, q1 = 0.0, q2 = 0.0, q3 = 0.0;
+        const double *col = a.partials + c;
+        const size_t st = (size_t)8 * a.d;
+        int i = sl;
+        for (; i + 24 < a.G; i += 32) {
+          q0 += col[(size_t)i * a.d];
+          q1 += col[(size_t)i * a.d + st];
+          q2 += col[(size_t)i * a.d + 2 * st];
+          q3 += col[(size_t)i * a.d + 3 * st];
+        }
+        for (; i < a.G; i += 8) q0 += col[(size_t)i * a.d];
+        acc = (q0 + q1) + (q2 + q3);
         if (a.zero_partials && sl == 0) const_cast<double *>(a.partials)[c] = 0.0;
       }
     }

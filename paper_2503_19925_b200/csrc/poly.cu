@@ -93,15 +93,17 @@ NcclApi *nccl_api() {
 // ------------------------------------------------------- kernel variants
 struct DenseVariant {
   int V, WPR, NW, RPS;
-  const void *fn[2];  // [LOSS]
+  const void *fn[2][2];  // [FULL][LOSS]
 };
 
-#define DV(T, V, WPR, NW, RPS)                                              \
-  DenseVariant {                                                            \
-    V, WPR, NW, RPS, {                                                      \
-      (const void *)&k_dense_loss_grad<T, V, WPR, NW, RPS, false>,          \
-          (const void *)&k_dense_loss_grad<T, V, WPR, NW, RPS, true>        \
-    }                                                                       \
+#define DV(T, V, WPR, NW, RPS)                                                          \
+  DenseVariant {                                                                        \
+    V, WPR, NW, RPS, {                                                                  \
+      {(const void *)&k_dense_loss_grad<T, V, WPR, NW, RPS, false, false>,              \
+       (const void *)&k_dense_loss_grad<T, V, WPR, NW, RPS, true, false>},              \
+          {(const void *)&k_dense_loss_grad<T, V, WPR, NW, RPS, false, true>,           \
+           (const void *)&k_dense_loss_grad<T, V, WPR, NW, RPS, true, true>}            \
+    }                                                                                   \
   }
 
 // columns per slab: 32 lanes x (16 B / elsize) x V
@@ -170,6 +172,7 @@ struct poly_handle {
   double *spec = nullptr, *center = nullptr;
   // K1
   const DenseVariant *dv = nullptr;
+  int full = 0;
   int k1_grid = 0, k1_threads = 0, k1_stages = 0, k1_side = 0;
   size_t k1_smem = 0;
   int k4_grid = 0;
@@ -265,7 +268,7 @@ int enqueue_pass(poly_handle *h, const double *x, bool loss) {
     a.loss_partials = h->loss_partials;
     a.stages = h->k1_stages;
     a.side_stride = h->k1_side;
-    return launch(h, h->dv->fn[loss ? 1 : 0], dim3(h->k1_grid), dim3(h->k1_threads), h->k1_smem,
+    return launch(h, h->dv->fn[h->full][loss ? 1 : 0], dim3(h->k1_grid), dim3(h->k1_threads), h->k1_smem,
                   true, a);
   }
   CsrArgs a{};
@@ -461,6 +464,7 @@ int setup_dense(poly_handle *h) {
   if (!dv) return fail(POLY_EUNSUPPORTED, "dense d = %lld exceeds the largest tile (%d columns)",
                        (long long)p.d, 32 * vec * 8 * 8);
   h->dv = dv;
+  h->full = (p.d == (int64_t)32 * vec * dv->V * dv->WPR) ? 1 : 0;
   h->k1_threads = 32 * (dv->NW + 1);
   const int G = dv->NW / dv->WPR;
   const int RG = dv->RPS / G;
@@ -483,7 +487,8 @@ int setup_dense(poly_handle *h) {
       return fail(POLY_EUNSUPPORTED, "row of %lld elements too large for the smem ring", (long long)p.lda);
   }
   for (int l = 0; l < 2; ++l)
-    CK(cudaFuncSetAttribute(dv->fn[l], cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->k1_smem));
+    CK(cudaFuncSetAttribute(dv->fn[h->full][l], cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            (int)h->k1_smem));
   const int64_t tiles = (p.n_local + dv->RPS - 1) / dv->RPS;
   h->k1_grid = (int)std::max<int64_t>(1, std::min<int64_t>(h->sms, tiles));
   h->G = h->k1_grid;

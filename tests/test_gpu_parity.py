@@ -45,7 +45,7 @@ def gpu_F(p, x):
     return g.cpu().numpy(), loss
 
 
-def test_points(w_or, prob, cfg, k_iter=3, gamma=None):
+def eval_points(w_or, prob, cfg, k_iter=3, gamma=None):
     """x = 0, x⋆, P_X(x⋆ + 0.3 u) for random unit u, first oracle iterates."""
     d = cfg.d
     xs = w_or["x_star"]
@@ -101,7 +101,7 @@ def test_c1_loss_grad_parity(cfg, tol):
     p = W.make_poly(wg)
     prob = wo["problem"]
     gam, _ = OW.step_size(prob, wo["s"], wo["mu"], cfg.I_bar)
-    for x in test_points(wo, prob, cfg, gamma=gam):
+    for x in eval_points(wo, prob, cfg, gamma=gam):
         g_ref, l_ref = prob.F(x)
         g, l = gpu_F(p, x)
         assert rel(g, g_ref) <= tol, (rel(g, g_ref), np.linalg.norm(x))
@@ -142,7 +142,7 @@ def test_c2_row_subset_parity(c2_gpu):
     p = W.make_poly(sub)
     prob = wo["problem"]
     assert prob.n_norm == G.C2.n
-    for x in test_points(wo, prob, G.C2):
+    for x in eval_points(wo, prob, G.C2):
         g_ref, l_ref = prob.F(x)
         g, l = gpu_F(p, x)
         assert rel(g, g_ref) <= TOL32, rel(g, g_ref)
@@ -215,7 +215,7 @@ def test_c3_reparam_rows_and_parity():
     assert np.max(np.abs(wg["s_row"][r0:r0 + m].cpu().numpy() - wb["s_row"])) <= 1e-7
     p = W.make_poly(sub)
     prob = wb["problem"]
-    for x in test_points(wb, prob, cfg):
+    for x in eval_points(wb, prob, cfg):
         g_ref, _ = prob.F(x)
         g, _ = gpu_F(p, x)
         assert rel(g, g_ref) <= TOL32, rel(g, g_ref)
@@ -242,7 +242,7 @@ def test_c4_full_size_parity(c4):
     cfg = G.C4
     p = _W().make_poly(wg)
     prob = wo["problem"]
-    for x in test_points(wo, prob, cfg):
+    for x in eval_points(wo, prob, cfg):
         g_ref, l_ref = prob.F(x)
         g, l = gpu_F(p, x)
         assert rel(g, g_ref) <= TOL32, rel(g, g_ref)
