@@ -128,17 +128,6 @@ def dist_setup(args):
     return rank, world, local
 
 
-def shard(cfg, rank, world):
-    """(global config, row0, n_local, scaling) for this rank."""
-    if world == 1:
-        return cfg, 0, cfg.n, "weak"
-    if cfg.name in STRONG:
-        a, b = cfg.n * rank // world, cfg.n * (rank + 1) // world
-        return cfg, a, b - a, "strong"
-    gcfg = G.scaled(cfg, cfg.n * world)
-    return gcfg, cfg.n * rank, cfg.n, "weak"
-
-
 def gamma_for(cfg):
     """Theorem 2 step 1/(4 Ī λmax(Σ) Σ s_j μ_j) (reading R5) with
     λmax from the Marchenko–Pastur edge (1 + sqrt(d/n))² for Gaussian A; the
@@ -173,14 +162,12 @@ def run_ours(args):
     import paper_2503_19925_b200 as P
     from paper_2503_19925_b200 import workloads as PW
 
+    from paper_2503_19925_b200 import dist as D
+
     cfg0 = G.CONFIGS[args.config]
-    cfg, row0, n_local, scaling = shard(cfg0, rank, world)
+    cfg, row0, n_local, scaling = D.shard(cfg0, rank, world, strong=cfg0.name in STRONG)
     w = PW.build(cfg, row0=row0, n_local=n_local)
-    nccl_id = None
-    if world > 1:
-        idb = [P.poly_nccl_unique_id() if rank == 0 else None]
-        dist.broadcast_object_list(idb, src=0)
-        nccl_id = idb[0]
+    nccl_id = D.exchange_id(P.poly_nccl_unique_id, rank, world)
     poly = PW.make_poly(w, rank=rank, world=world, nccl_id=nccl_id)
     gamma = gamma_for(cfg)
     x = torch.zeros(cfg.d, dtype=torch.float64, device="cuda")
@@ -201,17 +188,9 @@ def run_ours(args):
         e1.record(st)
         torch.cuda.synchronize()
     barrier()
-    ms = e0.elapsed_time(e1)
-    if world > 1:
-        t = torch.tensor([ms], dtype=torch.float64, device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
+    ms = D.max_over_ranks(e0.elapsed_time(e1), world)
     ab = a_bytes(w)
-    total_a = float(ab)
-    if world > 1:
-        tot = torch.tensor([total_a], dtype=torch.float64, device="cuda")
-        dist.all_reduce(tot)
-        total_a = float(tot.item())
+    total_a = D.sum_over_ranks(float(ab), world)
     gbs = 2.0 * args.steps * total_a / (ms * 1e-3) / 1e9
     iters = args.steps / (ms * 1e-3)
 
