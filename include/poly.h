@@ -77,6 +77,8 @@ extern "C" {
 #define POLY_FLAG_HOST_INPUTS 1u /* A/row_ptr/col/val/y/s_row/I_row are HOST pointers; copied at init */
 #define POLY_FLAG_NO_GRAPH 2u    /* poly_solve launches kernels directly instead of via a CUDA graph */
 #define POLY_FLAG_NO_PDL 4u      /* disable programmatic dependent launch between kernels */
+#define POLY_FLAG_COMM 8u        /* use the NCCL path (reduce -> ncclAllReduce -> step) even when
+                                    world == 1; needs nccl_id.  Exercises the collective path on one GPU */
 
 /* poly_solve flags */
 #define POLY_SOLVE_PROFILE 1u    /* time every kernel with CUDA events (implies no graph);

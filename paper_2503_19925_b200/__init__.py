@@ -18,7 +18,7 @@ POLY_DENSE, POLY_CSR = 0, 1
 POLY_F32, POLY_F64 = 0, 1
 POLY_Y_I32, POLY_Y_F32, POLY_Y_F64 = 0, 1, 2
 POLY_SET_NONE, POLY_SET_BALL, POLY_SET_NONNEG, POLY_SET_NONNEG_BALL = 0, 1, 2, 3
-POLY_FLAG_HOST_INPUTS, POLY_FLAG_NO_GRAPH, POLY_FLAG_NO_PDL = 1, 2, 4
+POLY_FLAG_HOST_INPUTS, POLY_FLAG_NO_GRAPH, POLY_FLAG_NO_PDL, POLY_FLAG_COMM = 1, 2, 4, 8
 POLY_SOLVE_PROFILE = 1
 
 EXPORTED = ["poly_init", "poly_loss_grad", "poly_solve", "poly_forward", "poly_expected_counts",

@@ -188,6 +188,7 @@ struct poly_handle {
   cudaGraphExec_t gexec[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};  // [loss][U>1]
   int graph_U = 8;
   ncclComm_t nccl = nullptr;
+  bool comm_path = false;  // world > 1 or POLY_FLAG_COMM: reduce -> allreduce -> step
   // profiling
   bool prof = false;
   std::vector<cudaEvent_t> evpool;
@@ -336,7 +337,7 @@ int enqueue_eval(poly_handle *h, const double *x, bool loss, bool step, const do
   f.anchor = anchor;
   f.x_out = x_out;
   f.g_out = g_out;
-  if (h->p.world == 1) {
+  if (!h->comm_path) {
     f.mode = step ? FIN_STEP : FIN_GRAD;
     return enqueue_fin(h, f);
   }
@@ -431,7 +432,8 @@ int validate(const poly_problem *p) {
     return fail(POLY_EINVAL, "ball radius must be > 0");
   if (p->set == POLY_SET_NONNEG_BALL && p->center) return fail(POLY_EINVAL, "NONNEG_BALL requires center = NULL");
   if (p->world < 1 || p->rank < 0 || p->rank >= p->world) return fail(POLY_EINVAL, "bad rank/world");
-  if (p->world > 1 && !p->nccl_id) return fail(POLY_EINVAL, "world > 1 needs nccl_id");
+  if ((p->world > 1 || (p->flags & POLY_FLAG_COMM)) && !p->nccl_id)
+    return fail(POLY_EINVAL, "world > 1 (or POLY_FLAG_COMM) needs nccl_id");
   if (p->n_local > 0) {
     if (!p->y) return fail(POLY_EINVAL, "y is NULL");
     if (p->layout == POLY_DENSE) {
@@ -653,7 +655,8 @@ int poly_init(const poly_problem *pin, poly_handle **out) {
     }
   }
 
-  if (p.world > 1) {
+  h->comm_path = p.world > 1 || (p.flags & POLY_FLAG_COMM);
+  if (h->comm_path) {
     NcclApi *api = nccl_api();
     if (!api) return bail(fail(POLY_ENCCL, "world > 1 but libnccl.so.2 cannot be loaded"));
     ncclUniqueId id;

@@ -452,3 +452,39 @@ def test_sharded_emulation_matches_full():
             acc += gr
             lacc += lr
         assert rel(acc.cpu().numpy(), g.cpu().numpy()) <= 1e-6 and abs(lacc - l) <= 1e-6 * abs(l)
+
+
+@pytest.mark.parametrize("kind", ["dense", "csr"])
+def test_comm_path_single_rank(kind):
+    """The NCCL path (K2 REDUCE -> ncclAllReduce of d+1 doubles -> K3 from the
+    comm buffer) on a 1-rank communicator (POLY_FLAG_COMM) gives the same bits
+    as the direct path, per call and through a graph-captured solve, and
+    matches the oracle."""
+    P = _P()
+    W = _W()
+    cfg = G.scaled(G.C2, 20_000) if kind == "dense" else G.C4
+    w = W.build(cfg)
+    wo = OW.build(cfg) if kind == "csr" else OW.build(cfg, rows=np.arange(cfg.n))
+    nid = P.poly_nccl_unique_id()
+    p0 = W.make_poly(w)
+    p1 = W.make_poly(w, flags=P.POLY_FLAG_COMM, nccl_id=nid)
+    x = torch.tensor(0.5 * wo["x_star"], device="cuda")
+    g0, l0 = p0.loss_grad(x)
+    g1, l1 = p1.loss_grad(x)
+    g_ref, l_ref = wo["problem"].F(0.5 * wo["x_star"])
+    assert rel(g1.cpu().numpy(), g_ref) <= TOL32
+    if kind == "dense":
+        assert torch.equal(g0, g1) and l0 == l1
+    else:  # fp64 atomics: same value up to accumulation order
+        assert rel(g1.cpu().numpy(), g0.cpu().numpy()) <= 1e-12
+    lam_bound = 4e-5 if kind == "csr" else 1.5   # >= λmax(Σ) (bench.gamma_for uses 2e-5 / MP edge)
+    gam = 1.0 / (4.0 * cfg.I_bar * lam_bound * float(np.dot(*cfg.spectrum)))
+    xa = torch.zeros(cfg.d, dtype=torch.float64, device="cuda")
+    xb = torch.zeros_like(xa)
+    p0.solve(xa, 10, gam)
+    p1.solve(xb, 10, gam)
+    x_ref, _, _ = wo["problem"].solve(10, gam)
+    assert rel(xb.cpu().numpy(), x_ref) <= 1e-3
+    assert rel(xb.cpu().numpy(), xa.cpu().numpy()) <= (0 if kind == "dense" else 1e-10)
+    p0.close()
+    p1.close()
