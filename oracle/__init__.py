@@ -66,6 +66,14 @@ def lib():
         _lib.oracle_lambda_max.argtypes = [P, C.c_int, C.c_double, C.POINTER(C.c_int)]
         _lib.oracle_reparam.argtypes = [C.c_int, dp, dp, C.c_double, C.c_int64, dp, C.c_int,
                                         dp, dp]
+        _lib.oracle_F_windows.argtypes = [P, C.c_int, dp, dp, dp, dp, dp, dp]
+        _lib.oracle_average.argtypes = [dp, C.c_int, C.c_int64, dp]
+        _lib.oracle_solve_avg.restype = C.c_int
+        _lib.oracle_solve_avg.argtypes = [P, C.c_int, C.c_double, C.c_double, dp, dp,
+                                          C.POINTER(C.c_int), dp]
+        _lib.oracle_objective.argtypes = [P, C.c_int, dp, dp, dp]
+        _lib.oracle_solve_gd.restype = C.c_int
+        _lib.oracle_solve_gd.argtypes = [P, C.c_int, C.c_int, C.c_double, dp]
         _lib.oracle_set_threads.argtypes = [C.c_int]
         _lib.oracle_max_threads.restype = C.c_int
     return _lib
@@ -173,6 +181,42 @@ class Problem:
         bad = lib().oracle_solve(self.ptr, int(T), float(gamma), _dp(x), _dp(tr))
         return x, tr, int(bad)
 
+    def F_windows(self, x, s_win, I_win, y_win):
+        """Stacked multi-window operator (oracle_F_windows): s_win [Ω, W],
+        I_win [Ω], y_win [Ω, n]."""
+        x = _f64(x)
+        s_win, I_win, y_win = _f64(s_win), _f64(I_win), _f64(y_win)
+        Om = I_win.shape[0]
+        assert s_win.shape == (Om, self.W) and y_win.shape == (Om, self.n)
+        g = np.zeros(self.d)
+        loss = C.c_double()
+        lib().oracle_F_windows(self.ptr, Om, _dp(s_win), _dp(I_win), _dp(y_win), _dp(x), _dp(g),
+                               C.byref(loss))
+        return g, loss.value
+
+    def solve_avg(self, T_max, gamma, tol=1e-5, x1=None):
+        """EXACT with the averaged-iterate stop: (x̄, x_last, iters, move, bad)."""
+        x = np.zeros(self.d) if x1 is None else np.array(x1, dtype=np.float64)
+        xb = np.zeros(self.d)
+        it = C.c_int()
+        mv = C.c_double()
+        bad = lib().oracle_solve_avg(self.ptr, int(T_max), float(gamma), float(tol), _dp(x),
+                                     _dp(xb), C.byref(it), C.byref(mv))
+        return xb, x, it.value, mv.value, int(bad)
+
+    def objective(self, x, mode):
+        """Baseline objective `mode` (1 L2, 2 L1, 3 NLL) and its (sub)gradient."""
+        x = _f64(x)
+        g = np.zeros(self.d)
+        loss = C.c_double()
+        lib().oracle_objective(self.ptr, int(mode), _dp(x), _dp(g), C.byref(loss))
+        return g, loss.value
+
+    def solve_gd(self, mode, T, gamma, x1=None):
+        x = np.zeros(self.d) if x1 is None else np.array(x1, dtype=np.float64)
+        bad = lib().oracle_solve_gd(self.ptr, int(mode), int(T), float(gamma), _dp(x))
+        return x, int(bad)
+
     def lambda_max(self, max_it=1000, tol=1e-8):
         it = C.c_int()
         lam = lib().oracle_lambda_max(self.ptr, int(max_it), float(tol), C.byref(it))
@@ -198,6 +242,14 @@ def project(set, R, center, v):
     v = _f64(v)
     out = np.empty_like(v)
     lib().oracle_project(int(set), v.shape[0], float(R), _dp(_f64(center)), _dp(v), _dp(out))
+    return out
+
+
+def average(hist, k):
+    """Mean of iterates ⌈k/2⌉..k (1-based) of hist [>=k, d]."""
+    hist = _f64(hist)
+    out = np.zeros(hist.shape[1])
+    lib().oracle_average(_dp(hist), int(k), hist.shape[1], _dp(out))
     return out
 
 

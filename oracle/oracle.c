@@ -306,3 +306,180 @@ void oracle_reparam(int W, const double *s, const double *mu, double I_bar, int6
     I_row[i] = I_bar * tot;
   }
 }
+
+/* ------------------------------------------------------------------ NEXT-1
+ * Stacked multi-window operator.  Footnote to Eq.(eq:model-orig)
+ * ("we do include multiple (distinct but overlapping) detector windows"), the
+ * window-indexed model Eq.(model:multi-material) PAPER.md:782-784 with M = 1
+ * (Ī_ω and s_{ω,j} per window, μ_j per wavelength), and
+ * SPEC.md:310 ("n is the total stacked ray count"):
+ *   F(x) = (1/n_tot) Σ_ω Σ_i [y_{ω,i} - Ī_ω h_ω(<a_i,x>)] a_i,
+ *   h_ω(t) = Σ_j s_{ω,j} exp(-μ_j t_+),   n_tot = Ω · n_norm,
+ *   ℓ(x) = (1/n_tot) Σ_ω Σ_i [y_{ω,i} z_i - Ī_ω H_ω(z_i)]   (reading R2 per window).
+ * s_win: [Ω*W] (window-major), I_win: [Ω], y_win: [Ω*n] (window-major).
+ * p->s, p->I_bar, p->y, p->s_row, p->I_row are not used.  Written as the
+ * double sum of the definition: windows outer, rows inner. */
+void oracle_F_windows(const oracle_problem *p, int Omega, const double *s_win,
+                      const double *I_win, const double *y_win, const double *x, double *g,
+                      double *loss) {
+  const int64_t n = p->n, d = p->d;
+  double *acc = (double *)calloc((size_t)d, sizeof(double));
+  double l = 0.0;
+  for (int w = 0; w < Omega; ++w) {
+    const double *sw = s_win + (size_t)w * p->W;
+    for (int64_t i = 0; i < n; ++i) {
+      const double z = row_dot(p, i, x);
+      const double yv = y_win[(size_t)w * n + i];
+      const double r = yv - I_win[w] * oracle_h(p->W, sw, p->mu, z, p->relu);
+      l += yv * z - I_win[w] * oracle_H(p->W, sw, p->mu, z, p->relu);
+      if (!p->csr) {
+        for (int64_t k = 0; k < d; ++k) acc[k] += r * a_at(p, i, k);
+      } else {
+        for (int64_t e = p->row_ptr[i]; e < p->row_ptr[i + 1]; ++e) acc[p->col[e]] += r * v_at(p, e);
+      }
+    }
+  }
+  const double ntot = (double)Omega * (double)p->n_norm;
+  if (g)
+    for (int64_t k = 0; k < d; ++k) g[k] = acc[k] / ntot;
+  if (loss) *loss = l / ntot;
+  free(acc);
+}
+
+/* Averaged iterate, PAPER.md:1277-1278 ("the average x̄_t of the previous t/2
+ * iterates"), window ⌈k/2⌉..k inclusive (reading R15):
+ * hist holds iterates x_1..x_k row by row ([k*d]); out = mean of rows
+ * ⌈k/2⌉..k (1-based). */
+void oracle_average(const double *hist, int k, int64_t d, double *out) {
+  const int lo = (k + 1) / 2;  /* ⌈k/2⌉ */
+  for (int64_t c = 0; c < d; ++c) out[c] = 0.0;
+  for (int j = lo; j <= k; ++j)
+    for (int64_t c = 0; c < d; ++c) out[c] += hist[(size_t)(j - 1) * d + c];
+  for (int64_t c = 0; c < d; ++c) out[c] /= (double)(k - lo + 1);
+}
+
+/* EXACT (Eq. extragrad-method) with the averaged-iterate stopping rule of
+ * PAPER.md:1279 ("the first iteration at which ||x̄_t - x̄_{t-1}||_2 <= 1e-5"):
+ * iterates x_1 = P_X(x_in), x_{k+1} from x_k by one EXACT iteration; after
+ * producing x_k (k >= 2) stop if ||x̄_k - x̄_{k-1}|| <= tol, or when k = T_max+1.
+ * Returns in xbar the x̄_k at the stop, in x the last iterate x_k, in *iters
+ * the EXACT iterations run (k - 1) and in *move the last ||x̄_k - x̄_{k-1}||.
+ * Return value: 0, or the iteration of a non-finite iterate. */
+int oracle_solve_avg(const oracle_problem *p, int T_max, double gamma, double tol, double *x,
+                     double *xbar, int *iters, double *move) {
+  const int64_t d = p->d;
+  double *hist = (double *)malloc((size_t)(T_max + 1) * (size_t)d * sizeof(double));
+  double *prev = (double *)malloc((size_t)d * sizeof(double));
+  int bad = 0, k = 1;
+  double mv = 0.0;
+  oracle_project(p->set, d, p->R, p->center, x, x);
+  memcpy(hist, x, (size_t)d * sizeof(double));
+  oracle_average(hist, 1, d, xbar);
+  double *g = (double *)malloc((size_t)d * sizeof(double));
+  double *xh = (double *)malloc((size_t)d * sizeof(double));
+  double *v = (double *)malloc((size_t)d * sizeof(double));
+  for (int t = 1; t <= T_max; ++t) {
+    /* one EXACT iteration, both half-steps anchored at x_t */
+    oracle_F(p, x, g, NULL);
+    for (int64_t c = 0; c < d; ++c) v[c] = x[c] - gamma * g[c];
+    oracle_project(p->set, d, p->R, p->center, v, xh);
+    oracle_F(p, xh, g, NULL);
+    for (int64_t c = 0; c < d; ++c) v[c] = x[c] - gamma * g[c];
+    oracle_project(p->set, d, p->R, p->center, v, x);
+    for (int64_t c = 0; c < d; ++c)
+      if (!isfinite(x[c])) bad = t;
+    if (bad) break;
+    k = t + 1;
+    memcpy(hist + (size_t)t * d, x, (size_t)d * sizeof(double));
+    memcpy(prev, xbar, (size_t)d * sizeof(double));
+    oracle_average(hist, k, d, xbar);
+    double s = 0.0;
+    for (int64_t c = 0; c < d; ++c) s += (xbar[c] - prev[c]) * (xbar[c] - prev[c]);
+    mv = sqrt(s);
+    if (mv <= tol) break;
+  }
+  if (iters) *iters = k - 1;
+  if (move) *move = mv;
+  free(hist);
+  free(prev);
+  free(g);
+  free(xh);
+  free(v);
+  return bad;
+}
+
+/* ------------------------------------------------------------------ NEXT-3
+ * The comparison objectives of §3.1, evaluated on the same data:
+ *   mode 1  L2(x) = (1/n) Σ_i (Ī h(z_i) - y_i)^2
+ *   mode 2  L1(x) = (1/n) Σ_i |Ī h(z_i) - y_i|
+ *   mode 3  NLL(x) = (1/n) Σ_i [Ī h(z_i) - y_i log(Ī h(z_i))]
+ *           (Loss(z) at z = A x, scaled by 1/n like the other two)
+ * and their (sub)gradients by the chain rule, with h's a.e. derivative
+ * h'(t) = -Σ_j s_j μ_j exp(-μ_j t) for t > 0 and h'(t) = 0 for t <= 0 under
+ * relu ("taken as 0 ... at exactly 0"); relu = 0: the
+ * formula for every t.  sign(0) = 0 for L1.
+ *   ∇L2  = (1/n) Σ_i 2 (Ī h - y_i) Ī h'(z_i) a_i
+ *   ∂L1  = (1/n) Σ_i sign(Ī h - y_i) Ī h'(z_i) a_i
+ *   ∇NLL = (1/n) Σ_i (Ī - y_i / h(z_i)) h'(z_i) a_i
+ * Ī, s are per row when s_row/I_row are given. */
+static double hprime(int W, const double *s, const double *mu, double t, int relu) {
+  if (relu && !(t > 0.0)) return 0.0;
+  double v = 0.0;
+  for (int j = 0; j < W; ++j) v += s[j] * mu[j] * exp(-mu[j] * t);
+  return -v;
+}
+
+void oracle_objective(const oracle_problem *p, int mode, const double *x, double *g,
+                      double *loss) {
+  const int64_t n = p->n, d = p->d;
+  double *acc = (double *)calloc((size_t)d, sizeof(double));
+  double l = 0.0;
+  for (int64_t i = 0; i < n; ++i) {
+    const double z = row_dot(p, i, x);
+    const double *si = row_s(p, i);
+    const double Ii = row_I(p, i);
+    const double h = oracle_h(p->W, si, p->mu, z, p->relu);
+    const double hp = hprime(p->W, si, p->mu, z, p->relu);
+    const double m = Ii * h;
+    double phi = 0.0;
+    if (mode == 1) {
+      l += (m - p->y[i]) * (m - p->y[i]);
+      phi = 2.0 * (m - p->y[i]) * Ii * hp;
+    } else if (mode == 2) {
+      const double r = m - p->y[i];
+      l += fabs(r);
+      phi = (r > 0.0 ? 1.0 : (r < 0.0 ? -1.0 : 0.0)) * Ii * hp;
+    } else {
+      l += m - p->y[i] * log(m);
+      phi = (Ii - p->y[i] / h) * hp;
+    }
+    if (!p->csr) {
+      for (int64_t k = 0; k < d; ++k) acc[k] += phi * a_at(p, i, k);
+    } else {
+      for (int64_t e = p->row_ptr[i]; e < p->row_ptr[i + 1]; ++e) acc[p->col[e]] += phi * v_at(p, e);
+    }
+  }
+  if (g)
+    for (int64_t k = 0; k < d; ++k) g[k] = acc[k] / (double)p->n_norm;
+  if (loss) *loss = l / (double)p->n_norm;
+  free(acc);
+}
+
+/* Projected gradient descent, the MSE-GD baseline's iteration (§3.1,
+ * PAPER.md:1225-1229): x_1 = P_X(x_in), x_{t+1} = P_X(x_t - γ ∇L(x_t)) for the
+ * objective `mode` of oracle_objective.  Returns 0 or the non-finite iteration. */
+int oracle_solve_gd(const oracle_problem *p, int mode, int T, double gamma, double *x) {
+  const int64_t d = p->d;
+  double *g = (double *)malloc((size_t)d * sizeof(double));
+  int bad = 0;
+  oracle_project(p->set, d, p->R, p->center, x, x);
+  for (int t = 1; t <= T && !bad; ++t) {
+    oracle_objective(p, mode, x, g, NULL);
+    for (int64_t k = 0; k < d; ++k) x[k] = x[k] - gamma * g[k];
+    oracle_project(p->set, d, p->R, p->center, x, x);
+    for (int64_t k = 0; k < d; ++k)
+      if (!isfinite(x[k])) { bad = t; break; }
+  }
+  free(g);
+  return bad;
+}

@@ -38,6 +38,8 @@ struct FinArgs {
   int32_t mode;
   int32_t d;
   int32_t G;                 // number of partial rows
+  int32_t GL;                // number of loss partials
+  int32_t split;             // 1: skip the last-block tail; k_fin_apply finishes the step
   int32_t set;
   int64_t n_norm;            // the n of Eq.(operator)
   const double *partials;    // [G][d]
@@ -48,7 +50,6 @@ struct FinArgs {
   double *x_out;             // [d] (may alias anchor)
   double *v_scratch;         // [d]
   double *block_norm;        // [gridDim.x]
-  int32_t zero_partials;     // 1: reset partials[0][*] and loss_partials[0] to 0 after reading (G == 1)
   const double *center;      // [d] or null
   double R;
   SolveState *state;
@@ -88,7 +89,6 @@ __global__ void __launch_bounds__(256) k_finalize(const FinArgs a) {
         }
         for (; i < a.G; i += 8) q0 += col[(size_t)i * a.d];
         acc = (q0 + q1) + (q2 + q3);
-        if (a.zero_partials && sl == 0) const_cast<double *>(a.partials)[c] = 0.0;
       }
     }
     sm[sl][cl] = acc;
@@ -99,10 +99,9 @@ __global__ void __launch_bounds__(256) k_finalize(const FinArgs a) {
     if (from_comm) {
       l = (cl == 0) ? a.comm[a.d] : 0.0;
     } else {
-      for (int i = cl; i < a.G; i += 32) l += a.loss_partials[i];
+      for (int i = cl; i < a.GL; i += 32) l += a.loss_partials[i];
     }
     l = warp_sum(l);
-    if (a.zero_partials && cl == 0 && !from_comm) const_cast<double *>(a.loss_partials)[0] = 0.0;
     if (cl == 0) s_loss = l;
   }
   __syncthreads();
@@ -144,6 +143,11 @@ __global__ void __launch_bounds__(256) k_finalize(const FinArgs a) {
     if (cl == 0) {
       a.block_norm[blockIdx.x] = q;
       if (blockIdx.x == 0 && needs_g) a.state->loss_cur = s_loss / nn;
+    }
+  }
+  if (a.split) return;  // k_fin_apply (next kernel) forms the norm and writes x_out
+  if (sl == 0) {
+    if (cl == 0) {
       __threadfence();
       const uint32_t prev = atomicAdd(&a.state->ticket, 1u);
       s_last = (prev == gridDim.x - 1);
@@ -180,6 +184,51 @@ __global__ void __launch_bounds__(256) k_finalize(const FinArgs a) {
     if (needs_g) {
       const int k = s->counter;
       if (s->trace && k < s->trace_cap) s->trace[k] = *(volatile double *)&s->loss_cur;
+      s->counter = k + 1;
+      if (!isfinite(nrm) && s->bad == 0) s->bad = k + 1;
+    } else if (!isfinite(nrm) && s->bad == 0) {
+      s->bad = -1;
+    }
+  }
+}
+
+// Tail of the step for large d (FinArgs.split = 1): every block forms
+// ||v - c||² from the block partials of k_finalize in the same fixed order
+// (identical bits in every block), then scales its slice of v into x_out.
+// Replaces the single-block tail, which serialised d/256 dependent loads.
+__global__ void __launch_bounds__(256) k_fin_apply(const FinArgs a) {
+  __shared__ double s_nr;
+  pdl_wait();
+  pdl_trigger();
+  const int tid = threadIdx.x;
+  const int nb = (a.d + 31) / 32;  // k_finalize blocks
+  if (tid < 32) {
+    double nr = 0.0;
+    for (int b = tid; b < nb; b += 32) nr += a.block_norm[b];
+    nr = warp_sum(nr);
+    if (tid == 0) s_nr = nr;
+  }
+  __syncthreads();
+  const double nrm = sqrt(s_nr);
+  double scale = 1.0;
+  if ((a.set == 1 || a.set == 3) && nrm > a.R) scale = a.R / nrm;
+  for (int k = blockIdx.x * blockDim.x + tid; k < a.d; k += gridDim.x * blockDim.x) {
+    const double v = a.v_scratch[k];
+    double xo;
+    if (a.set == 1) {
+      const double ck = a.center ? a.center[k] : 0.0;
+      xo = scale == 1.0 ? v : ck + (v - ck) * scale;
+    } else {
+      xo = v * scale;
+    }
+    a.x_out[k] = xo;
+  }
+  if (blockIdx.x == 0 && tid == 0) {
+    SolveState *s = a.state;
+    const bool needs_g = (a.mode != FIN_PROJECT);
+    if (needs_g) {
+      const int k = s->counter;
+      if (s->trace && k < s->trace_cap) s->trace[k] = s->loss_cur;
       s->counter = k + 1;
       if (!isfinite(nrm) && s->bad == 0) s->bad = k + 1;
     } else if (!isfinite(nrm) && s->bad == 0) {

@@ -16,6 +16,9 @@
 #include <stdio.h>
 #include <string.h>
 
+#include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_scan.cuh>
+
 #include <algorithm>
 #include <cmath>
 #include <vector>
@@ -118,13 +121,13 @@ const DenseVariant kDenseF64[] = {
     DV(double, 8, 8, 8, 1),
 };
 
-constexpr int kCsrKreg = 16;
-const void *kCsrFn[2][2] = {
-    {(const void *)&k_csr_loss_grad<float, kCsrKreg, false>,
-     (const void *)&k_csr_loss_grad<float, kCsrKreg, true>},
-    {(const void *)&k_csr_loss_grad<double, kCsrKreg, false>,
-     (const void *)&k_csr_loss_grad<double, kCsrKreg, true>},
+const void *kCsrFwd[2][2] = {
+    {(const void *)&k_csr_forward<float, false>, (const void *)&k_csr_forward<float, true>},
+    {(const void *)&k_csr_forward<double, false>, (const void *)&k_csr_forward<double, true>},
 };
+const void *kCscBwd[2] = {(const void *)&k_csc_backward<float>,
+                          (const void *)&k_csc_backward<double>};
+constexpr int kSplitFinD = 8192;  // d above which the step tail runs as k_fin_apply
 
 constexpr size_t kSmemLimit = 227 * 1024;
 constexpr size_t kRingBudget = 200 * 1024;
@@ -135,6 +138,18 @@ __global__ void k_min_i32(const int32_t *y, int64_t n, int32_t *out) {
        i += (int64_t)gridDim.x * blockDim.x)
     m = min(m, y[i]);
   if (m < 0) atomicMin(out, m);
+}
+
+__global__ void k_iota(int32_t *v, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    v[i] = (int32_t)i;
+}
+
+__global__ void k_widen(const int32_t *c, int64_t d, int64_t *out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i <= d;
+       i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = i < d ? c[i] : 0;
 }
 
 __global__ void k_check_csr(const int64_t *rp, const int32_t *col, int64_t n, int64_t nnz, int d,
@@ -175,7 +190,13 @@ struct poly_handle {
   int full = 0;
   int k1_grid = 0, k1_threads = 0, k1_stages = 0, k1_side = 0;
   size_t k1_smem = 0;
-  int k4_grid = 0;
+  int k4_grid = 0;                     // K4f blocks (= loss partials)
+  int nslices = 0;                     // K4b blocks: 32-column SELL slices of A^T
+  void *sell = nullptr;                // CscEnt<T>[slice_off[nslices] * 32]
+  int64_t *slice_off = nullptr;        // [nslices + 1] slice start, in 32-entry steps
+  float *rbuf = nullptr;               // [n_local] residuals between K4f and K4b
+  int64_t sell_steps = 0;              // slice_off[nslices]
+  int fin_split = 0;
   // workspaces
   int G = 0;  // partial rows
   double *partials = nullptr, *loss_partials = nullptr, *comm = nullptr;
@@ -272,12 +293,11 @@ int enqueue_pass(poly_handle *h, const double *x, bool loss) {
     return launch(h, h->dv->fn[h->full][loss ? 1 : 0], dim3(h->k1_grid), dim3(h->k1_threads), h->k1_smem,
                   true, a);
   }
-  CsrArgs a{};
+  CsrFwdArgs a{};
   a.row_ptr = p.row_ptr;
   a.col = p.col;
   a.val = p.val;
   a.n = p.n_local;
-  a.d = (int32_t)p.d;
   a.W = p.W;
   a.y = p.y;
   a.ytype = p.ytype;
@@ -287,9 +307,17 @@ int enqueue_pass(poly_handle *h, const double *x, bool loss) {
   a.I_bar = p.I_bar;
   a.x = x;
   a.spec = h->spec;
-  a.gacc = h->partials;
-  a.lacc = h->loss_partials;
-  return launch(h, kCsrFn[p.dtype][loss ? 1 : 0], dim3(h->k4_grid), dim3(256), 0, true, a);
+  a.r = h->rbuf;
+  a.loss_partials = h->loss_partials;
+  TRY(launch(h, kCsrFwd[p.dtype][loss ? 1 : 0], dim3(h->k4_grid), dim3(256), 0, true, a));
+  int32_t d32 = (int32_t)p.d;
+  const float *rb = h->rbuf;
+  double *gp = h->partials;
+  if (p.dtype == POLY_F32)
+    return launch(h, kCscBwd[0], dim3(h->nslices), dim3(128), 0, true,
+                  (const CscEnt<float> *)h->sell, (const int64_t *)h->slice_off, d32, rb, gp);
+  return launch(h, kCscBwd[1], dim3(h->nslices), dim3(128), 0, true,
+                (const CscEnt<double> *)h->sell, (const int64_t *)h->slice_off, d32, rb, gp);
 }
 
 FinArgs fin_base(poly_handle *h, int mode) {
@@ -297,6 +325,8 @@ FinArgs fin_base(poly_handle *h, int mode) {
   f.mode = mode;
   f.d = (int32_t)h->p.d;
   f.G = h->G;
+  f.GL = h->p.layout == POLY_CSR ? h->k4_grid : h->G;
+  f.split = h->fin_split;
   f.set = h->p.set;
   f.n_norm = h->p.n_global;
   f.partials = h->partials;
@@ -304,7 +334,6 @@ FinArgs fin_base(poly_handle *h, int mode) {
   f.comm = h->comm;
   f.v_scratch = h->vscratch;
   f.block_norm = h->block_norm;
-  f.zero_partials = h->p.layout == POLY_CSR ? 1 : 0;
   f.center = h->center;
   f.R = h->p.R;
   f.state = h->state;
@@ -313,7 +342,13 @@ FinArgs fin_base(poly_handle *h, int mode) {
 
 int enqueue_fin(poly_handle *h, const FinArgs &f) {
   ProfScope ps(h, 1);
-  return launch(h, (const void *)&k_finalize, dim3(h->fin_grid), dim3(256), 0, true, f);
+  TRY(launch(h, (const void *)&k_finalize, dim3(h->fin_grid), dim3(256), 0, true, f));
+  const bool steps = f.mode == FIN_STEP || f.mode == FIN_STEP_COMM || f.mode == FIN_PROJECT;
+  if (f.split && steps) {
+    const int grid = (int)std::min<int64_t>(h->sms, (h->p.d + 255) / 256);
+    TRY(launch(h, (const void *)&k_fin_apply, dim3(grid), dim3(256), 0, true, f));
+  }
+  return POLY_OK;
 }
 
 int enqueue_allreduce(poly_handle *h) {
@@ -346,7 +381,6 @@ int enqueue_eval(poly_handle *h, const double *x, bool loss, bool step, const do
   TRY(enqueue_fin(h, r));
   TRY(enqueue_allreduce(h));
   f.mode = step ? FIN_STEP_COMM : FIN_GRAD_COMM;
-  f.zero_partials = 0;
   return enqueue_fin(h, f);
 }
 
@@ -497,9 +531,93 @@ int setup_dense(poly_handle *h) {
   return POLY_OK;
 }
 
+// SELL-32 copy of Aᵀ for K4b (poly_init only): stable radix sort of the
+// entries by column (ties keep CSR order = ascending row), column pointers by
+// histogram + scan, slice length = longest column of 32, zero padding.
+template <typename T>
+int build_sell_t(poly_handle *h) {
+  const poly_problem &p = h->p;
+  const int64_t nnz = p.nnz, d = p.d;
+  if (nnz >= (int64_t)1 << 31) return fail(POLY_EUNSUPPORTED, "nnz >= 2^31");
+  h->nslices = (int)((d + 31) / 32);
+  TRY(dev_alloc(h, &h->slice_off, (size_t)h->nslices + 1));
+  cudaStream_t st = h->work;
+  std::vector<void *> tmp;
+  auto talloc = [&](size_t bytes, void **ptr) -> int {
+    if (cudaMalloc(ptr, std::max<size_t>(bytes, 16)) != cudaSuccess) {
+      cudaGetLastError();
+      return fail(POLY_ENOMEM, "SELL build: cudaMalloc(%zu) failed", bytes);
+    }
+    tmp.push_back(*ptr);
+    return POLY_OK;
+  };
+  auto done = [&](int code) {
+    cudaStreamSynchronize(st);
+    for (void *q : tmp) cudaFree(q);
+    return code;
+  };
+  int32_t *rows = nullptr, *perm_in = nullptr, *perm = nullptr, *keys = nullptr, *cnt = nullptr;
+  int64_t *cnt64 = nullptr, *colptr = nullptr, *slen = nullptr;
+  int rc;
+  if ((rc = talloc(nnz * 4, (void **)&rows)) || (rc = talloc(nnz * 4, (void **)&perm_in)) ||
+      (rc = talloc(nnz * 4, (void **)&perm)) || (rc = talloc(nnz * 4, (void **)&keys)) ||
+      (rc = talloc(d * 4, (void **)&cnt)) || (rc = talloc((d + 1) * 8, (void **)&cnt64)) ||
+      (rc = talloc((d + 1) * 8, (void **)&colptr)) ||
+      (rc = talloc((size_t)(h->nslices + 1) * 8, (void **)&slen)))
+    return done(rc);
+  const int g = 148 * 8;
+  if (nnz > 0) {
+    k_entry_rows<<<g, 256, 0, st>>>(p.row_ptr, p.n_local, rows);
+    k_iota<<<g, 256, 0, st>>>(perm_in, nnz);
+  }
+  cudaMemsetAsync(cnt, 0, d * 4, st);
+  if (nnz > 0) k_col_count<<<g, 256, 0, st>>>(p.col, nnz, cnt);
+  size_t tb = 0, tb2 = 0, tb3 = 0;
+  cub::DeviceRadixSort::SortPairs(nullptr, tb, p.col, keys, perm_in, perm, (int)nnz, 0,
+                                  32 - __builtin_clz((unsigned)std::max<int64_t>(1, d)), st);
+  cub::DeviceScan::ExclusiveSum(nullptr, tb2, cnt64, colptr, (int)d + 1, st);
+  cub::DeviceScan::ExclusiveSum(nullptr, tb3, slen, h->slice_off, h->nslices + 1, st);
+  void *tstore = nullptr;
+  if ((rc = talloc(std::max(tb, std::max(tb2, tb3)), &tstore))) return done(rc);
+  if (nnz > 0) {
+    size_t t = tb;
+    if (cub::DeviceRadixSort::SortPairs(tstore, t, p.col, keys, perm_in, perm, (int)nnz, 0,
+                                        32 - __builtin_clz((unsigned)std::max<int64_t>(1, d)),
+                                        st) != cudaSuccess)
+      return done(fail(POLY_ECUDA, "SELL build: radix sort failed"));
+  }
+  k_widen<<<(int)std::min<int64_t>(4096, (d + 256) / 256), 256, 0, st>>>(cnt, d, cnt64);
+  size_t t2 = tb2;
+  cub::DeviceScan::ExclusiveSum(tstore, t2, cnt64, colptr, (int)d + 1, st);
+  k_slice_len<<<(h->nslices + 255) / 256, 256, 0, st>>>(cnt, (int32_t)d, h->nslices, slen);
+  cudaMemsetAsync(slen + h->nslices, 0, 8, st);
+  size_t t3 = tb3;
+  cub::DeviceScan::ExclusiveSum(tstore, t3, slen, h->slice_off, h->nslices + 1, st);
+  int64_t steps = 0;
+  cudaMemcpyAsync(&steps, h->slice_off + h->nslices, 8, cudaMemcpyDeviceToHost, st);
+  if (cudaStreamSynchronize(st) != cudaSuccess)
+    return done(fail(POLY_ECUDA, "SELL build: %s", cudaGetErrorString(cudaGetLastError())));
+  CscEnt<T> *ent = nullptr;
+  if ((rc = dev_alloc(h, &ent, (size_t)std::max<int64_t>(1, steps) * 32))) return done(rc);
+  cudaMemsetAsync(ent, 0, (size_t)std::max<int64_t>(1, steps) * 32 * sizeof(CscEnt<T>), st);
+  if (nnz > 0)
+    k_sell_fill<T><<<g, 256, 0, st>>>(keys, perm, rows, (const T *)p.val, colptr, h->slice_off,
+                                      nnz, ent);
+  h->sell = ent;
+  h->sell_steps = steps;
+  if (cudaStreamSynchronize(st) != cudaSuccess)
+    return done(fail(POLY_ECUDA, "SELL build: %s", cudaGetErrorString(cudaGetLastError())));
+  return done(POLY_OK);
+}
+
+int build_sell(poly_handle *h) {
+  return h->p.dtype == POLY_F32 ? build_sell_t<float>(h) : build_sell_t<double>(h);
+}
+
 }  // namespace
 
 extern "C" {
+
 
 int poly_abi_version(void) { return POLY_ABI_VERSION; }
 const char *poly_last_error(void) { return g_err; }
@@ -611,12 +729,13 @@ int poly_init(const poly_problem *pin, poly_handle **out) {
     const int64_t warps = std::max<int64_t>(1, p.n_local);
     h->k4_grid = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)h->sms * 8, (warps + 7) / 8));
     if ((rc = dev_alloc(h, &h->partials, (size_t)p.d)) != POLY_OK) return bail(rc);
-    if ((rc = dev_alloc(h, &h->loss_partials, 1)) != POLY_OK) return bail(rc);
-    if (cudaMemsetAsync(h->partials, 0, p.d * 8, h->work) != cudaSuccess ||
-        cudaMemsetAsync(h->loss_partials, 0, 8, h->work) != cudaSuccess)
+    if ((rc = dev_alloc(h, &h->loss_partials, (size_t)h->k4_grid)) != POLY_OK) return bail(rc);
+    if ((rc = dev_alloc(h, &h->rbuf, (size_t)std::max<int64_t>(1, p.n_local))) != POLY_OK) return bail(rc);
+    if (cudaMemsetAsync(h->rbuf, 0, std::max<int64_t>(1, p.n_local) * 4, h->work) != cudaSuccess)
       return bail(fail(POLY_ECUDA, "memset failed"));
   }
   h->fin_grid = (int)((p.d + 31) / 32);
+  h->fin_split = p.d > kSplitFinD ? 1 : 0;
   if ((rc = dev_alloc(h, &h->comm, (size_t)p.d + 1)) != POLY_OK) return bail(rc);
   if ((rc = dev_alloc(h, &h->xa, (size_t)p.d)) != POLY_OK) return bail(rc);
   if ((rc = dev_alloc(h, &h->xh, (size_t)p.d)) != POLY_OK) return bail(rc);
@@ -654,6 +773,7 @@ int poly_init(const poly_problem *pin, poly_handle **out) {
       if (hv) return bail(fail(POLY_EINVAL, "invalid CSR structure (code %d)", hv));
     }
   }
+  if (p.layout == POLY_CSR && (rc = build_sell(h)) != POLY_OK) return bail(rc);
 
   h->comm_path = p.world > 1 || (p.flags & POLY_FLAG_COMM);
   if (h->comm_path) {
@@ -871,10 +991,10 @@ int poly_describe(poly_handle *h, int64_t *out, int32_t nout) {
     v[3] = h->k1_stages;
     v[4] = (int64_t)h->k1_smem;
   } else {
-    v[0] = h->k4_grid;
+    v[0] = h->k4_grid;   // K4f blocks (K4b: one 128-thread block per 32-column slice)
     v[1] = 256;
-    v[2] = 1;
-    v[3] = 0;
+    v[2] = h->nslices;
+    v[3] = h->sell_steps;
     v[4] = 0;
   }
   v[5] = h->sms;
