@@ -47,7 +47,7 @@
 extern "C" {
 #endif
 
-#define POLY_ABI_VERSION 1
+#define POLY_ABI_VERSION 2
 
 /* status codes */
 #define POLY_OK 0
@@ -79,6 +79,17 @@ extern "C" {
 #define POLY_FLAG_NO_PDL 4u      /* disable programmatic dependent launch between kernels */
 #define POLY_FLAG_COMM 8u        /* use the NCCL path (reduce -> ncclAllReduce -> step) even when
                                     world == 1; needs nccl_id.  Exercises the collective path on one GPU */
+
+/* poly_problem.mode: which per-row scalar the fused pass evaluates.  Every mode
+ * streams A once and returns g = (1/n) Σ_i φ_i a_i and a scalar objective.   */
+#define POLY_MODE_EXACT 0    /* φ_i = y_i - Ī h(z_i): g = F(x), Eq.(operator); ℓ of reading R2 */
+#define POLY_MODE_L2 1       /* MSE-GD baseline: L2 = (1/n) Σ (Ī h - y)^2,
+                                φ_i = 2 (Ī h - y_i) Ī h'(z_i)                               */
+#define POLY_MODE_L1 2       /* PolyakSGM baseline: L1 = (1/n) Σ |Ī h - y|,
+                                φ_i = sign(Ī h - y_i) Ī h'(z_i), sign(0) = 0                 */
+#define POLY_MODE_NLL 3      /* Poisson NLL scaled by 1/n:
+                                (1/n) Σ [Ī h - y log(Ī h)], φ_i = (Ī - y_i/h) h'(z_i)        */
+/* h'(t) = -Σ_j s_j μ_j e^{-μ_j t} for t > 0; 0 for t <= 0 when relu = 1. */
 
 /* poly_solve flags */
 #define POLY_SOLVE_PROFILE 1u    /* time every kernel with CUDA events (implies no graph);
@@ -116,7 +127,18 @@ typedef struct poly_problem {
   const void *nccl_id; /* host, 128-byte ncclUniqueId from poly_nccl_unique_id on rank 0 */
   void *stream;        /* cudaStream_t (NULL = legacy default stream)                    */
   uint32_t flags;      /* POLY_FLAG_*                                                    */
-  int32_t reserved;
+  int32_t mode;        /* POLY_MODE_* (0 = EXACT's operator F)                           */
+  /* Multiple detector windows (footnote PAPER.md:842; Eq. model:multi-material
+   * PAPER.md:782-799 with M = 1): windows = Ω > 1 stacks Ω measurements of
+   * every ray.  Then s is host [Ω*W] (window-major, each window a spectrum
+   * with the invariants above), mu is host [W] (per wavelength, shared),
+   * I_win is host [Ω] (Ī_ω > 0; I_bar is ignored), y is device [Ω*n_local]
+   * (window-major, same ytype for all windows), and
+   *   F(x) = (1/(Ω n_global)) Σ_ω Σ_i [y_ωi - Ī_ω h_ω(<a_i,x>)] a_i.
+   * Needs mode = EXACT and no per-row spectra (POLY_EUNSUPPORTED otherwise).
+   * windows = 0 or 1: a single window as above. */
+  int32_t windows;
+  const double *I_win;
 } poly_problem;
 
 /* Validate *p, copy host parameters, pick the kernel configuration for
@@ -145,6 +167,40 @@ int poly_loss_grad(poly_handle *h, const double *x, double *g, double *loss);
  * NULL).  Synchronises the stream before returning. */
 int poly_solve(poly_handle *h, double *x, int T, double gamma, uint32_t flags,
                double *trace, int *bad_iter);
+
+/* Options of poly_solve_ex. */
+#define POLY_METHOD_EXTRAGRADIENT 0 /* EXACT, Eq.(extragrad-method): 2 passes per iteration        */
+#define POLY_METHOD_GD 1            /* projected gradient x_{t+1} = P_X(x_t - γ g(x_t)): the MSE-GD
+                                       baseline's iteration (§3.1); 1 pass per iteration            */
+typedef struct poly_solve_opts {
+  int32_t T_max;       /* >= 0 iterations at most                                               */
+  int32_t method;      /* POLY_METHOD_*                                                         */
+  double gamma;        /* > 0 constant step                                                     */
+  double tol;          /* averaging: stop at the first k >= 2 with ||x̄_k - x̄_{k-1}||_2 <= tol
+                          (1e-5); 0 = never stop early                            */
+  int32_t average;     /* 1: x̄_k = mean of iterates ⌈k/2⌉..k (reading R15)        */
+  uint32_t flags;      /* POLY_SOLVE_* (PROFILE)                                                */
+} poly_solve_opts;
+
+typedef struct poly_solve_info {
+  int32_t iters;       /* iterations run up to the stop (k - 1 for the stopping iterate x_k)    */
+  int32_t stopped;     /* 1 if the tolerance was met                                            */
+  int32_t bad_iter;    /* 1-based iteration of a non-finite iterate, else 0                     */
+  int32_t reserved;
+  double move;         /* ||x̄_k - x̄_{k-1}||_2 at the stop / last iterate (averaging), else 0    */
+} poly_solve_info;
+
+/* Iterative solve with the options above (Eq. extragrad-method or projected
+ * GD, optional averaged iterate and stopping rule of PAPER.md:1277-1280).
+ * x: device or host [d] fp64; in: x_in (x_1 = P_X(x_in)); out: x̄_k when
+ * opts->average, else the last iterate.  x_last: NULL or device/host [d]
+ * receiving the last iterate x_k at the stop.  info: host, may be NULL.
+ * Iterations run as CUDA-graph replays; the stop is detected on the device
+ * and polled by the host one graph behind, so a few iterations past the stop
+ * may execute — they change neither the returned x̄_k nor x_last nor info.
+ * Errors: as poly_solve; POLY_ENONFINITE sets info->bad_iter. */
+int poly_solve_ex(poly_handle *h, const poly_solve_opts *opts, double *x, double *x_last,
+                  poly_solve_info *info);
 
 /* Forward projection z_i = <a_i, x> for the local rows, accumulated in fp64
  * (fp32 A values promoted exactly), fixed reduction order.

@@ -20,10 +20,12 @@ POLY_Y_I32, POLY_Y_F32, POLY_Y_F64 = 0, 1, 2
 POLY_SET_NONE, POLY_SET_BALL, POLY_SET_NONNEG, POLY_SET_NONNEG_BALL = 0, 1, 2, 3
 POLY_FLAG_HOST_INPUTS, POLY_FLAG_NO_GRAPH, POLY_FLAG_NO_PDL, POLY_FLAG_COMM = 1, 2, 4, 8
 POLY_SOLVE_PROFILE = 1
+POLY_MODE_EXACT, POLY_MODE_L2, POLY_MODE_L1, POLY_MODE_NLL = 0, 1, 2, 3
+POLY_METHOD_EXTRAGRADIENT, POLY_METHOD_GD = 0, 1
 
 EXPORTED = ["poly_init", "poly_loss_grad", "poly_solve", "poly_forward", "poly_expected_counts",
             "poly_reparameterize", "poly_kernel_times", "poly_describe", "poly_nccl_unique_id",
-            "poly_free", "poly_last_error", "poly_abi_version"]
+            "poly_free", "poly_last_error", "poly_abi_version", "poly_solve_ex"]
 
 
 class PolyProblem(C.Structure):
@@ -38,8 +40,21 @@ class PolyProblem(C.Structure):
         ("s_row", C.c_void_p), ("I_row", C.c_void_p),
         ("relu", C.c_int32), ("set", C.c_int32), ("R", C.c_double), ("center", C.c_void_p),
         ("rank", C.c_int32), ("world", C.c_int32), ("nccl_id", C.c_void_p),
-        ("stream", C.c_void_p), ("flags", C.c_uint32), ("reserved", C.c_int32),
+        ("stream", C.c_void_p), ("flags", C.c_uint32), ("mode", C.c_int32),
+        ("windows", C.c_int32), ("I_win", C.c_void_p),
     ]
+
+
+class PolySolveOpts(C.Structure):
+    """Mirror of `poly_solve_opts`."""
+    _fields_ = [("T_max", C.c_int32), ("method", C.c_int32), ("gamma", C.c_double),
+                ("tol", C.c_double), ("average", C.c_int32), ("flags", C.c_uint32)]
+
+
+class PolySolveInfo(C.Structure):
+    """Mirror of `poly_solve_info`."""
+    _fields_ = [("iters", C.c_int32), ("stopped", C.c_int32), ("bad_iter", C.c_int32),
+                ("reserved", C.c_int32), ("move", C.c_double)]
 
 
 class PolyError(RuntimeError):
@@ -58,6 +73,7 @@ def _load():
     lib.poly_init.argtypes = [C.POINTER(PolyProblem), C.POINTER(vp)]
     lib.poly_loss_grad.argtypes = [vp, vp, vp, dp]
     lib.poly_solve.argtypes = [vp, vp, C.c_int, dbl, C.c_uint32, dp, C.POINTER(C.c_int)]
+    lib.poly_solve_ex.argtypes = [vp, C.POINTER(PolySolveOpts), vp, vp, C.POINTER(PolySolveInfo)]
     lib.poly_forward.argtypes = [vp, vp, vp]
     lib.poly_expected_counts.argtypes = [vp, vp, vp]
     lib.poly_reparameterize.argtypes = [i32, dp, dp, dbl, i64, vp, i32, vp, vp, vp]
@@ -114,6 +130,15 @@ def poly_solve(h: int, x_ptr: int, T: int, gamma: float, flags: int = 0, trace=N
     if rc == POLY_ENONFINITE:
         raise PolyError(rc, f"{poly_last_error()} (bad_iter={bad.value})")
     _check(rc)
+
+
+def poly_solve_ex(h: int, x_ptr: int, opts: PolySolveOpts, x_last_ptr=None) -> PolySolveInfo:
+    info = PolySolveInfo()
+    rc = _lib.poly_solve_ex(h, C.byref(opts), x_ptr, x_last_ptr, C.byref(info))
+    if rc == POLY_ENONFINITE:
+        raise PolyError(rc, f"{poly_last_error()} (bad_iter={info.bad_iter})")
+    _check(rc)
+    return info
 
 
 def poly_forward(h: int, x_ptr: int, z_ptr: int):

@@ -10,10 +10,11 @@ import ctypes as C
 
 import torch
 
-from . import (POLY_CSR, POLY_DENSE, POLY_F32, POLY_F64, POLY_FLAG_HOST_INPUTS, POLY_SET_BALL,
-               POLY_SOLVE_PROFILE, POLY_Y_F32, POLY_Y_F64, POLY_Y_I32, PolyProblem, poly_describe,
-               poly_expected_counts, poly_forward, poly_free, poly_init, poly_kernel_times,
-               poly_loss_grad, poly_solve)
+from . import (POLY_CSR, POLY_DENSE, POLY_F32, POLY_F64, POLY_FLAG_HOST_INPUTS,
+               POLY_METHOD_EXTRAGRADIENT, POLY_SET_BALL, POLY_SOLVE_PROFILE, POLY_Y_F32, POLY_Y_F64,
+               POLY_Y_I32, PolyProblem, PolySolveOpts, poly_describe, poly_expected_counts,
+               poly_forward, poly_free, poly_init, poly_kernel_times, poly_loss_grad, poly_solve,
+               poly_solve_ex)
 
 _DT = {torch.float32: POLY_F32, torch.float64: POLY_F64}
 _YT = {torch.int32: POLY_Y_I32, torch.float32: POLY_Y_F32, torch.float64: POLY_Y_F64}
@@ -33,7 +34,7 @@ class Poly:
     def __init__(self, *, y, s, mu, I_bar, d=None, A=None, row_ptr=None, col=None, val=None,
                  s_row=None, I_row=None, relu=1, set=POLY_SET_BALL, R=1.0, center=None,
                  n_global=None, row_offset=0, rank=0, world=1, nccl_id=None, stream=None,
-                 flags=0):
+                 flags=0, mode=0, I_win=None):
         p = PolyProblem()
         host = bool(flags & POLY_FLAG_HOST_INPUTS)
         self._keep = [y, A, row_ptr, col, val, s_row, I_row]
@@ -53,11 +54,19 @@ class Poly:
         p.n_global = p.n_local if n_global is None else int(n_global)
         p.row_offset = int(row_offset)
         p.ytype, p.y = _YT[y.dtype], _ptr(y)
-        s = [float(v) for v in s]
+        if I_win is not None:   # Ω windows: s [Ω, W], y [Ω, n_local] (window-major)
+            iw = [float(v) for v in I_win]
+            self._iw = (C.c_double * len(iw))(*iw)
+            p.windows, p.I_win = len(iw), C.addressof(self._iw)
+            assert y.is_contiguous() and y.numel() == len(iw) * p.n_local
+            s = [float(v) for row in s for v in row]
+        else:
+            s = [float(v) for v in s]
         mu = [float(v) for v in mu]
         self._s = (C.c_double * len(s))(*s)
         self._mu = (C.c_double * len(mu))(*mu)
-        p.W, p.s, p.mu = len(s), C.addressof(self._s), C.addressof(self._mu)
+        p.W, p.s, p.mu = len(mu), C.addressof(self._s), C.addressof(self._mu)
+        p.mode = int(mode)
         p.I_bar = float(I_bar)
         if s_row is not None:
             assert s_row.dtype == torch.float32 and I_row.dtype == torch.float32
@@ -106,6 +115,16 @@ class Poly:
         tr = (C.c_double * (2 * T))() if trace else None
         poly_solve(self.h, x.data_ptr(), T, gamma, POLY_SOLVE_PROFILE if profile else 0, tr)
         return list(tr) if trace else None
+
+    def solve_ex(self, x, T_max, gamma, *, method=POLY_METHOD_EXTRAGRADIENT, average=False,
+                 tol=0.0, profile=False, x_last=None):
+        """poly_solve_ex: x is overwritten with x̄_k (average) or the last
+        iterate; returns the PolySolveInfo (iters, stopped, move, bad_iter)."""
+        assert x.dtype == torch.float64 and x.is_contiguous() and x.numel() == self.d
+        o = PolySolveOpts()
+        o.T_max, o.method, o.gamma, o.tol = int(T_max), int(method), float(gamma), float(tol)
+        o.average, o.flags = int(bool(average)), POLY_SOLVE_PROFILE if profile else 0
+        return poly_solve_ex(self.h, x.data_ptr(), o, None if x_last is None else x_last.data_ptr())
 
     def forward(self, x):
         z = torch.empty(self.n_local, dtype=torch.float64, device=x.device)

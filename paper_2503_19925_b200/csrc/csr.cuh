@@ -1,9 +1,11 @@
 // K4 — CSR loss+gradient for the CT-like sparse system matrix
 // (BASELINE.json configs[3]; A nonnegative), two passes:
 //
-//   K4f k_csr_forward   one warp per row (grid-stride): z_i = Σ_e val_e x[col_e]
-//                       (fp64), the W-bin link and residual exactly as K1
-//                       (row_residual), r_i stored as fp32, ℓ per block.
+//   K4f k_sell_forward  z_i = Σ_e val_e x[col_e] (fp64) from a SELL-32 copy of
+//                       A (32 consecutive rows per slice, lane = row), the
+//                       W-bin link and residual in-lane (lane_residual, the
+//                       same quantities as K1's row_residual), r_i stored fp32,
+//                       ℓ per block.
 //   K4b k_csc_backward  g_k = Σ_{i in column k} val_ik r_i  (Aᵀ r)
 //                       from a SELL-32 copy of Aᵀ built once at poly_init: a
 //                       slice holds 32 consecutive columns, step s of lane t is
@@ -11,6 +13,9 @@
 //                       so each warp-step is one coalesced 256-byte load and
 //                       every lane owns its column's sum in registers — no
 //                       atomics, fixed summation order (deterministic).
+// Both SELL copies are built once at poly_init from the caller's CSR; a
+// warp-per-row CSR forward was latency-bound (dependent row_ptr -> col -> x
+// loads, 2.0 TB/s in ncu) where the SELL stream runs at HBM rate.
 //
 // Why two passes: a one-pass fused kernel must scatter g[col] += r val for
 // every nonzero (red.global at ~1 lane/1.3 cycles per SM, B300_MICROARCH.md
@@ -44,51 +49,9 @@ struct CsrFwdArgs {
   const double *x;
   const double *spec;
   float *r;               // [n] residuals r_i (output)
+  int32_t mode;
   double *loss_partials;  // [gridDim.x]
 };
-
-template <typename T, bool LOSS>
-__global__ void __launch_bounds__(256) k_csr_forward(const CsrFwdArgs a) {
-  __shared__ double sp[3 * kMaxW];
-  __shared__ double wl[8];
-  for (int i = threadIdx.x; i < 3 * kMaxW; i += blockDim.x) sp[i] = a.spec[i];
-  __syncthreads();
-  pdl_wait();  // x is written by the previous kernel; r is read by the previous backward
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
-  const T *val = (const T *)a.val;
-  double lacc = 0.0;
-  for (int64_t row = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp; row < a.n; row += nwarps) {
-    const int64_t e0 = a.row_ptr[row], e1 = a.row_ptr[row + 1];
-    double p0 = 0.0, p1 = 0.0;
-    int64_t e = e0 + lane;
-    for (; e + 32 < e1; e += 64) {
-      const int32_t c0 = __ldcs(a.col + e), c1 = __ldcs(a.col + e + 32);
-      const T v0 = __ldcs(val + e), v1 = __ldcs(val + e + 32);
-      p0 = fma((double)v0, a.x[c0], p0);
-      p1 = fma((double)v1, a.x[c1], p1);
-    }
-    if (e < e1) p0 = fma((double)__ldcs(val + e), a.x[__ldcs(a.col + e)], p0);
-    const double z = warp_sum(p0 + p1);
-    double yv;
-    if (a.ytype == 0) yv = (double)((const int32_t *)a.y)[row];
-    else if (a.ytype == 1) yv = (double)((const float *)a.y)[row];
-    else yv = ((const double *)a.y)[row];
-    const double Ii = a.I_row ? (double)a.I_row[row] : a.I_bar;
-    const float *srow = a.I_row ? a.s_row + row * a.W : nullptr;
-    const double r = row_residual<LOSS>(sp, a.W, a.relu, z, yv, Ii, srow, true, &lacc);
-    if (lane == 0) a.r[row] = (float)r;
-  }
-  // per-block loss partial, warps combined in order (deterministic)
-  if (lane == 0) wl[warp] = lacc;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    double l = 0.0;
-    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) l += wl[w];
-    a.loss_partials[blockIdx.x] = l;
-  }
-  pdl_trigger();
-}
 
 // 4 warps per 32-column slice; warp w takes steps w, w+4, w+8, ...; the four
 // warps' sums are combined in warp order.
@@ -125,6 +88,122 @@ __global__ void __launch_bounds__(128) k_csc_backward(const CscEnt<T> *__restric
     if (c < d) g[c] = v;
   }
   pdl_trigger();
+}
+
+// Link and per-row scalar when ONE lane owns the row (SELL forward): the
+// same quantities as row_residual, bins looped in-lane.
+template <bool LOSS>
+__device__ __forceinline__ double lane_residual(const double *sp, int W, int relu, double z,
+                                                double yv, double Ii, const float *srow,
+                                                double *lacc, int mode) {
+  const bool neg = relu && z < 0.0;
+  const double zc = neg ? 0.0 : z;
+  double hs = 0.0, Hs = 0.0, hp = 0.0;
+  for (int j = 0; j < W; ++j) {
+    const double sj = srow ? (double)srow[j] : sp[j];
+    const double e = (relu || mode == 0) ? exp_nonpos(-sp[kMaxW + j] * zc) : exp(-sp[kMaxW + j] * z);
+    hs += sj * e;
+    if (mode == 0) {
+      if (LOSS) Hs += neg ? sj * z : sj * sp[2 * kMaxW + j] * (1.0 - e);
+    } else {
+      hp += sj * sp[kMaxW + j] * e;
+    }
+  }
+  if (mode == 0) {
+    if (LOSS) *lacc += yv * z - Ii * Hs;
+    return yv - Ii * hs;
+  }
+  hp = (relu && !(z > 0.0)) ? 0.0 : -hp;
+  const double m = Ii * hs;
+  if (mode == 1) {
+    if (LOSS) *lacc += (m - yv) * (m - yv);
+    return 2.0 * (m - yv) * Ii * hp;
+  }
+  if (mode == 2) {
+    const double r = m - yv;
+    if (LOSS) *lacc += fabs(r);
+    return (r > 0.0 ? 1.0 : (r < 0.0 ? -1.0 : 0.0)) * Ii * hp;
+  }
+  if (LOSS) *lacc += m - yv * log(m);
+  return (Ii - yv / hs) * hp;
+}
+
+// K4f on a SELL-32 copy of A (rows as slices): block = 32 consecutive rows,
+// warp w takes steps w, w+4, ...; z_i combined in warp order, then lane i of
+// warp 0 evaluates row i's link and residual.
+template <typename T, bool LOSS>
+__global__ void __launch_bounds__(128) k_sell_forward(const CscEnt<T> *__restrict__ ent,
+                                                      const int64_t *__restrict__ slice_off,
+                                                      const CsrFwdArgs a) {
+  __shared__ double sp[3 * kMaxW];
+  __shared__ double part[4][32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int i = threadIdx.x; i < 3 * kMaxW; i += blockDim.x) sp[i] = a.spec[i];
+  const int64_t s0 = slice_off[blockIdx.x], s1 = slice_off[blockIdx.x + 1];
+  const CscEnt<T> *p = ent + s0 * 32 + lane;
+  const int64_t len = s1 - s0;
+  pdl_wait();  // x is written by the previous kernel; r is read by the previous backward
+  double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+  int64_t k = warp;
+  for (; k + 12 < len; k += 16) {
+    const CscEnt<T> q0 = p[(k) * 32], q1 = p[(k + 4) * 32], q2 = p[(k + 8) * 32],
+                    q3 = p[(k + 12) * 32];
+    a0 = fma((double)q0.val, __ldg(a.x + q0.row), a0);
+    a1 = fma((double)q1.val, __ldg(a.x + q1.row), a1);
+    a2 = fma((double)q2.val, __ldg(a.x + q2.row), a2);
+    a3 = fma((double)q3.val, __ldg(a.x + q3.row), a3);
+  }
+  for (; k < len; k += 4) {
+    const CscEnt<T> q = p[k * 32];
+    a0 = fma((double)q.val, __ldg(a.x + q.row), a0);
+  }
+  part[warp][lane] = (a0 + a1) + (a2 + a3);
+  __syncthreads();
+  if (warp == 0) {
+    const int64_t row = (int64_t)blockIdx.x * 32 + lane;
+    double lacc = 0.0;
+    if (row < a.n) {
+      const double z = (part[0][lane] + part[1][lane]) + (part[2][lane] + part[3][lane]);
+      double yv;
+      if (a.ytype == 0) yv = (double)((const int32_t *)a.y)[row];
+      else if (a.ytype == 1) yv = (double)((const float *)a.y)[row];
+      else yv = ((const double *)a.y)[row];
+      const double Ii = a.I_row ? (double)a.I_row[row] : a.I_bar;
+      const float *srow = a.I_row ? a.s_row + row * a.W : nullptr;
+      a.r[row] = (float)lane_residual<LOSS>(sp, a.W, a.relu, z, yv, Ii, srow, &lacc, a.mode);
+    }
+    lacc = warp_sum(lacc);
+    if (lane == 0) a.loss_partials[blockIdx.x] = lacc;
+  }
+  pdl_trigger();
+}
+
+// (poly_init only) SELL-32 copy of A itself: entry j of row i -> step j, lane i % 32
+template <typename T>
+__global__ void k_sell_rows_fill(const int64_t *row_ptr, const int32_t *col, const T *val,
+                                 int64_t n, const int64_t *slice_off, CscEnt<T> *ent) {
+  const int lane = threadIdx.x & 31;
+  const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t i = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); i < n; i += nw) {
+    const int64_t e0 = row_ptr[i], e1 = row_ptr[i + 1];
+    CscEnt<T> *dst = ent + slice_off[i >> 5] * 32 + (i & 31);
+    for (int64_t e = e0 + lane; e < e1; e += 32) {
+      CscEnt<T> q;
+      q.row = col[e];
+      q.val = val[e];
+      dst[(e - e0) * 32] = q;
+    }
+  }
+}
+
+// slice length for row slices: longest row of 32
+__global__ void k_row_slice_len(const int64_t *row_ptr, int64_t n, int64_t nslices, int64_t *len) {
+  for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < nslices;
+       s += (int64_t)gridDim.x * blockDim.x) {
+    int64_t m = 0;
+    for (int64_t i = 32 * s; i < min(n, 32 * s + 32); ++i) m = max(m, row_ptr[i + 1] - row_ptr[i]);
+    len[s] = m;
+  }
 }
 
 // ---------------------------------------------------------------- SELL build

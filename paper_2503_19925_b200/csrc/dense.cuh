@@ -42,31 +42,65 @@ struct DenseArgs {
   double *loss_partials; // [gridDim.x]
   int32_t stages;
   int32_t side_stride;   // bytes of side data per stage
+  int32_t mode;          // POLY_MODE_*
 };
 
-// Link + residual for one row (warp-uniform z).  Lanes take bins j = lane,
-// lane+32, ...; two fp64 warp sums give h and H.  Returns r_i; accumulates
-// ℓ_i into *lacc on lane 0 when `count_loss`.
+// Link + per-row scalar for one row (warp-uniform z).  Lanes take bins
+// j = lane, lane+32, ...; fp64 warp sums give h, H (and h' for the baseline
+// modes).  Returns φ_i (mode EXACT: r_i = y_i - Ī_i h(z_i)); accumulates the
+// row's objective term into *lacc on lane 0 when `count_loss`.
+//   mode 0 EXACT  φ = y - Ī h,            ℓ_i = y z - Ī H(z)        (Eq. operator; R2)
+//   mode 1 L2     φ = 2 (Ī h - y) Ī h',   (Ī h - y)^2
+//   mode 2 L1     φ = sign(Ī h - y) Ī h', |Ī h - y|
+//   mode 3 NLL    φ = (Ī - y / h) h',     Ī h - y log(Ī h)
+// h'(z) = -Σ_j s_j μ_j e^{-μ_j z}, and 0 for z <= 0 under relu.
 template <bool LOSS>
 __device__ __forceinline__ double row_residual(const double *sp, int W, int relu, double z,
                                                double yv, double Ii, const float *srow,
-                                               bool count_loss, double *lacc) {
+                                               bool count_loss, double *lacc, int mode = 0) {
   const int lane = threadIdx.x & 31;
   const bool neg = relu && z < 0.0;
   const double zc = neg ? 0.0 : z;
   double hs = 0.0, Hs = 0.0;
+  if (mode == 0) {
+    for (int j = lane; j < W; j += 32) {
+      const double sj = srow ? (double)srow[j] : sp[j];
+      const double e = exp_nonpos(-sp[kMaxW + j] * zc);
+      hs += sj * e;
+      if (LOSS) Hs += neg ? sj * z : sj * sp[2 * kMaxW + j] * (1.0 - e);
+    }
+    hs = warp_sum(hs);
+    if (LOSS) {
+      Hs = warp_sum(Hs);
+      if (count_loss && lane == 0) *lacc += yv * z - Ii * Hs;
+    }
+    return yv - Ii * hs;
+  }
+  double hp = 0.0;  // Σ s_j μ_j e_j
   for (int j = lane; j < W; j += 32) {
     const double sj = srow ? (double)srow[j] : sp[j];
-    const double e = exp_nonpos(-sp[kMaxW + j] * zc);
+    const double e = relu ? exp_nonpos(-sp[kMaxW + j] * zc) : exp(-sp[kMaxW + j] * z);
     hs += sj * e;
-    if (LOSS) Hs += neg ? sj * z : sj * sp[2 * kMaxW + j] * (1.0 - e);
+    hp += sj * sp[kMaxW + j] * e;
   }
   hs = warp_sum(hs);
-  if (LOSS) {
-    Hs = warp_sum(Hs);
-    if (count_loss && lane == 0) *lacc += yv * z - Ii * Hs;
+  hp = -warp_sum(hp);
+  if (relu && !(z > 0.0)) hp = 0.0;
+  const double m = Ii * hs;
+  double phi, l;
+  if (mode == 1) {
+    phi = 2.0 * (m - yv) * Ii * hp;
+    l = (m - yv) * (m - yv);
+  } else if (mode == 2) {
+    const double r = m - yv;
+    phi = (r > 0.0 ? 1.0 : (r < 0.0 ? -1.0 : 0.0)) * Ii * hp;
+    l = fabs(r);
+  } else {
+    phi = (Ii - yv / hs) * hp;
+    l = m - yv * log(m);
   }
-  return yv - Ii * hs;
+  if (LOSS && count_loss && lane == 0) *lacc += l;
+  return phi;
 }
 
 __device__ __forceinline__ double load_y(const unsigned char *yb, int ytype, int r) {
@@ -291,7 +325,8 @@ __global__ void __launch_bounds__(32 * (NW + 1), 1) k_dense_loss_grad(const Dens
         const double yv = load_y(sd + yoff, a.ytype, lr);
         const double Ii = has_rowspec ? (double)((const float *)(sd + ioff))[lr] : a.I_bar;
         const float *srow = has_rowspec ? (const float *)(sd + soff) + lr * a.W : nullptr;
-        const double r = row_residual<LOSS>(sp, a.W, a.relu, zp[q], yv, Ii, srow, w == 0, &lacc);
+        const double r = row_residual<LOSS>(sp, a.W, a.relu, zp[q], yv, Ii, srow, w == 0, &lacc,
+                                             a.mode);
         const T rt = (T)r;
         const T *rowp = tile + (size_t)lr * lda + lane_off;
 #pragma unroll

@@ -32,6 +32,13 @@ struct SolveState {
   int32_t counter;     // F evaluations folded into a step so far
   int32_t bad;         // 0 or first (1-based) step counter whose iterate was non-finite
   uint32_t ticket;
+  // averaged iterate (poly_solve_ex): x̄_k over iterates ⌈k/2⌉..k
+  int32_t k;           // index of the last iterate folded into the window sum
+  int32_t stopped;     // 1 once ||x̄_k - x̄_{k-1}|| <= tol (k >= 2)
+  int32_t k_stop;
+  int32_t pad;
+  double tol;
+  double move;
 };
 
 struct FinArgs {
@@ -233,6 +240,76 @@ __global__ void __launch_bounds__(256) k_fin_apply(const FinArgs a) {
       if (!isfinite(nrm) && s->bad == 0) s->bad = k + 1;
     } else if (!isfinite(nrm) && s->bad == 0) {
       s->bad = -1;
+    }
+  }
+}
+
+// ------------------------------------------------------------ averaged iterate
+// x̄_k = mean of iterates x_{⌈k/2⌉..k} (SPEC.md:357 window,
+// reading R15), maintained as a window sum S: after x_k arrives,
+//   S += x_k,  and for odd k (⌈k/2⌉ grows by one) S -= x_{(k-1)/2},
+// with the iterates kept in a ring hist[cap][d], cap > k/2 + 1.  The stop rule
+// ||x̄_k - x̄_{k-1}||_2 <= tol is decided in k_avg_b.  Once
+// stopped, both kernels are no-ops, so iterations the host launched past the
+// stop leave x̄, the ring and the state untouched.
+struct AvgArgs {
+  const double *x;      // [d] the new iterate x_k
+  double *hist;         // [cap][d]
+  double *S;            // [d] window sum
+  double *xbar;         // [d] x̄_{k-1} in, x̄_k out
+  double *block_norm;   // [ceil(d/256)]
+  int32_t d;
+  int32_t cap;
+  SolveState *state;
+};
+
+__global__ void __launch_bounds__(256) k_avg_a(const AvgArgs a) {
+  __shared__ double wsum[8];
+  pdl_wait();
+  pdl_trigger();
+  if (a.state->stopped) return;
+  const int k = a.state->k + 1;
+  const int lo = (k + 1) / 2;  // ⌈k/2⌉
+  const double cnt = (double)(k - lo + 1);
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  double q = 0.0;
+  if (c < a.d) {
+    const double xk = a.x[c];
+    double s = a.S[c] + xk;
+    if (k & 1) s -= a.hist[(size_t)(((k - 1) / 2) % a.cap) * a.d + c];
+    a.hist[(size_t)(k % a.cap) * a.d + c] = xk;
+    a.S[c] = s;
+    const double xb = s / cnt;
+    const double df = xb - a.xbar[c];
+    a.xbar[c] = xb;
+    q = df * df;
+  }
+  q = warp_sum(q);
+  if ((threadIdx.x & 31) == 0) wsum[threadIdx.x >> 5] = q;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += wsum[w];
+    a.block_norm[blockIdx.x] = t;
+  }
+}
+
+__global__ void __launch_bounds__(32) k_avg_b(const AvgArgs a, int32_t nblocks) {
+  pdl_wait();
+  pdl_trigger();
+  SolveState *s = a.state;
+  if (s->stopped) return;
+  double q = 0.0;
+  for (int b = threadIdx.x; b < nblocks; b += 32) q += a.block_norm[b];
+  q = warp_sum(q);
+  if (threadIdx.x == 0) {
+    const int k = s->k + 1;
+    const double mv = sqrt(q);
+    s->k = k;
+    s->move = mv;
+    if (k >= 2 && mv <= s->tol) {
+      s->stopped = 1;
+      s->k_stop = k;
     }
   }
 }

@@ -122,8 +122,8 @@ const DenseVariant kDenseF64[] = {
 };
 
 const void *kCsrFwd[2][2] = {
-    {(const void *)&k_csr_forward<float, false>, (const void *)&k_csr_forward<float, true>},
-    {(const void *)&k_csr_forward<double, false>, (const void *)&k_csr_forward<double, true>},
+    {(const void *)&k_sell_forward<float, false>, (const void *)&k_sell_forward<float, true>},
+    {(const void *)&k_sell_forward<double, false>, (const void *)&k_sell_forward<double, true>},
 };
 const void *kCscBwd[2] = {(const void *)&k_csc_backward<float>,
                           (const void *)&k_csc_backward<double>};
@@ -138,6 +138,25 @@ __global__ void k_min_i32(const int32_t *y, int64_t n, int32_t *out) {
        i += (int64_t)gridDim.x * blockDim.x)
     m = min(m, y[i]);
   if (m < 0) atomicMin(out, m);
+}
+
+__global__ void k_sum_windows(const void *y, int ytype, int Om, int64_t n, void *out,
+                              int32_t *overflow) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    if (ytype == POLY_Y_I32) {
+      int64_t t = 0;
+      for (int w = 0; w < Om; ++w) t += ((const int32_t *)y)[(size_t)w * n + i];
+      if (t > INT32_MAX) atomicOr(overflow, 1);
+      ((int32_t *)out)[i] = (int32_t)t;
+    } else {
+      double t = 0.0;
+      for (int w = 0; w < Om; ++w)
+        t += ytype == POLY_Y_F32 ? (double)((const float *)y)[(size_t)w * n + i]
+                                 : ((const double *)y)[(size_t)w * n + i];
+      ((double *)out)[i] = t;
+    }
+  }
 }
 
 __global__ void k_iota(int32_t *v, int64_t n) {
@@ -181,6 +200,8 @@ struct poly_handle {
   poly_problem p{};
   int dev = 0, sms = 0;
   int elsize = 4, ysz = 4;
+  int Om = 1;          // detector windows (folded into one spectrum at init)
+  int64_t n_norm = 1;  // the n of Eq.(operator): Ω n_global
   cudaStream_t user = nullptr, work = nullptr;
   cudaEvent_t ev_in = nullptr, ev_out = nullptr;
   std::vector<void *> owned;  // library-owned device buffers
@@ -190,12 +211,15 @@ struct poly_handle {
   int full = 0;
   int k1_grid = 0, k1_threads = 0, k1_stages = 0, k1_side = 0;
   size_t k1_smem = 0;
-  int k4_grid = 0;                     // K4f blocks (= loss partials)
+  int k4_grid = 0;                     // K4f blocks: 32-row SELL slices of A (= loss partials)
+  void *sell_rows = nullptr;           // CscEnt<T>[row_slice_off[k4_grid] * 32]: {col, val}
+  int64_t *row_slice_off = nullptr;    // [k4_grid + 1]
   int nslices = 0;                     // K4b blocks: 32-column SELL slices of A^T
   void *sell = nullptr;                // CscEnt<T>[slice_off[nslices] * 32]
   int64_t *slice_off = nullptr;        // [nslices + 1] slice start, in 32-entry steps
   float *rbuf = nullptr;               // [n_local] residuals between K4f and K4b
   int64_t sell_steps = 0;              // slice_off[nslices]
+  int64_t sell_row_steps = 0;          // row_slice_off[k4_grid]
   int fin_split = 0;
   // workspaces
   int G = 0;  // partial rows
@@ -207,6 +231,10 @@ struct poly_handle {
   int fin_grid = 0;
   bool pdl = true, use_graph = true;
   cudaGraphExec_t gexec[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};  // [loss][U>1]
+  cudaGraphExec_t gexec_ex[2][2][2] = {};  // poly_solve_ex: [method][average][U>1]
+  // averaged iterate workspaces (allocated on first use)
+  double *hist = nullptr, *Ssum = nullptr, *xbar = nullptr, *avg_norm = nullptr;
+  int avg_cap = 0;
   int graph_U = 8;
   ncclComm_t nccl = nullptr;
   bool comm_path = false;  // world > 1 or POLY_FLAG_COMM: reduce -> allreduce -> step
@@ -289,6 +317,7 @@ int enqueue_pass(poly_handle *h, const double *x, bool loss) {
     a.partials = h->partials;
     a.loss_partials = h->loss_partials;
     a.stages = h->k1_stages;
+    a.mode = p.mode;
     a.side_stride = h->k1_side;
     return launch(h, h->dv->fn[h->full][loss ? 1 : 0], dim3(h->k1_grid), dim3(h->k1_threads), h->k1_smem,
                   true, a);
@@ -308,8 +337,10 @@ int enqueue_pass(poly_handle *h, const double *x, bool loss) {
   a.x = x;
   a.spec = h->spec;
   a.r = h->rbuf;
+  a.mode = p.mode;
   a.loss_partials = h->loss_partials;
-  TRY(launch(h, kCsrFwd[p.dtype][loss ? 1 : 0], dim3(h->k4_grid), dim3(256), 0, true, a));
+  TRY(launch(h, kCsrFwd[p.dtype][loss ? 1 : 0], dim3(h->k4_grid), dim3(128), 0, true,
+             (const void *)h->sell_rows, (const int64_t *)h->row_slice_off, a));
   int32_t d32 = (int32_t)p.d;
   const float *rb = h->rbuf;
   double *gp = h->partials;
@@ -328,7 +359,7 @@ FinArgs fin_base(poly_handle *h, int mode) {
   f.GL = h->p.layout == POLY_CSR ? h->k4_grid : h->G;
   f.split = h->fin_split;
   f.set = h->p.set;
-  f.n_norm = h->p.n_global;
+  f.n_norm = h->n_norm;
   f.partials = h->partials;
   f.loss_partials = h->loss_partials;
   f.comm = h->comm;
@@ -388,6 +419,55 @@ int enqueue_eval(poly_handle *h, const double *x, bool loss, bool step, const do
 int enqueue_iteration(poly_handle *h, bool loss) {
   TRY(enqueue_eval(h, h->xa, loss, true, h->xa, h->xh, nullptr));
   return enqueue_eval(h, h->xh, loss, true, h->xa, h->xa, nullptr);
+}
+
+AvgArgs avg_args(poly_handle *h) {
+  AvgArgs a{};
+  a.x = h->xa;
+  a.hist = h->hist;
+  a.S = h->Ssum;
+  a.xbar = h->xbar;
+  a.block_norm = h->avg_norm;
+  a.d = (int32_t)h->p.d;
+  a.cap = h->avg_cap;
+  a.state = h->state;
+  return a;
+}
+
+int enqueue_avg(poly_handle *h) {
+  ProfScope ps(h, 1);
+  const AvgArgs a = avg_args(h);
+  const int nb = (int)((h->p.d + 255) / 256);
+  TRY(launch(h, (const void *)&k_avg_a, dim3(nb), dim3(256), 0, true, a));
+  return launch(h, (const void *)&k_avg_b, dim3(1), dim3(32), 0, true, a, (int32_t)nb);
+}
+
+// one iteration of poly_solve_ex: EXACT (2 passes) or projected GD (1 pass)
+// on the internal iterate xa, then the averaged-iterate update
+int enqueue_iteration_ex(poly_handle *h, int method, bool average) {
+  if (method == POLY_METHOD_EXTRAGRADIENT)
+    TRY(enqueue_iteration(h, false));
+  else
+    TRY(enqueue_eval(h, h->xa, false, true, h->xa, h->xa, nullptr));
+  if (average) TRY(enqueue_avg(h));
+  return POLY_OK;
+}
+
+int build_graph_ex(poly_handle *h, int method, bool average, int U, cudaGraphExec_t *out) {
+  cudaGraph_t g = nullptr;
+  CK(cudaStreamBeginCapture(h->work, cudaStreamCaptureModeThreadLocal));
+  int rc = POLY_OK;
+  for (int u = 0; u < U && rc == POLY_OK; ++u) rc = enqueue_iteration_ex(h, method, average);
+  cudaError_t e = cudaStreamEndCapture(h->work, &g);
+  if (rc != POLY_OK) {
+    if (g) cudaGraphDestroy(g);
+    return rc;
+  }
+  if (e != cudaSuccess) return fail(POLY_ECUDA, "graph capture: %s", cudaGetErrorString(e));
+  e = cudaGraphInstantiate(out, g, 0);
+  cudaGraphDestroy(g);
+  if (e != cudaSuccess) return fail(POLY_ECUDA, "graph instantiate: %s", cudaGetErrorString(e));
+  return POLY_OK;
 }
 
 int build_graph(poly_handle *h, bool loss, int U, cudaGraphExec_t *out) {
@@ -451,14 +531,26 @@ int validate(const poly_problem *p) {
   if (p->W < 1) return fail(POLY_EINVAL, "W < 1 (SPEC.md:28)");
   if (p->W > kMaxW) return fail(POLY_EUNSUPPORTED, "W > %d", kMaxW);
   if (!p->s || !p->mu) return fail(POLY_EINVAL, "spectrum pointers are NULL");
-  double tot = 0.0;
-  for (int j = 0; j < p->W; ++j) {
-    if (!(p->s[j] > 0.0 && p->s[j] <= 1.0)) return fail(POLY_EINVAL, "s[%d] not in (0,1] (SPEC.md:25)", j);
-    if (!(p->mu[j] > 0.0) || !std::isfinite(p->mu[j])) return fail(POLY_EINVAL, "mu[%d] must be > 0 (SPEC.md:26)", j);
-    tot += p->s[j];
+  if (p->windows < 0) return fail(POLY_EINVAL, "windows < 0");
+  const int Om = p->windows > 1 ? p->windows : 1;
+  if (Om > 1 && !p->I_win) return fail(POLY_EINVAL, "windows > 1 needs I_win");
+  for (int w = 0; w < Om; ++w) {
+    double tot = 0.0;
+    for (int j = 0; j < p->W; ++j) {
+      const double sj = p->s[(size_t)w * p->W + j];
+      if (!(sj > 0.0 && sj <= 1.0)) return fail(POLY_EINVAL, "s[%d] of window %d not in (0,1] (SPEC.md:25)", j, w);
+      tot += sj;
+    }
+    if (std::fabs(tot - 1.0) > 1e-12) return fail(POLY_EINVAL, "window %d: sum_j s_j = %.17g != 1 (SPEC.md:25)", w, tot);
+    if (Om > 1 && (!(p->I_win[w] > 0.0) || !std::isfinite(p->I_win[w])))
+      return fail(POLY_EINVAL, "I_win[%d] must be > 0", w);
   }
-  if (std::fabs(tot - 1.0) > 1e-12) return fail(POLY_EINVAL, "sum_j s_j = %.17g != 1 (SPEC.md:25)", tot);
-  if (!(p->I_bar > 0.0) || !std::isfinite(p->I_bar)) return fail(POLY_EINVAL, "I_bar must be > 0 (SPEC.md:27)");
+  for (int j = 0; j < p->W; ++j)
+    if (!(p->mu[j] > 0.0) || !std::isfinite(p->mu[j])) return fail(POLY_EINVAL, "mu[%d] must be > 0 (SPEC.md:26)", j);
+  if (Om == 1 && (!(p->I_bar > 0.0) || !std::isfinite(p->I_bar))) return fail(POLY_EINVAL, "I_bar must be > 0 (SPEC.md:27)");
+  if (p->mode < POLY_MODE_EXACT || p->mode > POLY_MODE_NLL) return fail(POLY_EINVAL, "bad mode");
+  if (Om > 1 && (p->mode != POLY_MODE_EXACT || p->s_row))
+    return fail(POLY_EUNSUPPORTED, "windows > 1 needs mode EXACT and no per-row spectra");
   if ((p->s_row == nullptr) != (p->I_row == nullptr)) return fail(POLY_EINVAL, "s_row and I_row must both be given or both NULL");
   if (p->relu != 0 && p->relu != 1) return fail(POLY_EINVAL, "relu must be 0 or 1");
   if (p->set < POLY_SET_NONE || p->set > POLY_SET_NONNEG_BALL) return fail(POLY_EINVAL, "bad set");
@@ -605,6 +697,31 @@ int build_sell_t(poly_handle *h) {
                                       nnz, ent);
   h->sell = ent;
   h->sell_steps = steps;
+  // SELL-32 of A (row slices) for K4f
+  const int64_t nrs = h->k4_grid;
+  TRY(dev_alloc(h, &h->row_slice_off, (size_t)nrs + 1));
+  int64_t *rlen = nullptr;
+  if ((rc = talloc((size_t)(nrs + 1) * 8, (void **)&rlen))) return done(rc);
+  size_t tb4 = 0;
+  cub::DeviceScan::ExclusiveSum(nullptr, tb4, rlen, h->row_slice_off, (int)nrs + 1, st);
+  void *tstore2 = nullptr;
+  if ((rc = talloc(tb4, &tstore2))) return done(rc);
+  cudaMemsetAsync(rlen, 0, (size_t)(nrs + 1) * 8, st);
+  if (p.n_local > 0) k_row_slice_len<<<(int)std::min<int64_t>(4096, (nrs + 255) / 256), 256, 0, st>>>(
+      p.row_ptr, p.n_local, nrs, rlen);
+  cub::DeviceScan::ExclusiveSum(tstore2, tb4, rlen, h->row_slice_off, (int)nrs + 1, st);
+  int64_t rsteps = 0;
+  cudaMemcpyAsync(&rsteps, h->row_slice_off + nrs, 8, cudaMemcpyDeviceToHost, st);
+  if (cudaStreamSynchronize(st) != cudaSuccess)
+    return done(fail(POLY_ECUDA, "SELL build: %s", cudaGetErrorString(cudaGetLastError())));
+  CscEnt<T> *rent = nullptr;
+  if ((rc = dev_alloc(h, &rent, (size_t)std::max<int64_t>(1, rsteps) * 32))) return done(rc);
+  cudaMemsetAsync(rent, 0, (size_t)std::max<int64_t>(1, rsteps) * 32 * sizeof(CscEnt<T>), st);
+  if (p.n_local > 0)
+    k_sell_rows_fill<T><<<g, 256, 0, st>>>(p.row_ptr, p.col, (const T *)p.val, p.n_local,
+                                           h->row_slice_off, rent);
+  h->sell_rows = rent;
+  h->sell_row_steps = rsteps;
   if (cudaStreamSynchronize(st) != cudaSuccess)
     return done(fail(POLY_ECUDA, "SELL build: %s", cudaGetErrorString(cudaGetLastError())));
   return done(POLY_OK);
@@ -639,6 +756,10 @@ void poly_free(poly_handle *h) {
   for (auto &a : h->gexec)
     for (auto &g : a)
       if (g) cudaGraphExecDestroy(g);
+  for (auto &a : h->gexec_ex)
+    for (auto &b : a)
+      for (auto &g : b)
+        if (g) cudaGraphExecDestroy(g);
   if (h->nccl) {
     NcclApi *api = nccl_api();
     if (api) api->commDestroy(h->nccl);
@@ -671,6 +792,8 @@ int poly_init(const poly_problem *pin, poly_handle **out) {
     return fail(POLY_ECUDA, "no CUDA device available");
   }
   h->elsize = p.dtype == POLY_F32 ? 4 : 8;
+  h->Om = p.windows > 1 ? p.windows : 1;
+  h->n_norm = (int64_t)h->Om * p.n_global;
   h->ysz = p.ytype == POLY_Y_F64 ? 8 : 4;
   h->user = (cudaStream_t)p.stream;
   h->pdl = !(p.flags & POLY_FLAG_NO_PDL);
@@ -694,7 +817,7 @@ int poly_init(const poly_problem *pin, poly_handle **out) {
       p.row_ptr = (const int64_t *)rp;
       p.col = (const int32_t *)cl;
     }
-    if ((rc = copy_in(h, &p.y, n * h->ysz)) != POLY_OK) return bail(rc);
+    if ((rc = copy_in(h, &p.y, n * h->ysz * (size_t)h->Om)) != POLY_OK) return bail(rc);
     const void *sr = p.s_row, *ir = p.I_row;
     if ((rc = copy_in(h, &sr, n * p.W * 4)) != POLY_OK) return bail(rc);
     if ((rc = copy_in(h, &ir, n * 4)) != POLY_OK) return bail(rc);
@@ -703,9 +826,25 @@ int poly_init(const poly_problem *pin, poly_handle **out) {
   }
 
   // spectrum [s | mu | 1/mu] and centre
+  // Ω windows share a_i and μ_j, so Σ_ω [y_ωi - Ī_ω h_ω(z)] = y_i^Σ - Ī_Σ h̃(z) with
+  // Ī_Σ = Σ_ω Ī_ω, s̃_j = Σ_ω Ī_ω s_ωj / Ī_Σ, y^Σ = Σ_ω y_ω: one link of W bins
+  // per row; the loss is linear in y too.
+  std::vector<double> s_eff(p.W, 0.0);
+  if (h->Om == 1) {
+    for (int j = 0; j < p.W; ++j) s_eff[j] = p.s[j];
+  } else {
+    double It = 0.0;
+    for (int w = 0; w < h->Om; ++w) It += p.I_win[w];
+    for (int j = 0; j < p.W; ++j) {
+      double c = 0.0;
+      for (int w = 0; w < h->Om; ++w) c += p.I_win[w] * p.s[(size_t)w * p.W + j];
+      s_eff[j] = c / It;
+    }
+    p.I_bar = It;
+  }
   std::vector<double> spec(3 * kMaxW, 0.0);
   for (int j = 0; j < p.W; ++j) {
-    spec[j] = p.s[j];
+    spec[j] = s_eff[j];
     spec[kMaxW + j] = p.mu[j];
     spec[2 * kMaxW + j] = 1.0 / p.mu[j];
   }
@@ -717,7 +856,7 @@ int poly_init(const poly_problem *pin, poly_handle **out) {
     if (cudaMemcpy(h->center, p.center, p.d * 8, cudaMemcpyHostToDevice) != cudaSuccess)
       return bail(fail(POLY_ECUDA, "centre upload failed"));
   }
-  p.s = p.mu = p.center = nullptr;  // host copies are not kept
+  p.s = p.mu = p.center = p.I_win = nullptr;  // host copies are not kept
 
   // tile configuration and workspaces
   if (p.layout == POLY_DENSE) {
@@ -726,8 +865,7 @@ int poly_init(const poly_problem *pin, poly_handle **out) {
     if ((rc = dev_alloc(h, &h->loss_partials, (size_t)h->G)) != POLY_OK) return bail(rc);
   } else {
     h->G = 1;
-    const int64_t warps = std::max<int64_t>(1, p.n_local);
-    h->k4_grid = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)h->sms * 8, (warps + 7) / 8));
+    h->k4_grid = (int)std::max<int64_t>(1, (p.n_local + 31) / 32);
     if ((rc = dev_alloc(h, &h->partials, (size_t)p.d)) != POLY_OK) return bail(rc);
     if ((rc = dev_alloc(h, &h->loss_partials, (size_t)h->k4_grid)) != POLY_OK) return bail(rc);
     if ((rc = dev_alloc(h, &h->rbuf, (size_t)std::max<int64_t>(1, p.n_local))) != POLY_OK) return bail(rc);
@@ -757,8 +895,8 @@ int poly_init(const poly_problem *pin, poly_handle **out) {
     int32_t hv = 0;
     cudaMemsetAsync(flag, 0, 4, h->work);
     if (p.ytype == POLY_Y_I32) {
-      k_min_i32<<<std::min<int64_t>(1024, (p.n_local + 255) / 256), 256, 0, h->work>>>(
-          (const int32_t *)p.y, p.n_local, flag);
+      k_min_i32<<<std::min<int64_t>(1024, (p.n_local * h->Om + 255) / 256), 256, 0, h->work>>>(
+          (const int32_t *)p.y, p.n_local * h->Om, flag);
       cudaMemcpyAsync(&hv, flag, 4, cudaMemcpyDeviceToHost, h->work);
       if (cudaStreamSynchronize(h->work) != cudaSuccess)
         return bail(fail(POLY_ECUDA, "count check failed: %s", cudaGetErrorString(cudaGetLastError())));
@@ -774,6 +912,25 @@ int poly_init(const poly_problem *pin, poly_handle **out) {
     }
   }
   if (p.layout == POLY_CSR && (rc = build_sell(h)) != POLY_OK) return bail(rc);
+  if (h->Om > 1 && p.n_local > 0) {  // y^Σ_i = Σ_ω y_ωi (ω ascending), library-owned
+    const bool ints = p.ytype == POLY_Y_I32;
+    void *ys = nullptr;
+    if ((rc = dev_alloc(h, (unsigned char **)&ys, (size_t)p.n_local * (ints ? 4 : 8))) != POLY_OK)
+      return bail(rc);
+    int32_t *flag = nullptr;
+    if ((rc = dev_alloc(h, &flag, 1)) != POLY_OK) return bail(rc);
+    int32_t hv = 0;
+    cudaMemsetAsync(flag, 0, 4, h->work);
+    k_sum_windows<<<std::min<int64_t>(4096, (p.n_local + 255) / 256), 256, 0, h->work>>>(
+        p.y, p.ytype, h->Om, p.n_local, ys, flag);
+    cudaMemcpyAsync(&hv, flag, 4, cudaMemcpyDeviceToHost, h->work);
+    if (cudaStreamSynchronize(h->work) != cudaSuccess)
+      return bail(fail(POLY_ECUDA, "window sum failed: %s", cudaGetErrorString(cudaGetLastError())));
+    if (hv) return bail(fail(POLY_EUNSUPPORTED, "sum of window counts exceeds int32"));
+    p.y = ys;
+    p.ytype = ints ? POLY_Y_I32 : POLY_Y_F64;
+    h->ysz = ints ? 4 : 8;
+  }
 
   h->comm_path = p.world > 1 || (p.flags & POLY_FLAG_COMM);
   if (h->comm_path) {
@@ -817,6 +974,148 @@ int poly_loss_grad(poly_handle *h, const double *x, double *g, double *loss) {
   }
   TRY(sync_out(h));
   CK(cudaGetLastError());
+  return POLY_OK;
+}
+
+int poly_solve_ex(poly_handle *h, const poly_solve_opts *o, double *x, double *x_last,
+                  poly_solve_info *info) {
+  if (!h || !o || !x) return fail(POLY_EINVAL, "NULL handle, opts or x");
+  if (o->T_max < 0) return fail(POLY_EINVAL, "T_max < 0");
+  if (o->method != POLY_METHOD_EXTRAGRADIENT && o->method != POLY_METHOD_GD)
+    return fail(POLY_EINVAL, "bad method");
+  if (!(o->gamma > 0.0) || !std::isfinite(o->gamma)) return fail(POLY_EINVAL, "gamma must be > 0");
+  if (!(o->tol >= 0.0)) return fail(POLY_EINVAL, "tol must be >= 0");
+  if (info) memset(info, 0, sizeof(*info));
+  const int d = (int)h->p.d;
+  const bool avg = o->average != 0;
+  const int method = o->method;
+  TRY(sync_in(h));
+  const bool x_dev = is_device_ptr(x);
+  CK(cudaMemcpyAsync(h->xa, x, (size_t)d * 8, x_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice,
+                     h->work));
+  if (avg) {
+    const int cap = (o->T_max + 1) / 2 + 3;
+    if (cap > h->avg_cap) {
+      // graphs captured with the old ring baked in must be rebuilt
+      for (auto &a : h->gexec_ex)
+        for (auto &g : a[1])
+          if (g) {
+            cudaGraphExecDestroy(g);
+            g = nullptr;
+          }
+      TRY(dev_alloc(h, &h->hist, (size_t)cap * d));
+      if (!h->Ssum) {
+        TRY(dev_alloc(h, &h->Ssum, (size_t)d));
+        TRY(dev_alloc(h, &h->xbar, (size_t)d));
+        TRY(dev_alloc(h, &h->avg_norm, (size_t)(d + 255) / 256));
+      }
+      h->avg_cap = cap;
+    }
+    CK(cudaMemsetAsync(h->hist, 0, (size_t)d * 8, h->work));  // slot 0: "x_0" = 0
+    CK(cudaMemsetAsync(h->Ssum, 0, (size_t)d * 8, h->work));
+    CK(cudaMemsetAsync(h->xbar, 0, (size_t)d * 8, h->work));
+  }
+  SolveState st{};
+  st.gamma = o->gamma;
+  st.tol = o->tol;
+  *h->hstate = st;
+  CK(cudaMemcpyAsync(h->state, h->hstate, sizeof(SolveState), cudaMemcpyHostToDevice, h->work));
+  h->prof = (o->flags & POLY_SOLVE_PROFILE) != 0;
+  h->recs.clear();
+  h->evused = 0;
+  {
+    FinArgs f = fin_base(h, FIN_PROJECT);  // x_1 = P_X(x_in)
+    f.anchor = h->xa;
+    f.x_out = h->xa;
+    TRY(enqueue_fin(h, f));
+  }
+  if (avg) TRY(enqueue_avg(h));  // folds x_1: S = x_1, x̄_1 = x_1, k = 1
+  const int T = o->T_max;
+  const bool poll = avg && o->tol > 0.0;
+  int done = 0;
+  if (h->use_graph && !h->prof) {
+    const int U = h->graph_U;
+    cudaGraphExec_t *gU = &h->gexec_ex[method][avg ? 1 : 0][1];
+    cudaGraphExec_t *g1 = &h->gexec_ex[method][avg ? 1 : 0][0];
+    int rc = POLY_OK;
+    if (T >= U && !*gU) rc = build_graph_ex(h, method, avg, U, gU);
+    if (rc == POLY_OK && (T % U) && !*g1) rc = build_graph_ex(h, method, avg, 1, g1);
+    if (rc != POLY_OK) return rc;
+    SolveState *snap = h->hstate;  // pinned; copied after every launch, read one launch behind
+    cudaEvent_t ev[2] = {nullptr, nullptr};
+    if (poll)
+      for (auto &e : ev) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    int launches = 0;
+    bool stop = false;
+    while (done < T && !stop) {
+      const int step = (T - done >= U) ? U : 1;
+      CK(cudaGraphLaunch(step == U ? *gU : *g1, h->work));
+      done += step;
+      if (poll) {
+        if (launches >= 1) {
+          CK(cudaEventSynchronize(ev[(launches - 1) & 1]));
+          if (snap->stopped) stop = true;
+        }
+        CK(cudaMemcpyAsync(snap, h->state, sizeof(SolveState), cudaMemcpyDeviceToHost, h->work));
+        CK(cudaEventRecord(ev[launches & 1], h->work));
+        ++launches;
+      }
+    }
+    CK(cudaStreamSynchronize(h->work));
+    for (auto &e : ev)
+      if (e) cudaEventDestroy(e);
+  } else {
+    for (; done < T; ++done) {
+      TRY(enqueue_iteration_ex(h, method, avg));
+      if (poll && (done % 64) == 63) {
+        CK(cudaMemcpyAsync(h->hstate, h->state, sizeof(SolveState), cudaMemcpyDeviceToHost, h->work));
+        CK(cudaStreamSynchronize(h->work));
+        if (h->hstate->stopped) {
+          ++done;
+          break;
+        }
+      }
+    }
+  }
+  CK(cudaMemcpyAsync(h->hstate, h->state, sizeof(SolveState), cudaMemcpyDeviceToHost, h->work));
+  CK(cudaStreamSynchronize(h->work));
+  const SolveState fin = *h->hstate;
+  const bool stopped = avg && fin.stopped;
+  const double *last = stopped ? h->hist + (size_t)(fin.k_stop % h->avg_cap) * d : h->xa;
+  const double *outv = avg ? h->xbar : h->xa;
+  CK(cudaMemcpyAsync(x, outv, (size_t)d * 8, x_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost,
+                     h->work));
+  if (x_last)
+    CK(cudaMemcpyAsync(x_last, last, (size_t)d * 8,
+                       is_device_ptr(x_last) ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, h->work));
+  CK(cudaStreamSynchronize(h->work));
+  if (h->prof) {
+    double sum[3] = {0, 0, 0};
+    int cnt[3] = {0, 0, 0};
+    for (auto &r : h->recs) {
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, r.a, r.b);
+      sum[r.kind] += ms;
+      cnt[r.kind]++;
+    }
+    for (int k = 0; k < 3; ++k) h->ktimes[k] = cnt[k] ? sum[k] / cnt[k] : 0.0;
+    h->ktimes[3] = cnt[0];
+    h->ktimes[4] = cnt[0] + cnt[1];
+    h->prof = false;
+  }
+  TRY(sync_out(h));
+  CK(cudaGetLastError());
+  const int per = method == POLY_METHOD_EXTRAGRADIENT ? 2 : 1;
+  if (info) {
+    info->stopped = stopped ? 1 : 0;
+    info->iters = stopped ? fin.k_stop - 1 : done;
+    info->move = avg ? fin.move : 0.0;
+  }
+  if (fin.bad != 0) {
+    const int b = fin.bad > 0 ? (fin.bad + per - 1) / per : 0;
+    if (info) info->bad_iter = b;
+    return fail(POLY_ENONFINITE, "non-finite iterate at iteration %d", b);
+  }
   return POLY_OK;
 }
 
@@ -991,8 +1290,8 @@ int poly_describe(poly_handle *h, int64_t *out, int32_t nout) {
     v[3] = h->k1_stages;
     v[4] = (int64_t)h->k1_smem;
   } else {
-    v[0] = h->k4_grid;   // K4f blocks (K4b: one 128-thread block per 32-column slice)
-    v[1] = 256;
+    v[0] = h->k4_grid;   // K4f blocks (32-row slices); K4b: one block per 32-column slice
+    v[1] = 128;
     v[2] = h->nslices;
     v[3] = h->sell_steps;
     v[4] = 0;

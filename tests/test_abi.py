@@ -89,6 +89,8 @@ def _problem(**kw):
     (dict(world=2), 1), (dict(rank=1), 1), (dict(lda=7), 1), (dict(lda=10), 1), (dict(A=0x1004), 1),
     (dict(n_global=5), 1), (dict(d=0), 1), (dict(y=0), 1), (dict(W=65, s=[1.0 / 65] * 65, mu=[1.0] * 65), 6),
     (dict(layout=1, row_ptr=0), 1), (dict(s_row=0x4000), 1), (dict(relu=2), 1),
+    (dict(mode=4), 1), (dict(mode=-1), 1), (dict(windows=-1), 1), (dict(windows=2), 1),
+    (dict(flags=8), 1),
 ])
 def test_init_validation(built, kw, code):
     import paper_2503_19925_b200 as P
@@ -98,6 +100,22 @@ def test_init_validation(built, kw, code):
     assert rc == code, P.poly_last_error()
     assert h.value is None
     assert P.poly_last_error()
+
+
+def test_windows_validation(built):
+    """Ω = 2 windows: s is [Ω*W]; each window must be a spectrum; I_win > 0;
+    baseline modes and per-row spectra are not supported with windows."""
+    import paper_2503_19925_b200 as P
+    L = P.lib()
+    for s, I, mode, code in [([0.25, 0.75, 0.5, 0.6], (1.0, 2.0), 0, 1),
+                             ([0.25, 0.75, 0.5, 0.5], (1.0, 0.0), 0, 1),
+                             ([0.25, 0.75, 0.5, 0.5], (1.0, 2.0), 1, 6)]:
+        p = _problem()
+        sa = (C.c_double * 4)(*s)
+        ia = (C.c_double * 2)(*I)
+        p.s, p.W, p.windows, p.I_win, p.mode = C.addressof(sa), 2, 2, C.addressof(ia), mode
+        h = C.c_void_p()
+        assert L.poly_init(C.byref(p), C.byref(h)) == code, P.poly_last_error()
 
 
 def test_reparameterize_validation(built):
@@ -113,8 +131,9 @@ def test_reparameterize_validation(built):
 
 def test_abi_version_and_null_handle(built):
     import paper_2503_19925_b200 as P
-    assert P.poly_abi_version() == 1
+    assert P.poly_abi_version() == 2
     assert P.lib().poly_loss_grad(None, None, None, None) == P.POLY_EINVAL
+    assert P.lib().poly_solve_ex(None, None, None, None, None) == P.POLY_EINVAL
     assert P.lib().poly_solve(None, None, 1, 1.0, 0, None, None) == P.POLY_EINVAL
     P.poly_free(None)
 
