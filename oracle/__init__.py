@@ -74,6 +74,16 @@ def lib():
         _lib.oracle_objective.argtypes = [P, C.c_int, dp, dp, dp]
         _lib.oracle_solve_gd.restype = C.c_int
         _lib.oracle_solve_gd.argtypes = [P, C.c_int, C.c_int, C.c_double, dp]
+        _lib.oracle_tv_norm.restype = C.c_double
+        _lib.oracle_tv_norm.argtypes = [C.c_int, dp]
+        _lib.oracle_prox_tv.restype = C.c_int
+        _lib.oracle_prox_tv.argtypes = [C.c_int, dp, C.c_double, C.c_double, C.c_int, dp, dp]
+        _lib.oracle_project_tv.restype = C.c_int
+        _lib.oracle_project_tv.argtypes = [C.c_int, dp, C.c_double, C.c_double, C.c_double,
+                                           C.c_int, dp]
+        _lib.oracle_project_tv_nonneg.restype = C.c_int
+        _lib.oracle_project_tv_nonneg.argtypes = [C.c_int, dp, C.c_double, C.c_double, C.c_double,
+                                                  C.c_int, C.c_double, C.c_int, dp]
         _lib.oracle_set_threads.argtypes = [C.c_int]
         _lib.oracle_max_threads.restype = C.c_int
     return _lib
@@ -251,6 +261,44 @@ def average(hist, k):
     out = np.zeros(hist.shape[1])
     lib().oracle_average(_dp(hist), int(k), hist.shape[1], _dp(out))
     return out
+
+
+def _side(z):
+    z = _f64(z)
+    side = int(round(np.sqrt(z.shape[0])))
+    assert side * side == z.shape[0], "TV needs a square image"
+    return z, side
+
+
+def tv_norm(x):
+    """Anisotropic TV of a square image (row-major)."""
+    x, side = _side(np.ravel(x))
+    return float(lib().oracle_tv_norm(side, _dp(x)))
+
+
+def prox_tv(z, lam, rtol=1e-6, max_it=5000):
+    """argmin ||x - z||^2 + lam ||x||_TV: (x, u, iterations)."""
+    z, side = _side(np.ravel(z))
+    x = np.zeros_like(z)
+    u = np.zeros(max(1, 2 * side * (side - 1)))
+    it = lib().oracle_prox_tv(side, _dp(z), float(lam), float(rtol), int(max_it), _dp(x), _dp(u))
+    return x, u[:2 * side * (side - 1)], int(it)
+
+
+def project_tv(z, tau, tv_tol=0.01, rtol=1e-6, max_it=5000):
+    z, side = _side(np.ravel(z))
+    x = np.zeros_like(z)
+    steps = lib().oracle_project_tv(side, _dp(z), float(tau), float(tv_tol), float(rtol),
+                                    int(max_it), _dp(x))
+    return x, int(steps)
+
+
+def project_tv_nonneg(z, tau, tv_tol=0.01, rtol=1e-6, max_it=5000, tol=1e-4, max_outer=100000):
+    z, side = _side(np.ravel(z))
+    x = np.zeros_like(z)
+    it = lib().oracle_project_tv_nonneg(side, _dp(z), float(tau), float(tv_tol), float(rtol),
+                                        int(max_it), float(tol), int(max_outer), _dp(x))
+    return x, int(it)
 
 
 def reparam(s, mu, I_bar, b, clamp=1):

@@ -483,3 +483,180 @@ int oracle_solve_gd(const oracle_problem *p, int mode, int T, double gamma, doub
   free(g);
   return bad;
 }
+
+/* ------------------------------------------------------------------ NEXT-2
+ * The paper's CT constraint set X = X1 ∩ X2, X1 = {||x||_TV <= τ},
+ * X2 = R_+^d, for a side x side image stored row-major
+ * (pixel (r, c) at r*side + c).  Readings (R19-R21, after
+ * SPEC.md:214-282): anisotropic TV with forward differences; the TV prox by
+ * FISTA on the dual; λ bracketed by doubling from 1 then bisected. */
+
+/* D x: horizontal differences h(r,c) = x[r][c+1] - x[r][c] at index
+ * r*(side-1) + c (c < side-1), then vertical v(r,c) = x[r+1][c] - x[r][c] at
+ * index side*(side-1) + r*side + c (r < side-1). */
+static void tv_D(int side, const double *x, double *dx) {
+  const int nh = side * (side - 1);
+  for (int r = 0; r < side; ++r)
+    for (int c = 0; c + 1 < side; ++c) dx[r * (side - 1) + c] = x[r * side + c + 1] - x[r * side + c];
+  for (int r = 0; r + 1 < side; ++r)
+    for (int c = 0; c < side; ++c) dx[nh + r * side + c] = x[(r + 1) * side + c] - x[r * side + c];
+}
+
+/* D^T u (the adjoint of tv_D). */
+static void tv_Dt(int side, const double *u, double *out) {
+  const int nh = side * (side - 1);
+  for (int k = 0; k < side * side; ++k) out[k] = 0.0;
+  for (int r = 0; r < side; ++r)
+    for (int c = 0; c + 1 < side; ++c) {
+      const double uh = u[r * (side - 1) + c];
+      out[r * side + c + 1] += uh;
+      out[r * side + c] -= uh;
+    }
+  for (int r = 0; r + 1 < side; ++r)
+    for (int c = 0; c < side; ++c) {
+      const double uv = u[nh + r * side + c];
+      out[(r + 1) * side + c] += uv;
+      out[r * side + c] -= uv;
+    }
+}
+
+/* ||x||_TV = Σ |D x|. */
+double oracle_tv_norm(int side, const double *x) {
+  const int m = 2 * side * (side - 1);
+  double *dx = (double *)malloc((size_t)(m > 0 ? m : 1) * sizeof(double));
+  tv_D(side, x, dx);
+  double t = 0.0;
+  for (int k = 0; k < m; ++k) t += fabs(dx[k]);
+  free(dx);
+  return t;
+}
+
+/* x = argmin ||x - z||^2 + λ ||x||_TV, Eq.(TV-regularization) PAPER.md:1257-1259.
+ * Dual: x = z - D^T u with u = argmin_{|u_k| <= λ/2} ½||z - D^T u||^2,
+ * solved by FISTA (Beck-Teboulle) with step 1/8 (||D||^2 <= 8): from w,
+ *   x_w = z - D^T w,  u+ = clip(w + D x_w / 8, ±λ/2),  t+ = (1 + sqrt(1 + 4t^2))/2,
+ *   w = u+ + ((t - 1)/t+)(u+ - u);
+ * stop when the primal x(u) = z - D^T u moves by <= rtol ||x(u)|| or after
+ * max_it iterations.  u_out (may be NULL) receives u [2 side (side-1)].
+ * Returns the iterations used. */
+int oracle_prox_tv(int side, const double *z, double lam, double rtol, int max_it, double *x,
+                   double *u_out) {
+  const int d = side * side, m = 2 * side * (side - 1);
+  double *u = (double *)calloc((size_t)(m > 0 ? m : 1), sizeof(double));
+  double *w = (double *)calloc((size_t)(m > 0 ? m : 1), sizeof(double));
+  double *un = (double *)malloc((size_t)(m > 0 ? m : 1) * sizeof(double));
+  double *dx = (double *)malloc((size_t)(m > 0 ? m : 1) * sizeof(double));
+  double *xw = (double *)malloc((size_t)d * sizeof(double));
+  double *xp = (double *)malloc((size_t)d * sizeof(double));
+  double t = 1.0;
+  int it = 0;
+  for (int k = 0; k < d; ++k) x[k] = z[k];
+  if (lam > 0.0 && m > 0) {
+    for (it = 1; it <= max_it; ++it) {
+      tv_Dt(side, w, xw);
+      for (int k = 0; k < d; ++k) xw[k] = z[k] - xw[k];
+      tv_D(side, xw, dx);
+      for (int k = 0; k < m; ++k) {
+        double v = w[k] + dx[k] / 8.0;
+        un[k] = v > lam / 2.0 ? lam / 2.0 : (v < -lam / 2.0 ? -lam / 2.0 : v);
+      }
+      const double tn = (1.0 + sqrt(1.0 + 4.0 * t * t)) / 2.0;
+      for (int k = 0; k < m; ++k) {
+        w[k] = un[k] + ((t - 1.0) / tn) * (un[k] - u[k]);
+        u[k] = un[k];
+      }
+      t = tn;
+      for (int k = 0; k < d; ++k) xp[k] = x[k];
+      tv_Dt(side, u, x);
+      for (int k = 0; k < d; ++k) x[k] = z[k] - x[k];
+      double dn = 0.0, xn = 0.0;
+      for (int k = 0; k < d; ++k) {
+        dn += (x[k] - xp[k]) * (x[k] - xp[k]);
+        xn += x[k] * x[k];
+      }
+      if (sqrt(dn) <= rtol * sqrt(xn)) break;
+    }
+    if (it > max_it) it = max_it;
+  }
+  if (u_out)
+    for (int k = 0; k < m; ++k) u_out[k] = u[k];
+  free(u);
+  free(w);
+  free(un);
+  free(dx);
+  free(xw);
+  free(xp);
+  return it;
+}
+
+/* Approximate projection onto X1 = {||x||_TV <= τ}: z
+ * itself if ||z||_TV <= τ; else the prox of Eq.(TV-regularization) with λ
+ * "tuned via a binary search" until | ||x̄||_TV - τ | <= tv_tol (0.01 in the
+ * paper).  Bracket: λ_hi = 1, doubled while ||prox(z, λ_hi)||_TV
+ * > τ; bisection of [λ_lo, λ_hi] for at most 60 steps.  Returns the bisection
+ * steps used (0 if z ∈ X1). */
+int oracle_project_tv(int side, const double *z, double tau, double tv_tol, double rtol,
+                      int max_it, double *x) {
+  const int d = side * side;
+  if (oracle_tv_norm(side, z) <= tau) {
+    for (int k = 0; k < d; ++k) x[k] = z[k];
+    return 0;
+  }
+  double lo = 0.0, hi = 1.0;
+  for (int g = 0; g < 200; ++g) {
+    oracle_prox_tv(side, z, hi, rtol, max_it, x, NULL);
+    if (oracle_tv_norm(side, x) <= tau) break;
+    lo = hi;
+    hi *= 2.0;
+  }
+  int steps = 0;
+  for (steps = 1; steps <= 60; ++steps) {
+    const double lam = 0.5 * (lo + hi);
+    oracle_prox_tv(side, z, lam, rtol, max_it, x, NULL);
+    const double tv = oracle_tv_norm(side, x);
+    if (fabs(tv - tau) <= tv_tol) break;
+    if (tv > tau) lo = lam;
+    else hi = lam;
+  }
+  return steps;
+}
+
+/* Dykstra's algorithm for X1 ∩ X2, Eq.(projection-intersection)
+ * z_0 = z, p_0 = q_0 = 0,
+ *   y_k = P_X1(z_k + p_k),  p_{k+1} = z_k + p_k - y_k,
+ *   z_{k+1} = P_X2(y_k + q_k),  q_{k+1} = y_k + q_k - z_{k+1},
+ * stopping at ||z_{k+1} - z_k||_2 <= tol (1e-4 in the paper) or max_outer.
+ * P_X2 keeps the positive entries.  Returns the sweeps. */
+int oracle_project_tv_nonneg(int side, const double *z, double tau, double tv_tol, double rtol,
+                             int max_it, double tol, int max_outer, double *out) {
+  const int d = side * side;
+  double *zk = (double *)malloc((size_t)d * sizeof(double));
+  double *p = (double *)calloc((size_t)d, sizeof(double));
+  double *q = (double *)calloc((size_t)d, sizeof(double));
+  double *y = (double *)malloc((size_t)d * sizeof(double));
+  double *v = (double *)malloc((size_t)d * sizeof(double));
+  for (int k = 0; k < d; ++k) zk[k] = z[k];
+  int it;
+  for (it = 1; it <= max_outer; ++it) {
+    for (int k = 0; k < d; ++k) v[k] = zk[k] + p[k];
+    oracle_project_tv(side, v, tau, tv_tol, rtol, max_it, y);
+    for (int k = 0; k < d; ++k) p[k] = zk[k] + p[k] - y[k];
+    double dn = 0.0;
+    for (int k = 0; k < d; ++k) {
+      const double s = y[k] + q[k];
+      const double zn = s > 0.0 ? s : 0.0;
+      q[k] = y[k] + q[k] - zn;
+      dn += (zn - zk[k]) * (zn - zk[k]);
+      zk[k] = zn;
+    }
+    if (sqrt(dn) <= tol) break;
+  }
+  if (it > max_outer) it = max_outer;
+  for (int k = 0; k < d; ++k) out[k] = zk[k];
+  free(zk);
+  free(p);
+  free(q);
+  free(y);
+  free(v);
+  return it;
+}

@@ -92,27 +92,26 @@ __device__ __forceinline__ void named_bar_sync(int id, int nthreads) {
 }
 
 // exp(x) for x <= 0 in fp64: Cody-Waite reduction x = k ln2 + r, |r| <= ln2/2,
-// degree-13 Taylor polynomial (truncation < 5e-18 relative), scale by 2^k.
-// Compact (few registers) replacement for libm exp on the link path.
+// Taylor polynomial of degree DEG, scale by 2^k.  Branch-free: x is clamped at
+// -708 (exp(-708) ~ 3e-308, below any count the link can resolve).  Truncation
+// r^(DEG+1)/(DEG+1)! relative: DEG 13 -> 5e-18 (fp64 path), DEG 9 -> 7e-12
+// (fp32 path, whose budget is 1e-4).  Compact replacement for libm exp.
+__host__ __device__ constexpr double inv_factorial(int n) {
+  double f = 1.0;
+  for (int i = 2; i <= n; ++i) f *= (double)i;
+  return 1.0 / f;
+}
+
+template <int DEG = 13>
 __device__ __forceinline__ double exp_nonpos(double x) {
-  if (x < -708.0) return 0.0;
+  x = fmax(x, -708.0);
   const double k = rint(x * 1.4426950408889634);
   double r = fma(-k, 6.93147180369123816490e-01, x);
   r = fma(-k, 1.90821492927058770002e-10, r);
-  double p = 1.6059043836821613e-10;           // 1/13!
-  p = fma(p, r, 2.08767569878681e-09);         // 1/12!
-  p = fma(p, r, 2.505210838544172e-08);        // 1/11!
-  p = fma(p, r, 2.755731922398589e-07);        // 1/10!
-  p = fma(p, r, 2.7557319223985893e-06);       // 1/9!
-  p = fma(p, r, 2.48015873015873e-05);         // 1/8!
-  p = fma(p, r, 1.984126984126984e-04);        // 1/7!
-  p = fma(p, r, 1.388888888888889e-03);        // 1/6!
-  p = fma(p, r, 8.333333333333333e-03);        // 1/5!
-  p = fma(p, r, 4.1666666666666664e-02);       // 1/4!
-  p = fma(p, r, 1.6666666666666666e-01);       // 1/3!
-  p = fma(p, r, 0.5);
-  p = fma(p, r, 1.0);
-  p = fma(p, r, 1.0);
+  // Horner on the Taylor coefficients 1/i!, i = DEG .. 0
+  double p = inv_factorial(DEG);
+#pragma unroll
+  for (int i = DEG - 1; i >= 0; --i) p = fma(p, r, inv_factorial(i));
   return p * __longlong_as_double((long long)(1023 + (int)k) << 52);
 }
 

@@ -2,10 +2,10 @@
 // (BASELINE.json configs[3]; A nonnegative), two passes:
 //
 //   K4f k_sell_forward  z_i = Σ_e val_e x[col_e] (fp64) from a SELL-32 copy of
-//                       A (32 consecutive rows per slice, lane = row), the
-//                       W-bin link and residual in-lane (lane_residual, the
-//                       same quantities as K1's row_residual), r_i stored fp32,
-//                       ℓ per block.
+//                       A (32 consecutive rows per slice, lane = row), then
+//                       the W-bin link and per-row scalar with 8 lanes per
+//                       row (group8_residual: the quantities of K1's
+//                       row_residual), r_i stored fp32, ℓ per block.
 //   K4b k_csc_backward  g_k = Σ_{i in column k} val_ik r_i  (Aᵀ r)
 //                       from a SELL-32 copy of Aᵀ built once at poly_init: a
 //                       slice holds 32 consecutive columns, step s of lane t is
@@ -15,7 +15,9 @@
 //                       atomics, fixed summation order (deterministic).
 // Both SELL copies are built once at poly_init from the caller's CSR; a
 // warp-per-row CSR forward was latency-bound (dependent row_ptr -> col -> x
-// loads, 2.0 TB/s in ncu) where the SELL stream runs at HBM rate.
+// loads, 2.0 TB/s in ncu).  A persistent TMA-ring variant of both passes (one
+// CTA per SM, 8 consumer warps) was slower (1.5 TB/s): the x / r gathers are
+// latency-bound and need the warps of many resident 128-thread CTAs.
 //
 // Why two passes: a one-pass fused kernel must scatter g[col] += r val for
 // every nonzero (red.global at ~1 lane/1.3 cycles per SM, B300_MICROARCH.md
@@ -46,7 +48,7 @@ struct CsrFwdArgs {
   const float *s_row;
   const float *I_row;
   double I_bar;
-  const double *x;
+  const float *x;         // [d] fp32 copy of the iterate (L1-resident gathers)
   const double *spec;
   float *r;               // [n] residuals r_i (output)
   int32_t mode;
@@ -90,16 +92,15 @@ __global__ void __launch_bounds__(128) k_csc_backward(const CscEnt<T> *__restric
   pdl_trigger();
 }
 
-// Link and per-row scalar when ONE lane owns the row (SELL forward): the
-// same quantities as row_residual, bins looped in-lane.
+// link + per-row scalar with a group of 8 lanes per row (bins j = sub, sub+8, ...)
 template <bool LOSS>
-__device__ __forceinline__ double lane_residual(const double *sp, int W, int relu, double z,
-                                                double yv, double Ii, const float *srow,
-                                                double *lacc, int mode) {
+__device__ __forceinline__ double group8_residual(const double *sp, int W, int relu, double z,
+                                                  double yv, double Ii, const float *srow,
+                                                  int sub, double *lacc, int mode) {
   const bool neg = relu && z < 0.0;
   const double zc = neg ? 0.0 : z;
   double hs = 0.0, Hs = 0.0, hp = 0.0;
-  for (int j = 0; j < W; ++j) {
+  for (int j = sub; j < W; j += 8) {
     const double sj = srow ? (double)srow[j] : sp[j];
     const double e = (relu || mode == 0) ? exp_nonpos(-sp[kMaxW + j] * zc) : exp(-sp[kMaxW + j] * z);
     hs += sj * e;
@@ -109,23 +110,33 @@ __device__ __forceinline__ double lane_residual(const double *sp, int W, int rel
       hp += sj * sp[kMaxW + j] * e;
     }
   }
+#pragma unroll
+  for (int o = 4; o > 0; o >>= 1) {
+    hs += __shfl_xor_sync(0xffffffffu, hs, o);
+    if (LOSS && mode == 0) Hs += __shfl_xor_sync(0xffffffffu, Hs, o);
+    if (mode != 0) hp += __shfl_xor_sync(0xffffffffu, hp, o);
+  }
+  double phi, l;
   if (mode == 0) {
-    if (LOSS) *lacc += yv * z - Ii * Hs;
-    return yv - Ii * hs;
+    phi = yv - Ii * hs;
+    l = yv * z - Ii * Hs;
+  } else {
+    hp = (relu && !(z > 0.0)) ? 0.0 : -hp;
+    const double m = Ii * hs;
+    if (mode == 1) {
+      phi = 2.0 * (m - yv) * Ii * hp;
+      l = (m - yv) * (m - yv);
+    } else if (mode == 2) {
+      const double rr = m - yv;
+      phi = (rr > 0.0 ? 1.0 : (rr < 0.0 ? -1.0 : 0.0)) * Ii * hp;
+      l = fabs(rr);
+    } else {
+      phi = (Ii - yv / hs) * hp;
+      l = m - yv * log(m);
+    }
   }
-  hp = (relu && !(z > 0.0)) ? 0.0 : -hp;
-  const double m = Ii * hs;
-  if (mode == 1) {
-    if (LOSS) *lacc += (m - yv) * (m - yv);
-    return 2.0 * (m - yv) * Ii * hp;
-  }
-  if (mode == 2) {
-    const double r = m - yv;
-    if (LOSS) *lacc += fabs(r);
-    return (r > 0.0 ? 1.0 : (r < 0.0 ? -1.0 : 0.0)) * Ii * hp;
-  }
-  if (LOSS) *lacc += m - yv * log(m);
-  return (Ii - yv / hs) * hp;
+  if (LOSS && sub == 0) *lacc += l;
+  return phi;
 }
 
 // K4f on a SELL-32 copy of A (rows as slices): block = 32 consecutive rows,
@@ -148,33 +159,54 @@ __global__ void __launch_bounds__(128) k_sell_forward(const CscEnt<T> *__restric
   for (; k + 12 < len; k += 16) {
     const CscEnt<T> q0 = p[(k) * 32], q1 = p[(k + 4) * 32], q2 = p[(k + 8) * 32],
                     q3 = p[(k + 12) * 32];
-    a0 = fma((double)q0.val, __ldg(a.x + q0.row), a0);
-    a1 = fma((double)q1.val, __ldg(a.x + q1.row), a1);
-    a2 = fma((double)q2.val, __ldg(a.x + q2.row), a2);
-    a3 = fma((double)q3.val, __ldg(a.x + q3.row), a3);
+    a0 = fma((double)q0.val, (double)__ldg(a.x + q0.row), a0);
+    a1 = fma((double)q1.val, (double)__ldg(a.x + q1.row), a1);
+    a2 = fma((double)q2.val, (double)__ldg(a.x + q2.row), a2);
+    a3 = fma((double)q3.val, (double)__ldg(a.x + q3.row), a3);
   }
   for (; k < len; k += 4) {
     const CscEnt<T> q = p[k * 32];
-    a0 = fma((double)q.val, __ldg(a.x + q.row), a0);
+    a0 = fma((double)q.val, (double)__ldg(a.x + q.row), a0);
   }
   part[warp][lane] = (a0 + a1) + (a2 + a3);
   __syncthreads();
-  if (warp == 0) {
-    const int64_t row = (int64_t)blockIdx.x * 32 + lane;
-    double lacc = 0.0;
-    if (row < a.n) {
-      const double z = (part[0][lane] + part[1][lane]) + (part[2][lane] + part[3][lane]);
-      double yv;
+  // link + residual: 8 lanes per row (bins across the group), warp w takes
+  // rows 8w .. 8w+7 in two rounds of four; every lane runs the group
+  // reduction (full-mask shuffles), rows past n are evaluated on dummies
+  const int sub = lane & 7;
+  double lacc = 0.0;
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const int rr = warp * 8 + h * 4 + (lane >> 3);
+    const int64_t row = (int64_t)blockIdx.x * 32 + rr;
+    const bool valid = row < a.n;
+    double z = (part[0][rr] + part[1][rr]) + (part[2][rr] + part[3][rr]);
+    double yv = 0.0, Ii = a.I_bar;
+    const float *srow = nullptr;
+    if (valid) {
       if (a.ytype == 0) yv = (double)((const int32_t *)a.y)[row];
       else if (a.ytype == 1) yv = (double)((const float *)a.y)[row];
       else yv = ((const double *)a.y)[row];
-      const double Ii = a.I_row ? (double)a.I_row[row] : a.I_bar;
-      const float *srow = a.I_row ? a.s_row + row * a.W : nullptr;
-      a.r[row] = (float)lane_residual<LOSS>(sp, a.W, a.relu, z, yv, Ii, srow, &lacc, a.mode);
+      if (a.I_row) {
+        Ii = (double)a.I_row[row];
+        srow = a.s_row + row * a.W;
+      }
+    } else {
+      z = 0.0;
     }
-    lacc = warp_sum(lacc);
-    if (lane == 0) a.loss_partials[blockIdx.x] = lacc;
+    double lrow = 0.0;
+    const double phi = group8_residual<LOSS>(sp, a.W, a.relu, z, yv, Ii, srow, sub, &lrow, a.mode);
+    if (valid) {
+      lacc += lrow;
+      if (sub == 0) a.r[row] = (float)phi;
+    }
   }
+  // per-block loss partial, warps combined in order (deterministic)
+  lacc = warp_sum(lacc);
+  __syncthreads();
+  if (lane == 0) part[0][warp] = lacc;
+  __syncthreads();
+  if (threadIdx.x == 0) a.loss_partials[blockIdx.x] = (part[0][0] + part[0][1]) + (part[0][2] + part[0][3]);
   pdl_trigger();
 }
 

@@ -103,6 +103,35 @@ __device__ __forceinline__ double row_residual(const double *sp, int W, int relu
   return phi;
 }
 
+// Mode-0 (EXACT) link for K1, branch-free in the bins: lane j (and j + 32
+// when W > 32) evaluates bin j; bins >= W carry s_j = 0 (the spectrum table
+// is zero-padded to kMaxW, per-row spectra are masked).  DEG: exp polynomial
+// degree (13 for fp64 A, 9 for fp32 A; see exp_nonpos).
+template <bool LOSS, int DEG>
+__device__ __forceinline__ double link_exact(const double *sp, int W, int relu, double z,
+                                             double yv, double Ii, const float *srow,
+                                             bool count_loss, double *lacc) {
+  const int lane = threadIdx.x & 31;
+  const bool neg = relu && z < 0.0;
+  const double zc = neg ? 0.0 : z;
+  double hs = 0.0, Hs = 0.0;
+#pragma unroll
+  for (int b = 0; b < 2; ++b) {
+    if (b == 1 && W <= 32) break;  // warp-uniform
+    const int j = lane + 32 * b;
+    const double sj = srow ? (j < W ? (double)srow[j] : 0.0) : sp[j];
+    const double e = exp_nonpos<DEG>(-sp[kMaxW + j] * zc);
+    hs = fma(sj, e, hs);
+    if (LOSS) Hs += neg ? sj * z : sj * sp[2 * kMaxW + j] * (1.0 - e);
+  }
+  hs = warp_sum(hs);
+  if (LOSS) {
+    Hs = warp_sum(Hs);
+    if (count_loss && lane == 0) *lacc += yv * z - Ii * Hs;
+  }
+  return yv - Ii * hs;
+}
+
 __device__ __forceinline__ double load_y(const unsigned char *yb, int ytype, int r) {
   if (ytype == 0) return (double)((const int32_t *)yb)[2 * r];
   if (ytype == 1) return (double)((const float *)yb)[2 * r];
@@ -325,8 +354,11 @@ __global__ void __launch_bounds__(32 * (NW + 1), 1) k_dense_loss_grad(const Dens
         const double yv = load_y(sd + yoff, a.ytype, lr);
         const double Ii = has_rowspec ? (double)((const float *)(sd + ioff))[lr] : a.I_bar;
         const float *srow = has_rowspec ? (const float *)(sd + soff) + lr * a.W : nullptr;
-        const double r = row_residual<LOSS>(sp, a.W, a.relu, zp[q], yv, Ii, srow, w == 0, &lacc,
-                                             a.mode);
+        const double r =
+            a.mode == 0
+                ? link_exact<LOSS, std::is_same<T, double>::value ? 13 : 9>(sp, a.W, a.relu, zp[q], yv,
+                                                                           Ii, srow, w == 0, &lacc)
+                : row_residual<LOSS>(sp, a.W, a.relu, zp[q], yv, Ii, srow, w == 0, &lacc, a.mode);
         const T rt = (T)r;
         const T *rowp = tile + (size_t)lr * lda + lane_off;
 #pragma unroll

@@ -55,6 +55,7 @@ struct FinArgs {
   double *g_out;             // optional [d]
   const double *anchor;      // [d]
   double *x_out;             // [d] (may alias anchor)
+  float *x32_out;            // optional [d]: fp32 copy of x_out (gathered by the CSR pass)
   double *v_scratch;         // [d]
   double *block_norm;        // [gridDim.x]
   const double *center;      // [d] or null
@@ -184,6 +185,7 @@ __global__ void __launch_bounds__(256) k_finalize(const FinArgs a) {
       xo = v * scale;
     }
     a.x_out[k] = xo;
+    if (a.x32_out) a.x32_out[k] = (float)xo;
   }
   if (tid == 0) {
     SolveState *s = a.state;
@@ -203,6 +205,14 @@ __global__ void __launch_bounds__(256) k_finalize(const FinArgs a) {
 // ||v - c||² from the block partials of k_finalize in the same fixed order
 // (identical bits in every block), then scales its slice of v into x_out.
 // Replaces the single-block tail, which serialised d/256 dependent loads.
+__global__ void k_to_f32(const double *x, int64_t d, float *out) {
+  pdl_wait();
+  pdl_trigger();
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < d;
+       k += (int64_t)gridDim.x * blockDim.x)
+    out[k] = (float)x[k];
+}
+
 __global__ void __launch_bounds__(256) k_fin_apply(const FinArgs a) {
   __shared__ double s_nr;
   pdl_wait();
@@ -229,6 +239,7 @@ __global__ void __launch_bounds__(256) k_fin_apply(const FinArgs a) {
       xo = v * scale;
     }
     a.x_out[k] = xo;
+    if (a.x32_out) a.x32_out[k] = (float)xo;
   }
   if (blockIdx.x == 0 && tid == 0) {
     SolveState *s = a.state;

@@ -218,6 +218,7 @@ struct poly_handle {
   void *sell = nullptr;                // CscEnt<T>[slice_off[nslices] * 32]
   int64_t *slice_off = nullptr;        // [nslices + 1] slice start, in 32-entry steps
   float *rbuf = nullptr;               // [n_local] residuals between K4f and K4b
+  float *xa32 = nullptr, *xh32 = nullptr, *xin32 = nullptr;  // CSR: fp32 copies of xa, xh, a caller's x
   int64_t sell_steps = 0;              // slice_off[nslices]
   int64_t sell_row_steps = 0;          // row_slice_off[k4_grid]
   int fin_split = 0;
@@ -334,7 +335,15 @@ int enqueue_pass(poly_handle *h, const double *x, bool loss) {
   a.s_row = p.s_row;
   a.I_row = p.I_row;
   a.I_bar = p.I_bar;
-  a.x = x;
+  // fp32 copy of x for the gathers: written by the step kernel for the
+  // internal iterates, converted here for a caller's x
+  const float *x32 = x == h->xa ? h->xa32 : (x == h->xh ? h->xh32 : nullptr);
+  if (!x32) {
+    TRY(launch(h, (const void *)&k_to_f32, dim3((unsigned)std::min<int64_t>(1024, (p.d + 255) / 256)),
+               dim3(256), 0, true, x, (int64_t)p.d, h->xin32));
+    x32 = h->xin32;
+  }
+  a.x = x32;
   a.spec = h->spec;
   a.r = h->rbuf;
   a.mode = p.mode;
@@ -349,6 +358,10 @@ int enqueue_pass(poly_handle *h, const double *x, bool loss) {
                   (const CscEnt<float> *)h->sell, (const int64_t *)h->slice_off, d32, rb, gp);
   return launch(h, kCscBwd[1], dim3(h->nslices), dim3(128), 0, true,
                 (const CscEnt<double> *)h->sell, (const int64_t *)h->slice_off, d32, rb, gp);
+}
+
+float *x32_of(poly_handle *h, const double *x) {
+  return x == h->xa ? h->xa32 : (x == h->xh ? h->xh32 : nullptr);
 }
 
 FinArgs fin_base(poly_handle *h, int mode) {
@@ -402,6 +415,7 @@ int enqueue_eval(poly_handle *h, const double *x, bool loss, bool step, const do
   FinArgs f = fin_base(h, 0);
   f.anchor = anchor;
   f.x_out = x_out;
+  f.x32_out = x32_of(h, x_out);
   f.g_out = g_out;
   if (!h->comm_path) {
     f.mode = step ? FIN_STEP : FIN_GRAD;
@@ -869,6 +883,9 @@ int poly_init(const poly_problem *pin, poly_handle **out) {
     if ((rc = dev_alloc(h, &h->partials, (size_t)p.d)) != POLY_OK) return bail(rc);
     if ((rc = dev_alloc(h, &h->loss_partials, (size_t)h->k4_grid)) != POLY_OK) return bail(rc);
     if ((rc = dev_alloc(h, &h->rbuf, (size_t)std::max<int64_t>(1, p.n_local))) != POLY_OK) return bail(rc);
+    if ((rc = dev_alloc(h, &h->xa32, (size_t)p.d)) != POLY_OK) return bail(rc);
+    if ((rc = dev_alloc(h, &h->xh32, (size_t)p.d)) != POLY_OK) return bail(rc);
+    if ((rc = dev_alloc(h, &h->xin32, (size_t)p.d)) != POLY_OK) return bail(rc);
     if (cudaMemsetAsync(h->rbuf, 0, std::max<int64_t>(1, p.n_local) * 4, h->work) != cudaSuccess)
       return bail(fail(POLY_ECUDA, "memset failed"));
   }
@@ -1027,6 +1044,7 @@ int poly_solve_ex(poly_handle *h, const poly_solve_opts *o, double *x, double *x
     FinArgs f = fin_base(h, FIN_PROJECT);  // x_1 = P_X(x_in)
     f.anchor = h->xa;
     f.x_out = h->xa;
+    f.x32_out = h->xa32;
     TRY(enqueue_fin(h, f));
   }
   if (avg) TRY(enqueue_avg(h));  // folds x_1: S = x_1, x̄_1 = x_1, k = 1
@@ -1151,6 +1169,7 @@ int poly_solve(poly_handle *h, double *x, int T, double gamma, uint32_t flags, d
     FinArgs f = fin_base(h, FIN_PROJECT);
     f.anchor = h->xa;
     f.x_out = h->xa;
+    f.x32_out = h->xa32;
     TRY(enqueue_fin(h, f));
   }
   const bool loss = want_trace;

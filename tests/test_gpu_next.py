@@ -79,6 +79,19 @@ def test_modes_dense_parity(dtype, tol, mode, relu):
         g, l = p.loss_grad(torch.tensor(x, device="cuda"))
         if np.linalg.norm(g_ref) == 0.0:
             assert torch.count_nonzero(g).item() == 0
+        elif mode == 2:
+            # L1: sign(Ī h - y) is decided from z and h, whose summation order
+            # differs from the oracle's (fp32 dot: ~1e-6 relative; at x = 0 with
+            # relu = 0, Ī h = Ī Σ s_j ties with y = Ī up to rounding); rows with
+            # |Ī h - y| inside that band may flip, each moving g by at most
+            # 2 Ī |h'| ||a_i|| / n <= 2 Ī Σ s_j μ_j ||a_i|| / n.
+            m = o.mean(x)
+            A64 = pb["A"][:, :pb["d"]].astype(np.float64)
+            tie = np.abs(m - pb["y"]) <= 1e-5 * np.maximum(1.0, m)
+            slack = 2 * pb["I_bar"] * float(np.dot(pb["s"], pb["mu"])) * \
+                np.linalg.norm(A64[tie], axis=1).sum() / pb["n"]
+            err = np.linalg.norm(g.cpu().numpy() - g_ref)
+            assert err <= tol * np.linalg.norm(g_ref) + slack, (err, slack, int(tie.sum()))
         else:
             assert rel(g.cpu().numpy(), g_ref) <= tol, (mode, relu, rel(g.cpu().numpy(), g_ref))
         assert abs(l - l_ref) <= tol * max(1.0, abs(l_ref))
