@@ -210,18 +210,62 @@ __global__ void __launch_bounds__(128) k_sell_forward(const CscEnt<T> *__restric
   pdl_trigger();
 }
 
-// (poly_init only) SELL-32 copy of A itself: entry j of row i -> step j, lane i % 32
+// (poly_init only) Gather locality of a K4f slice: at step k its 32 lanes
+// read x at the k-th column of 32 consecutive rows.  When d = s² (an s x s
+// image, row-major) the library also keeps the transposed copy of x; for
+// each slice it counts the distinct 32-byte fp32 sectors the gathers touch
+// under both layouts and marks the slice for the transposed copy when that
+// touches fewer (CT rays near 0° / 180° walk along image rows, so adjacent
+// rays' k-th pixels are adjacent in the column-major layout).
+__device__ __forceinline__ int32_t tr_index(int32_t c, int32_t s) { return (c % s) * s + c / s; }
+
+__global__ void k_slice_layout(const int64_t *row_ptr, const int32_t *col, int64_t n, int32_t s,
+                               int64_t nslices, int8_t *use_tr) {
+  const int lane = threadIdx.x & 31;
+  const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t sl = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); sl < nslices;
+       sl += nw) {
+    const int64_t row = sl * 32 + lane;
+    const int64_t e0 = row < n ? row_ptr[row] : 0;
+    const int64_t len = row < n ? row_ptr[row + 1] - e0 : 0;
+    int64_t mx = len;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) mx = max(mx, (int64_t)__shfl_xor_sync(0xffffffffu, mx, o));
+    int64_t c_row = 0, c_tr = 0;
+    for (int64_t k = 0; k < mx; ++k) {
+      const bool act = k < len;
+      const int32_t cc = act ? col[e0 + k] : 0;
+      const int32_t a = act ? (cc >> 3) : -1 - lane;
+      const int32_t b = act ? (tr_index(cc, s) >> 3) : -1 - lane;
+      const unsigned ma = __match_any_sync(0xffffffffu, a), mb = __match_any_sync(0xffffffffu, b);
+      c_row += act && (__ffs(ma) - 1) == lane;
+      c_tr += act && (__ffs(mb) - 1) == lane;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      c_row += __shfl_xor_sync(0xffffffffu, c_row, o);
+      c_tr += __shfl_xor_sync(0xffffffffu, c_tr, o);
+    }
+    if (lane == 0) use_tr[sl] = c_tr < c_row ? 1 : 0;
+  }
+}
+
+// (poly_init only) SELL-32 copy of A itself: entry j of row i -> step j,
+// lane i % 32; columns of slices marked in use_tr index the transposed copy
+// of x (d + tr(col)).
 template <typename T>
 __global__ void k_sell_rows_fill(const int64_t *row_ptr, const int32_t *col, const T *val,
-                                 int64_t n, const int64_t *slice_off, CscEnt<T> *ent) {
+                                 int64_t n, const int64_t *slice_off, const int8_t *use_tr,
+                                 int32_t s, int32_t d, CscEnt<T> *ent) {
   const int lane = threadIdx.x & 31;
   const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
   for (int64_t i = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); i < n; i += nw) {
     const int64_t e0 = row_ptr[i], e1 = row_ptr[i + 1];
+    const bool tr = use_tr && use_tr[i >> 5];
     CscEnt<T> *dst = ent + slice_off[i >> 5] * 32 + (i & 31);
     for (int64_t e = e0 + lane; e < e1; e += 32) {
       CscEnt<T> q;
-      q.row = col[e];
+      q.row = tr ? d + tr_index(col[e], s) : col[e];
       q.val = val[e];
       dst[(e - e0) * 32] = q;
     }

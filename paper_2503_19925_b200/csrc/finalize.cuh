@@ -56,6 +56,7 @@ struct FinArgs {
   const double *anchor;      // [d]
   double *x_out;             // [d] (may alias anchor)
   float *x32_out;            // optional [d]: fp32 copy of x_out (gathered by the CSR pass)
+  int32_t tr_side;           // > 0: x32_out is [2d] and x32_out[d + tr(k)] holds the transposed copy
   double *v_scratch;         // [d]
   double *block_norm;        // [gridDim.x]
   const double *center;      // [d] or null
@@ -185,7 +186,10 @@ __global__ void __launch_bounds__(256) k_finalize(const FinArgs a) {
       xo = v * scale;
     }
     a.x_out[k] = xo;
-    if (a.x32_out) a.x32_out[k] = (float)xo;
+    if (a.x32_out) {
+      a.x32_out[k] = (float)xo;
+      if (a.tr_side) a.x32_out[a.d + (k % a.tr_side) * a.tr_side + k / a.tr_side] = (float)xo;
+    }
   }
   if (tid == 0) {
     SolveState *s = a.state;
@@ -205,12 +209,14 @@ __global__ void __launch_bounds__(256) k_finalize(const FinArgs a) {
 // ||v - c||² from the block partials of k_finalize in the same fixed order
 // (identical bits in every block), then scales its slice of v into x_out.
 // Replaces the single-block tail, which serialised d/256 dependent loads.
-__global__ void k_to_f32(const double *x, int64_t d, float *out) {
+__global__ void k_to_f32(const double *x, int64_t d, int32_t tr_side, float *out) {
   pdl_wait();
   pdl_trigger();
   for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < d;
-       k += (int64_t)gridDim.x * blockDim.x)
+       k += (int64_t)gridDim.x * blockDim.x) {
     out[k] = (float)x[k];
+    if (tr_side) out[d + (k % tr_side) * tr_side + k / tr_side] = (float)x[k];
+  }
 }
 
 __global__ void __launch_bounds__(256) k_fin_apply(const FinArgs a) {
@@ -239,7 +245,10 @@ __global__ void __launch_bounds__(256) k_fin_apply(const FinArgs a) {
       xo = v * scale;
     }
     a.x_out[k] = xo;
-    if (a.x32_out) a.x32_out[k] = (float)xo;
+    if (a.x32_out) {
+      a.x32_out[k] = (float)xo;
+      if (a.tr_side) a.x32_out[a.d + (k % a.tr_side) * a.tr_side + k / a.tr_side] = (float)xo;
+    }
   }
   if (blockIdx.x == 0 && tid == 0) {
     SolveState *s = a.state;

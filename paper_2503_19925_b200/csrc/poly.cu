@@ -14,6 +14,7 @@
 #include <nccl.h>
 #include <stdarg.h>
 #include <stdio.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include <cub/device/device_radix_sort.cuh>
@@ -111,9 +112,14 @@ struct DenseVariant {
 
 // columns per slab: 32 lanes x (16 B / elsize) x V
 const DenseVariant kDenseF32[] = {
-    DV(float, 1, 1, 16, 64), DV(float, 2, 1, 16, 32), DV(float, 4, 1, 16, 16),
-    DV(float, 8, 1, 12, 12), DV(float, 8, 2, 12, 6),  DV(float, 8, 4, 12, 3),
+    DV(float, 1, 1, 16, 64), DV(float, 2, 1, 16, 32), DV(float, 4, 1, 16, 32),
+    DV(float, 8, 1, 12, 12), DV(float, 8, 2, 12, 6),  DV(float, 8, 4, 12, 6),
     DV(float, 8, 8, 8, 1),
+};
+// alternative tiles, selectable with POLY_K1_TUNE=<index> (tuning runs only)
+const DenseVariant kDenseTuneF32[] = {
+    DV(float, 8, 1, 12, 24), DV(float, 8, 1, 16, 16), DV(float, 8, 4, 12, 3),  DV(float, 4, 1, 16, 16),
+    DV(float, 8, 2, 12, 12), DV(float, 4, 1, 16, 48), DV(float, 8, 1, 8, 16),  DV(float, 8, 4, 8, 4),
 };
 const DenseVariant kDenseF64[] = {
     DV(double, 1, 1, 16, 64), DV(double, 2, 1, 16, 32), DV(double, 4, 1, 16, 16),
@@ -219,6 +225,8 @@ struct poly_handle {
   int64_t *slice_off = nullptr;        // [nslices + 1] slice start, in 32-entry steps
   float *rbuf = nullptr;               // [n_local] residuals between K4f and K4b
   float *xa32 = nullptr, *xh32 = nullptr, *xin32 = nullptr;  // CSR: fp32 copies of xa, xh, a caller's x
+  int tr_side = 0;                     // CSR, d = s²: fp32 copies also hold x transposed at [d, 2d)
+  int64_t tr_slices = 0;               // K4f slices that gather from the transposed copy
   int64_t sell_steps = 0;              // slice_off[nslices]
   int64_t sell_row_steps = 0;          // row_slice_off[k4_grid]
   int fin_split = 0;
@@ -340,7 +348,7 @@ int enqueue_pass(poly_handle *h, const double *x, bool loss) {
   const float *x32 = x == h->xa ? h->xa32 : (x == h->xh ? h->xh32 : nullptr);
   if (!x32) {
     TRY(launch(h, (const void *)&k_to_f32, dim3((unsigned)std::min<int64_t>(1024, (p.d + 255) / 256)),
-               dim3(256), 0, true, x, (int64_t)p.d, h->xin32));
+               dim3(256), 0, true, x, (int64_t)p.d, (int32_t)h->tr_side, h->xin32));
     x32 = h->xin32;
   }
   a.x = x32;
@@ -416,6 +424,7 @@ int enqueue_eval(poly_handle *h, const double *x, bool loss, bool step, const do
   f.anchor = anchor;
   f.x_out = x_out;
   f.x32_out = x32_of(h, x_out);
+  f.tr_side = h->tr_side;
   f.g_out = g_out;
   if (!h->comm_path) {
     f.mode = step ? FIN_STEP : FIN_GRAD;
@@ -605,6 +614,13 @@ int setup_dense(poly_handle *h) {
   }
   if (!dv) return fail(POLY_EUNSUPPORTED, "dense d = %lld exceeds the largest tile (%d columns)",
                        (long long)p.d, 32 * vec * 8 * 8);
+  if (const char *tv = getenv("POLY_K1_TUNE")) {
+    const int i = atoi(tv);
+    const int nt = (int)(sizeof(kDenseTuneF32) / sizeof(kDenseTuneF32[0]));
+    if (p.dtype == POLY_F32 && i >= 0 && i < nt &&
+        p.d <= (int64_t)32 * vec * kDenseTuneF32[i].V * kDenseTuneF32[i].WPR)
+      dv = &kDenseTuneF32[i];
+  }
   h->dv = dv;
   h->full = (p.d == (int64_t)32 * vec * dv->V * dv->WPR) ? 1 : 0;
   h->k1_threads = 32 * (dv->NW + 1);
@@ -731,9 +747,24 @@ int build_sell_t(poly_handle *h) {
   CscEnt<T> *rent = nullptr;
   if ((rc = dev_alloc(h, &rent, (size_t)std::max<int64_t>(1, rsteps) * 32))) return done(rc);
   cudaMemsetAsync(rent, 0, (size_t)std::max<int64_t>(1, rsteps) * 32 * sizeof(CscEnt<T>), st);
+  int8_t *use_tr = nullptr;
+  if (h->tr_side && p.n_local > 0) {
+    if ((rc = talloc((size_t)nrs, (void **)&use_tr))) return done(rc);
+    k_slice_layout<<<(int)std::min<int64_t>(4096, (nrs + 7) / 8), 256, 0, st>>>(
+        p.row_ptr, p.col, p.n_local, h->tr_side, nrs, use_tr);
+    std::vector<int8_t> ut((size_t)nrs);
+    if (cudaMemcpyAsync(ut.data(), use_tr, (size_t)nrs, cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+        cudaStreamSynchronize(st) != cudaSuccess)
+      return done(fail(POLY_ECUDA, "SELL layout: %s", cudaGetErrorString(cudaGetLastError())));
+    h->tr_slices = 0;
+    for (int8_t v : ut) h->tr_slices += v;
+  }
+  const int fill_side = h->tr_side;
+  if (!h->tr_slices) h->tr_side = 0;  // no slice gains: no transposed copy is maintained
   if (p.n_local > 0)
     k_sell_rows_fill<T><<<g, 256, 0, st>>>(p.row_ptr, p.col, (const T *)p.val, p.n_local,
-                                           h->row_slice_off, rent);
+                                           h->row_slice_off, h->tr_slices ? use_tr : nullptr,
+                                           fill_side, (int32_t)p.d, rent);
   h->sell_rows = rent;
   h->sell_row_steps = rsteps;
   if (cudaStreamSynchronize(st) != cudaSuccess)
@@ -883,9 +914,14 @@ int poly_init(const poly_problem *pin, poly_handle **out) {
     if ((rc = dev_alloc(h, &h->partials, (size_t)p.d)) != POLY_OK) return bail(rc);
     if ((rc = dev_alloc(h, &h->loss_partials, (size_t)h->k4_grid)) != POLY_OK) return bail(rc);
     if ((rc = dev_alloc(h, &h->rbuf, (size_t)std::max<int64_t>(1, p.n_local))) != POLY_OK) return bail(rc);
-    if ((rc = dev_alloc(h, &h->xa32, (size_t)p.d)) != POLY_OK) return bail(rc);
-    if ((rc = dev_alloc(h, &h->xh32, (size_t)p.d)) != POLY_OK) return bail(rc);
-    if ((rc = dev_alloc(h, &h->xin32, (size_t)p.d)) != POLY_OK) return bail(rc);
+    {  // a square d may be an image: the fp32 copies get room for x transposed
+      const int64_t s = (int64_t)llround(std::sqrt((double)p.d));
+      if (s * s == p.d && s > 1) h->tr_side = (int)s;
+    }
+    const size_t n32 = (size_t)p.d * (h->tr_side ? 2 : 1);
+    if ((rc = dev_alloc(h, &h->xa32, n32)) != POLY_OK) return bail(rc);
+    if ((rc = dev_alloc(h, &h->xh32, n32)) != POLY_OK) return bail(rc);
+    if ((rc = dev_alloc(h, &h->xin32, n32)) != POLY_OK) return bail(rc);
     if (cudaMemsetAsync(h->rbuf, 0, std::max<int64_t>(1, p.n_local) * 4, h->work) != cudaSuccess)
       return bail(fail(POLY_ECUDA, "memset failed"));
   }
@@ -1045,6 +1081,7 @@ int poly_solve_ex(poly_handle *h, const poly_solve_opts *o, double *x, double *x
     f.anchor = h->xa;
     f.x_out = h->xa;
     f.x32_out = h->xa32;
+    f.tr_side = h->tr_side;
     TRY(enqueue_fin(h, f));
   }
   if (avg) TRY(enqueue_avg(h));  // folds x_1: S = x_1, x̄_1 = x_1, k = 1
@@ -1170,6 +1207,7 @@ int poly_solve(poly_handle *h, double *x, int T, double gamma, uint32_t flags, d
     f.anchor = h->xa;
     f.x_out = h->xa;
     f.x32_out = h->xa32;
+    f.tr_side = h->tr_side;
     TRY(enqueue_fin(h, f));
   }
   const bool loss = want_trace;
