@@ -139,40 +139,14 @@ __device__ __forceinline__ double group8_residual(const double *sp, int W, int r
   return phi;
 }
 
-// K4f on a SELL-32 copy of A (rows as slices): block = 32 consecutive rows,
-// warp w takes steps w, w+4, ...; z_i combined in warp order, then lane i of
-// warp 0 evaluates row i's link and residual.
-template <typename T, bool LOSS>
-__global__ void __launch_bounds__(128) k_sell_forward(const CscEnt<T> *__restrict__ ent,
-                                                      const int64_t *__restrict__ slice_off,
-                                                      const CsrFwdArgs a) {
-  __shared__ double sp[3 * kMaxW];
-  __shared__ double part[4][32];
+// K4f epilogue: z of the slice's 32 rows from the four warps' partials, then
+// the link + residual with 8 lanes per row (bins across the group), warp w
+// taking rows 8w .. 8w+7 in two rounds of four; every lane runs the group
+// reduction (full-mask shuffles), rows past n are evaluated on dummies.
+template <bool LOSS>
+__device__ __forceinline__ void forward_tail(double (*part)[32], const double *sp,
+                                             const CsrFwdArgs &a) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  for (int i = threadIdx.x; i < 3 * kMaxW; i += blockDim.x) sp[i] = a.spec[i];
-  const int64_t s0 = slice_off[blockIdx.x], s1 = slice_off[blockIdx.x + 1];
-  const CscEnt<T> *p = ent + s0 * 32 + lane;
-  const int64_t len = s1 - s0;
-  pdl_wait();  // x is written by the previous kernel; r is read by the previous backward
-  double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
-  int64_t k = warp;
-  for (; k + 12 < len; k += 16) {
-    const CscEnt<T> q0 = p[(k) * 32], q1 = p[(k + 4) * 32], q2 = p[(k + 8) * 32],
-                    q3 = p[(k + 12) * 32];
-    a0 = fma((double)q0.val, (double)__ldg(a.x + q0.row), a0);
-    a1 = fma((double)q1.val, (double)__ldg(a.x + q1.row), a1);
-    a2 = fma((double)q2.val, (double)__ldg(a.x + q2.row), a2);
-    a3 = fma((double)q3.val, (double)__ldg(a.x + q3.row), a3);
-  }
-  for (; k < len; k += 4) {
-    const CscEnt<T> q = p[k * 32];
-    a0 = fma((double)q.val, (double)__ldg(a.x + q.row), a0);
-  }
-  part[warp][lane] = (a0 + a1) + (a2 + a3);
-  __syncthreads();
-  // link + residual: 8 lanes per row (bins across the group), warp w takes
-  // rows 8w .. 8w+7 in two rounds of four; every lane runs the group
-  // reduction (full-mask shuffles), rows past n are evaluated on dummies
   const int sub = lane & 7;
   double lacc = 0.0;
 #pragma unroll
@@ -207,7 +181,152 @@ __global__ void __launch_bounds__(128) k_sell_forward(const CscEnt<T> *__restric
   if (lane == 0) part[0][warp] = lacc;
   __syncthreads();
   if (threadIdx.x == 0) a.loss_partials[blockIdx.x] = (part[0][0] + part[0][1]) + (part[0][2] + part[0][3]);
+}
+
+// K4f on a SELL-32 copy of A (rows as slices): block = 32 consecutive rows,
+// warp w takes steps w, w+4, ...; z_i combined in warp order, then lane i of
+// warp 0 evaluates row i's link and residual.
+template <typename T, bool LOSS>
+__global__ void __launch_bounds__(128) k_sell_forward(const CscEnt<T> *__restrict__ ent,
+                                                      const int64_t *__restrict__ slice_off,
+                                                      const CsrFwdArgs a) {
+  __shared__ double sp[3 * kMaxW];
+  __shared__ double part[4][32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int i = threadIdx.x; i < 3 * kMaxW; i += blockDim.x) sp[i] = a.spec[i];
+  const int64_t s0 = slice_off[blockIdx.x], s1 = slice_off[blockIdx.x + 1];
+  const CscEnt<T> *p = ent + s0 * 32 + lane;
+  const int64_t len = s1 - s0;
+  pdl_wait();  // x is written by the previous kernel; r is read by the previous backward
+  double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+  int64_t k = warp;
+  for (; k + 12 < len; k += 16) {
+    const CscEnt<T> q0 = p[(k) * 32], q1 = p[(k + 4) * 32], q2 = p[(k + 8) * 32],
+                    q3 = p[(k + 12) * 32];
+    a0 = fma((double)q0.val, (double)__ldg(a.x + q0.row), a0);
+    a1 = fma((double)q1.val, (double)__ldg(a.x + q1.row), a1);
+    a2 = fma((double)q2.val, (double)__ldg(a.x + q2.row), a2);
+    a3 = fma((double)q3.val, (double)__ldg(a.x + q3.row), a3);
+  }
+  for (; k < len; k += 4) {
+    const CscEnt<T> q = p[k * 32];
+    a0 = fma((double)q.val, (double)__ldg(a.x + q.row), a0);
+  }
+  part[warp][lane] = (a0 + a1) + (a2 + a3);
+  __syncthreads();
+  forward_tail<LOSS>(part, sp, a);
   pdl_trigger();
+}
+
+// ------------------------------------------------------------------------
+// Compact SELL-32 ("SELL16"): the same slices and steps, stored as two SoA
+// arrays per step — 32 int16 index deltas and 32 values — i.e. 6 bytes per
+// fp32 entry instead of 8.  The four warps of a slice's CTA each take a
+// contiguous quarter of the steps; lane t of warp w starts from the absolute
+// index base[(slice*4 + w)*32 + t] and adds the deltas (0 on padding and at
+// quarter starts).  Built at poly_init from the SELL copies when every delta
+// fits int16 (CT rays: |Δcol| <= side + 1; Aᵀ columns: Δrow <= views x bins
+// gaps), else the library keeps the 8-byte form.
+struct Sell16 {
+  const int16_t *dl;
+  const void *val;
+  const int32_t *base;
+  const int64_t *slice_off;
+};
+
+template <typename T>
+__device__ __forceinline__ double sell16_dot(const Sell16 &s, int64_t slice, int warp, int lane,
+                                             const float *__restrict__ gv) {
+  const int64_t o0 = s.slice_off[slice], len = s.slice_off[slice + 1] - o0;
+  const int64_t q = (len + 3) / 4;
+  int64_t k = (int64_t)warp * q;
+  const int64_t ke = min(len, k + q);
+  int32_t idx = s.base[(slice * 4 + warp) * 32 + lane];
+  const int16_t *dp = s.dl + (o0 + k) * 32 + lane;
+  const T *vp = (const T *)s.val + (o0 + k) * 32 + lane;
+  double a0 = 0.0, a1 = 0.0;
+  for (; k + 3 < ke; k += 4) {
+    const int16_t d0 = __ldcs(dp), d1 = __ldcs(dp + 32), d2 = __ldcs(dp + 64), d3 = __ldcs(dp + 96);
+    const T v0 = __ldcs(vp), v1 = __ldcs(vp + 32), v2 = __ldcs(vp + 64), v3 = __ldcs(vp + 96);
+    const int32_t i0 = idx + d0, i1 = i0 + d1, i2 = i1 + d2, i3 = i2 + d3;
+    idx = i3;
+    const float g0 = __ldg(gv + i0), g1 = __ldg(gv + i1), g2 = __ldg(gv + i2), g3 = __ldg(gv + i3);
+    a0 = fma((double)v0, (double)g0, a0);
+    a1 = fma((double)v1, (double)g1, a1);
+    a0 = fma((double)v2, (double)g2, a0);
+    a1 = fma((double)v3, (double)g3, a1);
+    dp += 128;
+    vp += 128;
+  }
+  for (; k < ke; ++k) {
+    idx += __ldcs(dp);
+    a0 = fma((double)__ldcs(vp), (double)__ldg(gv + idx), a0);
+    dp += 32;
+    vp += 32;
+  }
+  return a0 + a1;
+}
+
+template <typename T, bool LOSS>
+__global__ void __launch_bounds__(128) k_sell16_forward(const Sell16 s, const CsrFwdArgs a) {
+  __shared__ double sp[3 * kMaxW];
+  __shared__ double part[4][32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int i = threadIdx.x; i < 3 * kMaxW; i += blockDim.x) sp[i] = a.spec[i];
+  pdl_wait();  // x is written by the previous kernel; r is read by the previous backward
+  part[warp][lane] = sell16_dot<T>(s, blockIdx.x, warp, lane, a.x);
+  __syncthreads();
+  forward_tail<LOSS>(part, sp, a);
+  pdl_trigger();
+}
+
+template <typename T>
+__global__ void __launch_bounds__(128) k_sell16_backward(const Sell16 s, int32_t d,
+                                                         const float *__restrict__ r,
+                                                         double *__restrict__ g) {
+  __shared__ double part[4][32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  pdl_wait();  // r is written by the forward pass
+  part[warp][lane] = sell16_dot<T>(s, blockIdx.x, warp, lane, r);
+  __syncthreads();
+  if (warp == 0) {
+    const int c = blockIdx.x * 32 + lane;
+    const double v = (part[0][lane] + part[1][lane]) + (part[2][lane] + part[3][lane]);
+    if (c < d) g[c] = v;
+  }
+  pdl_trigger();
+}
+
+// (poly_init only) SELL -> SELL16.  lens: per-lane entry counts (row lengths
+// from row_ptr, or column counts); one 128-thread block per slice.
+template <typename T>
+__global__ void k_sell16_pack(const CscEnt<T> *ent, const int64_t *slice_off, int64_t nslices,
+                              const int64_t *row_ptr, const int32_t *cnt, int64_t nlanes,
+                              int16_t *dl, T *val, int32_t *base, int32_t *overflow) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int64_t sl = blockIdx.x; sl < nslices; sl += gridDim.x) {
+    const int64_t o0 = slice_off[sl], len = slice_off[sl + 1] - o0;
+    const int64_t li = sl * 32 + lane;
+    const int64_t mylen = li < nlanes ? (row_ptr ? row_ptr[li + 1] - row_ptr[li] : (int64_t)cnt[li]) : 0;
+    const int64_t q = (len + 3) / 4;
+    const int64_t k0 = (int64_t)warp * q, ke = min(len, k0 + q);
+    int32_t prev = (k0 < mylen) ? ent[(o0 + k0) * 32 + lane].row : 0;
+    base[(sl * 4 + warp) * 32 + lane] = prev;
+    for (int64_t k = k0; k < ke; ++k) {
+      const CscEnt<T> e = ent[(o0 + k) * 32 + lane];
+      int32_t dlt = 0;
+      T v = (T)0;
+      if (k < mylen) {
+        const int64_t dd = (int64_t)e.row - prev;
+        if (dd < -32768 || dd > 32767) atomicOr(overflow, 1);
+        dlt = (int32_t)dd;
+        prev = e.row;
+        v = e.val;
+      }
+      dl[(o0 + k) * 32 + lane] = (int16_t)dlt;
+      val[(o0 + k) * 32 + lane] = v;
+    }
+  }
 }
 
 // (poly_init only) Gather locality of a K4f slice: at step k its 32 lanes

@@ -133,6 +133,12 @@ const void *kCsrFwd[2][2] = {
 };
 const void *kCscBwd[2] = {(const void *)&k_csc_backward<float>,
                           (const void *)&k_csc_backward<double>};
+const void *kSell16Fwd[2][2] = {
+    {(const void *)&k_sell16_forward<float, false>, (const void *)&k_sell16_forward<float, true>},
+    {(const void *)&k_sell16_forward<double, false>, (const void *)&k_sell16_forward<double, true>},
+};
+const void *kSell16Bwd[2] = {(const void *)&k_sell16_backward<float>,
+                             (const void *)&k_sell16_backward<double>};
 constexpr int kSplitFinD = 8192;  // d above which the step tail runs as k_fin_apply
 
 constexpr size_t kSmemLimit = 227 * 1024;
@@ -227,6 +233,8 @@ struct poly_handle {
   float *xa32 = nullptr, *xh32 = nullptr, *xin32 = nullptr;  // CSR: fp32 copies of xa, xh, a caller's x
   int tr_side = 0;                     // CSR, d = s²: fp32 copies also hold x transposed at [d, 2d)
   int64_t tr_slices = 0;               // K4f slices that gather from the transposed copy
+  bool sell16 = false;                 // both SELL copies in the 6-byte delta form
+  Sell16 fwd16{}, bwd16{};
   int64_t sell_steps = 0;              // slice_off[nslices]
   int64_t sell_row_steps = 0;          // row_slice_off[k4_grid]
   int fin_split = 0;
@@ -356,6 +364,12 @@ int enqueue_pass(poly_handle *h, const double *x, bool loss) {
   a.r = h->rbuf;
   a.mode = p.mode;
   a.loss_partials = h->loss_partials;
+  if (h->sell16) {
+    TRY(launch(h, kSell16Fwd[p.dtype][loss ? 1 : 0], dim3(h->k4_grid), dim3(128), 0, true,
+               h->fwd16, a));
+    return launch(h, kSell16Bwd[p.dtype], dim3(h->nslices), dim3(128), 0, true, h->bwd16,
+                  (int32_t)p.d, (const float *)h->rbuf, h->partials);
+  }
   TRY(launch(h, kCsrFwd[p.dtype][loss ? 1 : 0], dim3(h->k4_grid), dim3(128), 0, true,
              (const void *)h->sell_rows, (const int64_t *)h->row_slice_off, a));
   int32_t d32 = (int32_t)p.d;
@@ -532,6 +546,15 @@ int dev_alloc(poly_handle *h, T **ptr, size_t count) {
   h->owned.push_back(p);
   *ptr = (T *)p;
   return POLY_OK;
+}
+
+void dev_release(poly_handle *h, void *ptr) {
+  for (auto it = h->owned.begin(); it != h->owned.end(); ++it)
+    if (*it == ptr) {
+      cudaFree(ptr);
+      h->owned.erase(it);
+      return;
+    }
 }
 
 int copy_in(poly_handle *h, const void **field, size_t bytes) {
@@ -767,6 +790,39 @@ int build_sell_t(poly_handle *h) {
                                            fill_side, (int32_t)p.d, rent);
   h->sell_rows = rent;
   h->sell_row_steps = rsteps;
+  // compact delta form of both copies, when every delta fits int16
+  if (!getenv("POLY_NO_SELL16") && p.n_local > 0) {
+    int32_t *ovf = nullptr;
+    if ((rc = talloc(4, (void **)&ovf))) return done(rc);
+    cudaMemsetAsync(ovf, 0, 4, st);
+    int16_t *fdl = nullptr, *bdl = nullptr;
+    T *fval = nullptr, *bval = nullptr;
+    int32_t *fbase = nullptr, *bbase = nullptr;
+    const size_t fe = (size_t)std::max<int64_t>(1, rsteps) * 32, be = (size_t)std::max<int64_t>(1, steps) * 32;
+    if ((rc = dev_alloc(h, &fdl, fe)) || (rc = dev_alloc(h, &fval, fe)) ||
+        (rc = dev_alloc(h, &fbase, (size_t)nrs * 128)) || (rc = dev_alloc(h, &bdl, be)) ||
+        (rc = dev_alloc(h, &bval, be)) || (rc = dev_alloc(h, &bbase, (size_t)h->nslices * 128)))
+      return done(rc);
+    k_sell16_pack<T><<<(int)std::min<int64_t>(65535, nrs), 128, 0, st>>>(
+        rent, h->row_slice_off, nrs, p.row_ptr, nullptr, p.n_local, fdl, fval, fbase, ovf);
+    k_sell16_pack<T><<<(int)std::min<int64_t>(65535, h->nslices), 128, 0, st>>>(
+        ent, h->slice_off, h->nslices, nullptr, cnt, d, bdl, bval, bbase, ovf);
+    int32_t hov = 0;
+    cudaMemcpyAsync(&hov, ovf, 4, cudaMemcpyDeviceToHost, st);
+    if (cudaStreamSynchronize(st) != cudaSuccess)
+      return done(fail(POLY_ECUDA, "SELL16 pack: %s", cudaGetErrorString(cudaGetLastError())));
+    if (!hov) {
+      h->sell16 = true;
+      h->fwd16 = Sell16{fdl, fval, fbase, h->row_slice_off};
+      h->bwd16 = Sell16{bdl, bval, bbase, h->slice_off};
+      dev_release(h, rent);  // the 8-byte copies are no longer needed
+      dev_release(h, ent);
+      h->sell_rows = h->sell = nullptr;
+    } else {
+      dev_release(h, fdl), dev_release(h, fval), dev_release(h, fbase);
+      dev_release(h, bdl), dev_release(h, bval), dev_release(h, bbase);
+    }
+  }
   if (cudaStreamSynchronize(st) != cudaSuccess)
     return done(fail(POLY_ECUDA, "SELL build: %s", cudaGetErrorString(cudaGetLastError())));
   return done(POLY_OK);

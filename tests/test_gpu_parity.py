@@ -488,3 +488,19 @@ def test_comm_path_single_rank(kind):
     assert rel(xb.cpu().numpy(), xa.cpu().numpy()) <= (0 if kind == "dense" else 1e-10)
     p0.close()
     p1.close()
+
+
+def test_c4_compact_and_wide_sell_agree(c4, monkeypatch):
+    """K4 stores both SELL copies as int16 index deltas + values (6 B/entry)
+    when every delta fits; POLY_NO_SELL16 keeps the 8-byte {index, value}
+    form.  Same sums up to accumulation order, both at oracle parity."""
+    wg, wo = c4
+    W = _W()
+    x = torch.tensor(0.7 * wo["x_star"], device="cuda")
+    g16, l16 = W.make_poly(wg).loss_grad(x)
+    monkeypatch.setenv("POLY_NO_SELL16", "1")
+    g32, l32 = W.make_poly(wg).loss_grad(x)
+    g_ref, l_ref = wo["problem"].F(0.7 * wo["x_star"])
+    assert rel(g16.cpu().numpy(), g32.cpu().numpy()) <= 1e-12
+    assert abs(l16 - l32) <= 1e-12 * abs(l32)
+    assert rel(g16.cpu().numpy(), g_ref) <= TOL32
