@@ -219,56 +219,81 @@ __global__ void __launch_bounds__(128) k_sell_forward(const CscEnt<T> *__restric
 }
 
 // ------------------------------------------------------------------------
-// Compact SELL-32 ("SELL16"): the same slices and steps, stored as two SoA
-// arrays per step — 32 int16 index deltas and 32 values — i.e. 6 bytes per
-// fp32 entry instead of 8.  The four warps of a slice's CTA each take a
-// contiguous quarter of the steps; lane t of warp w starts from the absolute
-// index base[(slice*4 + w)*32 + t] and adds the deltas (0 on padding and at
-// quarter starts).  Built at poly_init from the SELL copies when every delta
-// fits int16 (CT rays: |Δcol| <= side + 1; Aᵀ columns: Δrow <= views x bins
-// gaps), else the library keeps the 8-byte form.
+// Compact SELL-32 ("SELL16"): the same slices, steps grouped by four; per
+// group every lane holds four int16 index deltas (8 B) and four values (16 B
+// for fp32), stored as two lane-contiguous arrays — 6 bytes per fp32 entry
+// instead of 8, two vector loads per four entries.  Groups are dealt to the
+// slice's four warps round-robin (group g to warp g % 4, as the wide form
+// deals steps); each warp follows its own delta chain: the first entry of a
+// group is relative to the lane's last entry in that warp's previous group,
+// the chain starts at base[(slice*4 + w)*32 + lane].  Padding carries delta 0
+// and value 0.  Built at poly_init when every delta fits int16 (CT: |Δ| <=
+// 13 (side + 1) along a ray; Δrow within a column), else the 8-byte form.
 struct Sell16 {
-  const int16_t *dl;
-  const void *val;
-  const int32_t *base;
-  const int64_t *slice_off;
+  const short4 *dl;        // [groups * 32]
+  const void *val;         // [groups * 32] float4 / 4 doubles
+  const int32_t *base;     // [nslices * 4 * 32]
+  const int64_t *slice_off;  // [nslices + 1] slice start, in groups of 4 steps
+};
+
+template <typename T>
+struct Val4;
+template <>
+struct Val4<float> {
+  using type = float4;
+  __device__ static float4 load(const void *p, int64_t i) { return __ldcs((const float4 *)p + i); }
+};
+template <>
+struct Val4<double> {
+  struct type {
+    double x, y, z, w;
+  };
+  __device__ static type load(const void *p, int64_t i) {
+    const double2 *q = (const double2 *)p + 2 * i;
+    const double2 a = __ldcs(q), b = __ldcs(q + 1);
+    return type{a.x, a.y, b.x, b.y};
+  }
 };
 
 template <typename T>
 __device__ __forceinline__ double sell16_dot(const Sell16 &s, int64_t slice, int warp, int lane,
                                              const float *__restrict__ gv) {
-  const int64_t o0 = s.slice_off[slice], len = s.slice_off[slice + 1] - o0;
-  const int64_t q = (len + 3) / 4;
-  int64_t k = (int64_t)warp * q;
-  const int64_t ke = min(len, k + q);
+  const int64_t o0 = s.slice_off[slice], ng = s.slice_off[slice + 1] - o0;
   int32_t idx = s.base[(slice * 4 + warp) * 32 + lane];
-  const int16_t *dp = s.dl + (o0 + k) * 32 + lane;
-  const T *vp = (const T *)s.val + (o0 + k) * 32 + lane;
   double a0 = 0.0, a1 = 0.0;
-  for (; k + 3 < ke; k += 4) {
-    const int16_t d0 = __ldcs(dp), d1 = __ldcs(dp + 32), d2 = __ldcs(dp + 64), d3 = __ldcs(dp + 96);
-    const T v0 = __ldcs(vp), v1 = __ldcs(vp + 32), v2 = __ldcs(vp + 64), v3 = __ldcs(vp + 96);
-    const int32_t i0 = idx + d0, i1 = i0 + d1, i2 = i1 + d2, i3 = i2 + d3;
-    idx = i3;
+  int64_t g = warp;
+  for (; g + 4 < ng; g += 8) {
+    const short4 d0 = __ldcs(s.dl + (o0 + g) * 32 + lane), d1 = __ldcs(s.dl + (o0 + g + 4) * 32 + lane);
+    const auto v0 = Val4<T>::load(s.val, (o0 + g) * 32 + lane);
+    const auto v1 = Val4<T>::load(s.val, (o0 + g + 4) * 32 + lane);
+    const int32_t i0 = idx + d0.x, i1 = i0 + d0.y, i2 = i1 + d0.z, i3 = i2 + d0.w;
+    const int32_t i4 = i3 + d1.x, i5 = i4 + d1.y, i6 = i5 + d1.z, i7 = i6 + d1.w;
+    idx = i7;
     const float g0 = __ldg(gv + i0), g1 = __ldg(gv + i1), g2 = __ldg(gv + i2), g3 = __ldg(gv + i3);
-    a0 = fma((double)v0, (double)g0, a0);
-    a1 = fma((double)v1, (double)g1, a1);
-    a0 = fma((double)v2, (double)g2, a0);
-    a1 = fma((double)v3, (double)g3, a1);
-    dp += 128;
-    vp += 128;
+    const float g4 = __ldg(gv + i4), g5 = __ldg(gv + i5), g6 = __ldg(gv + i6), g7 = __ldg(gv + i7);
+    a0 = fma((double)v0.x, (double)g0, a0);
+    a1 = fma((double)v0.y, (double)g1, a1);
+    a0 = fma((double)v0.z, (double)g2, a0);
+    a1 = fma((double)v0.w, (double)g3, a1);
+    a0 = fma((double)v1.x, (double)g4, a0);
+    a1 = fma((double)v1.y, (double)g5, a1);
+    a0 = fma((double)v1.z, (double)g6, a0);
+    a1 = fma((double)v1.w, (double)g7, a1);
   }
-  for (; k < ke; ++k) {
-    idx += __ldcs(dp);
-    a0 = fma((double)__ldcs(vp), (double)__ldg(gv + idx), a0);
-    dp += 32;
-    vp += 32;
+  if (g < ng) {
+    const short4 d0 = __ldcs(s.dl + (o0 + g) * 32 + lane);
+    const auto v0 = Val4<T>::load(s.val, (o0 + g) * 32 + lane);
+    const int32_t i0 = idx + d0.x, i1 = i0 + d0.y, i2 = i1 + d0.z, i3 = i2 + d0.w;
+    a0 = fma((double)v0.x, (double)__ldg(gv + i0), a0);
+    a1 = fma((double)v0.y, (double)__ldg(gv + i1), a1);
+    a0 = fma((double)v0.z, (double)__ldg(gv + i2), a0);
+    a1 = fma((double)v0.w, (double)__ldg(gv + i3), a1);
   }
   return a0 + a1;
 }
 
 template <typename T, bool LOSS>
-__global__ void __launch_bounds__(128) k_sell16_forward(const Sell16 s, const CsrFwdArgs a) {
+__global__ void __launch_bounds__(128, 12) k_sell16_forward(const Sell16 s, const CsrFwdArgs a) {
   __shared__ double sp[3 * kMaxW];
   __shared__ double part[4][32];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -298,35 +323,49 @@ __global__ void __launch_bounds__(128) k_sell16_backward(const Sell16 s, int32_t
 }
 
 // (poly_init only) SELL -> SELL16.  lens: per-lane entry counts (row lengths
-// from row_ptr, or column counts); one 128-thread block per slice.
+// from row_ptr, or column counts cnt); off16: group offsets of the slices;
+// one 128-thread block per slice, warp w packs groups w, w+4, ...
 template <typename T>
 __global__ void k_sell16_pack(const CscEnt<T> *ent, const int64_t *slice_off, int64_t nslices,
                               const int64_t *row_ptr, const int32_t *cnt, int64_t nlanes,
-                              int16_t *dl, T *val, int32_t *base, int32_t *overflow) {
+                              const int64_t *off16, short4 *dl, T *val, int32_t *base,
+                              int32_t *overflow) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   for (int64_t sl = blockIdx.x; sl < nslices; sl += gridDim.x) {
     const int64_t o0 = slice_off[sl], len = slice_off[sl + 1] - o0;
+    const int64_t g0 = off16[sl], ng = off16[sl + 1] - g0;
     const int64_t li = sl * 32 + lane;
     const int64_t mylen = li < nlanes ? (row_ptr ? row_ptr[li + 1] - row_ptr[li] : (int64_t)cnt[li]) : 0;
-    const int64_t q = (len + 3) / 4;
-    const int64_t k0 = (int64_t)warp * q, ke = min(len, k0 + q);
-    int32_t prev = (k0 < mylen) ? ent[(o0 + k0) * 32 + lane].row : 0;
+    int32_t prev = (4 * warp < min(mylen, len)) ? ent[(o0 + 4 * warp) * 32 + lane].row : 0;
     base[(sl * 4 + warp) * 32 + lane] = prev;
-    for (int64_t k = k0; k < ke; ++k) {
-      const CscEnt<T> e = ent[(o0 + k) * 32 + lane];
-      int32_t dlt = 0;
-      T v = (T)0;
-      if (k < mylen) {
-        const int64_t dd = (int64_t)e.row - prev;
-        if (dd < -32768 || dd > 32767) atomicOr(overflow, 1);
-        dlt = (int32_t)dd;
-        prev = e.row;
-        v = e.val;
+    for (int64_t g = warp; g < ng; g += 4) {
+      int32_t dd[4];
+      T vv[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int64_t k = 4 * g + j;
+        dd[j] = 0;
+        vv[j] = (T)0;
+        if (k < mylen) {
+          const CscEnt<T> e = ent[(o0 + k) * 32 + lane];
+          const int64_t dlt = (int64_t)e.row - prev;
+          if (dlt < -32768 || dlt > 32767) atomicOr(overflow, 1);
+          dd[j] = (int32_t)dlt;
+          prev = e.row;
+          vv[j] = e.val;
+        }
       }
-      dl[(o0 + k) * 32 + lane] = (int16_t)dlt;
-      val[(o0 + k) * 32 + lane] = v;
+      dl[(g0 + g) * 32 + lane] = make_short4((short)dd[0], (short)dd[1], (short)dd[2], (short)dd[3]);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) val[((g0 + g) * 32 + lane) * 4 + j] = vv[j];
     }
   }
+}
+
+__global__ void k_groups_of(const int64_t *slice_off, int64_t nslices, int64_t *len16) {
+  for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s <= nslices;
+       s += (int64_t)gridDim.x * blockDim.x)
+    len16[s] = s < nslices ? (slice_off[s + 1] - slice_off[s] + 3) / 4 : 0;
 }
 
 // (poly_init only) Gather locality of a K4f slice: at step k its 32 lanes

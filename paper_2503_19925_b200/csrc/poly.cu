@@ -793,38 +793,55 @@ int build_sell_t(poly_handle *h) {
   // compact delta form of both copies, when every delta fits int16
   if (!getenv("POLY_NO_SELL16") && p.n_local > 0) {
     int32_t *ovf = nullptr;
-    if ((rc = talloc(4, (void **)&ovf))) return done(rc);
+    int64_t *len16 = nullptr, *foff = nullptr, *boff = nullptr;
+    const int64_t nmax = std::max<int64_t>(nrs, h->nslices) + 1;
+    if ((rc = talloc(4, (void **)&ovf)) || (rc = talloc((size_t)nmax * 8, (void **)&len16)))
+      return done(rc);
+    if ((rc = dev_alloc(h, &foff, (size_t)nrs + 1)) || (rc = dev_alloc(h, &boff, (size_t)h->nslices + 1)))
+      return done(rc);
+    size_t tb5 = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, tb5, len16, foff, (int)nmax, st);
+    void *ts5 = nullptr;
+    if ((rc = talloc(tb5, &ts5))) return done(rc);
+    int64_t fgroups = 0, bgroups = 0;
+    k_groups_of<<<64, 256, 0, st>>>(h->row_slice_off, nrs, len16);
+    cub::DeviceScan::ExclusiveSum(ts5, tb5, len16, foff, (int)nrs + 1, st);
+    cudaMemcpyAsync(&fgroups, foff + nrs, 8, cudaMemcpyDeviceToHost, st);
+    if (cudaStreamSynchronize(st) != cudaSuccess) return done(fail(POLY_ECUDA, "SELL16 scan"));
+    k_groups_of<<<64, 256, 0, st>>>(h->slice_off, h->nslices, len16);
+    cub::DeviceScan::ExclusiveSum(ts5, tb5, len16, boff, (int)h->nslices + 1, st);
+    cudaMemcpyAsync(&bgroups, boff + h->nslices, 8, cudaMemcpyDeviceToHost, st);
     cudaMemsetAsync(ovf, 0, 4, st);
-    int16_t *fdl = nullptr, *bdl = nullptr;
+    if (cudaStreamSynchronize(st) != cudaSuccess) return done(fail(POLY_ECUDA, "SELL16 scan"));
+    short4 *fdl = nullptr, *bdl = nullptr;
     T *fval = nullptr, *bval = nullptr;
     int32_t *fbase = nullptr, *bbase = nullptr;
-    const size_t fe = (size_t)std::max<int64_t>(1, rsteps) * 32, be = (size_t)std::max<int64_t>(1, steps) * 32;
-    if ((rc = dev_alloc(h, &fdl, fe)) || (rc = dev_alloc(h, &fval, fe)) ||
+    const size_t fe = (size_t)std::max<int64_t>(1, fgroups) * 32, be = (size_t)std::max<int64_t>(1, bgroups) * 32;
+    if ((rc = dev_alloc(h, &fdl, fe)) || (rc = dev_alloc(h, &fval, fe * 4)) ||
         (rc = dev_alloc(h, &fbase, (size_t)nrs * 128)) || (rc = dev_alloc(h, &bdl, be)) ||
-        (rc = dev_alloc(h, &bval, be)) || (rc = dev_alloc(h, &bbase, (size_t)h->nslices * 128)))
+        (rc = dev_alloc(h, &bval, be * 4)) || (rc = dev_alloc(h, &bbase, (size_t)h->nslices * 128)))
       return done(rc);
     k_sell16_pack<T><<<(int)std::min<int64_t>(65535, nrs), 128, 0, st>>>(
-        rent, h->row_slice_off, nrs, p.row_ptr, nullptr, p.n_local, fdl, fval, fbase, ovf);
+        rent, h->row_slice_off, nrs, p.row_ptr, nullptr, p.n_local, foff, fdl, fval, fbase, ovf);
     k_sell16_pack<T><<<(int)std::min<int64_t>(65535, h->nslices), 128, 0, st>>>(
-        ent, h->slice_off, h->nslices, nullptr, cnt, d, bdl, bval, bbase, ovf);
+        ent, h->slice_off, h->nslices, nullptr, cnt, d, boff, bdl, bval, bbase, ovf);
     int32_t hov = 0;
     cudaMemcpyAsync(&hov, ovf, 4, cudaMemcpyDeviceToHost, st);
     if (cudaStreamSynchronize(st) != cudaSuccess)
       return done(fail(POLY_ECUDA, "SELL16 pack: %s", cudaGetErrorString(cudaGetLastError())));
     if (!hov) {
       h->sell16 = true;
-      h->fwd16 = Sell16{fdl, fval, fbase, h->row_slice_off};
-      h->bwd16 = Sell16{bdl, bval, bbase, h->slice_off};
+      h->fwd16 = Sell16{fdl, fval, fbase, foff};
+      h->bwd16 = Sell16{bdl, bval, bbase, boff};
       dev_release(h, rent);  // the 8-byte copies are no longer needed
       dev_release(h, ent);
       h->sell_rows = h->sell = nullptr;
     } else {
-      dev_release(h, fdl), dev_release(h, fval), dev_release(h, fbase);
-      dev_release(h, bdl), dev_release(h, bval), dev_release(h, bbase);
+      for (void *q : {(void *)fdl, (void *)fval, (void *)fbase, (void *)bdl, (void *)bval,
+                      (void *)bbase, (void *)foff, (void *)boff})
+        dev_release(h, q);
     }
   }
-  if (cudaStreamSynchronize(st) != cudaSuccess)
-    return done(fail(POLY_ECUDA, "SELL build: %s", cudaGetErrorString(cudaGetLastError())));
   return done(POLY_OK);
 }
 

@@ -504,3 +504,71 @@ def test_c4_compact_and_wide_sell_agree(c4, monkeypatch):
     assert rel(g16.cpu().numpy(), g32.cpu().numpy()) <= 1e-12
     assert abs(l16 - l32) <= 1e-12 * abs(l32)
     assert rel(g16.cpu().numpy(), g_ref) <= TOL32
+
+
+# ------------------------------------------------------------------ C5 (full size, 131 GB)
+@pytest.fixture(scope="module")
+def c5_gpu():
+    free, _ = torch.cuda.mem_get_info()
+    if free < 140e9:
+        pytest.skip(f"C5 needs ~135 GB of HBM, {free / 1e9:.0f} GB free")
+    w = _W().build(G.C5)
+    yield w
+    del w
+    torch.cuda.empty_cache()
+
+
+def test_c5_full_size_parity(c5_gpu):
+    """C5 at its full size in the bench's launch configuration: sampled rows
+    (generated A bit-exact, counts bit-exact, z per row vs the oracle), shard
+    additivity over two row blocks, the Stein population closed form (P4b),
+    and the T = 20 EXACT trajectory against the population recursion (P13)."""
+    from scipy.special import erfcx
+    W = _W()
+    cfg = G.C5
+    w = c5_gpu
+    rows = np.array([0, 1, 4_000_000, 7_999_999])
+    wo = OW.build(cfg, rows=rows)
+    A_s = w["A"][torch.tensor(rows, device="cuda")][:, :cfg.d].cpu().numpy()
+    assert np.array_equal(A_s, wo["A"])
+    assert np.array_equal(w["counts"][torch.tensor(rows, device="cuda")].cpu().numpy(), wo["counts"])
+    p = W.make_poly(w)
+    xs = w["x_star"].cpu().numpy()
+    z = p.forward(w["x_star"]).cpu().numpy()[rows]
+    assert np.allclose(z, wo["problem"].forward(xs), rtol=1e-12, atol=1e-12)
+    r = np.random.default_rng(9)
+    x = r.standard_normal(cfg.d)
+    x *= 0.6 / np.linalg.norm(x)
+    g, l = gpu_F(p, x)
+    half = cfg.n // 2
+    acc, lacc = np.zeros(cfg.d), 0.0
+    for a, b in ((0, half), (half, cfg.n)):
+        sub = dict(w)
+        sub.update(row0=a, n_local=b - a, y=w["y"][a:b], mat=dict(A=w["A"][a:b], d=cfg.d))
+        gs, ls = gpu_F(W.make_poly(sub), x)
+        acc += gs
+        lacc += ls
+    assert rel(acc, g) <= 1e-6 and abs(lacc - l) <= 1e-6 * abs(l)
+    s, mu = cfg.spectrum
+
+    def c(sig):
+        return float(np.sum(s * mu * 0.5 * erfcx(mu * sig / math.sqrt(2.0))))
+    band = 3 * 1.1 * math.sqrt(cfg.d / cfg.n)
+    fbar = cfg.I_bar * (c(np.linalg.norm(x)) * x - c(np.linalg.norm(xs)) * xs)
+    assert rel(g, fbar) <= band
+    # P13: from x_1 = 0 the iterates follow α_t u, u = x⋆/||x⋆||
+    rho = float(np.linalg.norm(xs))
+    u = xs / rho
+    gam = 1.0 / (4.0 * cfg.I_bar * float(np.dot(s, mu)) * 1.05)
+    xt = torch.zeros(cfg.d, dtype=torch.float64, device="cuda")
+    p.solve(xt, cfg.T, gam)
+    xt = xt.cpu().numpy()
+
+    def Fbar(a):
+        return cfg.I_bar * (c(abs(a)) * a - c(rho) * rho)
+    a = 0.0
+    for _ in range(cfg.T):
+        ah = float(np.clip(a - gam * Fbar(a), -cfg.radius, cfg.radius))
+        a = float(np.clip(a - gam * Fbar(ah), -cfg.radius, cfg.radius))
+    assert abs(np.dot(xt, u) - a) <= band and np.linalg.norm(xt - np.dot(xt, u) * u) <= band
+    p.close()
