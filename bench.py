@@ -261,7 +261,7 @@ def run_e2e(P, PW, w, cfg, gamma, args):
         return None
     try:
         import psutil
-        host_ok = a_bytes(w) * 1.5 < psutil.virtual_memory().available
+        host_ok = a_bytes(w) * 1.5 < psutil.virtual_memory().available and a_bytes(w) < 48e9
     except Exception:
         host_ok = a_bytes(w) < 32e9
     if not host_ok:   # C5: a 131 GB pinned host copy of A does not fit the host

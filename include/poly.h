@@ -73,6 +73,11 @@ extern "C" {
 #define POLY_SET_BALL 1      /* X = B(R; center), center NULL = 0 */
 #define POLY_SET_NONNEG 2    /* X = R_+^d */
 #define POLY_SET_NONNEG_BALL 3 /* X = R_+^d ∩ B(R), center must be NULL (P_B ∘ P_+ is exact) */
+#define POLY_SET_TV_NONNEG 4 /* X = {||x||_TV <= tv_tau} ∩ R_+^d for an s x s image (d = s^2),
+                                the paper's CT set: Dykstra (Eq.
+                                projection-intersection) over the TV ball, approximated by the TV
+                                prox with λ bisected to |TV - tau| <= tv_tol, and the orthant */
+#define POLY_SET_TV 5        /* X = {||x||_TV <= tv_tau} alone (same approximate projection)   */
 /* poly_problem.flags */
 #define POLY_FLAG_HOST_INPUTS 1u /* A/row_ptr/col/val/y/s_row/I_row are HOST pointers; copied at init */
 #define POLY_FLAG_NO_GRAPH 2u    /* poly_solve launches kernels directly instead of via a CUDA graph */
@@ -139,6 +144,14 @@ typedef struct poly_problem {
    * windows = 0 or 1: a single window as above. */
   int32_t windows;
   const double *I_win;
+  /* TV sets (POLY_SET_TV_NONNEG, POLY_SET_TV): anisotropic TV of the s x s image
+   * (forward differences, R21).  Zero selects the default in brackets. */
+  double tv_tau;         /* TV radius τ >= 0 (the paper: the truth's TV)          */
+  double tv_tol;         /* [0.01] bisection stop |TV(x̄) - τ| <= tv_tol          */
+  double tv_rtol;        /* [1e-6] prox: FISTA stops at relative primal change <= tv_rtol         */
+  double tv_dykstra_tol; /* [1e-4] Dykstra stops at ||z_{k+1} - z_k|| <= tol    */
+  int32_t tv_max_it;     /* [5000] FISTA iterations per prox                                    */
+  int32_t tv_max_outer;  /* [1000] Dykstra sweeps                                              */
 } poly_problem;
 
 /* Validate *p, copy host parameters, pick the kernel configuration for
@@ -218,6 +231,12 @@ int poly_expected_counts(poly_handle *h, const double *x, double *lam);
  * I_row: device [n] fp32; s, mu: host [W].  Enqueued on `stream`. */
 int poly_reparameterize(int32_t W, const double *s, const double *mu, double I_bar, int64_t n,
                         const double *b, int32_t clamp, float *s_row, float *I_row, void *stream);
+
+/* x = P_X(v) for the handle's constraint set (the projection step a7 alone).
+ * v, x: device [d] fp64 (may alias).  For the TV sets also returns, in
+ * stats (host [3], may be NULL), the Dykstra sweeps, bisection steps and
+ * FISTA iterations that projection used.  Synchronises the stream. */
+int poly_project(poly_handle *h, const double *v, double *x, int64_t *stats);
 
 /* Average device time (ms) of each kernel class over the last poly_solve
  * called with POLY_SOLVE_PROFILE: out[0] loss+grad pass (the fused A-stream

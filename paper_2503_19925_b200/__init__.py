@@ -18,6 +18,7 @@ POLY_DENSE, POLY_CSR = 0, 1
 POLY_F32, POLY_F64 = 0, 1
 POLY_Y_I32, POLY_Y_F32, POLY_Y_F64 = 0, 1, 2
 POLY_SET_NONE, POLY_SET_BALL, POLY_SET_NONNEG, POLY_SET_NONNEG_BALL = 0, 1, 2, 3
+POLY_SET_TV_NONNEG, POLY_SET_TV = 4, 5
 POLY_FLAG_HOST_INPUTS, POLY_FLAG_NO_GRAPH, POLY_FLAG_NO_PDL, POLY_FLAG_COMM = 1, 2, 4, 8
 POLY_SOLVE_PROFILE = 1
 POLY_MODE_EXACT, POLY_MODE_L2, POLY_MODE_L1, POLY_MODE_NLL = 0, 1, 2, 3
@@ -25,7 +26,7 @@ POLY_METHOD_EXTRAGRADIENT, POLY_METHOD_GD = 0, 1
 
 EXPORTED = ["poly_init", "poly_loss_grad", "poly_solve", "poly_forward", "poly_expected_counts",
             "poly_reparameterize", "poly_kernel_times", "poly_describe", "poly_nccl_unique_id",
-            "poly_free", "poly_last_error", "poly_abi_version", "poly_solve_ex"]
+            "poly_free", "poly_last_error", "poly_abi_version", "poly_solve_ex", "poly_project"]
 
 
 class PolyProblem(C.Structure):
@@ -42,6 +43,8 @@ class PolyProblem(C.Structure):
         ("rank", C.c_int32), ("world", C.c_int32), ("nccl_id", C.c_void_p),
         ("stream", C.c_void_p), ("flags", C.c_uint32), ("mode", C.c_int32),
         ("windows", C.c_int32), ("I_win", C.c_void_p),
+        ("tv_tau", C.c_double), ("tv_tol", C.c_double), ("tv_rtol", C.c_double),
+        ("tv_dykstra_tol", C.c_double), ("tv_max_it", C.c_int32), ("tv_max_outer", C.c_int32),
     ]
 
 
@@ -75,6 +78,7 @@ def _load():
     lib.poly_solve.argtypes = [vp, vp, C.c_int, dbl, C.c_uint32, dp, C.POINTER(C.c_int)]
     lib.poly_solve_ex.argtypes = [vp, C.POINTER(PolySolveOpts), vp, vp, C.POINTER(PolySolveInfo)]
     lib.poly_forward.argtypes = [vp, vp, vp]
+    lib.poly_project.argtypes = [vp, vp, vp, C.POINTER(C.c_int64)]
     lib.poly_expected_counts.argtypes = [vp, vp, vp]
     lib.poly_reparameterize.argtypes = [i32, dp, dp, dbl, i64, vp, i32, vp, vp, vp]
     lib.poly_kernel_times.argtypes = [vp, dp, i32]
@@ -139,6 +143,14 @@ def poly_solve_ex(h: int, x_ptr: int, opts: PolySolveOpts, x_last_ptr=None) -> P
         raise PolyError(rc, f"{poly_last_error()} (bad_iter={info.bad_iter})")
     _check(rc)
     return info
+
+
+def poly_project(h: int, v_ptr: int, x_ptr: int):
+    """x = P_X(v); returns the TV statistics (Dykstra sweeps, bisection steps,
+    FISTA iterations) — zeros for the other sets."""
+    st = (C.c_int64 * 3)()
+    _check(_lib.poly_project(h, v_ptr, x_ptr, st))
+    return list(st)
 
 
 def poly_forward(h: int, x_ptr: int, z_ptr: int):

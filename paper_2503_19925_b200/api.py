@@ -13,8 +13,8 @@ import torch
 from . import (POLY_CSR, POLY_DENSE, POLY_F32, POLY_F64, POLY_FLAG_HOST_INPUTS,
                POLY_METHOD_EXTRAGRADIENT, POLY_SET_BALL, POLY_SOLVE_PROFILE, POLY_Y_F32, POLY_Y_F64,
                POLY_Y_I32, PolyProblem, PolySolveOpts, poly_describe, poly_expected_counts,
-               poly_forward, poly_free, poly_init, poly_kernel_times, poly_loss_grad, poly_solve,
-               poly_solve_ex)
+               poly_forward, poly_free, poly_init, poly_kernel_times, poly_loss_grad, poly_project,
+               poly_solve, poly_solve_ex)
 
 _DT = {torch.float32: POLY_F32, torch.float64: POLY_F64}
 _YT = {torch.int32: POLY_Y_I32, torch.float32: POLY_Y_F32, torch.float64: POLY_Y_F64}
@@ -34,7 +34,7 @@ class Poly:
     def __init__(self, *, y, s, mu, I_bar, d=None, A=None, row_ptr=None, col=None, val=None,
                  s_row=None, I_row=None, relu=1, set=POLY_SET_BALL, R=1.0, center=None,
                  n_global=None, row_offset=0, rank=0, world=1, nccl_id=None, stream=None,
-                 flags=0, mode=0, I_win=None):
+                 flags=0, mode=0, I_win=None, tv=None):
         p = PolyProblem()
         host = bool(flags & POLY_FLAG_HOST_INPUTS)
         self._keep = [y, A, row_ptr, col, val, s_row, I_row]
@@ -67,6 +67,8 @@ class Poly:
         self._mu = (C.c_double * len(mu))(*mu)
         p.W, p.s, p.mu = len(mu), C.addressof(self._s), C.addressof(self._mu)
         p.mode = int(mode)
+        for k, v in (tv or {}).items():   # tv_tau, tv_tol, tv_rtol, tv_dykstra_tol, tv_max_it, ...
+            setattr(p, k if k.startswith("tv_") else "tv_" + k, v)
         p.I_bar = float(I_bar)
         if s_row is not None:
             assert s_row.dtype == torch.float32 and I_row.dtype == torch.float32
@@ -125,6 +127,13 @@ class Poly:
         o.T_max, o.method, o.gamma, o.tol = int(T_max), int(method), float(gamma), float(tol)
         o.average, o.flags = int(bool(average)), POLY_SOLVE_PROFILE if profile else 0
         return poly_solve_ex(self.h, x.data_ptr(), o, None if x_last is None else x_last.data_ptr())
+
+    def project(self, v, out=None):
+        """P_X(v) for the handle's set; returns (x, TV statistics)."""
+        assert v.dtype == torch.float64 and v.is_contiguous() and v.numel() == self.d
+        out = torch.empty_like(v) if out is None else out
+        st = poly_project(self.h, v.data_ptr(), out.data_ptr())
+        return out, st
 
     def forward(self, x):
         z = torch.empty(self.n_local, dtype=torch.float64, device=x.device)

@@ -29,6 +29,7 @@
 #include "csr.cuh"
 #include "dense.cuh"
 #include "finalize.cuh"
+#include "tv.cuh"
 
 using namespace poly;
 
@@ -234,6 +235,11 @@ struct poly_handle {
   int tr_side = 0;                     // CSR, d = s²: fp32 copies also hold x transposed at [d, 2d)
   int64_t tr_slices = 0;               // K4f slices that gather from the transposed copy
   bool sell16 = false;                 // both SELL copies in the 6-byte delta form
+  // TV sets: Dykstra state, statistics, cluster launch shape
+  double *tv_zk = nullptr, *tv_p = nullptr, *tv_q = nullptr;
+  int32_t *tv_stats = nullptr;
+  int tv_cl = 0;
+  size_t tv_smem = 0;
   Sell16 fwd16{}, bwd16{};
   int64_t sell_steps = 0;              // slice_off[nslices]
   int64_t sell_row_steps = 0;          // row_slice_off[k4_grid]
@@ -406,10 +412,47 @@ FinArgs fin_base(poly_handle *h, int mode) {
   return f;
 }
 
+// P_X onto a TV set: one cluster of tv_cl CTAs (k_tv_project), in place allowed
+int enqueue_tv(poly_handle *h, const double *v, double *out) {
+  TvArgs a{};
+  a.v = v;
+  a.out = out;
+  a.zk = h->tv_zk;
+  a.p = h->tv_p;
+  a.q = h->tv_q;
+  a.s = (int32_t)llround(std::sqrt((double)h->p.d));
+  a.nonneg = h->p.set == POLY_SET_TV_NONNEG ? 1 : 0;
+  a.tau = h->p.tv_tau;
+  a.tv_tol = h->p.tv_tol > 0.0 ? h->p.tv_tol : 0.01;
+  a.rtol = h->p.tv_rtol > 0.0 ? h->p.tv_rtol : 1e-6;
+  a.tol = h->p.tv_dykstra_tol > 0.0 ? h->p.tv_dykstra_tol : 1e-4;
+  a.max_it = h->p.tv_max_it > 0 ? h->p.tv_max_it : 5000;
+  a.max_outer = h->p.tv_max_outer > 0 ? h->p.tv_max_outer : 1000;
+  a.stats = h->tv_stats;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(h->tv_cl);
+  cfg.blockDim = dim3(kTvThreads);
+  cfg.dynamicSmemBytes = h->tv_smem;
+  cfg.stream = h->work;
+  cudaLaunchAttribute attr[2];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = h->tv_cl;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = h->pdl ? 2 : 1;
+  void *argv[] = {(void *)&a};
+  CK(cudaLaunchKernelExC(&cfg, (const void *)&k_tv_project, argv));
+  return POLY_OK;
+}
+
 int enqueue_fin(poly_handle *h, const FinArgs &f) {
   ProfScope ps(h, 1);
   TRY(launch(h, (const void *)&k_finalize, dim3(h->fin_grid), dim3(256), 0, true, f));
   const bool steps = f.mode == FIN_STEP || f.mode == FIN_STEP_COMM || f.mode == FIN_PROJECT;
+  if (h->tv_cl && steps) TRY(enqueue_tv(h, f.v_scratch, f.v_scratch));
   if (f.split && steps) {
     const int grid = (int)std::min<int64_t>(h->sms, (h->p.d + 255) / 256);
     TRY(launch(h, (const void *)&k_fin_apply, dim3(grid), dim3(256), 0, true, f));
@@ -599,7 +642,15 @@ int validate(const poly_problem *p) {
     return fail(POLY_EUNSUPPORTED, "windows > 1 needs mode EXACT and no per-row spectra");
   if ((p->s_row == nullptr) != (p->I_row == nullptr)) return fail(POLY_EINVAL, "s_row and I_row must both be given or both NULL");
   if (p->relu != 0 && p->relu != 1) return fail(POLY_EINVAL, "relu must be 0 or 1");
-  if (p->set < POLY_SET_NONE || p->set > POLY_SET_NONNEG_BALL) return fail(POLY_EINVAL, "bad set");
+  if (p->set < POLY_SET_NONE || p->set > POLY_SET_TV) return fail(POLY_EINVAL, "bad set");
+  if (p->set == POLY_SET_TV_NONNEG || p->set == POLY_SET_TV) {
+    const int64_t s = (int64_t)llround(std::sqrt((double)p->d));
+    if (s * s != p->d || s < 2) return fail(POLY_EINVAL, "TV sets need d = s*s (an s x s image), s >= 2");
+    if (!(p->tv_tau >= 0.0) || p->tv_tol < 0.0 || p->tv_rtol < 0.0 || p->tv_dykstra_tol < 0.0 ||
+        p->tv_max_it < 0 || p->tv_max_outer < 0)
+      return fail(POLY_EINVAL, "TV parameters must be >= 0");
+    if (p->center) return fail(POLY_EINVAL, "TV sets take no center");
+  }
   if ((p->set == POLY_SET_BALL || p->set == POLY_SET_NONNEG_BALL) && !(p->R > 0.0))
     return fail(POLY_EINVAL, "ball radius must be > 0");
   if (p->set == POLY_SET_NONNEG_BALL && p->center) return fail(POLY_EINVAL, "NONNEG_BALL requires center = NULL");
@@ -999,7 +1050,24 @@ int poly_init(const poly_problem *pin, poly_handle **out) {
       return bail(fail(POLY_ECUDA, "memset failed"));
   }
   h->fin_grid = (int)((p.d + 31) / 32);
-  h->fin_split = p.d > kSplitFinD ? 1 : 0;
+  h->fin_split = (p.d > kSplitFinD || p.set == POLY_SET_TV_NONNEG || p.set == POLY_SET_TV) ? 1 : 0;
+  if (p.set == POLY_SET_TV_NONNEG || p.set == POLY_SET_TV) {
+    const int s = (int)llround(std::sqrt((double)p.d));
+    h->tv_cl = std::min(kTvMaxCL, s);
+    const int cap = ((s + h->tv_cl - 1) / h->tv_cl) * s;
+    h->tv_smem = (size_t)7 * cap * 8 + (4 + (kTvThreads / 32) * 4) * 8;
+    if (h->tv_smem > kSmemLimit)
+      return bail(fail(POLY_EUNSUPPORTED, "TV image side %d too large for one cluster", s));
+    if ((rc = dev_alloc(h, &h->tv_zk, (size_t)p.d)) || (rc = dev_alloc(h, &h->tv_p, (size_t)p.d)) ||
+        (rc = dev_alloc(h, &h->tv_q, (size_t)p.d)) || (rc = dev_alloc(h, &h->tv_stats, 3)))
+      return bail(rc);
+    if (cudaMemsetAsync(h->tv_stats, 0, 12, h->work) != cudaSuccess) return bail(fail(POLY_ECUDA, "memset"));
+    if (cudaFuncSetAttribute((const void *)&k_tv_project, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)h->tv_smem) != cudaSuccess ||
+        cudaFuncSetAttribute((const void *)&k_tv_project, cudaFuncAttributeNonPortableClusterSizeAllowed,
+                             1) != cudaSuccess)
+      return bail(fail(POLY_ECUDA, "TV kernel attributes: %s", cudaGetErrorString(cudaGetLastError())));
+  }
   if ((rc = dev_alloc(h, &h->comm, (size_t)p.d + 1)) != POLY_OK) return bail(rc);
   if ((rc = dev_alloc(h, &h->xa, (size_t)p.d)) != POLY_OK) return bail(rc);
   if ((rc = dev_alloc(h, &h->xh, (size_t)p.d)) != POLY_OK) return bail(rc);
@@ -1400,6 +1468,30 @@ int poly_reparameterize(int32_t W, const double *s, const double *mu, double I_b
   a.I_row = I_row;
   const int grid = (int)std::min<int64_t>(148 * 32, (n + 255) / 256);
   k_reparam<<<grid, 256, 0, (cudaStream_t)stream>>>(a);
+  CK(cudaGetLastError());
+  return POLY_OK;
+}
+
+int poly_project(poly_handle *h, const double *v, double *x, int64_t *stats) {
+  if (!h || !v || !x) return fail(POLY_EINVAL, "NULL argument");
+  TRY(sync_in(h));
+  if (h->tv_stats) CK(cudaMemsetAsync(h->tv_stats, 0, 12, h->work));
+  if (h->tv_cl) {
+    TRY(enqueue_tv(h, v, x));
+  } else {
+    FinArgs f = fin_base(h, FIN_PROJECT);
+    f.anchor = v;
+    f.x_out = x;
+    f.x32_out = nullptr;
+    f.tr_side = 0;
+    TRY(enqueue_fin(h, f));
+  }
+  int32_t hs[3] = {0, 0, 0};
+  if (h->tv_stats) CK(cudaMemcpyAsync(hs, h->tv_stats, 12, cudaMemcpyDeviceToHost, h->work));
+  CK(cudaStreamSynchronize(h->work));
+  if (stats)
+    for (int k = 0; k < 3; ++k) stats[k] = hs[k];
+  TRY(sync_out(h));
   CK(cudaGetLastError());
   return POLY_OK;
 }
