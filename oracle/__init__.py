@@ -17,7 +17,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 _SRC = os.path.join(_HERE, "oracle.c")
 _LIB = os.path.join(_HERE, "liboracle.so")
 
-SET_NONE, SET_BALL, SET_NONNEG, SET_NONNEG_BALL = 0, 1, 2, 3
+SET_NONE, SET_BALL, SET_NONNEG, SET_NONNEG_BALL, SET_TV_NONNEG, SET_TV = 0, 1, 2, 3, 4, 5
 
 
 def build(force: bool = False) -> str:
@@ -38,6 +38,9 @@ class _Problem(C.Structure):
         ("y", C.c_void_p), ("W", C.c_int), ("s", C.c_void_p), ("mu", C.c_void_p),
         ("I_bar", C.c_double), ("s_row", C.c_void_p), ("I_row", C.c_void_p),
         ("relu", C.c_int), ("set", C.c_int), ("R", C.c_double), ("center", C.c_void_p),
+        ("tv_side", C.c_int), ("tv_tau", C.c_double), ("tv_tol", C.c_double),
+        ("tv_rtol", C.c_double), ("tv_dtol", C.c_double), ("tv_max_it", C.c_int),
+        ("tv_max_outer", C.c_int),
     ]
 
 
@@ -112,7 +115,7 @@ class Problem:
 
     def __init__(self, *, y, s, mu, I_bar, d, A=None, row_ptr=None, col=None, val=None,
                  s_row=None, I_row=None, relu=1, set=SET_BALL, R=1.0, center=None,
-                 n_norm=None):
+                 n_norm=None, tv=None):
         self.csr = A is None
         if self.csr:
             self.row_ptr = np.ascontiguousarray(row_ptr, dtype=np.int64)
@@ -157,6 +160,16 @@ class Problem:
         st.I_row = None if self.I_row is None else self.I_row.ctypes.data
         st.relu, st.set, st.R = self.relu, self.set, self.R
         st.center = None if self.center is None else self.center.ctypes.data
+        if set in (SET_TV_NONNEG, SET_TV):
+            tv = dict(tv or {})
+            st.tv_side = int(round(np.sqrt(self.d)))
+            assert st.tv_side ** 2 == self.d
+            st.tv_tau = float(tv["tau"])
+            st.tv_tol = float(tv.get("tol", 0.01))
+            st.tv_rtol = float(tv.get("rtol", 1e-6))
+            st.tv_dtol = float(tv.get("dykstra_tol", 1e-4))
+            st.tv_max_it = int(tv.get("max_it", 5000))
+            st.tv_max_outer = int(tv.get("max_outer", 1000))
         self._st = st
 
     @property
@@ -183,6 +196,12 @@ class Problem:
         return lam
 
     def project(self, v):
+        if self.set in (SET_TV_NONNEG, SET_TV):
+            t = self._st
+            if self.set == SET_TV:
+                return project_tv(v, t.tv_tau, t.tv_tol, t.tv_rtol, t.tv_max_it)[0]
+            return project_tv_nonneg(v, t.tv_tau, t.tv_tol, t.tv_rtol, t.tv_max_it, t.tv_dtol,
+                                     t.tv_max_outer)[0]
         return project(self.set, self.R, self.center, v)
 
     def solve(self, T, gamma, x1=None, trace=False):

@@ -26,7 +26,8 @@
 
 #define ORACLE_CHUNK 4096
 
-enum { OR_SET_NONE = 0, OR_SET_BALL = 1, OR_SET_NONNEG = 2, OR_SET_NONNEG_BALL = 3 };
+enum { OR_SET_NONE = 0, OR_SET_BALL = 1, OR_SET_NONNEG = 2, OR_SET_NONNEG_BALL = 3,
+       OR_SET_TV_NONNEG = 4, OR_SET_TV = 5 };
 
 typedef struct {
   int64_t n, d;             /* rows held here, columns                        */
@@ -48,6 +49,10 @@ typedef struct {
   int set;                  /* constraint set X                               */
   double R;                 /* radius of the ball part of X                   */
   const double *center;     /* [d] or NULL (= 0)                              */
+  /* TV sets (NEXT-2): s x s image, d = s*s; see oracle_project_tv* below   */
+  int tv_side;
+  double tv_tau, tv_tol, tv_rtol, tv_dtol;
+  int tv_max_it, tv_max_outer;
 } oracle_problem;
 
 void oracle_set_threads(int t) {
@@ -218,6 +223,29 @@ void oracle_project(int set, int64_t d, double R, const double *c, const double 
   }
 }
 
+int oracle_project_tv(int side, const double *z, double tau, double tv_tol, double rtol,
+                      int max_it, double *x);
+int oracle_project_tv_nonneg(int side, const double *z, double tau, double tv_tol, double rtol,
+                             int max_it, double tol, int max_outer, double *out);
+
+/* P_X for the problem's set: the closed forms above, or the TV sets of
+ * NEXT-2.  out may alias v. */
+static void project_p(const oracle_problem *p, const double *v, double *out) {
+  if (p->set == OR_SET_TV_NONNEG || p->set == OR_SET_TV) {
+    const int64_t d = p->d;
+    double *t = (double *)malloc((size_t)d * sizeof(double));
+    if (p->set == OR_SET_TV_NONNEG)
+      oracle_project_tv_nonneg(p->tv_side, v, p->tv_tau, p->tv_tol, p->tv_rtol, p->tv_max_it,
+                               p->tv_dtol, p->tv_max_outer, t);
+    else
+      oracle_project_tv(p->tv_side, v, p->tv_tau, p->tv_tol, p->tv_rtol, p->tv_max_it, t);
+    memcpy(out, t, (size_t)d * sizeof(double));
+    free(t);
+    return;
+  }
+  oracle_project(p->set, p->d, p->R, p->center, v, out);
+}
+
 /* EXACT, Eq.(extragrad-method), constant step γ:
  *   x_1 = P_X(x_in)                       (x_1 ∈ X)
  *   x_{t+1/2} = P_X(x_t - γ F(x_t))
@@ -231,17 +259,17 @@ int oracle_solve(const oracle_problem *p, int T, double gamma, double *x, double
   double *xh = (double *)malloc((size_t)d * sizeof(double));
   double *v = (double *)malloc((size_t)d * sizeof(double));
   int bad = 0;
-  oracle_project(p->set, d, p->R, p->center, x, x);
+  project_p(p, x, x);
   for (int t = 1; t <= T && !bad; ++t) {
     double l;
     oracle_F(p, x, g, &l);
     if (trace) trace[2 * (t - 1)] = l;
     for (int64_t k = 0; k < d; ++k) v[k] = x[k] - gamma * g[k];
-    oracle_project(p->set, d, p->R, p->center, v, xh);
+    project_p(p, v, xh);
     oracle_F(p, xh, g, &l);
     if (trace) trace[2 * (t - 1) + 1] = l;
     for (int64_t k = 0; k < d; ++k) v[k] = x[k] - gamma * g[k];
-    oracle_project(p->set, d, p->R, p->center, v, x);
+    project_p(p, v, x);
     for (int64_t k = 0; k < d; ++k)
       if (!isfinite(x[k]) || !isfinite(xh[k])) { bad = t; break; }
   }
@@ -372,7 +400,7 @@ int oracle_solve_avg(const oracle_problem *p, int T_max, double gamma, double to
   double *prev = (double *)malloc((size_t)d * sizeof(double));
   int bad = 0, k = 1;
   double mv = 0.0;
-  oracle_project(p->set, d, p->R, p->center, x, x);
+  project_p(p, x, x);
   memcpy(hist, x, (size_t)d * sizeof(double));
   oracle_average(hist, 1, d, xbar);
   double *g = (double *)malloc((size_t)d * sizeof(double));
@@ -382,10 +410,10 @@ int oracle_solve_avg(const oracle_problem *p, int T_max, double gamma, double to
     /* one EXACT iteration, both half-steps anchored at x_t */
     oracle_F(p, x, g, NULL);
     for (int64_t c = 0; c < d; ++c) v[c] = x[c] - gamma * g[c];
-    oracle_project(p->set, d, p->R, p->center, v, xh);
+    project_p(p, v, xh);
     oracle_F(p, xh, g, NULL);
     for (int64_t c = 0; c < d; ++c) v[c] = x[c] - gamma * g[c];
-    oracle_project(p->set, d, p->R, p->center, v, x);
+    project_p(p, v, x);
     for (int64_t c = 0; c < d; ++c)
       if (!isfinite(x[c])) bad = t;
     if (bad) break;
@@ -472,11 +500,11 @@ int oracle_solve_gd(const oracle_problem *p, int mode, int T, double gamma, doub
   const int64_t d = p->d;
   double *g = (double *)malloc((size_t)d * sizeof(double));
   int bad = 0;
-  oracle_project(p->set, d, p->R, p->center, x, x);
+  project_p(p, x, x);
   for (int t = 1; t <= T && !bad; ++t) {
     oracle_objective(p, mode, x, g, NULL);
     for (int64_t k = 0; k < d; ++k) x[k] = x[k] - gamma * g[k];
-    oracle_project(p->set, d, p->R, p->center, x, x);
+    project_p(p, x, x);
     for (int64_t k = 0; k < d; ++k)
       if (!isfinite(x[k])) { bad = t; break; }
   }

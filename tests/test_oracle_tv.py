@@ -124,3 +124,28 @@ def test_dykstra_tv_nonneg_matches_qp():
     zi = np.abs(z)
     xi, it = oracle.project_tv_nonneg(zi, oracle.tv_norm(zi) + 1.0)
     assert it == 1 and np.array_equal(xi, zi)
+
+
+def test_solve_with_tv_set_reduces_to_orthant_for_large_tau():
+    """With τ above any reachable TV, X1 ∩ X2 = X2 and the Dykstra projection
+    returns max(z, 0) exactly, so EXACT with the TV set equals EXACT with the
+    orthant, iterate for iterate."""
+    r = np.random.default_rng(2)
+    n, d = 300, 36
+    A = np.abs(r.standard_normal((n, d))) / 6
+    s, mu = np.array([0.3, 0.7]), np.array([1.5, 0.8])
+    xs = np.abs(r.standard_normal(d)) * 0.4
+    y = oracle.Problem(A=A, y=np.zeros(n), s=s, mu=mu, I_bar=200.0, d=d).mean(xs)
+    p_tv = oracle.Problem(A=A, y=y, s=s, mu=mu, I_bar=200.0, d=d, set=oracle.SET_TV_NONNEG,
+                          tv={"tau": 1e9})
+    p_nn = oracle.Problem(A=A, y=y, s=s, mu=mu, I_bar=200.0, d=d, set=oracle.SET_NONNEG)
+    x1b, _, _ = p_tv.solve(15, 1e-3, x1=np.linspace(-1, 1, d))
+    x2b, _, _ = p_nn.solve(15, 1e-3, x1=np.linspace(-1, 1, d))
+    assert np.array_equal(x1b, x2b)
+    # a binding τ keeps every iterate in X (nonnegative, TV within the tolerance)
+    tau = 0.5 * oracle.tv_norm(xs)
+    p_b = oracle.Problem(A=A, y=y, s=s, mu=mu, I_bar=200.0, d=d, set=oracle.SET_TV_NONNEG,
+                         tv={"tau": tau, "tol": 1e-6, "rtol": 1e-10, "max_it": 100000,
+                             "dykstra_tol": 1e-9})
+    xb, _, _ = p_b.solve(5, 1e-3, x1=np.linspace(-1, 1, d))
+    assert xb.min() >= 0.0 and oracle.tv_norm(xb) <= tau + 1e-5
