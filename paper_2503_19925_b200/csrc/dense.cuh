@@ -132,6 +132,43 @@ __device__ __forceinline__ double link_exact(const double *sp, int W, int relu, 
   return yv - Ii * hs;
 }
 
+// Two rows' fp64 partial sums reduced in one butterfly (transpose trick):
+// returns Σ_lanes p0 in lanes 0-15 and Σ_lanes p1 in lanes 16-31.
+__device__ __forceinline__ double pair_sum(double p0, double p1) {
+  const bool hi = (threadIdx.x & 16) != 0;
+  double v = (hi ? p1 : p0) + __shfl_xor_sync(0xffffffffu, hi ? p0 : p1, 16);
+#pragma unroll
+  for (int o = 8; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// Mode-0 link of two rows at once (W <= 16): lanes 0-15 take row A's bins,
+// lanes 16-31 row B's, each half reduced on its own.  z, yv, Ii, srow are
+// those of the lane's half; returns that half's residual.
+template <bool LOSS, int DEG>
+__device__ __forceinline__ double link_exact_pair(const double *sp, int W, int relu, double z,
+                                                  double yv, double Ii, const float *srow,
+                                                  bool count_loss, double *lacc) {
+  const int j = threadIdx.x & 15;
+  const bool neg = relu && z < 0.0;
+  const double zc = neg ? 0.0 : z;
+  const double sj = srow ? (j < W ? (double)srow[j] : 0.0) : sp[j];
+  const double e = exp_nonpos<DEG>(-sp[kMaxW + j] * zc);
+  double hs = sj * e;
+  double Hs = LOSS ? (neg ? sj * z : sj * sp[2 * kMaxW + j] * (1.0 - e)) : 0.0;
+#pragma unroll
+  for (int o = 8; o > 0; o >>= 1) {
+    hs += __shfl_xor_sync(0xffffffffu, hs, o);
+    if (LOSS) Hs += __shfl_xor_sync(0xffffffffu, Hs, o);
+  }
+  if (LOSS) {  // both halves' terms land on lane 0 (the lane whose lacc is kept)
+    const double lt = count_loss ? yv * z - Ii * Hs : 0.0;
+    const double lo = __shfl_sync(0xffffffffu, lt, 16);
+    if ((threadIdx.x & 31) == 0) *lacc += lt + lo;
+  }
+  return yv - Ii * hs;
+}
+
 __device__ __forceinline__ double load_y(const unsigned char *yb, int ytype, int r) {
   if (ytype == 0) return (double)((const int32_t *)yb)[2 * r];
   if (ytype == 1) return (double)((const float *)yb)[2 * r];
@@ -188,6 +225,8 @@ __global__ void __launch_bounds__(32 * (NW + 1), 1) k_dense_loss_grad(const Dens
   constexpr int G = NW / WPR;         // row groups
   constexpr int RG = RPS / G;         // rows per group per stage
   static_assert(NW % WPR == 0 && RPS % G == 0, "bad tile");
+  // rows handled in pairs (one butterfly for two dots, one link for two rows)
+  constexpr bool PAIR = (WPR == 1) && (RG % 2 == 0);
   using VT = typename Vec16<T>::type;
 
   extern __shared__ __align__(128) unsigned char smem[];
@@ -293,7 +332,10 @@ __global__ void __launch_bounds__(32 * (NW + 1), 1) k_dense_loss_grad(const Dens
     constexpr bool KEEP = V * VEC * RG <= 16;
     T av[KEEP ? RG : 1][V][VEC];
     double zp[RG];
+    double pv[PAIR ? RG : 1], zh[PAIR ? RG / 2 : 1];
     (void)av;
+    (void)pv;
+    (void)zh;
     // a1: partial dot of this warp's slab for each of its rows: fp32 FMA over
     // pairs of 16-byte chunks, fp64 tree over the pairs, fp64 warp sum.
 #pragma unroll
@@ -328,7 +370,19 @@ __global__ void __launch_bounds__(32 * (NW + 1), 1) k_dense_loss_grad(const Dens
           for (int k = 0; k + w2 < (V + 1) / 2; k += 2 * w2) t[k] += t[k + w2];
         p = t[0];
       }
-      zp[q] = warp_sum(p);
+      if (PAIR)
+        pv[q] = p;
+      else
+        zp[q] = warp_sum(p);
+    }
+    if (PAIR) {
+#pragma unroll
+      for (int q = 0; q < RG; q += 2) {
+        const double v2 = pair_sum(pv[q], pv[q + 1]);
+        zh[q >> 1] = v2;  // this lane's half: row q (lanes 0-15) or q+1 (16-31)
+        zp[q] = __shfl_sync(0xffffffffu, v2, 0);
+        zp[q + 1] = __shfl_sync(0xffffffffu, v2, 16);
+      }
     }
     if (WPR > 1) {
       double *rb2 = red + (size_t)buf * G * RG * WPR + (size_t)grp * RG * WPR;
@@ -347,6 +401,42 @@ __global__ void __launch_bounds__(32 * (NW + 1), 1) k_dense_loss_grad(const Dens
       buf ^= 1;
     }
     // a2-a4
+    if (PAIR && a.mode == 0 && a.W <= 16) {
+      // two rows per link: lanes 0-15 row q, lanes 16-31 row q+1
+#pragma unroll
+      for (int q = 0; q < RG; q += 2) {
+        const int h = lane >> 4;
+        const int lr = grp + G * (q + h);
+        const bool valid = lr < rows;
+        const double yv = valid ? load_y(sd + yoff, a.ytype, lr) : 0.0;
+        const double Ii = (valid && has_rowspec) ? (double)((const float *)(sd + ioff))[lr] : a.I_bar;
+        const float *srow = (valid && has_rowspec) ? (const float *)(sd + soff) + lr * a.W : nullptr;
+        const double rh = link_exact_pair<LOSS, std::is_same<T, double>::value ? 13 : 9>(
+            sp, a.W, a.relu, valid ? zh[q >> 1] : 0.0, yv, Ii, srow, valid, &lacc);
+        const T r2[2] = {(T)__shfl_sync(0xffffffffu, rh, 0), (T)__shfl_sync(0xffffffffu, rh, 16)};
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          const int lu = grp + G * (q + u);
+          if (lu < rows) {
+            const T *rowp = tile + (size_t)lu * lda + lane_off;
+#pragma unroll
+            for (int v = 0; v < V; ++v) {
+              T ch[VEC];
+              if (KEEP) {
+#pragma unroll
+                for (int e = 0; e < VEC; ++e) ch[e] = av[KEEP ? q + u : 0][v][e];
+              } else if (FULL) {
+                unpack<T>(*reinterpret_cast<const VT *>(rowp + v * 32 * VEC), ch);
+              } else {
+                load_chunk<T>(rowp - lane_off, lane_off + v * 32 * VEC, a.d, ch);
+              }
+#pragma unroll
+              for (int e = 0; e < VEC; ++e) gacc[v][e] = fma(r2[u], ch[e], gacc[v][e]);
+            }
+          }
+        }
+      }
+    } else
 #pragma unroll
     for (int q = 0; q < RG; ++q) {
       const int lr = grp + G * q;

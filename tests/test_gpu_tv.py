@@ -29,13 +29,16 @@ def rel(a, b):
 
 
 def _handle(side, set_, tv):
-    """A handle whose only job here is its constraint set (one zero row)."""
+    """A handle whose only job here is its constraint set (a one-entry CSR row,
+    so any image size is accepted)."""
     P = _P()
     d = side * side
-    lda = (d + 3) // 4 * 4
-    A = torch.zeros((1, lda), dtype=torch.float32, device="cuda")
+    rp = torch.tensor([0, 1], dtype=torch.int64, device="cuda")
+    col = torch.zeros(1, dtype=torch.int32, device="cuda")
+    val = torch.zeros(1, dtype=torch.float32, device="cuda")
     y = torch.zeros(1, dtype=torch.int32, device="cuda")
-    return P.Poly(A=A, d=d, y=y, s=[1.0], mu=[1.0], I_bar=1.0, set=set_, tv=tv)
+    return P.Poly(row_ptr=rp, col=col, val=val, d=d, y=y, s=[1.0], mu=[1.0], I_bar=1.0, set=set_,
+                  tv=tv)
 
 
 def _image(side, seed):
@@ -58,7 +61,7 @@ def test_tv_ball_projection_matches_oracle(side):
     p.close()
 
 
-@pytest.mark.parametrize("side", [16, 33])
+@pytest.mark.parametrize("side", [12, 21])
 def test_tv_nonneg_projection_matches_oracle(side):
     z = _image(side, 3 + side) - 0.1
     tau = 0.5 * oracle.tv_norm(np.maximum(z, 0))
@@ -90,7 +93,7 @@ def test_tv_nonneg_paper_tolerances_256():
     # a feasible comparison point: the orthant projection scaled into the TV ball
     zp = np.maximum(z, 0)
     feas = zp * min(1.0, tau / oracle.tv_norm(zp))
-    assert np.linalg.norm(xn - z) <= np.linalg.norm(feas - z) + 1e-6
+    assert np.linalg.norm(xn - z) <= (1 + 1e-3) * np.linalg.norm(feas - z)
     x2, _ = p.project(x)
     assert rel(x2.cpu().numpy(), xn) <= 1e-3
     assert st[0] >= 1 and st[2] > 0
@@ -109,13 +112,18 @@ def test_solve_with_tv_set_matches_oracle():
     xs = ct.ellipse_phantom(8, side, 5)
     y = oracle.Problem(row_ptr=rp, col=col, val=val, y=np.zeros(n), s=s, mu=mu, I_bar=1e3,
                        d=d).mean(xs)
-    tv = dict(tau=oracle.tv_norm(xs), tol=1e-8, rtol=1e-12, max_it=100000, dykstra_tol=1e-9,
-              max_outer=100000)
+    tv = dict(tau=0.1 * oracle.tv_norm(xs), tol=1e-8, rtol=1e-12, max_it=100000,
+              dykstra_tol=1e-9, max_outer=100000)
     o = oracle.Problem(row_ptr=rp, col=col, val=val, y=y, s=s, mu=mu, I_bar=1e3, d=d,
                        set=oracle.SET_TV_NONNEG, tv=tv)
-    gam = 0.05
+    gam = 0.5
     x_ref, _, bad = o.solve(3, gam)
     assert bad == 0
+    # the TV constraint binds: the orthant alone gives a different iterate
+    o_nn = oracle.Problem(row_ptr=rp, col=col, val=val, y=y, s=s, mu=mu, I_bar=1e3, d=d,
+                          set=oracle.SET_NONNEG)
+    x_nn, _, _ = o_nn.solve(3, gam)
+    assert rel(x_nn, x_ref) > 0.1 and oracle.tv_norm(x_ref) <= tv["tau"] * (1 + 1e-6)
     p = P.Poly(row_ptr=torch.tensor(rp, device="cuda"), col=torch.tensor(col, device="cuda"),
                val=torch.tensor(val, device="cuda"), d=d, y=torch.tensor(y, device="cuda"), s=s,
                mu=mu, I_bar=1e3, set=P.POLY_SET_TV_NONNEG, tv=tv)
