@@ -208,11 +208,16 @@ def run_ours(args):
             traffic = json.load(open(tpath)).get("dram_bytes_per_launch")
         except Exception:
             traffic = None
+    read_ceiling = None
+    if "A" in w:   # K8: the same bytes through the same ring, no arithmetic
+        read_ceiling = ab / (poly.stream_probe(20) * 1e-3) / 1e9
     roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
             "frac": (achieved / peak) if achieved else None, "traffic": traffic,
             "kernel": "k_dense_loss_grad" if "A" in w else "k_csr_loss_grad",
             "kernel_ms": kt[0], "finalize_ms": kt[1], "allreduce_ms": kt[2],
             "bytes_per_launch": per_launch, "peak_source": peak_src,
+            "read_ceiling_k8": read_ceiling,
+            "frac_of_read_ceiling": (achieved / read_ceiling) if achieved and read_ceiling else None,
             "step_share": (2 * kt[0]) / (ms / args.steps) if ms > 0 else None}
 
     e2e = None

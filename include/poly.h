@@ -238,6 +238,12 @@ int poly_reparameterize(int32_t W, const double *s, const double *mu, double I_b
  * FISTA iterations that projection used.  Synchronises the stream. */
 int poly_project(poly_handle *h, const double *v, double *x, int64_t *stats);
 
+/* K8, the read-only streaming ceiling of a dense handle: streams the
+ * handle's A through K1's ring (same grid, stages, bulk copies) with no
+ * arithmetic, `reps` times back to back; *ms = average device time per pass.
+ * POLY_EUNSUPPORTED for CSR handles.  Synchronises the stream. */
+int poly_stream_probe(poly_handle *h, int32_t reps, double *ms);
+
 /* Average device time (ms) of each kernel class over the last poly_solve
  * called with POLY_SOLVE_PROFILE: out[0] loss+grad pass (the fused A-stream
  * kernel), out[1] reduce/project kernel(s), out[2] allreduce (0 if world==1),

@@ -26,7 +26,8 @@ POLY_METHOD_EXTRAGRADIENT, POLY_METHOD_GD = 0, 1
 
 EXPORTED = ["poly_init", "poly_loss_grad", "poly_solve", "poly_forward", "poly_expected_counts",
             "poly_reparameterize", "poly_kernel_times", "poly_describe", "poly_nccl_unique_id",
-            "poly_free", "poly_last_error", "poly_abi_version", "poly_solve_ex", "poly_project"]
+            "poly_free", "poly_last_error", "poly_abi_version", "poly_solve_ex", "poly_project",
+            "poly_stream_probe"]
 
 
 class PolyProblem(C.Structure):
@@ -79,6 +80,7 @@ def _load():
     lib.poly_solve_ex.argtypes = [vp, C.POINTER(PolySolveOpts), vp, vp, C.POINTER(PolySolveInfo)]
     lib.poly_forward.argtypes = [vp, vp, vp]
     lib.poly_project.argtypes = [vp, vp, vp, C.POINTER(C.c_int64)]
+    lib.poly_stream_probe.argtypes = [vp, i32, dp]
     lib.poly_expected_counts.argtypes = [vp, vp, vp]
     lib.poly_reparameterize.argtypes = [i32, dp, dp, dbl, i64, vp, i32, vp, vp, vp]
     lib.poly_kernel_times.argtypes = [vp, dp, i32]
@@ -151,6 +153,13 @@ def poly_project(h: int, v_ptr: int, x_ptr: int):
     st = (C.c_int64 * 3)()
     _check(_lib.poly_project(h, v_ptr, x_ptr, st))
     return list(st)
+
+
+def poly_stream_probe(h: int, reps: int = 20) -> float:
+    """K8: ms per read-only pass over the handle's A."""
+    ms = C.c_double()
+    _check(_lib.poly_stream_probe(h, int(reps), C.byref(ms)))
+    return ms.value
 
 
 def poly_forward(h: int, x_ptr: int, z_ptr: int):

@@ -14,7 +14,7 @@ from . import (POLY_CSR, POLY_DENSE, POLY_F32, POLY_F64, POLY_FLAG_HOST_INPUTS,
                POLY_METHOD_EXTRAGRADIENT, POLY_SET_BALL, POLY_SOLVE_PROFILE, POLY_Y_F32, POLY_Y_F64,
                POLY_Y_I32, PolyProblem, PolySolveOpts, poly_describe, poly_expected_counts,
                poly_forward, poly_free, poly_init, poly_kernel_times, poly_loss_grad, poly_project,
-               poly_solve, poly_solve_ex)
+               poly_solve, poly_solve_ex, poly_stream_probe)
 
 _DT = {torch.float32: POLY_F32, torch.float64: POLY_F64}
 _YT = {torch.int32: POLY_Y_I32, torch.float32: POLY_Y_F32, torch.float64: POLY_Y_F64}
@@ -144,6 +144,10 @@ class Poly:
         lam = torch.empty(self.n_local, dtype=torch.float64, device=x.device)
         poly_expected_counts(self.h, x.data_ptr(), lam.data_ptr())
         return lam
+
+    def stream_probe(self, reps=20):
+        """K8 read-only streaming ceiling over this handle's A (ms per pass)."""
+        return poly_stream_probe(self.h, reps)
 
     def kernel_times(self):
         return poly_kernel_times(self.h)

@@ -142,20 +142,25 @@ __device__ __forceinline__ double pair_sum(double p0, double p1) {
   return v;
 }
 
-// Mode-0 link of two rows at once (W <= 16): lanes 0-15 take row A's bins,
-// lanes 16-31 row B's, each half reduced on its own.  z, yv, Ii, srow are
+// Mode-0 link of two rows at once (W <= 32): lanes 0-15 take row A's bins
+// (j and j + 16), lanes 16-31 row B's, each half reduced on its own.  z, yv, Ii, srow are
 // those of the lane's half; returns that half's residual.
 template <bool LOSS, int DEG>
 __device__ __forceinline__ double link_exact_pair(const double *sp, int W, int relu, double z,
                                                   double yv, double Ii, const float *srow,
                                                   bool count_loss, double *lacc) {
-  const int j = threadIdx.x & 15;
   const bool neg = relu && z < 0.0;
   const double zc = neg ? 0.0 : z;
-  const double sj = srow ? (j < W ? (double)srow[j] : 0.0) : sp[j];
-  const double e = exp_nonpos<DEG>(-sp[kMaxW + j] * zc);
-  double hs = sj * e;
-  double Hs = LOSS ? (neg ? sj * z : sj * sp[2 * kMaxW + j] * (1.0 - e)) : 0.0;
+  double hs = 0.0, Hs = 0.0;
+#pragma unroll
+  for (int b = 0; b < 2; ++b) {
+    if (b == 1 && W <= 16) break;  // warp-uniform
+    const int j = (threadIdx.x & 15) + 16 * b;
+    const double sj = srow ? (j < W ? (double)srow[j] : 0.0) : sp[j];
+    const double e = exp_nonpos<DEG>(-sp[kMaxW + j] * zc);
+    hs = fma(sj, e, hs);
+    if (LOSS) Hs += neg ? sj * z : sj * sp[2 * kMaxW + j] * (1.0 - e);
+  }
 #pragma unroll
   for (int o = 8; o > 0; o >>= 1) {
     hs += __shfl_xor_sync(0xffffffffu, hs, o);
@@ -225,8 +230,9 @@ __global__ void __launch_bounds__(32 * (NW + 1), 1) k_dense_loss_grad(const Dens
   constexpr int G = NW / WPR;         // row groups
   constexpr int RG = RPS / G;         // rows per group per stage
   static_assert(NW % WPR == 0 && RPS % G == 0, "bad tile");
-  // rows handled in pairs (one butterfly for two dots, one link for two rows)
-  constexpr bool PAIR = (WPR == 1) && (RG % 2 == 0);
+  // rows handled in pairs (one butterfly for two dots, one link pass for two
+  // rows when W <= 32)
+  constexpr bool PAIR = (RG % 2 == 0);
   using VT = typename Vec16<T>::type;
 
   extern __shared__ __align__(128) unsigned char smem[];
@@ -380,13 +386,21 @@ __global__ void __launch_bounds__(32 * (NW + 1), 1) k_dense_loss_grad(const Dens
       for (int q = 0; q < RG; q += 2) {
         const double v2 = pair_sum(pv[q], pv[q + 1]);
         zh[q >> 1] = v2;  // this lane's half: row q (lanes 0-15) or q+1 (16-31)
-        zp[q] = __shfl_sync(0xffffffffu, v2, 0);
-        zp[q + 1] = __shfl_sync(0xffffffffu, v2, 16);
+        if (WPR == 1) {
+          zp[q] = __shfl_sync(0xffffffffu, v2, 0);
+          zp[q + 1] = __shfl_sync(0xffffffffu, v2, 16);
+        }
       }
     }
     if (WPR > 1) {
       double *rb2 = red + (size_t)buf * G * RG * WPR + (size_t)grp * RG * WPR;
-      if (lane == 0) {
+      if (PAIR) {
+        // lanes 0 and 16 hold this warp's partials of rows q and q+1
+        if ((lane & 15) == 0) {
+#pragma unroll
+          for (int q = 0; q < RG; q += 2) rb2[(q + (lane >> 4)) * WPR + w] = zh[q >> 1];
+        }
+      } else if (lane == 0) {
 #pragma unroll
         for (int q = 0; q < RG; ++q) rb2[q * WPR + w] = zp[q];
       }
@@ -398,10 +412,14 @@ __global__ void __launch_bounds__(32 * (NW + 1), 1) k_dense_loss_grad(const Dens
         for (int k = 0; k < WPR; ++k) z += rb2[q * WPR + k];
         zp[q] = z;
       }
+      if (PAIR) {
+#pragma unroll
+        for (int q = 0; q < RG; q += 2) zh[q >> 1] = (lane & 16) ? zp[q + 1] : zp[q];
+      }
       buf ^= 1;
     }
     // a2-a4
-    if (PAIR && a.mode == 0 && a.W <= 16) {
+    if (PAIR && a.mode == 0 && a.W <= 32) {
       // two rows per link: lanes 0-15 row q, lanes 16-31 row q+1
 #pragma unroll
       for (int q = 0; q < RG; q += 2) {
@@ -501,6 +519,61 @@ __global__ void __launch_bounds__(32 * (NW + 1), 1) k_dense_loss_grad(const Dens
     a.loss_partials[blockIdx.x] = l;
   }
   pdl_trigger();
+}
+
+// K8 — read-only streaming ceiling: K1's producer (the same bulk copies into
+// the same ring, the same stages and grid) with consumers that only wait for
+// each stage and release it.  Times the bytes K1 must move with no math;
+// bench.py reports it beside K1.
+__global__ void __launch_bounds__(64, 1) k_stream_probe(const void *A, int64_t row_bytes, int64_t n,
+                                                        int32_t rps, int32_t stages) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  const int S = stages;
+  const size_t stage_bytes = (size_t)rps * row_bytes;
+  uint64_t *full = reinterpret_cast<uint64_t *>(smem + (size_t)S * stage_bytes);
+  uint64_t *empty = full + S;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t rb = n * (int64_t)blockIdx.x / gridDim.x;
+  const int64_t re = n * (int64_t)(blockIdx.x + 1) / gridDim.x;
+  const int nstage = (int)((re - rb + rps - 1) / rps);
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < S; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+  if (warp == 0) {
+    if (lane == 0) {
+      const uint64_t pol = l2_evict_first_policy();
+      int slot = 0;
+      uint32_t eph = 1;
+      for (int st = 0; st < nstage; ++st) {
+        if (st >= S) mbar_wait(&empty[slot], eph);
+        const int64_t r0 = rb + (int64_t)st * rps;
+        const uint32_t bytes = (uint32_t)(min((int64_t)rps, re - r0) * row_bytes);
+        mbar_arrive_expect_tx(&full[slot], bytes);
+        bulk_g2s(smem + (size_t)slot * stage_bytes, (const unsigned char *)A + r0 * row_bytes, bytes,
+                 &full[slot], pol);
+        if (++slot == S) {
+          slot = 0;
+          eph ^= 1u;
+        }
+      }
+    }
+    return;
+  }
+  int slot = 0;
+  uint32_t fph = 0;
+  for (int st = 0; st < nstage; ++st) {
+    mbar_wait(&full[slot], fph);
+    if (lane == 0) mbar_arrive(&empty[slot]);
+    if (++slot == S) {
+      slot = 0;
+      fph ^= 1u;
+    }
+  }
 }
 
 }  // namespace poly

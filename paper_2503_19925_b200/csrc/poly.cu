@@ -1055,7 +1055,7 @@ int poly_init(const poly_problem *pin, poly_handle **out) {
     const int s = (int)llround(std::sqrt((double)p.d));
     h->tv_cl = std::min(kTvMaxCL, s);
     const int cap = ((s + h->tv_cl - 1) / h->tv_cl) * s;
-    h->tv_smem = (size_t)7 * cap * 8 + (4 + (kTvThreads / 32) * 4) * 8;
+    h->tv_smem = (size_t)7 * cap * 8 + (8 + 4 + (kTvThreads / 32) * 4) * 8;
     if (h->tv_smem > kSmemLimit)
       return bail(fail(POLY_EUNSUPPORTED, "TV image side %d too large for one cluster", s));
     if ((rc = dev_alloc(h, &h->tv_zk, (size_t)p.d)) || (rc = dev_alloc(h, &h->tv_p, (size_t)p.d)) ||
@@ -1491,6 +1491,35 @@ int poly_project(poly_handle *h, const double *v, double *x, int64_t *stats) {
   CK(cudaStreamSynchronize(h->work));
   if (stats)
     for (int k = 0; k < 3; ++k) stats[k] = hs[k];
+  TRY(sync_out(h));
+  CK(cudaGetLastError());
+  return POLY_OK;
+}
+
+int poly_stream_probe(poly_handle *h, int32_t reps, double *ms) {
+  if (!h || !ms || reps < 1) return fail(POLY_EINVAL, "bad arguments");
+  if (h->p.layout != POLY_DENSE) return fail(POLY_EUNSUPPORTED, "the probe streams dense A only");
+  const poly_problem &p = h->p;
+  const int64_t row_bytes = p.lda * h->elsize;
+  const int rps = h->dv->RPS;
+  const size_t smem = (size_t)h->k1_stages * rps * row_bytes + 2 * 8 * (size_t)h->k1_stages;
+  CK(cudaFuncSetAttribute((const void *)&k_stream_probe, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                          (int)smem));
+  TRY(sync_in(h));
+  cudaEvent_t e0, e1;
+  CK(cudaEventCreate(&e0));
+  CK(cudaEventCreate(&e1));
+  k_stream_probe<<<h->k1_grid, 64, smem, h->work>>>(p.A, row_bytes, p.n_local, rps, h->k1_stages);
+  CK(cudaEventRecord(e0, h->work));
+  for (int r = 0; r < reps; ++r)
+    k_stream_probe<<<h->k1_grid, 64, smem, h->work>>>(p.A, row_bytes, p.n_local, rps, h->k1_stages);
+  CK(cudaEventRecord(e1, h->work));
+  CK(cudaEventSynchronize(e1));
+  float t = 0.f;
+  cudaEventElapsedTime(&t, e0, e1);
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  *ms = (double)t / reps;
   TRY(sync_out(h));
   CK(cudaGetLastError());
   return POLY_OK;

@@ -47,17 +47,26 @@ struct TvArgs {
 struct TvBand {
   int s, r0, r1, npx, rank, CL;
   double *z, *uh, *uv, *wh, *wv, *x, *xw;  // [npx] band arrays (shared)
-  double *red;                             // [4] this CTA's cluster-reduction slot
+  double *red;                             // [2][4] this CTA's cluster-reduction slots
   double *wsum;                            // [warps * 4]
+  double *tot;                             // [4] reduced totals
+  int parity;
 };
 
 __device__ __forceinline__ int band_r0(int rank, int s, int CL) { return rank * s / CL; }
 
-// Sum NV per-thread values over the CTA, then over the cluster in rank order;
-// every thread of every CTA receives identical totals.
+// Sum NV per-thread values over the CTA, then over the cluster: warp 0's lane
+// r fetches rank r's partials (one DSMEM round trip) and a butterfly adds
+// them — the same instruction sequence on the same inputs in every CTA, so
+// all CTAs receive identical totals.  The partial slots alternate between
+// two buffers, so one cluster barrier per reduction suffices: a CTA can only
+// rewrite a buffer after every CTA passed the barrier of the reduction in
+// between, i.e. after all reads of it.
 template <int NV>
-__device__ __forceinline__ void cluster_sum(cg::cluster_group &cl, const TvBand &b, double *v) {
+__device__ __forceinline__ void cluster_sum(cg::cluster_group &cl, TvBand &b, double *v) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  double *slot = b.red + 4 * b.parity;
+  b.parity ^= 1;
 #pragma unroll
   for (int k = 0; k < NV; ++k) {
     double t = v[k];
@@ -69,21 +78,27 @@ __device__ __forceinline__ void cluster_sum(cg::cluster_group &cl, const TvBand 
   if (threadIdx.x < NV) {
     double t = 0.0;
     for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += b.wsum[w * 4 + threadIdx.x];
-    b.red[threadIdx.x] = t;
+    slot[threadIdx.x] = t;
   }
   cl.sync();
+  if (warp == 0) {
 #pragma unroll
-  for (int k = 0; k < NV; ++k) {
-    double t = 0.0;
-    for (int r = 0; r < b.CL; ++r) t += cl.map_shared_rank(b.red, r)[k];
-    v[k] = t;
+    for (int k = 0; k < NV; ++k) {
+      double t = lane < b.CL ? cl.map_shared_rank(slot, lane)[k] : 0.0;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+      if (lane == 0) b.tot[k] = t;
+    }
   }
-  cl.sync();  // the slots are rewritten by the next reduction
+  __syncthreads();
+#pragma unroll
+  for (int k = 0; k < NV; ++k) v[k] = b.tot[k];
+  __syncthreads();  // b.tot / b.wsum are rewritten by the next reduction
 }
 
 // ||x||_TV of the band-distributed image in b.x (forward differences; the
 // vertical difference of a band's last row uses the next band's first row).
-__device__ double tv_norm_x(cg::cluster_group &cl, const TvBand &b) {
+__device__ double tv_norm_x(cg::cluster_group &cl, TvBand &b) {
   const double *next_x = b.rank + 1 < b.CL ? cl.map_shared_rank(b.x, b.rank + 1) : nullptr;
   double acc[1] = {0.0};
   for (int i = threadIdx.x; i < b.npx; i += blockDim.x) {
@@ -100,7 +115,7 @@ __device__ double tv_norm_x(cg::cluster_group &cl, const TvBand &b) {
 
 // TV prox of b.z with parameter lam (FISTA on the dual, oracle_prox_tv's
 // iteration); leaves x = z - Dᵀu in b.x.  Returns the FISTA iterations.
-__device__ int tv_prox(cg::cluster_group &cl, const TvBand &b, double lam, double rtol, int max_it) {
+__device__ int tv_prox(cg::cluster_group &cl, TvBand &b, double lam, double rtol, int max_it) {
   const int s = b.s;
   for (int i = threadIdx.x; i < b.npx; i += blockDim.x) {
     b.uh[i] = b.uv[i] = b.wh[i] = b.wv[i] = 0.0;
@@ -113,14 +128,15 @@ __device__ int tv_prox(cg::cluster_group &cl, const TvBand &b, double lam, doubl
   const double *prev_wv = b.rank > 0 ? cl.map_shared_rank(b.wv, b.rank - 1) : nullptr;
   const double *prev_uv = b.rank > 0 ? cl.map_shared_rank(b.uv, b.rank - 1) : nullptr;
   const double *next_xw = b.rank + 1 < b.CL ? cl.map_shared_rank(b.xw, b.rank + 1) : nullptr;
+  const int i0r = (int)threadIdx.x / s, i0c = (int)threadIdx.x - i0r * s;
   double t = 1.0;
   int it = 1;
   for (;; ++it) {
     // phase A: x(u) = z - Dᵀu (the oracle's primal after iteration it-1) and
     // xw = z - Dᵀw; change of x against the previous primal
     double acc[2] = {0.0, 0.0};
-    for (int i = threadIdx.x; i < b.npx; i += blockDim.x) {
-      const int lr = i / s, c = i - lr * s, r = b.r0 + lr;
+    for (int i = threadIdx.x, lr = i0r, c = i0c; i < b.npx; i += blockDim.x) {
+      const int r = b.r0 + lr;
       double dw = 0.0, du = 0.0;
       if (c + 1 < s) dw -= b.wh[i], du -= b.uh[i];
       if (c > 0) dw += b.wh[i - 1], du += b.uh[i - 1];
@@ -135,6 +151,7 @@ __device__ int tv_prox(cg::cluster_group &cl, const TvBand &b, double lam, doubl
       acc[0] += dx * dx;
       acc[1] += xn * xn;
       b.x[i] = xn;
+      for (c += blockDim.x; c >= s; c -= s) ++lr;
     }
     cluster_sum<2>(cl, b, acc);  // also publishes xw to the band above
     if ((it > 1 && sqrt(acc[0]) <= rtol * sqrt(acc[1])) || it > max_it) break;
@@ -142,8 +159,8 @@ __device__ int tv_prox(cg::cluster_group &cl, const TvBand &b, double lam, doubl
     const double tn = 0.5 * (1.0 + sqrt(1.0 + 4.0 * t * t));
     const double beta = (t - 1.0) / tn;
     t = tn;
-    for (int i = threadIdx.x; i < b.npx; i += blockDim.x) {
-      const int lr = i / s, c = i - lr * s, r = b.r0 + lr;
+    for (int i = threadIdx.x, lr = i0r, c = i0c; i < b.npx; i += blockDim.x) {
+      const int r = b.r0 + lr;
       if (c + 1 < s) {
         const double un = fmin(hl, fmax(-hl, b.wh[i] + (b.xw[i + 1] - b.xw[i]) / 8.0));
         b.wh[i] = un + beta * (un - b.uh[i]);
@@ -155,6 +172,7 @@ __device__ int tv_prox(cg::cluster_group &cl, const TvBand &b, double lam, doubl
         b.wv[i] = un + beta * (un - b.uv[i]);
         b.uv[i] = un;
       }
+      for (c += blockDim.x; c >= s; c -= s) ++lr;
     }
     cl.sync();  // duals complete before the next phase A reads the neighbours'
   }
@@ -163,7 +181,7 @@ __device__ int tv_prox(cg::cluster_group &cl, const TvBand &b, double lam, doubl
 
 // P_X1 of the band input b.z into b.x (oracle_project_tv): b.z itself when
 // its TV is <= τ, else the prox with λ bracketed and bisected.
-__device__ void tv_project_ball(cg::cluster_group &cl, const TvBand &b, const TvArgs &a,
+__device__ void tv_project_ball(cg::cluster_group &cl, TvBand &b, const TvArgs &a,
                                 int *n_bis, int *n_fista) {
   for (int i = threadIdx.x; i < b.npx; i += blockDim.x) b.x[i] = b.z[i];
   cl.sync();
@@ -205,7 +223,9 @@ __global__ void __launch_bounds__(kTvThreads, 1) k_tv_project(const TvArgs a) {
   b.x = b.wv + cap;
   b.xw = b.x + cap;
   b.red = b.xw + cap;
-  b.wsum = b.red + 4;
+  b.tot = b.red + 8;
+  b.wsum = b.tot + 4;
+  b.parity = 0;
   pdl_wait();  // v is written by the previous kernel
   pdl_trigger();
   const int64_t g0 = (int64_t)b.r0 * a.s;
