@@ -140,6 +140,15 @@ def gamma_for(cfg):
     return 1.0 / (4.0 * cfg.I_bar * lam * float(np.dot(s, mu)))
 
 
+def launches_per_step(w, cfg, world):
+    """Our kernels per EXACT iteration (2 F evaluations): the pass (K1, or
+    K4f + K4b), the reduce/step kernel, + k_fin_apply when d > 8192, and with
+    world > 1 a REDUCE kernel per evaluation (the NCCL allreduce kernel is the
+    library's, not counted)."""
+    per_eval = (1 if "A" in w else 2) + 1 + (1 if cfg.d > 8192 else 0) + (1 if world > 1 else 0)
+    return 2 * per_eval
+
+
 def a_bytes(w):
     if "A" in w:
         n, d = w["n_local"], w["cfg"].d
@@ -248,7 +257,7 @@ def run_ours(args):
             "roofline": roof,
             "cpu_baseline": cpu,
             "e2e": e2e,
-            "gpu_launches": 4 * args.steps + 1 if world == 1 else 6 * args.steps + 1,
+            "gpu_launches": launches_per_step(w, cfg, world) * args.steps,
             "clocks": clocks,
         }
         print(json.dumps(line), flush=True)

@@ -430,7 +430,7 @@ __global__ void __launch_bounds__(32 * (NW + 1), 1) k_dense_loss_grad(const Dens
         const double Ii = (valid && has_rowspec) ? (double)((const float *)(sd + ioff))[lr] : a.I_bar;
         const float *srow = (valid && has_rowspec) ? (const float *)(sd + soff) + lr * a.W : nullptr;
         const double rh = link_exact_pair<LOSS, std::is_same<T, double>::value ? 13 : 9>(
-            sp, a.W, a.relu, valid ? zh[q >> 1] : 0.0, yv, Ii, srow, valid, &lacc);
+            sp, a.W, a.relu, valid ? zh[q >> 1] : 0.0, yv, Ii, srow, valid && w == 0, &lacc);
         const T r2[2] = {(T)__shfl_sync(0xffffffffu, rh, 0), (T)__shfl_sync(0xffffffffu, rh, 16)};
 #pragma unroll
         for (int u = 0; u < 2; ++u) {

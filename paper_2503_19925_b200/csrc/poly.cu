@@ -114,12 +114,12 @@ struct DenseVariant {
 // columns per slab: 32 lanes x (16 B / elsize) x V
 const DenseVariant kDenseF32[] = {
     DV(float, 1, 1, 16, 64), DV(float, 2, 1, 16, 32), DV(float, 4, 1, 16, 32),
-    DV(float, 8, 1, 12, 12), DV(float, 8, 2, 12, 6),  DV(float, 8, 4, 12, 6),
+    DV(float, 8, 1, 12, 24), DV(float, 8, 2, 12, 12), DV(float, 8, 4, 12, 6),
     DV(float, 8, 8, 8, 1),
 };
 // alternative tiles, selectable with POLY_K1_TUNE=<index> (tuning runs only)
 const DenseVariant kDenseTuneF32[] = {
-    DV(float, 8, 1, 12, 24), DV(float, 8, 1, 16, 16), DV(float, 8, 4, 12, 3),  DV(float, 4, 1, 16, 16),
+    DV(float, 8, 1, 12, 12), DV(float, 8, 1, 16, 16), DV(float, 8, 4, 12, 3),  DV(float, 4, 1, 16, 16),
     DV(float, 8, 2, 12, 12), DV(float, 4, 1, 16, 48), DV(float, 8, 1, 8, 16),  DV(float, 8, 4, 8, 4),
 };
 const DenseVariant kDenseF64[] = {
