@@ -129,13 +129,23 @@ __device__ int tv_prox(cg::cluster_group &cl, TvBand &b, double lam, double rtol
   const double *prev_uv = b.rank > 0 ? cl.map_shared_rank(b.uv, b.rank - 1) : nullptr;
   const double *next_xw = b.rank + 1 < b.CL ? cl.map_shared_rank(b.xw, b.rank + 1) : nullptr;
   const int i0r = (int)threadIdx.x / s, i0c = (int)threadIdx.x - i0r * s;
+  // this thread's last pixel (pixels i = tid + k * blockDim; at most one per row
+  // since s <= blockDim for every supported band)
+  const int last_i = (int)threadIdx.x < b.npx
+                         ? (int)threadIdx.x + ((b.npx - 1 - (int)threadIdx.x) / (int)blockDim.x) * (int)blockDim.x
+                         : -1;
+  const int last_r = last_i >= 0 ? last_i / s : -1, last_c = last_i >= 0 ? last_i - last_r * s : 0;
   double t = 1.0;
   int it = 1;
   for (;; ++it) {
     // phase A: x(u) = z - Dᵀu (the oracle's primal after iteration it-1) and
     // xw = z - Dᵀw; change of x against the previous primal
     double acc[2] = {0.0, 0.0};
-    for (int i = threadIdx.x, lr = i0r, c = i0c; i < b.npx; i += blockDim.x) {
+    // the band's first row needs the previous band's last-row duals (DSMEM):
+    // issued first, used last (pixels walked in reverse)
+    double hwv = 0.0, huv = 0.0;
+    if (i0r == 0 && b.rank > 0) hwv = prev_wv[prev_off + i0c], huv = prev_uv[prev_off + i0c];
+    for (int i = last_i, lr = last_r, c = last_c; i >= (int)threadIdx.x; i -= blockDim.x) {
       const int r = b.r0 + lr;
       double dw = 0.0, du = 0.0;
       if (c + 1 < s) dw -= b.wh[i], du -= b.uh[i];
@@ -143,7 +153,7 @@ __device__ int tv_prox(cg::cluster_group &cl, TvBand &b, double lam, double rtol
       if (r + 1 < s) dw -= b.wv[i], du -= b.uv[i];
       if (r > 0) {
         if (lr > 0) dw += b.wv[i - s], du += b.uv[i - s];
-        else dw += prev_wv[prev_off + c], du += prev_uv[prev_off + c];
+        else dw += hwv, du += huv;
       }
       const double xn = b.z[i] - du;
       b.xw[i] = b.z[i] - dw;
@@ -151,7 +161,7 @@ __device__ int tv_prox(cg::cluster_group &cl, TvBand &b, double lam, double rtol
       acc[0] += dx * dx;
       acc[1] += xn * xn;
       b.x[i] = xn;
-      for (c += blockDim.x; c >= s; c -= s) ++lr;
+      for (c -= blockDim.x; c < 0; c += s) --lr;
     }
     cluster_sum<2>(cl, b, acc);  // also publishes xw to the band above
     if ((it > 1 && sqrt(acc[0]) <= rtol * sqrt(acc[1])) || it > max_it) break;
@@ -159,6 +169,9 @@ __device__ int tv_prox(cg::cluster_group &cl, TvBand &b, double lam, double rtol
     const double tn = 0.5 * (1.0 + sqrt(1.0 + 4.0 * t * t));
     const double beta = (t - 1.0) / tn;
     t = tn;
+    // the band's last row needs the next band's first-row xw (DSMEM): issued
+    // first, used last (pixels walked forward)
+    const double hxw = (last_r == b.r1 - b.r0 - 1 && next_xw) ? next_xw[last_c] : 0.0;
     for (int i = threadIdx.x, lr = i0r, c = i0c; i < b.npx; i += blockDim.x) {
       const int r = b.r0 + lr;
       if (c + 1 < s) {
@@ -167,7 +180,7 @@ __device__ int tv_prox(cg::cluster_group &cl, TvBand &b, double lam, double rtol
         b.uh[i] = un;
       }
       if (r + 1 < s) {
-        const double below = (lr + 1 < b.r1 - b.r0) ? b.xw[i + s] : next_xw[c];
+        const double below = (lr + 1 < b.r1 - b.r0) ? b.xw[i + s] : hxw;
         const double un = fmin(hl, fmax(-hl, b.wv[i] + (below - b.xw[i]) / 8.0));
         b.wv[i] = un + beta * (un - b.uv[i]);
         b.uv[i] = un;
