@@ -144,15 +144,15 @@ __device__ __forceinline__ double group8_residual(const double *sp, int W, int r
 // taking rows 8w .. 8w+7 in two rounds of four; every lane runs the group
 // reduction (full-mask shuffles), rows past n are evaluated on dummies.
 template <bool LOSS>
-__device__ __forceinline__ void forward_tail(double (*part)[32], const double *sp,
-                                             const CsrFwdArgs &a) {
+__device__ __forceinline__ double forward_tail(double (*part)[32], const double *sp,
+                                               const CsrFwdArgs &a, int64_t slice) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int sub = lane & 7;
   double lacc = 0.0;
 #pragma unroll
   for (int h = 0; h < 2; ++h) {
     const int rr = warp * 8 + h * 4 + (lane >> 3);
-    const int64_t row = (int64_t)blockIdx.x * 32 + rr;
+    const int64_t row = slice * 32 + rr;
     const bool valid = row < a.n;
     double z = (part[0][rr] + part[1][rr]) + (part[2][rr] + part[3][rr]);
     double yv = 0.0, Ii = a.I_bar;
@@ -175,12 +175,17 @@ __device__ __forceinline__ void forward_tail(double (*part)[32], const double *s
       if (sub == 0) a.r[row] = (float)phi;
     }
   }
-  // per-block loss partial, warps combined in order (deterministic)
+  return lacc;
+}
+
+// per-block loss partial: warps combined in order (deterministic); reuses part
+__device__ __forceinline__ void block_loss(double (*part)[32], double lacc, double *out) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   lacc = warp_sum(lacc);
   __syncthreads();
   if (lane == 0) part[0][warp] = lacc;
   __syncthreads();
-  if (threadIdx.x == 0) a.loss_partials[blockIdx.x] = (part[0][0] + part[0][1]) + (part[0][2] + part[0][3]);
+  if (threadIdx.x == 0) out[blockIdx.x] = (part[0][0] + part[0][1]) + (part[0][2] + part[0][3]);
 }
 
 // K4f on a SELL-32 copy of A (rows as slices): block = 32 consecutive rows,
@@ -214,7 +219,7 @@ __global__ void __launch_bounds__(128) k_sell_forward(const CscEnt<T> *__restric
   }
   part[warp][lane] = (a0 + a1) + (a2 + a3);
   __syncthreads();
-  forward_tail<LOSS>(part, sp, a);
+  block_loss(part, forward_tail<LOSS>(part, sp, a, blockIdx.x), a.loss_partials);
   pdl_trigger();
 }
 
@@ -293,31 +298,40 @@ __device__ __forceinline__ double sell16_dot(const Sell16 &s, int64_t slice, int
 }
 
 template <typename T, bool LOSS>
-__global__ void __launch_bounds__(128, 12) k_sell16_forward(const Sell16 s, const CsrFwdArgs a) {
+__global__ void __launch_bounds__(128, 12) k_sell16_forward(const Sell16 s, int64_t nslices,
+                                                             const CsrFwdArgs a) {
   __shared__ double sp[3 * kMaxW];
   __shared__ double part[4][32];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   for (int i = threadIdx.x; i < 3 * kMaxW; i += blockDim.x) sp[i] = a.spec[i];
   pdl_wait();  // x is written by the previous kernel; r is read by the previous backward
-  part[warp][lane] = sell16_dot<T>(s, blockIdx.x, warp, lane, a.x);
-  __syncthreads();
-  forward_tail<LOSS>(part, sp, a);
+  double lacc = 0.0;
+  for (int64_t sl = blockIdx.x; sl < nslices; sl += gridDim.x) {  // fixed slice -> block map
+    part[warp][lane] = sell16_dot<T>(s, sl, warp, lane, a.x);
+    __syncthreads();
+    lacc += forward_tail<LOSS>(part, sp, a, sl);
+    __syncthreads();  // part is rewritten by the next slice
+  }
+  block_loss(part, lacc, a.loss_partials);
   pdl_trigger();
 }
 
 template <typename T>
-__global__ void __launch_bounds__(128) k_sell16_backward(const Sell16 s, int32_t d,
-                                                         const float *__restrict__ r,
-                                                         double *__restrict__ g) {
+__global__ void __launch_bounds__(128, 12) k_sell16_backward(const Sell16 s, int64_t nslices,
+                                                              int32_t d, const float *__restrict__ r,
+                                                              double *__restrict__ g) {
   __shared__ double part[4][32];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   pdl_wait();  // r is written by the forward pass
-  part[warp][lane] = sell16_dot<T>(s, blockIdx.x, warp, lane, r);
-  __syncthreads();
-  if (warp == 0) {
-    const int c = blockIdx.x * 32 + lane;
-    const double v = (part[0][lane] + part[1][lane]) + (part[2][lane] + part[3][lane]);
-    if (c < d) g[c] = v;
+  for (int64_t sl = blockIdx.x; sl < nslices; sl += gridDim.x) {
+    part[warp][lane] = sell16_dot<T>(s, sl, warp, lane, r);
+    __syncthreads();
+    if (warp == 0) {
+      const int64_t c = sl * 32 + lane;
+      const double v = (part[0][lane] + part[1][lane]) + (part[2][lane] + part[3][lane]);
+      if (c < d) g[c] = v;
+    }
+    __syncthreads();
   }
   pdl_trigger();
 }

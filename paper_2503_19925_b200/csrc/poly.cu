@@ -224,7 +224,8 @@ struct poly_handle {
   int full = 0;
   int k1_grid = 0, k1_threads = 0, k1_stages = 0, k1_side = 0;
   size_t k1_smem = 0;
-  int k4_grid = 0;                     // K4f blocks: 32-row SELL slices of A (= loss partials)
+  int k4_grid = 0;                     // K4f blocks (= loss partials)
+  int nrslices = 0;                    // 32-row SELL slices of A
   void *sell_rows = nullptr;           // CscEnt<T>[row_slice_off[k4_grid] * 32]: {col, val}
   int64_t *row_slice_off = nullptr;    // [k4_grid + 1]
   int nslices = 0;                     // K4b blocks: 32-column SELL slices of A^T
@@ -235,6 +236,7 @@ struct poly_handle {
   int tr_side = 0;                     // CSR, d = s²: fp32 copies also hold x transposed at [d, 2d)
   int64_t tr_slices = 0;               // K4f slices that gather from the transposed copy
   bool sell16 = false;                 // both SELL copies in the 6-byte delta form
+  int k4f16_grid = 0, k4b16_grid = 0;  // resident-slot grids (slices dealt grid-stride)
   // TV sets: Dykstra state, statistics, cluster launch shape
   double *tv_zk = nullptr, *tv_p = nullptr, *tv_q = nullptr;
   int32_t *tv_stats = nullptr;
@@ -371,10 +373,10 @@ int enqueue_pass(poly_handle *h, const double *x, bool loss) {
   a.mode = p.mode;
   a.loss_partials = h->loss_partials;
   if (h->sell16) {
-    TRY(launch(h, kSell16Fwd[p.dtype][loss ? 1 : 0], dim3(h->k4_grid), dim3(128), 0, true,
-               h->fwd16, a));
-    return launch(h, kSell16Bwd[p.dtype], dim3(h->nslices), dim3(128), 0, true, h->bwd16,
-                  (int32_t)p.d, (const float *)h->rbuf, h->partials);
+    TRY(launch(h, kSell16Fwd[p.dtype][loss ? 1 : 0], dim3(h->k4f16_grid), dim3(128), 0, true,
+               h->fwd16, (int64_t)h->nrslices, a));
+    return launch(h, kSell16Bwd[p.dtype], dim3(h->k4b16_grid), dim3(128), 0, true, h->bwd16,
+                  (int64_t)h->nslices, (int32_t)p.d, (const float *)h->rbuf, h->partials);
   }
   TRY(launch(h, kCsrFwd[p.dtype][loss ? 1 : 0], dim3(h->k4_grid), dim3(128), 0, true,
              (const void *)h->sell_rows, (const int64_t *)h->row_slice_off, a));
@@ -802,7 +804,7 @@ int build_sell_t(poly_handle *h) {
   h->sell = ent;
   h->sell_steps = steps;
   // SELL-32 of A (row slices) for K4f
-  const int64_t nrs = h->k4_grid;
+  const int64_t nrs = h->nrslices;
   TRY(dev_alloc(h, &h->row_slice_off, (size_t)nrs + 1));
   int64_t *rlen = nullptr;
   if ((rc = talloc((size_t)(nrs + 1) * 8, (void **)&rlen))) return done(rc);
@@ -882,6 +884,14 @@ int build_sell_t(poly_handle *h) {
       return done(fail(POLY_ECUDA, "SELL16 pack: %s", cudaGetErrorString(cudaGetLastError())));
     if (!hov) {
       h->sell16 = true;
+      int per = 0;
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kSell16Fwd[p.dtype][1], 128, 0);
+      h->k4f16_grid = (int)std::min<int64_t>(nrs, (int64_t)h->sms * std::max(1, per));
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kSell16Bwd[p.dtype], 128, 0);
+      h->k4b16_grid = (int)std::min<int64_t>(h->nslices, (int64_t)h->sms * std::max(1, per));
+      // the loss partials are per forward block
+      if (h->k4f16_grid > h->k4_grid) return done(fail(POLY_ECUDA, "SELL16 grid"));
+      h->k4_grid = h->k4f16_grid;
       h->fwd16 = Sell16{fdl, fval, fbase, foff};
       h->bwd16 = Sell16{bdl, bval, bbase, boff};
       dev_release(h, rent);  // the 8-byte copies are no longer needed
@@ -1034,7 +1044,8 @@ int poly_init(const poly_problem *pin, poly_handle **out) {
     if ((rc = dev_alloc(h, &h->loss_partials, (size_t)h->G)) != POLY_OK) return bail(rc);
   } else {
     h->G = 1;
-    h->k4_grid = (int)std::max<int64_t>(1, (p.n_local + 31) / 32);
+    h->nrslices = (int)std::max<int64_t>(1, (p.n_local + 31) / 32);
+    h->k4_grid = h->nrslices;
     if ((rc = dev_alloc(h, &h->partials, (size_t)p.d)) != POLY_OK) return bail(rc);
     if ((rc = dev_alloc(h, &h->loss_partials, (size_t)h->k4_grid)) != POLY_OK) return bail(rc);
     if ((rc = dev_alloc(h, &h->rbuf, (size_t)std::max<int64_t>(1, p.n_local))) != POLY_OK) return bail(rc);
