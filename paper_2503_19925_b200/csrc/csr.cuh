@@ -234,6 +234,11 @@ __global__ void __launch_bounds__(128) k_sell_forward(const CscEnt<T> *__restric
 // the chain starts at base[(slice*4 + w)*32 + lane].  Padding carries delta 0
 // and value 0.  Built at poly_init when every delta fits int16 (CT: |Δ| <=
 // 13 (side + 1) along a ray; Δrow within a column), else the 8-byte form.
+#ifndef POLY_SELL_UNROLL
+#define POLY_SELL_UNROLL 4
+#endif
+constexpr int kSellUnroll = POLY_SELL_UNROLL;  // groups of four steps in flight per warp
+
 struct Sell16 {
   const short4 *dl;        // [groups * 32]
   const void *val;         // [groups * 32] float4 / 4 doubles
@@ -260,45 +265,61 @@ struct Val4<double> {
   }
 };
 
+// One group of four steps: four deltas, four values, four gathers.
 template <typename T>
+__device__ __forceinline__ void sell16_group(const Sell16 &s, int64_t gi, int32_t &idx,
+                                             const float *__restrict__ gv, double &a0, double &a1) {
+  const short4 dd = __ldcs(s.dl + gi);
+  const auto v = Val4<T>::load(s.val, gi);
+  const int32_t i0 = idx + dd.x, i1 = i0 + dd.y, i2 = i1 + dd.z, i3 = i2 + dd.w;
+  idx = i3;
+  const float g0 = __ldg(gv + i0), g1 = __ldg(gv + i1), g2 = __ldg(gv + i2), g3 = __ldg(gv + i3);
+  a0 = fma((double)v.x, (double)g0, a0);
+  a1 = fma((double)v.y, (double)g1, a1);
+  a0 = fma((double)v.z, (double)g2, a0);
+  a1 = fma((double)v.w, (double)g3, a1);
+}
+
+// This warp's share of a slice: groups warp, warp+4, ..., UNR groups (4*UNR
+// gathers) in flight per iteration.
+template <typename T, int UNR>
 __device__ __forceinline__ double sell16_dot(const Sell16 &s, int64_t slice, int warp, int lane,
                                              const float *__restrict__ gv) {
   const int64_t o0 = s.slice_off[slice], ng = s.slice_off[slice + 1] - o0;
   int32_t idx = s.base[(slice * 4 + warp) * 32 + lane];
   double a0 = 0.0, a1 = 0.0;
   int64_t g = warp;
-  for (; g + 4 < ng; g += 8) {
-    const short4 d0 = __ldcs(s.dl + (o0 + g) * 32 + lane), d1 = __ldcs(s.dl + (o0 + g + 4) * 32 + lane);
-    const auto v0 = Val4<T>::load(s.val, (o0 + g) * 32 + lane);
-    const auto v1 = Val4<T>::load(s.val, (o0 + g + 4) * 32 + lane);
-    const int32_t i0 = idx + d0.x, i1 = i0 + d0.y, i2 = i1 + d0.z, i3 = i2 + d0.w;
-    const int32_t i4 = i3 + d1.x, i5 = i4 + d1.y, i6 = i5 + d1.z, i7 = i6 + d1.w;
-    idx = i7;
-    const float g0 = __ldg(gv + i0), g1 = __ldg(gv + i1), g2 = __ldg(gv + i2), g3 = __ldg(gv + i3);
-    const float g4 = __ldg(gv + i4), g5 = __ldg(gv + i5), g6 = __ldg(gv + i6), g7 = __ldg(gv + i7);
-    a0 = fma((double)v0.x, (double)g0, a0);
-    a1 = fma((double)v0.y, (double)g1, a1);
-    a0 = fma((double)v0.z, (double)g2, a0);
-    a1 = fma((double)v0.w, (double)g3, a1);
-    a0 = fma((double)v1.x, (double)g4, a0);
-    a1 = fma((double)v1.y, (double)g5, a1);
-    a0 = fma((double)v1.z, (double)g6, a0);
-    a1 = fma((double)v1.w, (double)g7, a1);
+  for (; g + 4 * (UNR - 1) < ng; g += 4 * UNR) {
+    // loads of all UNR groups first (independent), then the dependent gathers
+    short4 dd[UNR];
+    typename Val4<T>::type vv[UNR];
+#pragma unroll
+    for (int u = 0; u < UNR; ++u) {
+      dd[u] = __ldcs(s.dl + (o0 + g + 4 * u) * 32 + lane);
+      vv[u] = Val4<T>::load(s.val, (o0 + g + 4 * u) * 32 + lane);
+    }
+    float gg[4 * UNR];
+#pragma unroll
+    for (int u = 0; u < UNR; ++u) {
+      const int32_t i0 = idx + dd[u].x, i1 = i0 + dd[u].y, i2 = i1 + dd[u].z, i3 = i2 + dd[u].w;
+      idx = i3;
+      gg[4 * u] = __ldg(gv + i0), gg[4 * u + 1] = __ldg(gv + i1);
+      gg[4 * u + 2] = __ldg(gv + i2), gg[4 * u + 3] = __ldg(gv + i3);
+    }
+#pragma unroll
+    for (int u = 0; u < UNR; ++u) {
+      a0 = fma((double)vv[u].x, (double)gg[4 * u], a0);
+      a1 = fma((double)vv[u].y, (double)gg[4 * u + 1], a1);
+      a0 = fma((double)vv[u].z, (double)gg[4 * u + 2], a0);
+      a1 = fma((double)vv[u].w, (double)gg[4 * u + 3], a1);
+    }
   }
-  if (g < ng) {
-    const short4 d0 = __ldcs(s.dl + (o0 + g) * 32 + lane);
-    const auto v0 = Val4<T>::load(s.val, (o0 + g) * 32 + lane);
-    const int32_t i0 = idx + d0.x, i1 = i0 + d0.y, i2 = i1 + d0.z, i3 = i2 + d0.w;
-    a0 = fma((double)v0.x, (double)__ldg(gv + i0), a0);
-    a1 = fma((double)v0.y, (double)__ldg(gv + i1), a1);
-    a0 = fma((double)v0.z, (double)__ldg(gv + i2), a0);
-    a1 = fma((double)v0.w, (double)__ldg(gv + i3), a1);
-  }
+  for (; g < ng; g += 4) sell16_group<T>(s, (o0 + g) * 32 + lane, idx, gv, a0, a1);
   return a0 + a1;
 }
 
 template <typename T, bool LOSS>
-__global__ void __launch_bounds__(128, 12) k_sell16_forward(const Sell16 s, int64_t nslices,
+__global__ void __launch_bounds__(128) k_sell16_forward(const Sell16 s, int64_t nslices,
                                                              const CsrFwdArgs a) {
   __shared__ double sp[3 * kMaxW];
   __shared__ double part[4][32];
@@ -307,7 +328,7 @@ __global__ void __launch_bounds__(128, 12) k_sell16_forward(const Sell16 s, int6
   pdl_wait();  // x is written by the previous kernel; r is read by the previous backward
   double lacc = 0.0;
   for (int64_t sl = blockIdx.x; sl < nslices; sl += gridDim.x) {  // fixed slice -> block map
-    part[warp][lane] = sell16_dot<T>(s, sl, warp, lane, a.x);
+    part[warp][lane] = sell16_dot<T, kSellUnroll>(s, sl, warp, lane, a.x);
     __syncthreads();
     lacc += forward_tail<LOSS>(part, sp, a, sl);
     __syncthreads();  // part is rewritten by the next slice
@@ -317,14 +338,14 @@ __global__ void __launch_bounds__(128, 12) k_sell16_forward(const Sell16 s, int6
 }
 
 template <typename T>
-__global__ void __launch_bounds__(128, 12) k_sell16_backward(const Sell16 s, int64_t nslices,
+__global__ void __launch_bounds__(128) k_sell16_backward(const Sell16 s, int64_t nslices,
                                                               int32_t d, const float *__restrict__ r,
                                                               double *__restrict__ g) {
   __shared__ double part[4][32];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   pdl_wait();  // r is written by the forward pass
   for (int64_t sl = blockIdx.x; sl < nslices; sl += gridDim.x) {
-    part[warp][lane] = sell16_dot<T>(s, sl, warp, lane, r);
+    part[warp][lane] = sell16_dot<T, kSellUnroll>(s, sl, warp, lane, r);
     __syncthreads();
     if (warp == 0) {
       const int64_t c = sl * 32 + lane;

@@ -884,11 +884,10 @@ int build_sell_t(poly_handle *h) {
       return done(fail(POLY_ECUDA, "SELL16 pack: %s", cudaGetErrorString(cudaGetLastError())));
     if (!hov) {
       h->sell16 = true;
-      int per = 0;
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kSell16Fwd[p.dtype][1], 128, 0);
-      h->k4f16_grid = (int)std::min<int64_t>(nrs, (int64_t)h->sms * std::max(1, per));
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kSell16Bwd[p.dtype], 128, 0);
-      h->k4b16_grid = (int)std::min<int64_t>(h->nslices, (int64_t)h->sms * std::max(1, per));
+      // one block per slice: the block scheduler balances the uneven slices
+      // (a grid-stride deal over the resident slots measured 12 % slower)
+      h->k4f16_grid = (int)nrs;
+      h->k4b16_grid = h->nslices;
       // the loss partials are per forward block
       if (h->k4f16_grid > h->k4_grid) return done(fail(POLY_ECUDA, "SELL16 grid"));
       h->k4_grid = h->k4f16_grid;

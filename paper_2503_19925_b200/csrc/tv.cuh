@@ -129,6 +129,7 @@ __device__ int tv_prox(cg::cluster_group &cl, TvBand &b, double lam, double rtol
   const double *prev_uv = b.rank > 0 ? cl.map_shared_rank(b.uv, b.rank - 1) : nullptr;
   const double *next_xw = b.rank + 1 < b.CL ? cl.map_shared_rank(b.xw, b.rank + 1) : nullptr;
   const int i0r = (int)threadIdx.x / s, i0c = (int)threadIdx.x - i0r * s;
+  const int st_r = (int)blockDim.x / s, st_c = (int)blockDim.x - st_r * s;  // pixel stride as (rows, cols)
   // this thread's last pixel (pixels i = tid + k * blockDim; at most one per row
   // since s <= blockDim for every supported band)
   const int last_i = (int)threadIdx.x < b.npx
@@ -161,7 +162,8 @@ __device__ int tv_prox(cg::cluster_group &cl, TvBand &b, double lam, double rtol
       acc[0] += dx * dx;
       acc[1] += xn * xn;
       b.x[i] = xn;
-      for (c -= blockDim.x; c < 0; c += s) --lr;
+      c -= st_c, lr -= st_r;
+      if (c < 0) c += s, --lr;
     }
     cluster_sum<2>(cl, b, acc);  // also publishes xw to the band above
     if ((it > 1 && sqrt(acc[0]) <= rtol * sqrt(acc[1])) || it > max_it) break;
@@ -185,7 +187,8 @@ __device__ int tv_prox(cg::cluster_group &cl, TvBand &b, double lam, double rtol
         b.wv[i] = un + beta * (un - b.uv[i]);
         b.uv[i] = un;
       }
-      for (c += blockDim.x; c >= s; c -= s) ++lr;
+      c += st_c, lr += st_r;
+      if (c >= s) c -= s, ++lr;
     }
     cl.sync();  // duals complete before the next phase A reads the neighbours'
   }
