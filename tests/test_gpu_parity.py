@@ -572,3 +572,20 @@ def test_c5_full_size_parity(c5_gpu):
         a = float(np.clip(a - gam * Fbar(ah), -cfg.radius, cfg.radius))
     assert abs(np.dot(xt, u) - a) <= band and np.linalg.norm(xt - np.dot(xt, u) * u) <= band
     p.close()
+
+
+def test_stream_probe_is_the_read_ceiling(c2_gpu):
+    """K8 streams the same bytes as K1 through the same ring with no math: its
+    rate is a plausible HBM read rate and K1 is not faster than it."""
+    P = _P()
+    p = _W().make_poly(c2_gpu)
+    ms = p.stream_probe(10)
+    gbs = G.C2.n * G.C2.d * 4 / (ms * 1e-3) / 1e9
+    assert 3000.0 < gbs < 10000.0, gbs
+    x = torch.zeros(G.C2.d, dtype=torch.float64, device="cuda")
+    p.solve(x, 10, 1e-6, profile=True)
+    k1_ms = p.kernel_times()[0]
+    assert k1_ms >= 0.97 * ms, (k1_ms, ms)
+    with pytest.raises(P.PolyError):
+        wc = _W().build(G.scaled(G.C4, G.C4.n))
+        _W().make_poly(wc).stream_probe(1)
