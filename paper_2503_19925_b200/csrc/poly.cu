@@ -1071,7 +1071,7 @@ int poly_init(const poly_problem *pin, poly_handle **out) {
     h->tv_fn = ppl == 1 ? (const void *)&k_tv_project<1>
              : ppl == 2 ? (const void *)&k_tv_project<2>
              : ppl == 4 ? (const void *)&k_tv_project<4> : (const void *)&k_tv_project<8>;
-    h->tv_smem = (size_t)4 * kTvMaxRows * s * 8 + (8 + 4 + (kTvThreads / 32) * 4) * 8;
+    h->tv_smem = (size_t)4 * kTvMaxRows * tv_row_stride(s) * 8 + (8 + 4 + (kTvThreads / 32) * 4) * 8;
     if ((rc = dev_alloc(h, &h->tv_zk, (size_t)p.d)) || (rc = dev_alloc(h, &h->tv_p, (size_t)p.d)) ||
         (rc = dev_alloc(h, &h->tv_q, (size_t)p.d)) || (rc = dev_alloc(h, &h->tv_stats, 3)))
       return bail(rc);

@@ -55,8 +55,13 @@ __host__ __device__ __forceinline__ int band_r0(int rank, int s, int CL) { retur
 __host__ __device__ inline int tv_ppl(int s) { return s <= 32 ? 1 : s <= 64 ? 2 : s <= 128 ? 4 : 8; }
 
 // Per-CTA context: geometry, the published rows, reduction scratch.
+// Shared rows are padded by one double per eight (element c at sw(c)): lane t
+// touching element t*PPL + k then hits distinct banks within each half-warp.
+__host__ __device__ __forceinline__ int sw(int c) { return c + (c >> 3); }
+__host__ __device__ __forceinline__ int tv_row_stride(int s) { return s + (s >> 3) + 1; }
+
 struct TvCtx {
-  int s, r0, nrow, rank, CL, row, c0;  // row: image row of this warp; c0 = lane * PPL
+  int s, rs, r0, nrow, rank, CL, row, c0;  // rs: padded row stride; c0 = lane * PPL
   bool active;                         // this warp owns an image row of the band
   double *pub_a, *pub_b, *pub_c;       // [kTvMaxRows][s] shared rows: xw | x, wv, uv
   double *zrow;                        // [kTvMaxRows][s] the prox input z (this CTA's rows)
@@ -109,15 +114,15 @@ __device__ __forceinline__ void cluster_sum(cg::cluster_group &cl, TvCtx &t, dou
 __device__ __forceinline__ const double *row_below(cg::cluster_group &cl, const TvCtx &t,
                                                    const double *pub) {
   const int w = threadIdx.x >> 5;
-  if (w + 1 < t.nrow) return pub + (size_t)(w + 1) * t.s;
+  if (w + 1 < t.nrow) return pub + (size_t)(w + 1) * t.rs;
   return cl.map_shared_rank(pub, t.rank + 1);
 }
 __device__ __forceinline__ const double *row_above(cg::cluster_group &cl, const TvCtx &t,
                                                    const double *pub) {
   const int w = threadIdx.x >> 5;
-  if (w > 0) return pub + (size_t)(w - 1) * t.s;
+  if (w > 0) return pub + (size_t)(w - 1) * t.rs;
   const int prev_rows = t.r0 - band_r0(t.rank - 1, t.s, t.CL);
-  return cl.map_shared_rank(pub, t.rank - 1) + (size_t)(prev_rows - 1) * t.s;
+  return cl.map_shared_rank(pub, t.rank - 1) + (size_t)(prev_rows - 1) * t.rs;
 }
 
 // ||x||_TV (forward differences) of the register-resident image.
@@ -127,20 +132,20 @@ __device__ double tv_norm_x(cg::cluster_group &cl, TvCtx &t, const double (&x)[P
   if (t.active) {
 #pragma unroll
     for (int k = 0; k < PPL; ++k)
-      if (t.c0 + k < t.s) t.pub_a[(size_t)w * t.s + t.c0 + k] = x[k];
+      if (t.c0 + k < t.s) t.pub_a[(size_t)w * t.rs + sw(t.c0 + k)] = x[k];
   }
   cl.sync();  // rows published cluster-wide
   double acc[1] = {0.0};
   if (t.active) {
-    const double *mine = t.pub_a + (size_t)w * t.s;
+    const double *mine = t.pub_a + (size_t)w * t.rs;
     const bool has_below = t.row + 1 < t.s;
     const double *bel = has_below ? row_below(cl, t, t.pub_a) : nullptr;
 #pragma unroll
     for (int k = 0; k < PPL; ++k) {
       const int c = t.c0 + k;
       if (c < t.s) {
-        if (c + 1 < t.s) acc[0] += fabs(mine[c + 1] - x[k]);
-        if (has_below) acc[0] += fabs(bel[c] - x[k]);
+        if (c + 1 < t.s) acc[0] += fabs(mine[sw(c + 1)] - x[k]);
+        if (has_below) acc[0] += fabs(bel[sw(c)] - x[k]);
       }
     }
   }
@@ -156,21 +161,21 @@ __device__ int tv_prox(cg::cluster_group &cl, TvCtx &t, double (&x)[PPL], double
                        int max_it) {
   double uh[PPL], uv[PPL], wh[PPL], wv[PPL];
   const int w = threadIdx.x >> 5;
-  const double *z = t.zrow + (size_t)w * t.s + t.c0;  // this thread's pixels of z (shared)
+  const double *z = t.zrow + (size_t)w * t.rs;  // this warp's row of z (shared)
 #pragma unroll
   for (int k = 0; k < PPL; ++k) {
     uh[k] = uv[k] = wh[k] = wv[k] = 0.0;
-    x[k] = (t.active && t.c0 + k < t.s) ? z[k] : 0.0;
+    x[k] = (t.active && t.c0 + k < t.s) ? z[sw(t.c0 + k)] : 0.0;
   }
   if (!(lam > 0.0)) return 0;
   const double hl = 0.5 * lam;
   const bool has_above = t.active && t.row > 0, has_below = t.active && t.row + 1 < t.s;
-  double *mine_a = t.pub_a + (size_t)w * t.s;
-  double *mine_b = t.pub_b + (size_t)w * t.s, *mine_c = t.pub_c + (size_t)w * t.s;
+  double *mine_a = t.pub_a + (size_t)w * t.rs;
+  double *mine_b = t.pub_b + (size_t)w * t.rs, *mine_c = t.pub_c + (size_t)w * t.rs;
   if (t.active) {  // published vertical duals start at 0
 #pragma unroll
     for (int k = 0; k < PPL; ++k)
-      if (t.c0 + k < t.s) mine_b[t.c0 + k] = mine_c[t.c0 + k] = 0.0;
+      if (t.c0 + k < t.s) mine_b[sw(t.c0 + k)] = mine_c[sw(t.c0 + k)] = 0.0;
   }
   cl.sync();
   const double *ab_w = has_above ? row_above(cl, t, t.pub_b) : nullptr;
@@ -192,14 +197,14 @@ __device__ int tv_prox(cg::cluster_group &cl, TvCtx &t, double (&x)[PPL], double
           // uh/wh at c = s-1 and uv/wv at the last image row are never set: 0
           double dw = -wh[k] - wv[k], du = -uh[k] - uv[k];
           if (c > 0) dw += (k > 0 ? wh[k - 1] : whl), du += (k > 0 ? uh[k - 1] : uhl);
-          if (has_above) dw += ab_w[c], du += ab_u[c];
-          const double zk = z[k];
+          if (has_above) dw += ab_w[sw(c)], du += ab_u[sw(c)];
+          const double zk = z[sw(c)];
           const double xn = zk - du;
           const double dx = xn - x[k];
           acc[0] += dx * dx;
           acc[1] += xn * xn;
           x[k] = xn;
-          mine_a[c] = zk - dw;
+          mine_a[sw(c)] = zk - dw;
         }
       }
     }
@@ -215,19 +220,19 @@ __device__ int tv_prox(cg::cluster_group &cl, TvCtx &t, double (&x)[PPL], double
       for (int k = 0; k < PPL; ++k) {
         const int c = t.c0 + k;
         if (c < t.s) {
-          const double xc = mine_a[c];
+          const double xc = mine_a[sw(c)];
           if (c + 1 < t.s) {
-            const double un = fmin(hl, fmax(-hl, wh[k] + (mine_a[c + 1] - xc) / 8.0));
+            const double un = fmin(hl, fmax(-hl, wh[k] + (mine_a[sw(c + 1)] - xc) / 8.0));
             wh[k] = un + beta * (un - uh[k]);
             uh[k] = un;
           }
           if (has_below) {
-            const double un = fmin(hl, fmax(-hl, wv[k] + (bel_xw[c] - xc) / 8.0));
+            const double un = fmin(hl, fmax(-hl, wv[k] + (bel_xw[sw(c)] - xc) / 8.0));
             wv[k] = un + beta * (un - uv[k]);
             uv[k] = un;
           }
-          mine_b[c] = wv[k];
-          mine_c[c] = uv[k];
+          mine_b[sw(c)] = wv[k];
+          mine_c[sw(c)] = uv[k];
         }
       }
     }
@@ -243,9 +248,9 @@ __device__ int tv_prox(cg::cluster_group &cl, TvCtx &t, double (&x)[PPL], double
 template <int PPL>
 __device__ void tv_project_ball(cg::cluster_group &cl, TvCtx &t, const TvArgs &a, double (&x)[PPL],
                                 int *n_bis, int *n_fista) {
-  const double *z = t.zrow + (size_t)(threadIdx.x >> 5) * t.s + t.c0;
+  const double *z = t.zrow + (size_t)(threadIdx.x >> 5) * t.rs;
 #pragma unroll
-  for (int k = 0; k < PPL; ++k) x[k] = (t.active && t.c0 + k < t.s) ? z[k] : 0.0;
+  for (int k = 0; k < PPL; ++k) x[k] = (t.active && t.c0 + k < t.s) ? z[sw(t.c0 + k)] : 0.0;
   if (tv_norm_x<PPL>(cl, t, x) <= a.tau) return;
   double lo = 0.0, hi = 1.0;
   for (int g = 0; g < 200; ++g) {
@@ -271,6 +276,7 @@ __global__ void __launch_bounds__(kTvThreads, 1) k_tv_project(const TvArgs a) {
   cg::cluster_group cl = cg::this_cluster();
   TvCtx t;
   t.s = a.s;
+  t.rs = tv_row_stride(a.s);
   t.CL = (int)cl.num_blocks();
   t.rank = (int)cl.block_rank();
   t.r0 = band_r0(t.rank, a.s, t.CL);
@@ -280,10 +286,10 @@ __global__ void __launch_bounds__(kTvThreads, 1) k_tv_project(const TvArgs a) {
   t.row = t.r0 + w;
   t.c0 = lane * PPL;
   t.pub_a = tsm;
-  t.pub_b = t.pub_a + (size_t)kTvMaxRows * a.s;
-  t.pub_c = t.pub_b + (size_t)kTvMaxRows * a.s;
-  t.zrow = t.pub_c + (size_t)kTvMaxRows * a.s;
-  t.red = t.zrow + (size_t)kTvMaxRows * a.s;
+  t.pub_b = t.pub_a + (size_t)kTvMaxRows * t.rs;
+  t.pub_c = t.pub_b + (size_t)kTvMaxRows * t.rs;
+  t.zrow = t.pub_c + (size_t)kTvMaxRows * t.rs;
+  t.red = t.zrow + (size_t)kTvMaxRows * t.rs;
   t.tot = t.red + 8;
   t.wsum = t.tot + 4;
   t.parity = 0;
@@ -294,12 +300,12 @@ __global__ void __launch_bounds__(kTvThreads, 1) k_tv_project(const TvArgs a) {
 #pragma unroll
   for (int k = 0; k < PPL; ++k) own[k] = t.active && t.c0 + k < t.s;
   double x[PPL];
-  double *zr = t.zrow + (size_t)w * a.s + t.c0;  // own pixels of z (only this thread writes them)
+  double *zr = t.zrow + (size_t)w * t.rs;  // this warp's row of z (each thread writes its pixels)
   int n_bis = 0, n_fista = 0, sweeps = 0;
   if (!a.nonneg) {
 #pragma unroll
     for (int k = 0; k < PPL; ++k)
-      if (own[k]) zr[k] = a.v[g0 + k];
+      if (own[k]) zr[sw(t.c0 + k)] = a.v[g0 + k];
     tv_project_ball<PPL>(cl, t, a, x, &n_bis, &n_fista);
 #pragma unroll
     for (int k = 0; k < PPL; ++k)
@@ -312,7 +318,7 @@ __global__ void __launch_bounds__(kTvThreads, 1) k_tv_project(const TvArgs a) {
     for (sweeps = 1; sweeps <= a.max_outer; ++sweeps) {
 #pragma unroll
       for (int k = 0; k < PPL; ++k)
-        if (own[k]) zr[k] = a.zk[g0 + k] + a.p[g0 + k];
+        if (own[k]) zr[sw(t.c0 + k)] = a.zk[g0 + k] + a.p[g0 + k];
       tv_project_ball<PPL>(cl, t, a, x, &n_bis, &n_fista);  // y_k in x
       double acc[1] = {0.0};
 #pragma unroll
