@@ -65,7 +65,7 @@ struct TvCtx {
   bool active;                         // this warp owns an image row of the band
   double *pub_a, *pub_b, *pub_c;       // [kTvMaxRows][s] shared rows: xw | x, wv, uv
   double *zrow;                        // [kTvMaxRows][s] the prox input z (this CTA's rows)
-  double *red, *tot, *wsum;            // [2][4], [4], [warps][4]
+  double *red, *tot, *wsum;            // [2][4], [4] (unused), [warps][4]
   int parity;
 };
 
@@ -75,6 +75,14 @@ struct TvCtx {
 // all CTAs receive identical totals.  Partial slots alternate between two
 // buffers, so one cluster barrier per reduction suffices: a CTA can rewrite a
 // buffer only after every CTA passed the barrier of the reduction in between.
+// Cluster barrier with release/acquire at cluster scope (the cooperative
+// groups call also issues a GPU-scope MEMBAR, which showed up as the top
+// stall of this kernel).
+__device__ __forceinline__ void cluster_bar() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::
+                   : "memory");
+}
+
 template <int NV>
 __device__ __forceinline__ void cluster_sum(cg::cluster_group &cl, TvCtx &t, double *v) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -93,20 +101,16 @@ __device__ __forceinline__ void cluster_sum(cg::cluster_group &cl, TvCtx &t, dou
     for (int w = 0; w < (int)(blockDim.x >> 5); ++w) a += t.wsum[w * 4 + threadIdx.x];
     slot[threadIdx.x] = a;
   }
-  cl.sync();
-  if (warp == 0) {
+  cluster_bar();
+  // every warp sums the CL slots itself (lane r reads rank r): no further
+  // CTA barrier; all warps of all CTAs compute the same butterfly
 #pragma unroll
-    for (int k = 0; k < NV; ++k) {
-      double a = lane < t.CL ? cl.map_shared_rank(slot, lane)[k] : 0.0;
+  for (int k = 0; k < NV; ++k) {
+    double a = lane < t.CL ? cl.map_shared_rank(slot, lane)[k] : 0.0;
 #pragma unroll
-      for (int o = 16; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
-      if (lane == 0) t.tot[k] = a;
-    }
+    for (int o = 16; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
+    v[k] = a;
   }
-  __syncthreads();
-#pragma unroll
-  for (int k = 0; k < NV; ++k) v[k] = t.tot[k];
-  __syncthreads();
 }
 
 // The published row below / above this warp's row: the neighbour warp's row
@@ -134,7 +138,7 @@ __device__ double tv_norm_x(cg::cluster_group &cl, TvCtx &t, const double (&x)[P
     for (int k = 0; k < PPL; ++k)
       if (t.c0 + k < t.s) t.pub_a[(size_t)w * t.rs + sw(t.c0 + k)] = x[k];
   }
-  cl.sync();  // rows published cluster-wide
+  cluster_bar();  // rows published cluster-wide
   double acc[1] = {0.0};
   if (t.active) {
     const double *mine = t.pub_a + (size_t)w * t.rs;
@@ -177,7 +181,7 @@ __device__ int tv_prox(cg::cluster_group &cl, TvCtx &t, double (&x)[PPL], double
     for (int k = 0; k < PPL; ++k)
       if (t.c0 + k < t.s) mine_b[sw(t.c0 + k)] = mine_c[sw(t.c0 + k)] = 0.0;
   }
-  cl.sync();
+  cluster_bar();
   const double *ab_w = has_above ? row_above(cl, t, t.pub_b) : nullptr;
   const double *ab_u = has_above ? row_above(cl, t, t.pub_c) : nullptr;
   const double *bel_xw = has_below ? row_below(cl, t, t.pub_a) : nullptr;
@@ -238,7 +242,7 @@ __device__ int tv_prox(cg::cluster_group &cl, TvCtx &t, double (&x)[PPL], double
     }
     // duals published, and every read of the xw rows done before the next
     // phase A rewrites them
-    cl.sync();
+    cluster_bar();
   }
   return it - 1;
 }
