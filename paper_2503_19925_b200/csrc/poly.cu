@@ -242,7 +242,6 @@ struct poly_handle {
   int32_t *tv_stats = nullptr;
   int tv_cl = 0;
   size_t tv_smem = 0;
-  const void *tv_fn = nullptr;         // k_tv_project<PPL> for the image side
   Sell16 fwd16{}, bwd16{};
   int64_t sell_steps = 0;              // slice_off[nslices]
   int64_t sell_row_steps = 0;          // row_slice_off[k4_grid]
@@ -447,7 +446,7 @@ int enqueue_tv(poly_handle *h, const double *v, double *out) {
   cfg.attrs = attr;
   cfg.numAttrs = h->pdl ? 2 : 1;
   void *argv[] = {(void *)&a};
-  CK(cudaLaunchKernelExC(&cfg, h->tv_fn, argv));
+  CK(cudaLaunchKernelExC(&cfg, (const void *)&k_tv_project, argv));
   return POLY_OK;
 }
 
@@ -1064,21 +1063,19 @@ int poly_init(const poly_problem *pin, poly_handle **out) {
   h->fin_split = (p.d > kSplitFinD || p.set == POLY_SET_TV_NONNEG || p.set == POLY_SET_TV) ? 1 : 0;
   if (p.set == POLY_SET_TV_NONNEG || p.set == POLY_SET_TV) {
     const int s = (int)llround(std::sqrt((double)p.d));
-    if (s > kTvMaxSide)
-      return bail(fail(POLY_EUNSUPPORTED, "TV sets support images up to %d x %d", kTvMaxSide, kTvMaxSide));
     h->tv_cl = std::min(kTvMaxCL, s);
-    const int ppl = tv_ppl(s);
-    h->tv_fn = ppl == 1 ? (const void *)&k_tv_project<1>
-             : ppl == 2 ? (const void *)&k_tv_project<2>
-             : ppl == 4 ? (const void *)&k_tv_project<4> : (const void *)&k_tv_project<8>;
-    h->tv_smem = (size_t)4 * kTvMaxRows * tv_row_stride(s) * 8 + (8 + 4 + (kTvThreads / 32) * 4) * 8;
+    const int cap = ((s + h->tv_cl - 1) / h->tv_cl) * s;
+    h->tv_smem = (size_t)7 * cap * 8 + (8 + 4 + (kTvThreads / 32) * 4) * 8;
+    if (h->tv_smem > kSmemLimit)
+      return bail(fail(POLY_EUNSUPPORTED, "TV image side %d too large for one cluster", s));
     if ((rc = dev_alloc(h, &h->tv_zk, (size_t)p.d)) || (rc = dev_alloc(h, &h->tv_p, (size_t)p.d)) ||
         (rc = dev_alloc(h, &h->tv_q, (size_t)p.d)) || (rc = dev_alloc(h, &h->tv_stats, 3)))
       return bail(rc);
     if (cudaMemsetAsync(h->tv_stats, 0, 12, h->work) != cudaSuccess) return bail(fail(POLY_ECUDA, "memset"));
-    if (cudaFuncSetAttribute(h->tv_fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    if (cudaFuncSetAttribute((const void *)&k_tv_project, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)h->tv_smem) != cudaSuccess ||
-        cudaFuncSetAttribute(h->tv_fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess)
+        cudaFuncSetAttribute((const void *)&k_tv_project, cudaFuncAttributeNonPortableClusterSizeAllowed,
+                             1) != cudaSuccess)
       return bail(fail(POLY_ECUDA, "TV kernel attributes: %s", cudaGetErrorString(cudaGetLastError())));
   }
   if ((rc = dev_alloc(h, &h->comm, (size_t)p.d + 1)) != POLY_OK) return bail(rc);
