@@ -82,6 +82,8 @@ extern "C" {
 #define POLY_FLAG_HOST_INPUTS 1u /* A/row_ptr/col/val/y/s_row/I_row are HOST pointers; copied at init */
 #define POLY_FLAG_NO_GRAPH 2u    /* poly_solve launches kernels directly instead of via a CUDA graph */
 #define POLY_FLAG_NO_PDL 4u      /* disable programmatic dependent launch between kernels */
+#define POLY_FLAG_NO_SMALL 16u   /* never use the cluster-resident whole-solve kernel for small
+                                    dense problems (poly_solve then replays the general graph) */
 #define POLY_FLAG_COMM 8u        /* use the NCCL path (reduce -> ncclAllReduce -> step) even when
                                     world == 1; needs nccl_id.  Exercises the collective path on one GPU */
 
@@ -171,7 +173,10 @@ int poly_init(const poly_problem *p, poly_handle **out);
  * the fixed-order partial reduction and, for world > 1, one allreduce. */
 int poly_loss_grad(poly_handle *h, const double *x, double *g, double *loss);
 
-/* EXACT, Eq.(extragrad-method), T iterations with constant step γ > 0:
+/* EXACT, Eq.(extragrad-method), T iterations with constant step γ > 0.
+ * Small dense problems (single rank, A in fp32/fp64 fitting the shared memory
+ * of one 16-CTA cluster, d <= 256, no per-row spectra, ball/orthant sets) run
+ * all T iterations in one cluster-resident kernel; POLY_FLAG_NO_SMALL opts out.
  *   x_1 = P_X(x_in);  x_{t+1/2} = P_X(x_t - γ F(x_t));  x_{t+1} = P_X(x_t - γ F(x_{t+1/2})).
  * x: device or host [d] fp64; in: x_in, out: x_{T+1} (always in X).
  * trace: host [2T] fp64 or NULL; receives ℓ at each of the 2T points where F

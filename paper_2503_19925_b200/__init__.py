@@ -19,7 +19,7 @@ POLY_F32, POLY_F64 = 0, 1
 POLY_Y_I32, POLY_Y_F32, POLY_Y_F64 = 0, 1, 2
 POLY_SET_NONE, POLY_SET_BALL, POLY_SET_NONNEG, POLY_SET_NONNEG_BALL = 0, 1, 2, 3
 POLY_SET_TV_NONNEG, POLY_SET_TV = 4, 5
-POLY_FLAG_HOST_INPUTS, POLY_FLAG_NO_GRAPH, POLY_FLAG_NO_PDL, POLY_FLAG_COMM = 1, 2, 4, 8
+POLY_FLAG_HOST_INPUTS, POLY_FLAG_NO_GRAPH, POLY_FLAG_NO_PDL, POLY_FLAG_COMM, POLY_FLAG_NO_SMALL = 1, 2, 4, 8, 16
 POLY_SOLVE_PROFILE = 1
 POLY_MODE_EXACT, POLY_MODE_L2, POLY_MODE_L1, POLY_MODE_NLL = 0, 1, 2, 3
 POLY_METHOD_EXTRAGRADIENT, POLY_METHOD_GD = 0, 1

@@ -180,6 +180,12 @@ __device__ __forceinline__ double load_y(const unsigned char *yb, int ytype, int
   return ((const double *)yb)[r];
 }
 
+__device__ __forceinline__ double load_y_global(const void *y, int ytype, int64_t i) {
+  if (ytype == 0) return (double)((const int32_t *)y)[i];
+  if (ytype == 1) return (double)((const float *)y)[i];
+  return ((const double *)y)[i];
+}
+
 template <typename T>
 struct Vec16;
 template <>

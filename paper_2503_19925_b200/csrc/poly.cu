@@ -30,6 +30,7 @@
 #include "dense.cuh"
 #include "finalize.cuh"
 #include "tv.cuh"
+#include "small.cuh"
 
 using namespace poly;
 
@@ -447,6 +448,70 @@ int enqueue_tv(poly_handle *h, const double *v, double *out) {
   cfg.numAttrs = h->pdl ? 2 : 1;
   void *argv[] = {(void *)&a};
   CK(cudaLaunchKernelExC(&cfg, (const void *)&k_tv_project, argv));
+  return POLY_OK;
+}
+
+// Cluster-resident whole solve for small dense problems (csrc/small.cuh).
+// Returns POLY_EUNSUPPORTED (no error message) when the problem does not fit.
+int small_solve_config(poly_handle *h, int *cl, size_t *smem) {
+  const poly_problem &p = h->p;
+  if (p.layout != POLY_DENSE || h->comm_path || p.s_row || p.d > kSmallMaxD || p.n_local < 1 ||
+      p.set > POLY_SET_NONNEG_BALL || (p.flags & POLY_FLAG_NO_SMALL))
+    return POLY_EUNSUPPORTED;
+  const int C = (int)std::min<int64_t>(kSmallMaxCL, p.n_local);
+  const int64_t rows = (p.n_local + C - 1) / C;
+  const int64_t ldd = (p.d + 1) & ~1;
+  const size_t s = (size_t)rows * ldd * h->elsize + 8 + (size_t)rows * 8 + 3 * kMaxW * 8 +
+                   3 * kSmallMaxD * 8 + 2 * (kSmallMaxD + 1) * 8 +
+                   (kSmallThreads / 32) * (kSmallMaxD + 1) * 8 + (kSmallThreads / 32) * 8;
+  if (s > 200 * 1024) return POLY_EUNSUPPORTED;
+  *cl = C;
+  *smem = s;
+  return POLY_OK;
+}
+
+int launch_small_solve(poly_handle *h, double *x_dev, int T, bool loss, int C, size_t smem) {
+  const poly_problem &p = h->p;
+  SmallArgs a{};
+  a.A = p.A;
+  a.lda = p.lda;
+  a.n = (int32_t)p.n_local;
+  a.d = (int32_t)p.d;
+  a.W = p.W;
+  a.ytype = p.ytype;
+  a.relu = p.relu;
+  a.mode = p.mode;
+  a.set = p.set;
+  a.y = p.y;
+  a.I_bar = p.I_bar;
+  a.R = p.R;
+  a.gamma = h->hstate->gamma;
+  a.n_norm = h->n_norm;
+  a.spec = h->spec;
+  a.center = h->center;
+  a.x = x_dev;
+  a.T = T;
+  a.trace = loss ? h->trace : nullptr;
+  a.state = h->state;
+  const void *fn = p.dtype == POLY_F32
+                       ? (loss ? (const void *)&k_small_solve<float, true> : (const void *)&k_small_solve<float, false>)
+                       : (loss ? (const void *)&k_small_solve<double, true> : (const void *)&k_small_solve<double, false>);
+  CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  CK(cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(C);
+  cfg.blockDim = dim3(kSmallThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = h->work;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = C;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  void *argv[] = {(void *)&a};
+  CK(cudaLaunchKernelExC(&cfg, fn, argv));
   return POLY_OK;
 }
 
@@ -1349,6 +1414,27 @@ int poly_solve(poly_handle *h, double *x, int T, double gamma, uint32_t flags, d
   *h->hstate = st;
   CK(cudaMemcpyAsync(h->state, h->hstate, sizeof(SolveState), cudaMemcpyHostToDevice, h->work));
 
+  {  // small dense problems: the whole solve in one cluster-resident kernel
+    int C = 0;
+    size_t smem = 0;
+    if (!(flags & POLY_SOLVE_PROFILE) && T > 0 && small_solve_config(h, &C, &smem) == POLY_OK) {
+      TRY(launch_small_solve(h, h->xa, T, want_trace, C, smem));
+      CK(cudaMemcpyAsync(x, h->xa, h->p.d * 8, x_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost,
+                         h->work));
+      if (want_trace)
+        CK(cudaMemcpyAsync(trace, h->trace, (size_t)2 * T * 8, cudaMemcpyDeviceToHost, h->work));
+      CK(cudaMemcpyAsync(h->hstate, h->state, sizeof(SolveState), cudaMemcpyDeviceToHost, h->work));
+      CK(cudaStreamSynchronize(h->work));
+      TRY(sync_out(h));
+      CK(cudaGetLastError());
+      if (h->hstate->bad != 0) {
+        const int b = h->hstate->bad;
+        if (bad_iter) *bad_iter = b > 0 ? (b + 1) / 2 : 0;
+        return fail(POLY_ENONFINITE, "non-finite iterate at iteration %d", b > 0 ? (b + 1) / 2 : 0);
+      }
+      return POLY_OK;
+    }
+  }
   h->prof = (flags & POLY_SOLVE_PROFILE) != 0;
   h->recs.clear();
   h->evused = 0;

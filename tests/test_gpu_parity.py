@@ -589,3 +589,27 @@ def test_stream_probe_is_the_read_ceiling(c2_gpu):
     with pytest.raises(P.PolyError):
         wc = _W().build(G.scaled(G.C4, G.C4.n))
         _W().make_poly(wc).stream_probe(1)
+
+
+@pytest.mark.parametrize("cfg", [G.C1, G.C1F])
+def test_small_cluster_solve_matches_graph_path(cfg):
+    """C1-sized problems run the whole solve in one cluster-resident kernel
+    (A in shared memory); POLY_FLAG_NO_SMALL forces the general graph path.
+    Same iterates up to summation order, same trace, same oracle parity."""
+    P = _P()
+    W = _W()
+    wg = W.build(cfg)
+    wo = OW.build(cfg)
+    gam, _ = OW.step_size(wo["problem"], wo["s"], wo["mu"], cfg.I_bar)
+    xa = torch.zeros(cfg.d, dtype=torch.float64, device="cuda")
+    xb = torch.zeros_like(xa)
+    pa = W.make_poly(wg)
+    pb = W.make_poly(wg, flags=P.POLY_FLAG_NO_SMALL)
+    ta = pa.solve(xa, 50, gam, trace=True)
+    tb = pb.solve(xb, 50, gam, trace=True)
+    tol = 1e-12 if cfg.dtype == "f64" else 1e-6
+    assert rel(xa.cpu().numpy(), xb.cpu().numpy()) <= tol
+    assert rel(ta, tb) <= tol
+    x_ref, tr_ref, _ = wo["problem"].solve(50, gam, trace=True)
+    assert rel(xa.cpu().numpy(), x_ref) <= (1e-10 if cfg.dtype == "f64" else 1e-3)
+    assert rel(ta, tr_ref) <= (1e-10 if cfg.dtype == "f64" else 1e-4)
