@@ -24,7 +24,7 @@
 
 namespace poly {
 
-constexpr int kSmallThreads = 256;
+constexpr int kSmallThreads = 512;
 constexpr int kSmallMaxD = 256;   // fp64 g accumulators per lane: d / 32 <= 8
 constexpr int kSmallMaxCL = 16;
 
@@ -157,8 +157,13 @@ __global__ void __launch_bounds__(kSmallThreads, 1) k_small_solve(const SmallArg
     // ---- sum over the cluster in rank order, step from the anchor, project
     for (int c = threadIdx.x; c <= kSmallMaxD; c += blockDim.x) {
       if (c < d || c == kSmallMaxD) {
+        // all CL remote loads in flight before the (rank-ordered) sum
+        double pr[kSmallMaxCL];
+#pragma unroll
+        for (int r = 0; r < kSmallMaxCL; ++r) pr[r] = r < CL ? cl.map_shared_rank(pb, r)[c] : 0.0;
         double s = 0.0;
-        for (int r = 0; r < CL; ++r) s += cl.map_shared_rank(pb, r)[c];
+#pragma unroll
+        for (int r = 0; r < kSmallMaxCL; ++r) s += pr[r];
         if (c < d) vv[c] = xa[c] - a.gamma * (s * inv_n);
         else if (LOSS && rank == 0 && a.trace) a.trace[e] = s * inv_n;
       }

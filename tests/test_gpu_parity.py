@@ -122,10 +122,13 @@ def test_c1_solve_parity(cfg, tol):
     tr = p.solve(x, cfg.T, gam, trace=True)
     assert rel(x.cpu().numpy(), x_ref) <= tol
     assert np.allclose(tr, tr_ref, rtol=max(tol, 1e-9), atol=0)
-    # graph and direct launches agree bit for bit
+    # graph and direct launches of the general path agree bit for bit
+    pg = W.make_poly(wg, flags=_P().POLY_FLAG_NO_SMALL)
+    x1 = torch.zeros(cfg.d, dtype=torch.float64, device="cuda")
     x2 = torch.zeros(cfg.d, dtype=torch.float64, device="cuda")
-    p.solve(x2, cfg.T, gam, profile=True)
-    assert torch.equal(x, x2)
+    pg.solve(x1, cfg.T, gam)
+    pg.solve(x2, cfg.T, gam, profile=True)
+    assert torch.equal(x1, x2)
 
 
 # ------------------------------------------------------------------ C2
