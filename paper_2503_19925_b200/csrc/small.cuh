@@ -20,6 +20,8 @@
 
 #include <cooperative_groups.h>
 
+#include <type_traits>
+
 #include "dense.cuh"
 
 namespace poly {
@@ -120,7 +122,36 @@ __global__ void __launch_bounds__(kSmallThreads, 1) k_small_solve(const SmallArg
 #pragma unroll
     for (int k = 0; k < kSmallMaxD / 32; ++k) gacc[k] = 0.0;
     double lacc = 0.0;
-    for (int r = warp; r < rows; r += NWp) {
+    constexpr int DEG = std::is_same<T, double>::value ? 13 : 9;
+    const bool pairs = a.mode == 0 && a.W <= 32;
+    int r = warp;
+    if (pairs) {
+      // two rows per pass: one butterfly for both dots, one 16-lane link each
+      for (; r + NWp < rows; r += 2 * NWp) {
+        const T *ar0 = As + (size_t)r * ldd, *ar1 = As + (size_t)(r + NWp) * ldd;
+        double p0 = 0.0, p1 = 0.0;
+#pragma unroll
+        for (int k = 0; k < kSmallMaxD / 32; ++k) {
+          const int c = lane + 32 * k;
+          if (c < d) {
+            const double xc = xe[c];
+            p0 = fma((double)ar0[c], xc, p0);
+            p1 = fma((double)ar1[c], xc, p1);
+          }
+        }
+        const double zh = pair_sum(p0, p1);
+        const int hr = (lane & 16) ? r + NWp : r;
+        const double rh = link_exact_pair<LOSS, DEG>(sp, a.W, a.relu, zh, ys[hr], a.I_bar, nullptr,
+                                                      true, &lacc);
+        const double phi0 = __shfl_sync(0xffffffffu, rh, 0), phi1 = __shfl_sync(0xffffffffu, rh, 16);
+#pragma unroll
+        for (int k = 0; k < kSmallMaxD / 32; ++k) {
+          const int c = lane + 32 * k;
+          if (c < d) gacc[k] = fma(phi1, (double)ar1[c], fma(phi0, (double)ar0[c], gacc[k]));
+        }
+      }
+    }
+    for (; r < rows; r += NWp) {
       const T *ar = As + (size_t)r * ldd;
       double p = 0.0;
 #pragma unroll
@@ -129,8 +160,10 @@ __global__ void __launch_bounds__(kSmallThreads, 1) k_small_solve(const SmallArg
         if (c < d) p = fma((double)ar[c], xe[c], p);
       }
       const double z = warp_sum(p);
-      const double phi = row_residual<LOSS>(sp, a.W, a.relu, z, ys[r], a.I_bar, nullptr, true, &lacc,
-                                            a.mode);
+      const double phi = a.mode == 0
+                             ? link_exact<LOSS, DEG>(sp, a.W, a.relu, z, ys[r], a.I_bar, nullptr, true, &lacc)
+                             : row_residual<LOSS>(sp, a.W, a.relu, z, ys[r], a.I_bar, nullptr, true, &lacc,
+                                                  a.mode);
 #pragma unroll
       for (int k = 0; k < kSmallMaxD / 32; ++k) {
         const int c = lane + 32 * k;
