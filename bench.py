@@ -271,8 +271,6 @@ def run_e2e(P, PW, w, cfg, gamma, args):
     (pinned) to the device, poly_solve runs T iterations from a host x and
     returns x to the host; the timed region covers all of it."""
     import torch
-    if "A" not in w:
-        return None
     try:
         import psutil
         host_ok = a_bytes(w) * 1.5 < psutil.virtual_memory().available and a_bytes(w) < 48e9
@@ -280,8 +278,13 @@ def run_e2e(P, PW, w, cfg, gamma, args):
         host_ok = a_bytes(w) < 32e9
     if not host_ok:   # C5: a 131 GB pinned host copy of A does not fit the host
         return {"value": None, "unit": "GB/s", "skipped": "A does not fit in host memory"}
-    A_h = w["A"].cpu().pin_memory()
     y_h = w["y"].cpu().pin_memory()
+    if "A" in w:
+        A_h = w["A"].cpu().pin_memory()
+        mat = dict(A=A_h)
+    else:   # CSR: the caller's arrays; poly_init builds the SELL copies on the device
+        mat = dict(row_ptr=w["row_ptr"].cpu().pin_memory(), col=w["col"].cpu().pin_memory(),
+                   val=w["val"].cpu().pin_memory())
     extra = {}
     if w.get("s_row") is not None:
         extra = dict(s_row=w["s_row"].cpu().pin_memory(), I_row=w["I_row"].cpu().pin_memory())
@@ -293,9 +296,9 @@ def run_e2e(P, PW, w, cfg, gamma, args):
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(st)
-        p = P.Poly(A=A_h, d=cfg.d, y=y_h, s=w["s"], mu=w["mu"], I_bar=cfg.I_bar, set=cfg.set,
+        p = P.Poly(d=cfg.d, y=y_h, s=w["s"], mu=w["mu"], I_bar=cfg.I_bar, set=cfg.set,
                    R=w["R"], n_global=w["n_global"], flags=P.POLY_FLAG_HOST_INPUTS,
-                   stream=st.cuda_stream, **extra)
+                   stream=st.cuda_stream, **mat, **extra)
         p.solve(x_h, T, gamma)
         e1.record(st)
         torch.cuda.synchronize()
@@ -304,12 +307,12 @@ def run_e2e(P, PW, w, cfg, gamma, args):
             vals.append(e0.elapsed_time(e1))
     ms = statistics.median(vals)
     ab = a_bytes(w)
-    h2d = A_h.numel() * A_h.element_size() + y_h.numel() * y_h.element_size() + \
-        sum(v.numel() * v.element_size() for v in extra.values())
+    h2d = y_h.numel() * y_h.element_size() + \
+        sum(v.numel() * v.element_size() for v in list(mat.values()) + list(extra.values()))
     return {"value": 2.0 * T * ab / (ms * 1e-3) / 1e9, "unit": "GB/s",
             "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": 8 * cfg.d,
             "iterations_per_step": T, "ms_per_step": ms,
-            "note": "step = poly_init(host A,y) + poly_solve(T, host x) + free"}
+            "note": "step = poly_init(host A or CSR, y) + poly_solve(T, host x) + free"}
 
 
 def cpu_baseline(name, seconds=15.0, max_rows=None):
