@@ -47,7 +47,7 @@
 extern "C" {
 #endif
 
-#define POLY_ABI_VERSION 2
+#define POLY_ABI_VERSION 3
 
 /* status codes */
 #define POLY_OK 0
@@ -61,6 +61,10 @@ extern "C" {
 /* poly_problem.layout */
 #define POLY_DENSE 0         /* A row-major n_local x d, row pitch lda elements */
 #define POLY_CSR 1           /* row_ptr[n_local+1] (int64), col[nnz] (int32), val[nnz] */
+#define POLY_PARALLEL_BEAM 2 /* matrix-free CT projector: A[kB+b, rN+c] = length of the line
+                                {p : p·(cos θ_k, sin θ_k) = t_b} inside pixel (r, c) of an N x N
+                                image with pitch 1/N centred on pixel (N/2, N/2), θ_k = kπ/V,
+                                t_b = (b - (B-1)/2)/N (R12); A is never stored */
 /* poly_problem.dtype: element type of A (dense) or val (CSR) */
 #define POLY_F32 0
 #define POLY_F64 1
@@ -154,6 +158,11 @@ typedef struct poly_problem {
   double tv_dykstra_tol; /* [1e-4] Dykstra stops at ||z_{k+1} - z_k|| <= tol    */
   int32_t tv_max_it;     /* [5000] FISTA iterations per prox                                    */
   int32_t tv_max_outer;  /* [1000] Dykstra sweeps                                              */
+  /* POLY_PARALLEL_BEAM geometry: N = pb_side (d = N*N, N <= 4096), V = pb_views,
+   * B = pb_bins; this rank holds rows [row_offset, row_offset + n_local), both
+   * multiples of B (whole views).  fp32 chord lengths; mode EXACT, no per-row
+   * spectra.  A, row_ptr, col, val are unused. */
+  int32_t pb_side, pb_views, pb_bins, pb_reserved;
 } poly_problem;
 
 /* Validate *p, copy host parameters, pick the kernel configuration for

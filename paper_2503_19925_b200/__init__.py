@@ -14,7 +14,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libpoly.so")
 
 POLY_OK, POLY_EINVAL, POLY_ECUDA, POLY_ENCCL, POLY_ENONFINITE, POLY_ENOMEM, POLY_EUNSUPPORTED = range(7)
-POLY_DENSE, POLY_CSR = 0, 1
+POLY_DENSE, POLY_CSR, POLY_PARALLEL_BEAM = 0, 1, 2
 POLY_F32, POLY_F64 = 0, 1
 POLY_Y_I32, POLY_Y_F32, POLY_Y_F64 = 0, 1, 2
 POLY_SET_NONE, POLY_SET_BALL, POLY_SET_NONNEG, POLY_SET_NONNEG_BALL = 0, 1, 2, 3
@@ -46,6 +46,8 @@ class PolyProblem(C.Structure):
         ("windows", C.c_int32), ("I_win", C.c_void_p),
         ("tv_tau", C.c_double), ("tv_tol", C.c_double), ("tv_rtol", C.c_double),
         ("tv_dykstra_tol", C.c_double), ("tv_max_it", C.c_int32), ("tv_max_outer", C.c_int32),
+        ("pb_side", C.c_int32), ("pb_views", C.c_int32), ("pb_bins", C.c_int32),
+        ("pb_reserved", C.c_int32),
     ]
 
 

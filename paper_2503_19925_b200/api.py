@@ -10,7 +10,7 @@ import ctypes as C
 
 import torch
 
-from . import (POLY_CSR, POLY_DENSE, POLY_F32, POLY_F64, POLY_FLAG_HOST_INPUTS,
+from . import (POLY_CSR, POLY_DENSE, POLY_F32, POLY_F64, POLY_FLAG_HOST_INPUTS, POLY_PARALLEL_BEAM,
                POLY_METHOD_EXTRAGRADIENT, POLY_SET_BALL, POLY_SOLVE_PROFILE, POLY_Y_F32, POLY_Y_F64,
                POLY_Y_I32, PolyProblem, PolySolveOpts, poly_describe, poly_expected_counts,
                poly_forward, poly_free, poly_init, poly_kernel_times, poly_loss_grad, poly_project,
@@ -34,11 +34,16 @@ class Poly:
     def __init__(self, *, y, s, mu, I_bar, d=None, A=None, row_ptr=None, col=None, val=None,
                  s_row=None, I_row=None, relu=1, set=POLY_SET_BALL, R=1.0, center=None,
                  n_global=None, row_offset=0, rank=0, world=1, nccl_id=None, stream=None,
-                 flags=0, mode=0, I_win=None, tv=None):
+                 flags=0, mode=0, I_win=None, tv=None, pb=None):
         p = PolyProblem()
         host = bool(flags & POLY_FLAG_HOST_INPUTS)
         self._keep = [y, A, row_ptr, col, val, s_row, I_row]
-        if A is not None:
+        if pb is not None:   # matrix-free parallel beam: pb = dict(side=, views=, bins=)
+            p.layout, p.dtype = POLY_PARALLEL_BEAM, POLY_F32
+            p.pb_side, p.pb_views, p.pb_bins = int(pb["side"]), int(pb["views"]), int(pb["bins"])
+            p.n_local = y.numel() if I_win is None else y.numel() // len(I_win)
+            p.d = p.pb_side ** 2
+        elif A is not None:
             assert A.dim() == 2 and A.stride(1) == 1, "A must be row-major"
             p.layout, p.dtype = POLY_DENSE, _DT[A.dtype]
             p.n_local = A.shape[0]

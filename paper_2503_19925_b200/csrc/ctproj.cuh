@@ -1,0 +1,203 @@
+// Matrix-free parallel-beam projector for the CT workload (SURVEY.md §8(f)
+// NEXT-4: "a matrix-free Siddon/Joseph projector for CT, which removes the
+// 243 MB CSR stream and moves the bound from HBM to ALU").
+//
+// Geometry (reading R12, gen/ct.py): an N x N image with pixel
+// pitch Δ = 1/N, pixel (r, c) centred at (X_c, Y_r) = ((c - N/2)Δ, (r - N/2)Δ);
+// ray (k, b), k < V views, b < B bins, is the line {p : p·n_k = t_b} with
+// n_k = (cos θ_k, sin θ_k), θ_k = kπ/V and t_b = (b - (B-1)/2)Δ; row i = kB + b.
+// A[i, rN + c] is the length of that line inside pixel (r, c) — the
+// Siddon segment length ("fractional contribution of pixel k to
+// the line integral") — which for a square pixel is the closed-form chord
+//   L(δ) = Δ/max(a,b)          |δ| <= Δ|a-b|/2
+//        = (Δ(a+b)/2 - |δ|)/(ab)  Δ|a-b|/2 < |δ| < Δ(a+b)/2
+//        = 0                    otherwise,
+// with a = |cos θ|, b = |sin θ| and δ the signed distance of the pixel centre
+// from the line.  The kernels evaluate it on the fly instead of streaming A:
+//   K5f k_pb_forward   one block per view, one thread per ray: image rows are
+//                      staged through shared memory (for views with
+//                      |sin θ| > |cos θ| the rows of the transposed image, in
+//                      which the ray is again "steep"); each ray adds the at
+//                      most 3 pixels per row its footprint covers; then the
+//                      link and residual per ray (fp64) as K1, r stored fp32.
+//   K5b k_pb_backward  one thread per (pixel, half of the views): for every
+//                      view the at most 2 bins whose rays cross the pixel,
+//                      residuals staged per view chunk in shared memory; the
+//                      two halves are added in order (deterministic).
+#pragma once
+
+#include "dense.cuh"
+
+namespace poly {
+
+struct PbGeom {
+  int32_t N, V, B;
+  int32_t v0;          // first view of this handle's rows (row_offset / B)
+  int32_t nv;          // views held (n_local / B)
+  const double *trig;  // [2V]: cos θ_k, sin θ_k (host libm, θ_k = kπ/V)
+};
+
+// chord length / Δ for a pixel whose centre is u pixels (along the frame's
+// columns) from the ray's crossing point, a = |cos| >= b = |sin| of the frame
+__device__ __forceinline__ float chord(float u, float a, float b, float inv_a, float inv_ab) {
+  const float da = u * a;                    // |δ| / Δ
+  const float p1 = 0.5f * (a - b), p2 = 0.5f * (a + b);
+  if (da <= p1) return inv_a;
+  if (da >= p2) return 0.0f;
+  return (p2 - da) * inv_ab;
+}
+
+constexpr int kPbRows = 32;  // image rows staged per chunk in the forward
+
+// z_i for the rays of one view, then the residual (mode EXACT).  x32 holds
+// x (row-major) at [0, d) and its transpose at [d, 2d).
+template <bool LOSS>
+__global__ void __launch_bounds__(512) k_pb_forward(const PbGeom g, const float *__restrict__ x32,
+                                                    const CsrFwdArgs a) {
+  extern __shared__ __align__(16) float xs[];  // [kPbRows][N]
+  __shared__ double sp[3 * kMaxW];
+  __shared__ double wl[16];
+  const int N = g.N, B = g.B;
+  const int kl = blockIdx.x, k = g.v0 + kl;
+  const int b = threadIdx.x;
+  for (int i = threadIdx.x; i < 3 * kMaxW; i += blockDim.x) sp[i] = a.spec[i];
+  const double cth = g.trig[2 * k], sth = g.trig[2 * k + 1];
+  const bool steep = fabs(cth) >= fabs(sth);
+  const double cf = steep ? cth : sth, sf = steep ? sth : cth;  // frame cos / sin
+  const float *xsrc = steep ? x32 : x32 + (size_t)N * N;
+  const float a_ = (float)fabs(cf), b_ = (float)fabs(sf);
+  const float inv_a = 1.0f / a_, inv_ab = b_ > 0.0f ? 1.0f / (a_ * b_) : 0.0f;
+  const float w = 0.5f * (a_ + b_) * inv_a;  // footprint half-width in columns
+  // crossing column in frame row r: c*(r) = C0 - r tan
+  const double tb = ((double)b - 0.5 * (double)(B - 1)) / (double)N;
+  const double tanf_ = sf / cf;
+  const double C0 = 0.5 * N + tb * N / cf + 0.5 * N * tanf_;
+  pdl_wait();  // x is written by the previous kernel; r is read by the previous backward
+  float zf = 0.0f;
+  double z = 0.0;
+  for (int r0 = 0; r0 < N; r0 += kPbRows) {
+    __syncthreads();  // previous chunk consumed
+    const int nr = min(kPbRows, N - r0);
+    for (int i = threadIdx.x; i < nr * N; i += blockDim.x) xs[i] = __ldg(xsrc + (size_t)r0 * N + i);
+    __syncthreads();
+    if (b < B) {
+      for (int rr = 0; rr < nr; ++rr) {
+        // crossing column in fp64, split so the fraction keeps fp32 precision
+        const double csd = C0 - (double)(r0 + rr) * tanf_;
+        const double cfl = floor(csd);
+        const float fr = (float)(csd - cfl);
+        const int ci = (int)cfl;
+        const int j_lo = (int)ceilf(fr - w);  // candidates ci + j_lo .. ci + j_lo + 2
+        const float *xr = xs + rr * N;
+#pragma unroll
+        for (int j = 0; j < 3; ++j) {
+          const int cc = ci + j_lo + j;
+          if (cc >= 0 && cc < N) {
+            const float l = chord(fabsf(fr - (float)(j_lo + j)), a_, b_, inv_a, inv_ab);
+            zf = fmaf(l, xr[cc], zf);
+          }
+        }
+      }
+      z += (double)zf;  // fp32 partial per chunk, fp64 across chunks
+      zf = 0.0f;
+    }
+  }
+  z /= (double)N;  // chord lengths in units of Δ
+  double lacc = 0.0;
+  if (b < B) {
+    const int64_t row = (int64_t)kl * B + b;
+    const double yv = load_y_global(a.y, a.ytype, row);
+    // link in-lane (W bins), the quantities of K1's link_exact
+    const bool neg = a.relu && z < 0.0;
+    const double zc = neg ? 0.0 : z;
+    double hs = 0.0, Hs = 0.0;
+    for (int j = 0; j < a.W; ++j) {
+      const double e = exp_nonpos<9>(-sp[kMaxW + j] * zc);
+      hs = fma(sp[j], e, hs);
+      if (LOSS) Hs += neg ? sp[j] * z : sp[j] * sp[2 * kMaxW + j] * (1.0 - e);
+    }
+    a.r[row] = (float)(yv - a.I_bar * hs);
+    if (LOSS) lacc = yv * z - a.I_bar * Hs;
+  }
+  // per-block loss partial, warps in order
+  lacc = warp_sum(lacc);
+  if ((threadIdx.x & 31) == 0) wl[threadIdx.x >> 5] = lacc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double l = 0.0;
+    for (int i = 0; i < (int)(blockDim.x >> 5); ++i) l += wl[i];
+    a.loss_partials[blockIdx.x] = l;
+  }
+  pdl_trigger();
+}
+
+constexpr int kPbViews = 24;  // residual views staged per chunk in the backward
+
+// g_pixel = Σ_views Σ_bins L r: one thread per (pixel, half of the views).
+// half h covers views [h*ceil(nv/2), ...); out[h*d + pixel] (fp64).
+__global__ void __launch_bounds__(256) k_pb_backward(const PbGeom g, const float *__restrict__ r,
+                                                     double *__restrict__ out2) {
+  extern __shared__ __align__(16) float rs[];  // [kPbViews][B]
+  __shared__ double trig[2 * kPbViews];
+  const int N = g.N, B = g.B;
+  const int64_t d = (int64_t)N * N;
+  const int half = blockIdx.y;
+  const int vh = (g.nv + 1) / 2;
+  const int va = half * vh, vb = min(g.nv, va + vh);
+  const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int pr = (int)(p / N), pc = (int)(p - (int64_t)pr * N);
+  const double Xn = (double)(pc - N / 2), Yn = (double)(pr - N / 2);  // centre / Δ
+  pdl_wait();  // r is written by the forward pass
+  double acc = 0.0;
+  for (int v0 = va; v0 < vb; v0 += kPbViews) {
+    const int nv = min(kPbViews, vb - v0);
+    __syncthreads();
+    for (int i = threadIdx.x; i < nv * B; i += blockDim.x) rs[i] = __ldg(r + (int64_t)v0 * B + i);
+    for (int i = threadIdx.x; i < 2 * nv; i += blockDim.x) trig[i] = g.trig[2 * (g.v0 + v0) + i];
+    __syncthreads();
+    if (p < d) {
+      float accf = 0.0f;
+      for (int vv = 0; vv < nv; ++vv) {
+        const double cs = trig[2 * vv], sn = trig[2 * vv + 1];
+        const float a_ = (float)fabs(cs), b_ = (float)fabs(sn);
+        const float amax = fmaxf(a_, b_), amin = fminf(a_, b_);
+        const float inv_max = 1.0f / amax, inv_ab = amin > 0.0f ? 1.0f / (a_ * b_) : 0.0f;
+        // bin coordinate of the pixel centre, b* = (X cos + Y sin) N + (B-1)/2,
+        // in fp64 and split so the fraction keeps fp32 precision
+        const double bsd = fma(Xn, cs, Yn * sn) + 0.5 * (B - 1);
+        const double bfl = floor(bsd);
+        const float fr = (float)(bsd - bfl);
+        const int bi = (int)bfl;
+        const float wb = 0.5f * (a_ + b_);  // footprint half-width in bins
+        const int j_lo = (int)ceilf(fr - wb);
+        const float *rv = rs + vv * B;
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+          const int bb = bi + j_lo + j;
+          if (bb >= 0 && bb < B) {
+            const float dd = fabsf(fr - (float)(j_lo + j));  // |δ| / Δ
+            float l;
+            if (dd <= 0.5f * (amax - amin)) l = inv_max;
+            else if (dd >= wb) l = 0.0f;
+            else l = (wb - dd) * inv_ab;
+            accf = fmaf(l, rv[bb], accf);
+          }
+        }
+      }
+      acc += (double)accf;
+    }
+  }
+  if (p < d) out2[half * d + p] = acc / (double)N;
+  pdl_trigger();
+}
+
+// g = out2[0] + out2[1] (the two view halves, in order) into the partial row
+__global__ void k_pb_combine(const double *__restrict__ out2, int64_t d, double *__restrict__ g) {
+  pdl_wait();
+  pdl_trigger();
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < d;
+       i += (int64_t)gridDim.x * blockDim.x)
+    g[i] = out2[i] + out2[d + i];
+}
+
+}  // namespace poly

@@ -31,6 +31,7 @@
 #include "finalize.cuh"
 #include "tv.cuh"
 #include "small.cuh"
+#include "ctproj.cuh"
 
 using namespace poly;
 
@@ -237,6 +238,9 @@ struct poly_handle {
   int tr_side = 0;                     // CSR, d = s²: fp32 copies also hold x transposed at [d, 2d)
   int64_t tr_slices = 0;               // K4f slices that gather from the transposed copy
   bool sell16 = false;                 // both SELL copies in the 6-byte delta form
+  // POLY_PARALLEL_BEAM
+  PbGeom pb{};
+  double *pb_trig = nullptr, *pb_out2 = nullptr;
   int k4f16_grid = 0, k4b16_grid = 0;  // resident-slot grids (slices dealt grid-stride)
   // TV sets: Dykstra state, statistics, cluster launch shape
   double *tv_zk = nullptr, *tv_p = nullptr, *tv_q = nullptr;
@@ -360,6 +364,32 @@ int enqueue_pass(poly_handle *h, const double *x, bool loss) {
   a.s_row = p.s_row;
   a.I_row = p.I_row;
   a.I_bar = p.I_bar;
+  if (p.layout == POLY_PARALLEL_BEAM) {
+    const float *x32 = x == h->xa ? h->xa32 : (x == h->xh ? h->xh32 : nullptr);
+    if (!x32) {
+      TRY(launch(h, (const void *)&k_to_f32, dim3((unsigned)std::min<int64_t>(1024, (p.d + 255) / 256)),
+                 dim3(256), 0, true, x, (int64_t)p.d, (int32_t)h->tr_side, h->xin32));
+      x32 = h->xin32;
+    }
+    CsrFwdArgs a{};
+    a.n = p.n_local;
+    a.W = p.W;
+    a.y = p.y;
+    a.ytype = p.ytype;
+    a.relu = p.relu;
+    a.I_bar = p.I_bar;
+    a.spec = h->spec;
+    a.r = h->rbuf;
+    a.loss_partials = h->loss_partials;
+    a.mode = p.mode;
+    const int thr = std::max(32, (p.pb_bins + 31) / 32 * 32);
+    TRY(launch(h, loss ? (const void *)&k_pb_forward<true> : (const void *)&k_pb_forward<false>,
+               dim3(h->pb.nv), dim3(thr), (size_t)kPbRows * p.pb_side * 4, true, h->pb, x32, a));
+    TRY(launch(h, (const void *)&k_pb_backward, dim3((unsigned)((p.d + 255) / 256), 2), dim3(256),
+               (size_t)kPbViews * p.pb_bins * 4, true, h->pb, (const float *)h->rbuf, h->pb_out2));
+    return launch(h, (const void *)&k_pb_combine, dim3((unsigned)std::min<int64_t>(1024, (p.d + 255) / 256)),
+                  dim3(256), 0, true, (const double *)h->pb_out2, (int64_t)p.d, h->partials);
+  }
   // fp32 copy of x for the gathers: written by the step kernel for the
   // internal iterates, converted here for a caller's x
   const float *x32 = x == h->xa ? h->xa32 : (x == h->xh ? h->xh32 : nullptr);
@@ -400,7 +430,7 @@ FinArgs fin_base(poly_handle *h, int mode) {
   f.mode = mode;
   f.d = (int32_t)h->p.d;
   f.G = h->G;
-  f.GL = h->p.layout == POLY_CSR ? h->k4_grid : h->G;
+  f.GL = h->p.layout == POLY_CSR ? h->k4_grid : (h->p.layout == POLY_PARALLEL_BEAM ? h->pb.nv : h->G);
   f.split = h->fin_split;
   f.set = h->p.set;
   f.n_norm = h->n_norm;
@@ -681,7 +711,19 @@ int validate(const poly_problem *p) {
   if (p->n_local < 0) return fail(POLY_EINVAL, "n_local < 0");
   if (p->n_global < 1 || p->n_global < p->n_local) return fail(POLY_EINVAL, "n_global must be >= max(1, n_local)");
   if (p->d < 1 || p->d > (1 << 30)) return fail(POLY_EINVAL, "d out of range");
-  if (p->layout != POLY_DENSE && p->layout != POLY_CSR) return fail(POLY_EINVAL, "bad layout");
+  if (p->layout != POLY_DENSE && p->layout != POLY_CSR && p->layout != POLY_PARALLEL_BEAM)
+    return fail(POLY_EINVAL, "bad layout");
+  if (p->layout == POLY_PARALLEL_BEAM) {
+    if (p->pb_side < 2 || p->pb_side > 4096 || (int64_t)p->pb_side * p->pb_side != p->d)
+      return fail(POLY_EINVAL, "parallel beam: d must be pb_side^2, 2 <= pb_side <= 4096");
+    if (p->pb_views < 1 || p->pb_bins < 1 || p->pb_bins > 1024)
+      return fail(POLY_EINVAL, "parallel beam: need pb_views >= 1 and 1 <= pb_bins <= 1024");
+    if (p->n_local % p->pb_bins || p->row_offset % p->pb_bins ||
+        p->row_offset + p->n_local > (int64_t)p->pb_views * p->pb_bins)
+      return fail(POLY_EINVAL, "parallel beam: rows must be whole views of the V*B rays");
+    if (p->mode != POLY_MODE_EXACT || p->s_row)
+      return fail(POLY_EUNSUPPORTED, "parallel beam: mode EXACT without per-row spectra only");
+  }
   if (p->dtype != POLY_F32 && p->dtype != POLY_F64) return fail(POLY_EINVAL, "bad dtype");
   if (p->ytype < POLY_Y_I32 || p->ytype > POLY_Y_F64) return fail(POLY_EINVAL, "bad ytype");
   if (p->W < 1) return fail(POLY_EINVAL, "W < 1 (SPEC.md:28)");
@@ -733,7 +775,7 @@ int validate(const poly_problem *p) {
       if ((p->lda * es) % 16 != 0) return fail(POLY_EINVAL, "lda*elsize must be a multiple of 16 bytes");
       if (!(p->flags & POLY_FLAG_HOST_INPUTS) && ((uintptr_t)p->A % 16) != 0)
         return fail(POLY_EINVAL, "A must be 16-byte aligned");
-    } else {
+    } else if (p->layout == POLY_CSR) {
       if (!p->row_ptr || (p->nnz > 0 && (!p->col || !p->val))) return fail(POLY_EINVAL, "CSR arrays are NULL");
       if (p->nnz < 0) return fail(POLY_EINVAL, "nnz < 0");
     }
@@ -1111,6 +1153,35 @@ int poly_init(const poly_problem *pin, poly_handle **out) {
     h->nrslices = (int)std::max<int64_t>(1, (p.n_local + 31) / 32);
     h->k4_grid = h->nrslices;
     if ((rc = dev_alloc(h, &h->partials, (size_t)p.d)) != POLY_OK) return bail(rc);
+    if (p.layout == POLY_PARALLEL_BEAM) {  // geometry table, per-view loss partials, view halves
+      h->pb.N = p.pb_side;
+      h->pb.V = p.pb_views;
+      h->pb.B = p.pb_bins;
+      h->pb.v0 = (int32_t)(p.row_offset / p.pb_bins);
+      h->pb.nv = (int32_t)(p.n_local / p.pb_bins);
+      if (h->pb.nv < 1) return bail(fail(POLY_EINVAL, "parallel beam: no views"));
+      std::vector<double> trig((size_t)2 * p.pb_views);
+      for (int k = 0; k < p.pb_views; ++k) {
+        const double th = 3.14159265358979323846 * (double)k / (double)p.pb_views;
+        trig[2 * k] = std::cos(th);
+        trig[2 * k + 1] = std::sin(th);
+      }
+      if ((rc = dev_alloc(h, &h->pb_trig, trig.size())) != POLY_OK) return bail(rc);
+      if (cudaMemcpy(h->pb_trig, trig.data(), trig.size() * 8, cudaMemcpyHostToDevice) != cudaSuccess)
+        return bail(fail(POLY_ECUDA, "geometry upload failed"));
+      h->pb.trig = h->pb_trig;
+      if ((rc = dev_alloc(h, &h->pb_out2, (size_t)2 * p.d)) != POLY_OK) return bail(rc);
+      h->k4_grid = h->pb.nv;
+      for (int f = 0; f < 2; ++f) {
+        const void *fn = f ? (const void *)&k_pb_forward<true> : (const void *)&k_pb_forward<false>;
+        if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 kPbRows * p.pb_side * 4) != cudaSuccess)
+          return bail(fail(POLY_EUNSUPPORTED, "parallel beam: image too wide for the row stage"));
+      }
+      if (cudaFuncSetAttribute((const void *)&k_pb_backward, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               kPbViews * p.pb_bins * 4) != cudaSuccess)
+        return bail(fail(POLY_ECUDA, "parallel beam: backward attributes"));
+    }
     if ((rc = dev_alloc(h, &h->loss_partials, (size_t)h->k4_grid)) != POLY_OK) return bail(rc);
     if ((rc = dev_alloc(h, &h->rbuf, (size_t)std::max<int64_t>(1, p.n_local))) != POLY_OK) return bail(rc);
     {  // a square d may be an image: the fp32 copies get room for x transposed
@@ -1503,6 +1574,7 @@ namespace {
 int aux_rows(poly_handle *h, const double *x, double *out, int want_counts) {
   if (!h || !x || !out) return fail(POLY_EINVAL, "NULL argument");
   const poly_problem &p = h->p;
+  if (p.layout == POLY_PARALLEL_BEAM) return fail(POLY_EUNSUPPORTED, "forward/expected counts: dense or CSR only");
   if (p.n_local == 0) return POLY_OK;
   TRY(sync_in(h));
   AuxArgs a{};
