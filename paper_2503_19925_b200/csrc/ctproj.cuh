@@ -71,7 +71,8 @@ __global__ void __launch_bounds__(512) k_pb_forward(const PbGeom g, const float 
   // crossing column in frame row r: c*(r) = C0 - r tan
   const double tb = ((double)b - 0.5 * (double)(B - 1)) / (double)N;
   const double tanf_ = sf / cf;
-  const double C0 = 0.5 * N + tb * N / cf + 0.5 * N * tanf_;
+  const double c0 = (double)(N / 2);  // centre pixel index (integer N/2, as gen/ct.py)
+  const double C0 = c0 + tb * N / cf + c0 * tanf_;
   pdl_wait();  // x is written by the previous kernel; r is read by the previous backward
   float zf = 0.0f;
   double z = 0.0;
