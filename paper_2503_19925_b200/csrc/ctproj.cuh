@@ -65,7 +65,10 @@ __global__ void __launch_bounds__(512) k_pb_forward(const PbGeom g, const float 
   const bool steep = fabs(cth) >= fabs(sth);
   const double cf = steep ? cth : sth, sf = steep ? sth : cth;  // frame cos / sin
   const float *xsrc = steep ? x32 : x32 + (size_t)N * N;
-  const float a_ = (float)fabs(cf), b_ = (float)fabs(sf);
+  // axis-aligned views (|sin| below 1e-12, as gen/ct.py's 1e-15 direction test):
+  // a ray on a pixel edge belongs to the pixel on its positive side
+  const bool axis = fabs(sf) < 1e-12;
+  const float a_ = axis ? 1.0f : (float)fabs(cf), b_ = axis ? 0.0f : (float)fabs(sf);
   const float inv_a = 1.0f / a_, inv_ab = b_ > 0.0f ? 1.0f / (a_ * b_) : 0.0f;
   const float w = 0.5f * (a_ + b_) * inv_a;  // footprint half-width in columns
   // crossing column in frame row r: c*(r) = C0 - r tan
@@ -94,7 +97,9 @@ __global__ void __launch_bounds__(512) k_pb_forward(const PbGeom g, const float 
         for (int j = 0; j < 3; ++j) {
           const int cc = ci + j_lo + j;
           if (cc >= 0 && cc < N) {
-            const float l = chord(fabsf(fr - (float)(j_lo + j)), a_, b_, inv_a, inv_ab);
+            const float sd = fr - (float)(j_lo + j);  // c* - cc
+            const float l = axis ? ((sd >= -0.5f && sd < 0.5f) ? 1.0f : 0.0f)
+                                 : chord(fabsf(sd), a_, b_, inv_a, inv_ab);
             zf = fmaf(l, xr[cc], zf);
           }
         }
@@ -160,7 +165,9 @@ __global__ void __launch_bounds__(256) k_pb_backward(const PbGeom g, const float
       float accf = 0.0f;
       for (int vv = 0; vv < nv; ++vv) {
         const double cs = trig[2 * vv], sn = trig[2 * vv + 1];
-        const float a_ = (float)fabs(cs), b_ = (float)fabs(sn);
+        const bool axis = fabs(cs) < 1e-12 || fabs(sn) < 1e-12;  // see k_pb_forward
+        const float a_ = axis ? (fabs(cs) < 1e-12 ? 0.0f : 1.0f) : (float)fabs(cs);
+        const float b_ = axis ? (fabs(sn) < 1e-12 ? 0.0f : 1.0f) : (float)fabs(sn);
         const float amax = fmaxf(a_, b_), amin = fminf(a_, b_);
         const float inv_max = 1.0f / amax, inv_ab = amin > 0.0f ? 1.0f / (a_ * b_) : 0.0f;
         // bin coordinate of the pixel centre, b* = (X cos + Y sin) N + (B-1)/2,
@@ -176,9 +183,11 @@ __global__ void __launch_bounds__(256) k_pb_backward(const PbGeom g, const float
         for (int j = 0; j < 2; ++j) {
           const int bb = bi + j_lo + j;
           if (bb >= 0 && bb < B) {
-            const float dd = fabsf(fr - (float)(j_lo + j));  // |δ| / Δ
+            const float sdd = fr - (float)(j_lo + j);  // b* - b
+            const float dd = fabsf(sdd);                // |δ| / Δ
             float l;
-            if (dd <= 0.5f * (amax - amin)) l = inv_max;
+            if (axis) l = (sdd > -0.5f && sdd <= 0.5f) ? 1.0f : 0.0f;
+            else if (dd <= 0.5f * (amax - amin)) l = inv_max;
             else if (dd >= wb) l = 0.0f;
             else l = (wb - dd) * inv_ab;
             accf = fmaf(l, rv[bb], accf);
