@@ -73,6 +73,10 @@ __device__ __forceinline__ void cp_async8(void *smem_dst, const void *gmem_src) 
                "l"(gmem_src)
                : "memory");
 }
+__device__ __forceinline__ void cp_async16(void *smem_dst, const void *gmem_src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(smem_dst)), "l"(gmem_src)
+               : "memory");
+}
 // arrive on `bar` once all prior cp.async of this thread completed (.noinc:
 // the arrival is counted in the barrier's initial count).
 __device__ __forceinline__ void cp_async_mbar_arrive(uint64_t *bar) {

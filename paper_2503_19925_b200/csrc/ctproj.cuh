@@ -5,7 +5,8 @@
 // Geometry (reading R12, gen/ct.py): an N x N image with pixel
 // pitch Δ = 1/N, pixel (r, c) centred at (X_c, Y_r) = ((c - N/2)Δ, (r - N/2)Δ);
 // ray (k, b), k < V views, b < B bins, is the line {p : p·n_k = t_b} with
-// n_k = (cos θ_k, sin θ_k), θ_k = kπ/V and t_b = (b - (B-1)/2)Δ; row i = kB + b.
+// n_k = (cos θ_k, sin θ_k), θ_k = kπ/V and t_b = (b - (B-1)/2)Δ; row i = kB + b
+// (axis-aligned views take exact 0/±1 for cos/sin).
 // A[i, rN + c] is the length of that line inside pixel (r, c) — the
 // Siddon segment length ("fractional contribution of pixel k to
 // the line integral") — which for a square pixel is the closed-form chord
@@ -82,26 +83,39 @@ __global__ void __launch_bounds__(512) k_pb_forward(const PbGeom g, const float 
   for (int r0 = 0; r0 < N; r0 += kPbRows) {
     __syncthreads();  // previous chunk consumed
     const int nr = min(kPbRows, N - r0);
-    for (int i = threadIdx.x; i < nr * N; i += blockDim.x) xs[i] = __ldg(xsrc + (size_t)r0 * N + i);
+    // stage the chunk with async copies (many in flight; a load->store loop
+    // serialises on L2 latency): 16-byte pieces when the rows allow it
+    if ((N & 3) == 0) {
+      const float4 *src = reinterpret_cast<const float4 *>(xsrc + (size_t)r0 * N);
+      for (int i = threadIdx.x; i < nr * N / 4; i += blockDim.x) cp_async16(xs + 4 * i, src + i);
+    } else {
+      for (int i = threadIdx.x; i < nr * N; i += blockDim.x) cp_async4(xs + i, xsrc + (size_t)r0 * N + i);
+    }
+    asm volatile("cp.async.wait_all;" ::: "memory");
     __syncthreads();
     if (b < B) {
+      // crossing column at the chunk's first row in fp64, split into an
+      // integer and an fp32 fraction; within the chunk the fraction steps by
+      // -tan in fp32 (|rr tan| < 32: error ~2e-6 columns)
+      const double csd = C0 - (double)r0 * tanf_;
+      const double cfl = floor(csd);
+      const float fr0 = (float)(csd - cfl);
+      const int ci0 = (int)cfl;
+      const float tn = (float)tanf_;
       for (int rr = 0; rr < nr; ++rr) {
-        // crossing column in fp64, split so the fraction keeps fp32 precision
-        const double csd = C0 - (double)(r0 + rr) * tanf_;
-        const double cfl = floor(csd);
-        const float fr = (float)(csd - cfl);
-        const int ci = (int)cfl;
+        const float u = fmaf(-(float)rr, tn, fr0);
+        const float kf = floorf(u);
+        const float fr = u - kf;
+        const int ci = ci0 + (int)kf;
         const int j_lo = (int)ceilf(fr - w);  // candidates ci + j_lo .. ci + j_lo + 2
         const float *xr = xs + rr * N;
 #pragma unroll
         for (int j = 0; j < 3; ++j) {
           const int cc = ci + j_lo + j;
-          if (cc >= 0 && cc < N) {
-            const float sd = fr - (float)(j_lo + j);  // c* - cc
-            const float l = axis ? ((sd >= -0.5f && sd < 0.5f) ? 1.0f : 0.0f)
-                                 : chord(fabsf(sd), a_, b_, inv_a, inv_ab);
-            zf = fmaf(l, xr[cc], zf);
-          }
+          const float sd = fr - (float)(j_lo + j);  // c* - cc
+          const float l = axis ? ((sd >= -0.5f && sd < 0.5f) ? 1.0f : 0.0f)
+                               : chord(fabsf(sd), a_, b_, inv_a, inv_ab);
+          if (cc >= 0 && cc < N) zf = fmaf(l, xr[cc], zf);
         }
       }
       z += (double)zf;  // fp32 partial per chunk, fp64 across chunks
@@ -137,67 +151,91 @@ __global__ void __launch_bounds__(512) k_pb_forward(const PbGeom g, const float 
   pdl_trigger();
 }
 
-constexpr int kPbViews = 24;  // residual views staged per chunk in the backward
+constexpr int kPbViews = 32;  // residual views staged per chunk in the backward
+constexpr int kPbTile = 16;   // backward blocks cover 16 x 16 pixel tiles
+
+// Per-view record of the backward, built once per chunk: the bin coordinate
+// of the tile's corner pixel in fp64 split into an integer and an fp32
+// fraction, so that a pixel's own coordinate is base_f + dc cos + dr sin with
+// |dc|, |dr| < 16 (fp32 error ~1e-6 bins).
+struct PbView {
+  float cs, sn, base_f, wb;   // cos, sin, fraction at the tile corner, footprint half-width
+  float p1, inv_max, inv_ab;  // plateau half-width, plateau and ramp scales
+  int base_i;                 // integer part at the tile corner (axis flag in bit 30)
+};
 
 // g_pixel = Σ_views Σ_bins L r: one thread per (pixel, half of the views).
-// half h covers views [h*ceil(nv/2), ...); out[h*d + pixel] (fp64).
+// Block = one 16 x 16 tile; half h covers views [h*ceil(nv/2), ...);
+// out2[h*d + pixel] (fp64).
 __global__ void __launch_bounds__(256) k_pb_backward(const PbGeom g, const float *__restrict__ r,
                                                      double *__restrict__ out2) {
   extern __shared__ __align__(16) float rs[];  // [kPbViews][B]
-  __shared__ double trig[2 * kPbViews];
+  __shared__ PbView vw[kPbViews];
   const int N = g.N, B = g.B;
   const int64_t d = (int64_t)N * N;
   const int half = blockIdx.y;
   const int vh = (g.nv + 1) / 2;
   const int va = half * vh, vb = min(g.nv, va + vh);
-  const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const int pr = (int)(p / N), pc = (int)(p - (int64_t)pr * N);
-  const double Xn = (double)(pc - N / 2), Yn = (double)(pr - N / 2);  // centre / Δ
+  const int tiles_c = (N + kPbTile - 1) / kPbTile;
+  const int tr0 = (blockIdx.x / tiles_c) * kPbTile, tc0 = (blockIdx.x % tiles_c) * kPbTile;
+  const int dr = threadIdx.x / kPbTile, dc = threadIdx.x % kPbTile;
+  const int pr = tr0 + dr, pc = tc0 + dc;
+  const bool own = pr < N && pc < N;
   pdl_wait();  // r is written by the forward pass
   double acc = 0.0;
   for (int v0 = va; v0 < vb; v0 += kPbViews) {
     const int nv = min(kPbViews, vb - v0);
     __syncthreads();
-    for (int i = threadIdx.x; i < nv * B; i += blockDim.x) rs[i] = __ldg(r + (int64_t)v0 * B + i);
-    for (int i = threadIdx.x; i < 2 * nv; i += blockDim.x) trig[i] = g.trig[2 * (g.v0 + v0) + i];
+    for (int i = threadIdx.x; i < nv * B; i += blockDim.x) cp_async4(rs + i, r + (int64_t)v0 * B + i);
+    if (threadIdx.x < nv) {
+      const int k = g.v0 + v0 + threadIdx.x;
+      const double cs = g.trig[2 * k], sn = g.trig[2 * k + 1];
+      const bool axis = fabs(cs) < 1e-12 || fabs(sn) < 1e-12;
+      const float a_ = axis ? (fabs(cs) < 1e-12 ? 0.0f : 1.0f) : (float)fabs(cs);
+      const float b_ = axis ? (fabs(sn) < 1e-12 ? 0.0f : 1.0f) : (float)fabs(sn);
+      const float amax = fmaxf(a_, b_), amin = fminf(a_, b_);
+      // b* of the tile corner: (X cos + Y sin) N + (B-1)/2, X N = tc0 - N/2
+      const double bsd = fma((double)(tc0 - N / 2), cs, (double)(tr0 - N / 2) * sn) + 0.5 * (B - 1);
+      const double bfl = floor(bsd);
+      PbView v;
+      v.cs = axis ? (fabs(cs) < 1e-12 ? 0.0f : (float)cs) : (float)cs;
+      v.sn = axis ? (fabs(sn) < 1e-12 ? 0.0f : (float)sn) : (float)sn;
+      v.base_f = (float)(bsd - bfl);
+      v.wb = 0.5f * (a_ + b_);
+      v.p1 = 0.5f * (amax - amin);
+      v.inv_max = 1.0f / amax;
+      v.inv_ab = amin > 0.0f ? 1.0f / (a_ * b_) : 0.0f;
+      v.base_i = (int)bfl | (axis ? (1 << 30) : 0);
+      vw[threadIdx.x] = v;
+    }
+    asm volatile("cp.async.wait_all;" ::: "memory");
     __syncthreads();
-    if (p < d) {
+    if (own) {
       float accf = 0.0f;
       for (int vv = 0; vv < nv; ++vv) {
-        const double cs = trig[2 * vv], sn = trig[2 * vv + 1];
-        const bool axis = fabs(cs) < 1e-12 || fabs(sn) < 1e-12;  // see k_pb_forward
-        const float a_ = axis ? (fabs(cs) < 1e-12 ? 0.0f : 1.0f) : (float)fabs(cs);
-        const float b_ = axis ? (fabs(sn) < 1e-12 ? 0.0f : 1.0f) : (float)fabs(sn);
-        const float amax = fmaxf(a_, b_), amin = fminf(a_, b_);
-        const float inv_max = 1.0f / amax, inv_ab = amin > 0.0f ? 1.0f / (a_ * b_) : 0.0f;
-        // bin coordinate of the pixel centre, b* = (X cos + Y sin) N + (B-1)/2,
-        // in fp64 and split so the fraction keeps fp32 precision
-        const double bsd = fma(Xn, cs, Yn * sn) + 0.5 * (B - 1);
-        const double bfl = floor(bsd);
-        const float fr = (float)(bsd - bfl);
-        const int bi = (int)bfl;
-        const float wb = 0.5f * (a_ + b_);  // footprint half-width in bins
-        const int j_lo = (int)ceilf(fr - wb);
+        const PbView v = vw[vv];
+        const bool axis = (v.base_i >> 30) & 1;
+        const int base_i = v.base_i & ~(1 << 30);
+        const float u = fmaf((float)dc, v.cs, fmaf((float)dr, v.sn, v.base_f));
+        const float kf = floorf(u);
+        const float fr = u - kf;                   // fraction of this pixel's b*
+        const int bi = base_i + (int)kf;
+        const int j_lo = (int)ceilf(fr - v.wb);
         const float *rv = rs + vv * B;
 #pragma unroll
         for (int j = 0; j < 2; ++j) {
           const int bb = bi + j_lo + j;
-          if (bb >= 0 && bb < B) {
-            const float sdd = fr - (float)(j_lo + j);  // b* - b
-            const float dd = fabsf(sdd);                // |δ| / Δ
-            float l;
-            if (axis) l = (sdd > -0.5f && sdd <= 0.5f) ? 1.0f : 0.0f;
-            else if (dd <= 0.5f * (amax - amin)) l = inv_max;
-            else if (dd >= wb) l = 0.0f;
-            else l = (wb - dd) * inv_ab;
-            accf = fmaf(l, rv[bb], accf);
-          }
+          const float sdd = fr - (float)(j_lo + j);  // b* - b
+          const float dd = fabsf(sdd);                // |δ| / Δ
+          float l = dd <= v.p1 ? v.inv_max : fmaxf(0.0f, (v.wb - dd) * v.inv_ab);
+          if (axis) l = (sdd > -0.5f && sdd <= 0.5f) ? 1.0f : 0.0f;
+          if (bb >= 0 && bb < B) accf = fmaf(l, rv[bb], accf);
         }
       }
       acc += (double)accf;
     }
   }
-  if (p < d) out2[half * d + p] = acc / (double)N;
+  if (own) out2[half * d + (int64_t)pr * N + pc] = acc / (double)N;
   pdl_trigger();
 }
 

@@ -385,7 +385,8 @@ int enqueue_pass(poly_handle *h, const double *x, bool loss) {
     const int thr = std::max(32, (p.pb_bins + 31) / 32 * 32);
     TRY(launch(h, loss ? (const void *)&k_pb_forward<true> : (const void *)&k_pb_forward<false>,
                dim3(h->pb.nv), dim3(thr), (size_t)kPbRows * p.pb_side * 4, true, h->pb, x32, a));
-    TRY(launch(h, (const void *)&k_pb_backward, dim3((unsigned)((p.d + 255) / 256), 2), dim3(256),
+    const unsigned tiles = (unsigned)(((p.pb_side + kPbTile - 1) / kPbTile) * ((p.pb_side + kPbTile - 1) / kPbTile));
+    TRY(launch(h, (const void *)&k_pb_backward, dim3(tiles, 2), dim3(kPbTile * kPbTile),
                (size_t)kPbViews * p.pb_bins * 4, true, h->pb, (const float *)h->rbuf, h->pb_out2));
     return launch(h, (const void *)&k_pb_combine, dim3((unsigned)std::min<int64_t>(1024, (p.d + 255) / 256)),
                   dim3(256), 0, true, (const double *)h->pb_out2, (int64_t)p.d, h->partials);
@@ -1163,8 +1164,13 @@ int poly_init(const poly_problem *pin, poly_handle **out) {
       std::vector<double> trig((size_t)2 * p.pb_views);
       for (int k = 0; k < p.pb_views; ++k) {
         const double th = 3.14159265358979323846 * (double)k / (double)p.pb_views;
-        trig[2 * k] = std::cos(th);
-        trig[2 * k + 1] = std::sin(th);
+        double cs = std::cos(th), sn = std::sin(th);
+        // axis-aligned views exactly (cos(π/2) is 6e-17 in fp64): edge rays then sit
+        // exactly on pixel edges in both passes and take the same tie rule
+        if (std::fabs(cs) < 1e-12) cs = 0.0, sn = sn > 0 ? 1.0 : -1.0;
+        if (std::fabs(sn) < 1e-12) sn = 0.0, cs = cs > 0 ? 1.0 : -1.0;
+        trig[2 * k] = cs;
+        trig[2 * k + 1] = sn;
       }
       if ((rc = dev_alloc(h, &h->pb_trig, trig.size())) != POLY_OK) return bail(rc);
       if (cudaMemcpy(h->pb_trig, trig.data(), trig.size() * 8, cudaMemcpyHostToDevice) != cudaSuccess)
