@@ -39,13 +39,13 @@ struct PbGeom {
 };
 
 // chord length / Δ for a pixel whose centre is u pixels (along the frame's
-// columns) from the ray's crossing point, a = |cos| >= b = |sin| of the frame
-__device__ __forceinline__ float chord(float u, float a, float b, float inv_a, float inv_ab) {
-  const float da = u * a;                    // |δ| / Δ
-  const float p1 = 0.5f * (a - b), p2 = 0.5f * (a + b);
-  if (da <= p1) return inv_a;
-  if (da >= p2) return 0.0f;
-  return (p2 - da) * inv_ab;
+// columns) from the ray's crossing point, a = |cos| >= b = |sin| of the frame:
+// plateau 1/a for u a <= p1, ramp (p2 - u a)/(a b) up to p2, 0 beyond —
+// written as selects (no branches in the inner loops).
+__device__ __forceinline__ float chord(float u, float a, float p1, float p2, float inv_a, float inv_ab) {
+  const float da = u * a;
+  const float ramp = fmaxf(0.0f, (p2 - da) * inv_ab);
+  return da <= p1 ? inv_a : ramp;
 }
 
 constexpr int kPbRows = 32;  // image rows staged per chunk in the forward
@@ -102,20 +102,29 @@ __global__ void __launch_bounds__(512) k_pb_forward(const PbGeom g, const float 
       const float fr0 = (float)(csd - cfl);
       const int ci0 = (int)cfl;
       const float tn = (float)tanf_;
-      for (int rr = 0; rr < nr; ++rr) {
-        const float u = fmaf(-(float)rr, tn, fr0);
-        const float kf = floorf(u);
-        const float fr = u - kf;
-        const int ci = ci0 + (int)kf;
-        const int j_lo = (int)ceilf(fr - w);  // candidates ci + j_lo .. ci + j_lo + 2
-        const float *xr = xs + rr * N;
+      if (axis) {  // uniform per view: a ray on a pixel edge goes to the positive side
+        for (int rr = 0; rr < nr; ++rr) {
+          const float u = fmaf(-(float)rr, tn, fr0);
+          const float kf = floorf(u + 0.5f);       // the one pixel with -1/2 <= c* - cc < 1/2
+          const int cc = ci0 + (int)kf;
+          if (cc >= 0 && cc < N) zf += xs[rr * N + cc];
+        }
+      } else {
+        const float p1 = 0.5f * (a_ - b_), p2 = 0.5f * (a_ + b_);
+        for (int rr = 0; rr < nr; ++rr) {
+          const float u = fmaf(-(float)rr, tn, fr0);
+          const float kf = floorf(u);
+          const float fr = u - kf;
+          const int j_lo = (int)ceilf(fr - w);  // candidates ci + j_lo .. ci + j_lo + 2
+          const int cc0 = ci0 + (int)kf + j_lo;
+          const float sd0 = fr - (float)j_lo;    // c* - cc0
+          const float *xr = xs + rr * N;
 #pragma unroll
-        for (int j = 0; j < 3; ++j) {
-          const int cc = ci + j_lo + j;
-          const float sd = fr - (float)(j_lo + j);  // c* - cc
-          const float l = axis ? ((sd >= -0.5f && sd < 0.5f) ? 1.0f : 0.0f)
-                               : chord(fabsf(sd), a_, b_, inv_a, inv_ab);
-          if (cc >= 0 && cc < N) zf = fmaf(l, xr[cc], zf);
+          for (int j = 0; j < 3; ++j) {
+            const int cc = cc0 + j;
+            const float l = chord(fabsf(sd0 - (float)j), a_, p1, p2, inv_a, inv_ab);
+            if (cc >= 0 && cc < N) zf = fmaf(l, xr[cc], zf);
+          }
         }
       }
       z += (double)zf;  // fp32 partial per chunk, fp64 across chunks
@@ -217,19 +226,23 @@ __global__ void __launch_bounds__(256) k_pb_backward(const PbGeom g, const float
         const bool axis = (v.base_i >> 30) & 1;
         const int base_i = v.base_i & ~(1 << 30);
         const float u = fmaf((float)dc, v.cs, fmaf((float)dr, v.sn, v.base_f));
-        const float kf = floorf(u);
-        const float fr = u - kf;                   // fraction of this pixel's b*
-        const int bi = base_i + (int)kf;
-        const int j_lo = (int)ceilf(fr - v.wb);
         const float *rv = rs + vv * B;
+        if (axis) {  // the one bin with -1/2 < b* - b <= 1/2
+          const int bb = base_i + (int)ceilf(u - 0.5f);
+          if (bb >= 0 && bb < B) accf += rv[bb];
+        } else {
+          const float kf = floorf(u);
+          const float fr = u - kf;
+          const int j_lo = (int)ceilf(fr - v.wb);
+          const int bb0 = base_i + (int)kf + j_lo;
+          const float sd0 = fr - (float)j_lo;  // b* - bb0
 #pragma unroll
-        for (int j = 0; j < 2; ++j) {
-          const int bb = bi + j_lo + j;
-          const float sdd = fr - (float)(j_lo + j);  // b* - b
-          const float dd = fabsf(sdd);                // |δ| / Δ
-          float l = dd <= v.p1 ? v.inv_max : fmaxf(0.0f, (v.wb - dd) * v.inv_ab);
-          if (axis) l = (sdd > -0.5f && sdd <= 0.5f) ? 1.0f : 0.0f;
-          if (bb >= 0 && bb < B) accf = fmaf(l, rv[bb], accf);
+          for (int j = 0; j < 2; ++j) {
+            const int bb = bb0 + j;
+            const float dd = fabsf(sd0 - (float)j);
+            const float l = dd <= v.p1 ? v.inv_max : fmaxf(0.0f, (v.wb - dd) * v.inv_ab);
+            if (bb >= 0 && bb < B) accf = fmaf(l, rv[bb], accf);
+          }
         }
       }
       acc += (double)accf;
