@@ -11,7 +11,7 @@ import ctypes as C
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libpoly.so")
+LIB_PATH = os.environ.get("POLY_LIB_PATH") or os.path.join(_HERE, "libpoly.so")
 
 POLY_OK, POLY_EINVAL, POLY_ECUDA, POLY_ENCCL, POLY_ENONFINITE, POLY_ENOMEM, POLY_EUNSUPPORTED = range(7)
 POLY_DENSE, POLY_CSR, POLY_PARALLEL_BEAM = 0, 1, 2

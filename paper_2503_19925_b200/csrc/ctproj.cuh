@@ -170,7 +170,7 @@ constexpr int kPbTile = 16;   // backward blocks cover 16 x 16 pixel tiles
 struct PbView {
   float cs, sn, base_f, wb;   // cos, sin, fraction at the tile corner, footprint half-width
   float p1, inv_max, inv_ab;  // plateau half-width, plateau and ramp scales
-  int base_i;                 // integer part at the tile corner (axis flag in bit 30)
+  int base_i;                 // integer part at the tile corner
 };
 
 // g_pixel = Σ_views Σ_bins L r: one thread per (pixel, half of the views).
@@ -214,7 +214,7 @@ __global__ void __launch_bounds__(256) k_pb_backward(const PbGeom g, const float
       v.p1 = 0.5f * (amax - amin);
       v.inv_max = 1.0f / amax;
       v.inv_ab = amin > 0.0f ? 1.0f / (a_ * b_) : 0.0f;
-      v.base_i = (int)bfl | (axis ? (1 << 30) : 0);
+      v.base_i = (int)bfl;  // may be negative; axis views are the ones with inv_ab == 0
       vw[threadIdx.x] = v;
     }
     asm volatile("cp.async.wait_all;" ::: "memory");
@@ -223,8 +223,8 @@ __global__ void __launch_bounds__(256) k_pb_backward(const PbGeom g, const float
       float accf = 0.0f;
       for (int vv = 0; vv < nv; ++vv) {
         const PbView v = vw[vv];
-        const bool axis = (v.base_i >> 30) & 1;
-        const int base_i = v.base_i & ~(1 << 30);
+        const bool axis = v.inv_ab == 0.0f;
+        const int base_i = v.base_i;
         const float u = fmaf((float)dc, v.cs, fmaf((float)dr, v.sn, v.base_f));
         const float *rv = rs + vv * B;
         if (axis) {  // the one bin with -1/2 < b* - b <= 1/2
