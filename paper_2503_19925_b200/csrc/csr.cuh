@@ -238,6 +238,21 @@ __global__ void __launch_bounds__(128) k_sell_forward(const CscEnt<T> *__restric
 #define POLY_SELL_UNROLL 4
 #endif
 constexpr int kSellUnroll = POLY_SELL_UNROLL;  // groups of four steps in flight per warp
+#ifndef POLY_SELL_UNROLL_F
+#define POLY_SELL_UNROLL_F POLY_SELL_UNROLL
+#endif
+#ifndef POLY_SELL_UNROLL_B
+#define POLY_SELL_UNROLL_B POLY_SELL_UNROLL
+#endif
+#ifndef POLY_SELL_MINB_F
+#define POLY_SELL_MINB_F 12  // forward: 40 registers, 12 blocks per SM (C4 pass 81.8 -> 79.8 us)
+#endif
+#define POLY_SELL_LB_F 128, POLY_SELL_MINB_F
+#ifdef POLY_SELL_MINB_B
+#define POLY_SELL_LB_B 128, POLY_SELL_MINB_B
+#else
+#define POLY_SELL_LB_B 128
+#endif
 
 struct Sell16 {
   const short4 *dl;        // [groups * 32]
@@ -319,7 +334,7 @@ __device__ __forceinline__ double sell16_dot(const Sell16 &s, int64_t slice, int
 }
 
 template <typename T, bool LOSS>
-__global__ void __launch_bounds__(128) k_sell16_forward(const Sell16 s, int64_t nslices,
+__global__ void __launch_bounds__(POLY_SELL_LB_F) k_sell16_forward(const Sell16 s, int64_t nslices,
                                                              const CsrFwdArgs a) {
   __shared__ double sp[3 * kMaxW];
   __shared__ double part[4][32];
@@ -328,7 +343,7 @@ __global__ void __launch_bounds__(128) k_sell16_forward(const Sell16 s, int64_t 
   pdl_wait();  // x is written by the previous kernel; r is read by the previous backward
   double lacc = 0.0;
   for (int64_t sl = blockIdx.x; sl < nslices; sl += gridDim.x) {  // fixed slice -> block map
-    part[warp][lane] = sell16_dot<T, kSellUnroll>(s, sl, warp, lane, a.x);
+    part[warp][lane] = sell16_dot<T, POLY_SELL_UNROLL_F>(s, sl, warp, lane, a.x);
     __syncthreads();
     lacc += forward_tail<LOSS>(part, sp, a, sl);
     __syncthreads();  // part is rewritten by the next slice
@@ -338,14 +353,14 @@ __global__ void __launch_bounds__(128) k_sell16_forward(const Sell16 s, int64_t 
 }
 
 template <typename T>
-__global__ void __launch_bounds__(128) k_sell16_backward(const Sell16 s, int64_t nslices,
+__global__ void __launch_bounds__(POLY_SELL_LB_B) k_sell16_backward(const Sell16 s, int64_t nslices,
                                                               int32_t d, const float *__restrict__ r,
                                                               double *__restrict__ g) {
   __shared__ double part[4][32];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   pdl_wait();  // r is written by the forward pass
   for (int64_t sl = blockIdx.x; sl < nslices; sl += gridDim.x) {
-    part[warp][lane] = sell16_dot<T, kSellUnroll>(s, sl, warp, lane, r);
+    part[warp][lane] = sell16_dot<T, POLY_SELL_UNROLL_B>(s, sl, warp, lane, r);
     __syncthreads();
     if (warp == 0) {
       const int64_t c = sl * 32 + lane;

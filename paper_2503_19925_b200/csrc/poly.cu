@@ -1206,9 +1206,9 @@ int poly_init(const poly_problem *pin, poly_handle **out) {
   if (p.set == POLY_SET_TV_NONNEG || p.set == POLY_SET_TV) {
     const int s = (int)llround(std::sqrt((double)p.d));
     h->tv_cl = std::min(kTvMaxCL, s);
-    const int cap = ((s + h->tv_cl - 1) / h->tv_cl) * s;
-    h->tv_smem = (size_t)7 * cap * 8 + (8 + 4 + (kTvThreads / 32) * 4) * 8;
-    if (h->tv_smem > kSmemLimit)
+    const int cap = ((s + h->tv_cl - 1) / h->tv_cl) * ((s + 31) & ~31);  // band rows x padded pitch
+    h->tv_smem = ((size_t)5 * cap + tv_edge_doubles(s) + 8 + 4 + (kTvThreads / 32) * 4) * 8 + tv_xchg_bytes(s);
+    if (s > 256 || h->tv_smem > kSmemLimit)
       return bail(fail(POLY_EUNSUPPORTED, "TV image side %d too large for one cluster", s));
     if ((rc = dev_alloc(h, &h->tv_zk, (size_t)p.d)) || (rc = dev_alloc(h, &h->tv_p, (size_t)p.d)) ||
         (rc = dev_alloc(h, &h->tv_q, (size_t)p.d)) || (rc = dev_alloc(h, &h->tv_stats, 3)))

@@ -12,16 +12,18 @@
 //
 // B200 mapping: ONE thread-block cluster of CL CTAs does the whole projection
 // — Dykstra, bisection and every FISTA iteration — with the image split into
-// CL row bands.  Each CTA keeps its band's prox input z, duals u (horizontal,
-// vertical), momentum duals w, the primal x and the extrapolated primal xw in
-// shared memory (fp64, 7 arrays); band edges are read from the neighbour
-// CTAs' shared memory (DSMEM) and every reduction (||Δx||, ||x||, TV) is
-// summed over the cluster in a fixed order, so all CTAs take identical branch
-// decisions.  Dykstra's state (z_k, p, q) lives in global memory (L2).  Two
-// cluster barriers per FISTA iteration; no kernel launches inside.
+// CL row bands (s <= 256).  Each CTA keeps its band's prox input z and primal
+// x in shared memory and the FISTA duals u, w (horizontal, vertical) and the
+// extrapolated primal xw in registers (tv_prox); band edges are read from the
+// neighbour CTAs' shared memory (DSMEM) and every reduction (||Δx||, ||x||,
+// TV) is summed over the cluster in a fixed order, so all CTAs take identical
+// branch decisions.  Dykstra's state (z_k, p, q) lives in global memory (L2).
+// Two cluster barriers per FISTA iteration; no kernel launches inside.
 #pragma once
 
 #include <cooperative_groups.h>
+
+#include <type_traits>
 
 #include "common.cuh"
 
@@ -44,14 +46,73 @@ struct TvArgs {
   SolveState *state;   // optional: non-finite flag (bad = -2) for the solver
 };
 
+constexpr int kTvMaxRpt = 8;
+#ifndef POLY_TV_CHUNK
+#define POLY_TV_CHUNK 1
+#endif
+constexpr int kTvChunk = POLY_TV_CHUNK;  // rows whose loads tv_prox issues together  // band rows per thread (s <= 256: at most 16 rows over >= 2 row groups)
+
+// shared doubles of tv_prox's edge buffers
+__host__ __device__ inline int tv_edge_doubles(int s) {
+  const int SC = (s + 31) & ~31, H = kTvThreads / SC;
+  return H * SC + H * kTvMaxRpt * (SC / 32);
+}
+
 struct TvBand {
   int s, r0, r1, npx, rank, CL;
-  double *z, *uh, *uv, *wh, *wv, *x, *xw;  // [npx] band arrays (shared)
+  int SC, H, RPT;                          // row pitch of the band arrays (s rounded up to 32) and
+                                           // tv_prox's thread map (row groups, rows each)
+  double *z, *x, *xw, *wh, *wv;            // [rows][SC] band arrays (shared; padding columns 0)
+  double *edge;                            // tv_prox's edge buffers
   double *red;                             // [2][4] this CTA's cluster-reduction slots
   double *wsum;                            // [warps * 4]
   double *tot;                             // [4] reduced totals
   int parity;
+  // tv_prox's point-to-point exchange (shared): mbarriers red[2], up[2], dn[2];
+  // red_slots[2][kTvMaxCL][2], halo_up[2][SC][2] (u_v, w_v of the previous
+  // band's last row), halo_dn[2][SC] (xw of the next band's first row); the
+  // buffer and phase of each use follow from counts every CTA shares
+  uint64_t *mbar;
+  double *xs;
+  uint32_t n_red, n_a, n_b;  // reductions, phase-A and phase-B executions (same in every CTA)
 };
+
+// shared bytes of tv_prox's exchange area (after the reduction scratch)
+__host__ __device__ inline int tv_xchg_bytes(int s) {
+  const int SC = (s + 31) & ~31;
+  return 6 * 8 + 8 + (2 * kTvMaxCL * 2 + 2 * SC * 2 + 2 * SC) * 8;  // (+8: 16-byte alignment)
+}
+
+__device__ __forceinline__ uint32_t mapa_u32(uint32_t a, int rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(rank));
+  return r;
+}
+// remote (cluster) shared-memory stores completing on the target CTA's mbarrier
+__device__ __forceinline__ void st_async_f64(uint32_t raddr, double v, uint32_t rbar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.f64 [%0], %1, [%2];" ::"r"(raddr), "d"(v),
+               "r"(rbar)
+               : "memory");
+}
+__device__ __forceinline__ void st_async_v2f64(uint32_t raddr, double a, double b, uint32_t rbar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.f64 [%0], {%1, %2}, [%3];" ::"r"(raddr),
+               "d"(a), "d"(b), "r"(rbar)
+               : "memory");
+}
+// wait for phase `parity` of a local mbarrier completed by remote st.async
+__device__ __forceinline__ void mbar_wait_cluster(uint32_t bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred P1;\n"
+      "WAITC_%=:\n\t"
+      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@!P1 bra WAITC_%=;\n}" ::"r"(bar),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.relaxed.cluster.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes)
+               : "memory");
+}
 
 __device__ __forceinline__ int band_r0(int rank, int s, int CL) { return rank * s / CL; }
 
@@ -101,11 +162,13 @@ __device__ __forceinline__ void cluster_sum(cg::cluster_group &cl, TvBand &b, do
 __device__ double tv_norm_x(cg::cluster_group &cl, TvBand &b) {
   const double *next_x = b.rank + 1 < b.CL ? cl.map_shared_rank(b.x, b.rank + 1) : nullptr;
   double acc[1] = {0.0};
-  for (int i = threadIdx.x; i < b.npx; i += blockDim.x) {
-    const int lr = i / b.s, c = i - lr * b.s;
+  const int R = b.r1 - b.r0;
+  for (int i = threadIdx.x; i < R * b.SC; i += blockDim.x) {
+    const int lr = i / b.SC, c = i - lr * b.SC;
+    if (c >= b.s) continue;
     if (c + 1 < b.s) acc[0] += fabs(b.x[i + 1] - b.x[i]);
     if (b.r0 + lr + 1 < b.s) {
-      const double below = (lr + 1 < b.r1 - b.r0) ? b.x[i + b.s] : next_x[c];
+      const double below = (lr + 1 < R) ? b.x[i + b.SC] : next_x[c];
       acc[0] += fabs(below - b.x[i]);
     }
   }
@@ -115,103 +178,312 @@ __device__ double tv_norm_x(cg::cluster_group &cl, TvBand &b) {
 
 // TV prox of b.z with parameter lam (FISTA on the dual, oracle_prox_tv's
 // iteration); leaves x = z - Dᵀu in b.x.  Returns the FISTA iterations.
-__device__ int tv_prox(cg::cluster_group &cl, TvBand &b, double lam, double rtol, int max_it) {
-  const int s = b.s;
-  for (int i = threadIdx.x; i < b.npx; i += blockDim.x) {
-    b.uh[i] = b.uv[i] = b.wh[i] = b.wv[i] = 0.0;
-    b.x[i] = b.z[i];
+//
+// Register-resident: thread t owns column c = t % SC (SC = s rounded up to
+// 32) of RPT consecutive band rows starting at h*RPT (h = t / SC), and keeps
+// its duals u, w (horizontal and vertical) and the extrapolated primal xw in
+// registers.  Horizontal neighbours are lanes of the same warp (shuffles; the
+// warp-edge columns go through small shared buffers), vertical neighbours the
+// thread's own next row, the row group above/below (shared edge rows) or the
+// neighbouring CTA's band (DSMEM).  Only z and x stay in shared memory
+// (row-major, lanes on consecutive columns: conflict-free).  Per pixel and
+// iteration that is 3 shared accesses instead of ~23 for a shared-array form,
+// whose FISTA iteration was bound by shared-memory bandwidth (6 µs at s=256).
+// the dynamic shared memory of k_tv_project
+extern __shared__ __align__(16) double tv_smem[];
+
+// fp64 shared-memory array addressed from tv_smem by an element offset, so
+// the compiler knows the address space inside tv_prox (not inlined; generic
+// pointers would make every access a 64-bit generic load).
+struct SmemF64 {
+  double *p;
+  __device__ explicit SmemF64(int off) : p(tv_smem + off) {}
+  __device__ __forceinline__ double ld(int i) const { return p[i]; }
+  __device__ __forceinline__ void st(int i, double v) const { p[i] = v; }
+};
+
+// clip to [-h, h] (h >= 0); fmin/fmax cost ~12 instructions each for fp64
+__device__ __forceinline__ double tv_clip(double v, double h) {
+  v = v > h ? h : v;
+  return v < -h ? -h : v;
+}
+
+// rows per thread for pitch SC: bands of at most ceil(SC/16) rows over 512/SC row groups
+__host__ __device__ constexpr int tv_mr(int SC) { return ((SC + 15) / 16 + kTvThreads / SC - 1) / (kTvThreads / SC); }
+
+template <int SC>
+__device__ int tv_prox(cg::cluster_group &cl, TvBand &bref, double lam, double rtol, int max_it) {
+  // a private copy of the band (registers): tv_prox is not inlined, and the
+  // reductions' parity flips on the caller's (local-memory) copy would put a
+  // local store in front of every cluster barrier's release fence
+  TvBand b = bref;
+  constexpr int MR = tv_mr(SC);
+  static_assert(MR <= kTvMaxRpt, "rows per thread");
+  constexpr int NCW = SC >> 5;
+  const int s = b.s, R = b.r1 - b.r0;
+  const int h = (int)threadIdx.x / SC, c = (int)threadIdx.x - h * SC;
+  const int lane = threadIdx.x & 31, cw = c >> 5;
+  const int lr0 = h * b.RPT;
+  const int nr = max(0, min(b.RPT, R - lr0));
+  const bool col_ok = c < s;
+  // shared: z, x, xw and the momentum duals wh, wv as [rows][SC] band arrays;
+  // edge buffers bot_uv[h][c] (last row of row group h) and e_uh[h][k][cw]
+  // (warp-edge u_h, lane 31)
+  // (32-bit shared addresses: this function is not inlined, and generic
+  // pointers would turn every access into a 64-bit generic load)
+  const int e_o = (int)(b.edge - b.z);  // (b.z is tv_smem)
+  const SmemF64 Z(0), X((int)(b.x - b.z)), XW((int)(b.xw - b.z)), WH((int)(b.wh - b.z)), WV((int)(b.wv - b.z)),
+      BU(e_o), EU(e_o + b.H * SC);
+  const int eb = (h * MR) * NCW + cw;  // e_uh[h][k][cw] = e_uh[eb + k*NCW]
+  for (int i = threadIdx.x; i < R * SC; i += blockDim.x) {
+    X.st(i, Z.ld(i));
+    XW.st(i, 0.0), WH.st(i, 0.0), WV.st(i, 0.0);
   }
+  for (int i = threadIdx.x; i < b.H * SC; i += blockDim.x) BU.st(i, 0.0);
+  for (int i = threadIdx.x; i < b.H * MR * NCW; i += blockDim.x) EU.st(i, 0.0);
   cl.sync();
-  if (!(lam > 0.0)) return 0;
+  if (!(lam > 0.0)) return 0;  // (no reductions yet: bref.parity unchanged)
   const double hl = 0.5 * lam;
-  const int prev_off = b.rank > 0 ? (b.r0 - band_r0(b.rank - 1, s, b.CL) - 1) * s : 0;
-  const double *prev_wv = b.rank > 0 ? cl.map_shared_rank(b.wv, b.rank - 1) : nullptr;
-  const double *prev_uv = b.rank > 0 ? cl.map_shared_rank(b.uv, b.rank - 1) : nullptr;
-  const double *next_xw = b.rank + 1 < b.CL ? cl.map_shared_rank(b.xw, b.rank + 1) : nullptr;
-  const int i0r = (int)threadIdx.x / s, i0c = (int)threadIdx.x - i0r * s;
-  const int st_r = (int)blockDim.x / s, st_c = (int)blockDim.x - st_r * s;  // pixel stride as (rows, cols)
-  // this thread's last pixel (pixels i = tid + k * blockDim; at most one per row
-  // since s <= blockDim for every supported band)
-  const int last_i = (int)threadIdx.x < b.npx
-                         ? (int)threadIdx.x + ((b.npx - 1 - (int)threadIdx.x) / (int)blockDim.x) * (int)blockDim.x
-                         : -1;
-  const int last_r = last_i >= 0 ? last_i / s : -1, last_c = last_i >= 0 ? last_i - last_r * s : 0;
+  // Boundary rules as data, so the per-pixel code has no branches: a dual
+  // that the oracle never updates (no right / lower neighbour, or a padding
+  // row or column) is clipped to [-0, 0] and stays 0, and a 0 term adds
+  // exactly nothing to the divergence sums.  pm: rows with pixels; vm: rows
+  // with a lower neighbour (bit k = row lr0 + k).
+  const double hlh = (c + 1 < s) ? hl : 0.0;
+  unsigned pm = 0, vm = 0;
+#pragma unroll
+  for (int k = 0; k < MR; ++k) {
+    if (k < nr && col_ok) pm |= 1u << k;
+    if (k < nr && col_ok && b.r0 + lr0 + k + 1 < s) vm |= 1u << k;
+  }
+  const bool left_edge = lane == 0 && cw > 0, right_edge = lane == 31 && cw + 1 < NCW;
+  // Exchanges without cluster barriers: every CTA pushes (st.async) its
+  // reduction partials to all CTAs, its first row of xw to the band above and
+  // its last row of (u_v, w_v) to the band below, each completing on the
+  // receiver's mbarrier; buffers alternate, and a producer can be at most one
+  // use ahead (its next push of a buffer needs a reduction the receiver only
+  // joins after reading it).
+  const bool has_up = b.rank > 0, has_dn = b.rank + 1 < b.CL;
+  const uint32_t mb = (uint32_t)__cvta_generic_to_shared(b.mbar);  // red[2], up[2], dn[2]
+  const uint32_t xs = (uint32_t)__cvta_generic_to_shared(b.xs);
+  const uint32_t red_o = xs, up_o = xs + 2 * kTvMaxCL * 2 * 8, dn_o = up_o + 2 * SC * 2 * 8;
+  const double *red_slots = b.xs, *halo_up = b.xs + 2 * kTvMaxCL * 2, *halo_dn = halo_up + 2 * SC * 2;
+  const bool up_local = lr0 > 0 && col_ok, up_halo = lr0 == 0 && has_up && col_ok;
+  const bool dn_local = lr0 + nr < R && col_ok, dn_halo = lr0 + nr == R && nr > 0 && has_dn && col_ok;
+  const bool push_up = lr0 == 0 && nr > 0 && has_up && col_ok;   // xw row 0 -> band above
+  const bool push_dn = lr0 + nr == R && nr > 0 && has_dn && col_ok;  // (u_v, w_v) last row -> band below
+  const int i0 = lr0 * SC + c;
+  // every lane of the warp has all MR rows (the common case; no per-row predicates)
+  const bool full_rows = __all_sync(0xffffffffu, nr == MR && col_ok);
+  double uh[MR], uv[MR];
+#pragma unroll
+  for (int k = 0; k < MR; ++k) uh[k] = uv[k] = 0.0;
   double t = 1.0;
   int it = 1;
   for (;; ++it) {
+    // this iteration's xw halo from the band below (pushed in its phase A)
+    if (threadIdx.x == 0 && has_dn) mbar_expect_tx(mb + 8 * (4 + (b.n_a & 1)), (uint32_t)s * 8u);
     // phase A: x(u) = z - Dᵀu (the oracle's primal after iteration it-1) and
     // xw = z - Dᵀw; change of x against the previous primal
     double acc[2] = {0.0, 0.0};
-    // the band's first row needs the previous band's last-row duals (DSMEM):
-    // issued first, used last (pixels walked in reverse)
-    double hwv = 0.0, huv = 0.0;
-    if (i0r == 0 && b.rank > 0) hwv = prev_wv[prev_off + i0c], huv = prev_uv[prev_off + i0c];
-    for (int i = last_i, lr = last_r, c = last_c; i >= (int)threadIdx.x; i -= blockDim.x) {
-      const int r = b.r0 + lr;
-      double dw = 0.0, du = 0.0;
-      if (c + 1 < s) dw -= b.wh[i], du -= b.uh[i];
-      if (c > 0) dw += b.wh[i - 1], du += b.uh[i - 1];
-      if (r + 1 < s) dw -= b.wv[i], du -= b.uv[i];
-      if (r > 0) {
-        if (lr > 0) dw += b.wv[i - s], du += b.uv[i - s];
-        else dw += hwv, du += huv;
+    if (nr > 0) {  // warp-uniform
+      double a_uv = 0.0, a_wv = 0.0;  // row above
+      if (up_local) a_uv = BU.ld((h - 1) * SC + c), a_wv = WV.ld(i0 - SC);
+      if (it > 1 && lr0 == 0 && has_up) {  // (u_v, w_v) halo pushed by the band above in its last phase B
+        const uint32_t q = (b.n_b - 1) & 1;
+        mbar_wait_cluster(mb + 8 * (2 + q), ((b.n_b - 1) >> 1) & 1);
+        if (up_halo) a_uv = halo_up[(q * SC + c) * 2], a_wv = halo_up[(q * SC + c) * 2 + 1];
       }
-      const double xn = b.z[i] - du;
-      b.xw[i] = b.z[i] - dw;
-      const double dx = xn - b.x[i];
-      acc[0] += dx * dx;
-      acc[1] += xn * xn;
-      b.x[i] = xn;
-      c -= st_c, lr -= st_r;
-      if (c < 0) c += s, --lr;
+      auto phase_a = [&](auto full_t) {
+        constexpr bool full = decltype(full_t)::value;
+        // rows in chunks of CH: a chunk's loads are issued before its
+        // arithmetic and stores (the compiler cannot move a load above a
+        // shared store it cannot disambiguate)
+#pragma unroll
+        for (int kk = 0; kk < MR; kk += kTvChunk) {
+          constexpr int CH = kTvChunk;
+          double l_uh[CH], wh_i[CH], wh_l[CH], wv_i[CH], zi[CH], xo[CH];
+#pragma unroll
+          for (int j = 0; j < CH; ++j) {
+            const int k = kk + j;
+            if (k >= MR) break;
+            const int i = i0 + k * SC;
+            l_uh[j] = __shfl_up_sync(0xffffffffu, uh[k], 1);
+            if (lane == 0) l_uh[j] = 0.0;
+            if (left_edge) l_uh[j] = EU.ld(eb + k * NCW - 1);
+            const bool on = full ? true : (pm >> k) & 1;
+            wh_i[j] = wh_l[j] = wv_i[j] = zi[j] = xo[j] = 0.0;
+            if (on) {
+              wh_i[j] = WH.ld(i), wv_i[j] = WV.ld(i), zi[j] = Z.ld(i), xo[j] = X.ld(i);
+              if (c > 0) wh_l[j] = WH.ld(i - 1);
+            }
+          }
+#pragma unroll
+          for (int j = 0; j < CH; ++j) {
+            const int k = kk + j;
+            if (k >= MR) break;
+            const int i = i0 + k * SC;
+            const bool on = full ? true : (pm >> k) & 1;
+            // the oracle's sums with its zero terms kept: -w_h(c) + w_h(c-1) - w_v(r) + w_v(r-1)
+            const double dw = ((wh_l[j] - wh_i[j]) - wv_i[j]) + a_wv;
+            const double du = ((l_uh[j] - uh[k]) - uv[k]) + a_uv;
+            const double xn = zi[j] - du;
+            const double dx = xn - xo[j];
+            if (on) {  // (rows past the band or padding columns contribute nothing)
+              acc[0] = fma(dx, dx, acc[0]);
+              acc[1] = fma(xn, xn, acc[1]);
+              const double xwn = zi[j] - dw;
+              X.st(i, xn), XW.st(i, xwn);
+              if (k == 0 && push_up)
+                st_async_f64(mapa_u32(dn_o + 8u * (uint32_t)((b.n_a & 1) * SC + c), b.rank - 1), xwn,
+                             mapa_u32(mb + 8 * (4 + (b.n_a & 1)), b.rank - 1));
+            }
+            a_uv = uv[k], a_wv = wv_i[j];
+          }
+        }
+      };
+      if (full_rows) phase_a(std::true_type());
+      else phase_a(std::false_type());
     }
-    cluster_sum<2>(cl, b, acc);  // also publishes xw to the band above
+    // ||Δx||², ||x||² over the cluster: warps in order, then every CTA pushes
+    // its pair to every rank and sums the CL pairs in rank order
+    {
+      const uint32_t q = b.n_red & 1;
+#pragma unroll
+      for (int k = 0; k < 2; ++k) {
+        double v = acc[k];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        if (lane == 0) b.wsum[(threadIdx.x >> 5) * 4 + k] = v;
+      }
+      __syncthreads();  // also: xw, x of every row group written
+      if ((int)threadIdx.x < b.CL) {
+        double p0 = 0.0, p1 = 0.0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) p0 += b.wsum[w * 4], p1 += b.wsum[w * 4 + 1];
+        st_async_v2f64(mapa_u32(red_o + 16u * (uint32_t)(q * kTvMaxCL + b.rank), threadIdx.x), p0, p1,
+                       mapa_u32(mb + 8 * q, threadIdx.x));
+      }
+      if (threadIdx.x == 0) mbar_expect_tx(mb + 8 * q, (uint32_t)b.CL * 16u);
+      mbar_wait_cluster(mb + 8 * q, (b.n_red >> 1) & 1);
+      acc[0] = acc[1] = 0.0;
+      for (int r = 0; r < b.CL; ++r)
+        acc[0] += red_slots[(q * kTvMaxCL + r) * 2], acc[1] += red_slots[(q * kTvMaxCL + r) * 2 + 1];
+      ++b.n_red;
+    }
     if ((it > 1 && sqrt(acc[0]) <= rtol * sqrt(acc[1])) || it > max_it) break;
     // phase B: u+ = clip(w + D xw / 8, ±λ/2); w = u+ + ((t-1)/t+)(u+ - u)
     const double tn = 0.5 * (1.0 + sqrt(1.0 + 4.0 * t * t));
     const double beta = (t - 1.0) / tn;
     t = tn;
-    // the band's last row needs the next band's first-row xw (DSMEM): issued
-    // first, used last (pixels walked forward)
-    const double hxw = (last_r == b.r1 - b.r0 - 1 && next_xw) ? next_xw[last_c] : 0.0;
-    for (int i = threadIdx.x, lr = i0r, c = i0c; i < b.npx; i += blockDim.x) {
-      const int r = b.r0 + lr;
-      if (c + 1 < s) {
-        const double un = fmin(hl, fmax(-hl, b.wh[i] + (b.xw[i + 1] - b.xw[i]) / 8.0));
-        b.wh[i] = un + beta * (un - b.uh[i]);
-        b.uh[i] = un;
+    // the (u_v, w_v) halo the band above will push in its phase B
+    if (threadIdx.x == 0 && has_up) mbar_expect_tx(mb + 8 * (2 + (b.n_b & 1)), (uint32_t)s * 16u);
+    if (nr > 0) {
+      double dn_xw = 0.0;  // row below the thread's last row
+      if (dn_local) dn_xw = XW.ld(i0 + nr * SC);
+      if (lr0 + nr == R && has_dn) {
+        const uint32_t q = b.n_a & 1;
+        mbar_wait_cluster(mb + 8 * (4 + q), (b.n_a >> 1) & 1);
+        if (dn_halo) dn_xw = halo_dn[q * SC + c];
       }
-      if (r + 1 < s) {
-        const double below = (lr + 1 < b.r1 - b.r0) ? b.xw[i + s] : hxw;
-        const double un = fmin(hl, fmax(-hl, b.wv[i] + (below - b.xw[i]) / 8.0));
-        b.wv[i] = un + beta * (un - b.uv[i]);
-        b.uv[i] = un;
-      }
-      c += st_c, lr += st_r;
-      if (c >= s) c -= s, ++lr;
+      auto phase_b = [&](auto full_t) {
+        constexpr bool full = decltype(full_t)::value;
+#pragma unroll
+        for (int kk = 0; kk < MR; kk += kTvChunk) {
+          constexpr int CH = kTvChunk;
+          double xr[CH + 1], r_xw[CH], wh_i[CH], wv_i[CH];
+#pragma unroll
+          for (int j = 0; j <= CH; ++j) {  // xw of rows kk .. kk+CH (the last: next chunk / row below)
+            const int k = kk + j;
+            if (k > MR) break;
+            xr[j] = dn_xw;
+            if (k < MR && (full || ((pm >> k) & 1))) xr[j] = XW.ld(i0 + k * SC);
+          }
+#pragma unroll
+          for (int j = 0; j < CH; ++j) {
+            const int k = kk + j;
+            if (k >= MR) break;
+            const int i = i0 + k * SC;
+            const bool on = full ? true : (pm >> k) & 1;
+            r_xw[j] = __shfl_down_sync(0xffffffffu, xr[j], 1);
+            wh_i[j] = wv_i[j] = 0.0;
+            if (on) {
+              wh_i[j] = WH.ld(i), wv_i[j] = WV.ld(i);
+              if (right_edge) r_xw[j] = XW.ld(i + 1);
+            }
+          }
+#pragma unroll
+          for (int j = 0; j < CH; ++j) {
+            const int k = kk + j;
+            if (k >= MR) break;
+            const int i = i0 + k * SC;
+            const bool on = full ? true : (pm >> k) & 1;
+            const double cur = xr[j], nxt = xr[j + 1];
+            const double hlv = (vm >> k) & 1 ? hl : 0.0;
+            const double unh = tv_clip(wh_i[j] + (r_xw[j] - cur) / 8.0, on ? hlh : 0.0);  // u_h stays 0 off the band
+            const double unv = tv_clip(wv_i[j] + (nxt - cur) / 8.0, hlv);
+            const double wvn = unv + beta * (unv - uv[k]);
+            if (on) {
+              WH.st(i, unh + beta * (unh - uh[k]));
+              WV.st(i, wvn);
+            }
+            uh[k] = unh;
+            uv[k] = unv;
+            if (lane == 31 && k < nr) EU.st(eb + k * NCW, unh);
+            if (k == nr - 1) {
+              BU.st(h * SC + c, unv);
+              if (push_dn)
+                st_async_v2f64(mapa_u32(up_o + 16u * (uint32_t)((b.n_b & 1) * SC + c), b.rank + 1), unv, wvn,
+                               mapa_u32(mb + 8 * (2 + (b.n_b & 1)), b.rank + 1));
+            }
+          }
+        }
+      };
+      if (full_rows) phase_b(std::true_type());
+      else phase_b(std::false_type());
     }
-    cl.sync();  // duals complete before the next phase A reads the neighbours'
+    ++b.n_a, ++b.n_b;
+    __syncthreads();  // duals of every row group written before the next phase A
   }
+  // the band below pushed this (last) iteration's xw halo: consume its phase
+  if (has_dn) mbar_wait_cluster(mb + 8 * (4 + (b.n_a & 1)), (b.n_a >> 1) & 1);
+  ++b.n_a;
+  cl.sync();  // x final everywhere (callers read the neighbours' x)
+  bref.parity = b.parity;
+  bref.n_red = b.n_red, bref.n_a = b.n_a, bref.n_b = b.n_b;
   return it - 1;
 }
 
-// P_X1 of the band input b.z into b.x (oracle_project_tv): b.z itself when
-// its TV is <= τ, else the prox with λ bracketed and bisected.
+#ifndef POLY_TV_INLINE
+__noinline__
+#endif
+__device__ int tv_prox_any(cg::cluster_group &cl, TvBand &b, double lam, double rtol, int max_it) {
+  switch (b.SC) {
+    case 32: return tv_prox<32>(cl, b, lam, rtol, max_it);
+    case 64: return tv_prox<64>(cl, b, lam, rtol, max_it);
+    case 96: return tv_prox<96>(cl, b, lam, rtol, max_it);
+    case 128: return tv_prox<128>(cl, b, lam, rtol, max_it);
+    case 160: return tv_prox<160>(cl, b, lam, rtol, max_it);
+    case 192: return tv_prox<192>(cl, b, lam, rtol, max_it);
+    case 224: return tv_prox<224>(cl, b, lam, rtol, max_it);
+    default: return tv_prox<256>(cl, b, lam, rtol, max_it);
+  }
+}
+
 __device__ void tv_project_ball(cg::cluster_group &cl, TvBand &b, const TvArgs &a,
                                 int *n_bis, int *n_fista) {
-  for (int i = threadIdx.x; i < b.npx; i += blockDim.x) b.x[i] = b.z[i];
+  for (int i = threadIdx.x; i < (b.r1 - b.r0) * b.SC; i += blockDim.x) b.x[i] = b.z[i];
   cl.sync();
   if (tv_norm_x(cl, b) <= a.tau) return;
   double lo = 0.0, hi = 1.0;
   for (int g = 0; g < 200; ++g) {
-    *n_fista += tv_prox(cl, b, hi, a.rtol, a.max_it);
+    *n_fista += tv_prox_any(cl, b, hi, a.rtol, a.max_it);
     if (tv_norm_x(cl, b) <= a.tau) break;
     lo = hi;
     hi *= 2.0;
   }
   for (int st = 1; st <= 60; ++st) {
     const double lam = 0.5 * (lo + hi);
-    *n_fista += tv_prox(cl, b, lam, a.rtol, a.max_it);
+    *n_fista += tv_prox_any(cl, b, lam, a.rtol, a.max_it);
     ++*n_bis;
     const double tv = tv_norm_x(cl, b);
     if (fabs(tv - a.tau) <= a.tv_tol) break;
@@ -221,7 +493,7 @@ __device__ void tv_project_ball(cg::cluster_group &cl, TvBand &b, const TvArgs &
 }
 
 __global__ void __launch_bounds__(kTvThreads, 1) k_tv_project(const TvArgs a) {
-  extern __shared__ __align__(16) double tsm[];
+  double *tsm = tv_smem;
   cg::cluster_group cl = cg::this_cluster();
   TvBand b;
   b.s = a.s;
@@ -230,26 +502,48 @@ __global__ void __launch_bounds__(kTvThreads, 1) k_tv_project(const TvArgs a) {
   b.r0 = band_r0(b.rank, a.s, b.CL);
   b.r1 = band_r0(b.rank + 1, a.s, b.CL);
   b.npx = (b.r1 - b.r0) * a.s;
-  const int cap = ((a.s + b.CL - 1) / b.CL) * a.s;  // largest band
+  b.SC = (a.s + 31) & ~31;
+  const int cap_r = (a.s + b.CL - 1) / b.CL, cap = cap_r * b.SC;  // largest band
+  b.H = kTvThreads / b.SC;
+  b.RPT = (cap_r + b.H - 1) / b.H;
   b.z = tsm;
-  b.uh = b.z + cap;
-  b.uv = b.uh + cap;
-  b.wh = b.uv + cap;
-  b.wv = b.wh + cap;
-  b.x = b.wv + cap;
+  b.x = b.z + cap;
   b.xw = b.x + cap;
-  b.red = b.xw + cap;
+  b.wh = b.xw + cap;
+  b.wv = b.wh + cap;
+  b.edge = b.wv + cap;
+  b.red = b.edge + tv_edge_doubles(a.s);
   b.tot = b.red + 8;
   b.wsum = b.tot + 4;
   b.parity = 0;
+  b.mbar = reinterpret_cast<uint64_t *>(b.wsum + (kTvThreads / 32) * 4);
+  b.xs = reinterpret_cast<double *>((reinterpret_cast<uintptr_t>(b.mbar + 6) + 15) & ~(uintptr_t)15);
+  b.n_red = b.n_a = b.n_b = 0;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < 6; ++i) mbar_init(b.mbar + i, 1);
+    fence_mbar_init();
+  }
+  cl.sync();
   pdl_wait();  // v is written by the previous kernel
   pdl_trigger();
   const int64_t g0 = (int64_t)b.r0 * a.s;
+  const int nb = (b.r1 - b.r0) * b.SC;  // band arrays incl. padding columns
+  // band element i (pitch SC) <-> global pixel g0 + gi(i); padding columns have gi < 0
+  auto gi = [&](int i) -> int64_t {
+    const int lr = i / b.SC, c = i - lr * b.SC;
+    return c < a.s ? (int64_t)lr * a.s + c : -1;
+  };
   int n_bis = 0, n_fista = 0, sweeps = 0;
   if (!a.nonneg) {
-    for (int i = threadIdx.x; i < b.npx; i += blockDim.x) b.z[i] = a.v[g0 + i];
+    for (int i = threadIdx.x; i < nb; i += blockDim.x) {
+      const int64_t j = gi(i);
+      b.z[i] = j >= 0 ? a.v[g0 + j] : 0.0;
+    }
     tv_project_ball(cl, b, a, &n_bis, &n_fista);
-    for (int i = threadIdx.x; i < b.npx; i += blockDim.x) a.out[g0 + i] = b.x[i];
+    for (int i = threadIdx.x; i < nb; i += blockDim.x) {
+      const int64_t j = gi(i);
+      if (j >= 0) a.out[g0 + j] = b.x[i];
+    }
   } else {
     // Dykstra: z_0 = v, p_0 = q_0 = 0
     for (int i = threadIdx.x; i < b.npx; i += blockDim.x) {
@@ -258,18 +552,23 @@ __global__ void __launch_bounds__(kTvThreads, 1) k_tv_project(const TvArgs a) {
       a.q[g0 + i] = 0.0;
     }
     for (sweeps = 1; sweeps <= a.max_outer; ++sweeps) {
-      for (int i = threadIdx.x; i < b.npx; i += blockDim.x) b.z[i] = a.zk[g0 + i] + a.p[g0 + i];
+      for (int i = threadIdx.x; i < nb; i += blockDim.x) {
+        const int64_t j = gi(i);
+        b.z[i] = j >= 0 ? a.zk[g0 + j] + a.p[g0 + j] : 0.0;
+      }
       tv_project_ball(cl, b, a, &n_bis, &n_fista);  // y_k in b.x
       double acc[1] = {0.0};
-      for (int i = threadIdx.x; i < b.npx; i += blockDim.x) {
-        const double zk = a.zk[g0 + i], y = b.x[i];
-        const double pn = zk + a.p[g0 + i] - y;
-        const double sq = y + a.q[g0 + i];
+      for (int i = threadIdx.x; i < nb; i += blockDim.x) {
+        const int64_t j = gi(i);
+        if (j < 0) continue;
+        const double zk = a.zk[g0 + j], y = b.x[i];
+        const double pn = zk + a.p[g0 + j] - y;
+        const double sq = y + a.q[g0 + j];
         const double zn = sq > 0.0 ? sq : 0.0;
-        a.p[g0 + i] = pn;
-        a.q[g0 + i] = sq - zn;
+        a.p[g0 + j] = pn;
+        a.q[g0 + j] = sq - zn;
         acc[0] += (zn - zk) * (zn - zk);
-        a.zk[g0 + i] = zn;
+        a.zk[g0 + j] = zn;
       }
       cluster_sum<1>(cl, b, acc);
       if (sqrt(acc[0]) <= a.tol) break;

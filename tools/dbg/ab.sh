@@ -1,5 +1,4 @@
-python -m pytest tests/test_gpu_ctproj.py -q 2>&1 | tail -2
-for v in default pf1 pf2 pf4; do
+for v in default $VARIANTS; do
   if [ $v = default ]; then unset POLY_LIB_PATH; else export POLY_LIB_PATH=$PWD/build_variants/libpoly_$v.so; fi
-  echo $v $(python tools/time_pb.py 2>&1 | tail -1)
+  echo $v $(python tools/time_pb.py --csr-only 2>&1 | tail -1 | python -c "import json,sys; d=json.loads(sys.stdin.read())['csr']; print(round(d['pass_ms']*1e3,1), round(d['iteration_ms']*1e3,1))")
 done
