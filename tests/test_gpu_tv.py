@@ -131,3 +131,21 @@ def test_solve_with_tv_set_matches_oracle():
     p.solve(x, 3, gam)
     assert rel(x.cpu().numpy(), x_ref) <= 1e-4, rel(x.cpu().numpy(), x_ref)
     p.close()
+
+
+@pytest.mark.parametrize("side", [100, 200, 256])
+@pytest.mark.parametrize("max_it", [3, 50])
+def test_tv_ball_projection_fixed_iterations_matches_oracle(side, max_it):
+    """With rtol below reach both sides run exactly max_it FISTA iterations
+    per prox, so the cluster kernel must follow the oracle's iteration step
+    for step: sides whose bands give the kernel partial row groups (100, 200)
+    and the full 16-row bands of 256, every bisection step included."""
+    z = _image(side, side)
+    tau = 0.4 * oracle.tv_norm(z)
+    x_ref, steps = oracle.project_tv(z, tau, tv_tol=1e-3, rtol=1e-30, max_it=max_it)
+    p = _handle(side, _P().POLY_SET_TV, dict(tau=tau, tol=1e-3, rtol=1e-30, max_it=max_it))
+    x, st = p.project(torch.tensor(z, device="cuda"))
+    x = x.cpu().numpy()
+    assert st[1] == min(steps, 60) and st[2] % max_it == 0 and st[2] >= max_it * st[1]
+    assert np.abs(x - x_ref).max() <= 1e-12 * max(1.0, np.abs(x_ref).max())
+    p.close()

@@ -9,4 +9,5 @@ python tools/ncu_summary.py full gpurun_out/prof_k1_c2_$TAG.ncu-rep $OUT/${TAG}_
 python tools/ncu_summary.py full gpurun_out/prof_k1_c3_$TAG.ncu-rep $OUT/${TAG}_k1_c3_full.txt > /dev/null
 python tools/ncu_summary.py full gpurun_out/prof_k4_c4_$TAG.ncu-rep $OUT/${TAG}_k4_c4_full.txt > /dev/null
 python tools/ncu_summary.py full gpurun_out/prof_k1_c5_$TAG.ncu-rep $OUT/${TAG}_k1_c5_full.txt > /dev/null
+python tools/ncu_summary.py full gpurun_out/prof_tv_$TAG.ncu-rep $OUT/${TAG}_tv_k_tv_project_full.txt > /dev/null
 ls -la $OUT

@@ -24,6 +24,8 @@ ncu --set full --clock-control none --import-source on -k regex:"k_sell16" -s 4 
     python bench.py --config c4 --steps 10 --warmup 3 --no-cpu --no-e2e > /dev/null 2>&1; echo "full c4 rc=$?"
 ncu --set full --clock-control none -k regex:k_dense_loss_grad -s 2 -c 1 -o gpurun_out/prof_k1_c5_$TAG -f \
     python bench.py --config c5 --steps 3 --warmup 3 --no-cpu --no-e2e > /dev/null 2>&1; echo "full c5 rc=$?"
+ncu --set full --clock-control none --import-source on -k regex:k_tv_project -c 1 -o gpurun_out/prof_tv_$TAG -f \
+    python tools/tv_time.py 256 > /dev/null 2>&1; echo "full tv rc=$?"
 # summaries on the box (ncu -i), then drop the large reports so gpurun_out/ stays under 64 MiB
 bash tools/collect_profiles.sh $TAG gpurun_out/profiles_$TAG > /dev/null 2>&1; echo "collect rc=$?"
 rm -f gpurun_out/*.ncu-rep
