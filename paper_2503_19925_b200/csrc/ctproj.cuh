@@ -21,10 +21,12 @@
 //                      which the ray is again "steep"); each ray adds the at
 //                      most 3 pixels per row its footprint covers; then the
 //                      link and residual per ray (fp64) as K1, r stored fp32.
-//   K5b k_pb_backward  one thread per (pixel, half of the views): for every
-//                      view the at most 2 bins whose rays cross the pixel,
-//                      residuals staged per view chunk in shared memory; the
-//                      two halves are added in order (deterministic).
+//   K5b k_pb_backward  one thread per 4 pixels of a 16 x 16 tile row and a
+//                      quarter of the views: for every view the at most 2
+//                      bins whose rays cross each pixel, from the 32-bin
+//                      window of residuals the tile can reach (staged per
+//                      view chunk in shared memory); the quarters are added
+//                      in order (deterministic).
 #pragma once
 
 #include "dense.cuh"
@@ -38,24 +40,25 @@ struct PbGeom {
   const double *trig;  // [2V]: cos θ_k, sin θ_k (host libm, θ_k = kπ/V)
 };
 
-// chord length / Δ for a pixel whose centre is u pixels (along the frame's
-// columns) from the ray's crossing point, a = |cos| >= b = |sin| of the frame:
-// plateau 1/a for u a <= p1, ramp (p2 - u a)/(a b) up to p2, 0 beyond —
-// written as selects (no branches in the inner loops).
-__device__ __forceinline__ float chord(float u, float a, float p1, float p2, float inv_a, float inv_ab) {
-  const float da = u * a;
-  const float ramp = fmaxf(0.0f, (p2 - da) * inv_ab);
-  return da <= p1 ? inv_a : ramp;
+// chord length / Δ for a pixel whose centre is dd (>= 0) pixel widths from
+// the ray, measured along the axis the scales refer to:
+//   min(plateau, max(0, kp - dd * kd))
+// equals the plateau 1/max(a,b) for dd <= Δ|a-b|/2, the ramp beyond it and 0
+// past the footprint (the ramp reaches the plateau value exactly at the
+// plateau's edge) — three instructions, no branches.
+__device__ __forceinline__ float chord(float dd, float plateau, float kd, float kp) {
+  return fminf(plateau, fmaxf(0.0f, fmaf(-dd, kd, kp)));
 }
 
 constexpr int kPbRows = 32;  // image rows staged per chunk in the forward
+constexpr int kPbPad = 4;    // zero columns on either side of a staged row (no bounds checks)
 
 // z_i for the rays of one view, then the residual (mode EXACT).  x32 holds
 // x (row-major) at [0, d) and its transpose at [d, 2d).
 template <bool LOSS>
 __global__ void __launch_bounds__(512) k_pb_forward(const PbGeom g, const float *__restrict__ x32,
                                                     const CsrFwdArgs a) {
-  extern __shared__ __align__(16) float xs[];  // [kPbRows][N]
+  extern __shared__ __align__(16) float xs[];  // [kPbRows][N + 2 kPbPad], image columns at kPbPad
   __shared__ double sp[3 * kMaxW];
   __shared__ double wl[16];
   const int N = g.N, B = g.B;
@@ -72,6 +75,13 @@ __global__ void __launch_bounds__(512) k_pb_forward(const PbGeom g, const float 
   const float a_ = axis ? 1.0f : (float)fabs(cf), b_ = axis ? 0.0f : (float)fabs(sf);
   const float inv_a = 1.0f / a_, inv_ab = b_ > 0.0f ? 1.0f / (a_ * b_) : 0.0f;
   const float w = 0.5f * (a_ + b_) * inv_a;  // footprint half-width in columns
+  // chord in column units: distance dd columns = dd a perpendicular
+  const float kd = a_ * inv_ab, kp = 0.5f * (a_ + b_) * inv_ab;
+  const int NP = N + 2 * kPbPad;
+  for (int i = threadIdx.x; i < kPbRows * 2 * kPbPad; i += blockDim.x) {
+    const int rr = i / (2 * kPbPad), q = i - rr * 2 * kPbPad;
+    xs[rr * NP + (q < kPbPad ? q : N + q)] = 0.0f;
+  }
   // crossing column in frame row r: c*(r) = C0 - r tan
   const double tb = ((double)b - 0.5 * (double)(B - 1)) / (double)N;
   const double tanf_ = sf / cf;
@@ -87,9 +97,16 @@ __global__ void __launch_bounds__(512) k_pb_forward(const PbGeom g, const float 
     // serialises on L2 latency): 16-byte pieces when the rows allow it
     if ((N & 3) == 0) {
       const float4 *src = reinterpret_cast<const float4 *>(xsrc + (size_t)r0 * N);
-      for (int i = threadIdx.x; i < nr * N / 4; i += blockDim.x) cp_async16(xs + 4 * i, src + i);
+      const int q4 = N / 4;
+      for (int i = threadIdx.x; i < nr * q4; i += blockDim.x) {
+        const int rr = i / q4, q = i - rr * q4;
+        cp_async16(xs + rr * NP + kPbPad + 4 * q, src + i);
+      }
     } else {
-      for (int i = threadIdx.x; i < nr * N; i += blockDim.x) cp_async4(xs + i, xsrc + (size_t)r0 * N + i);
+      for (int i = threadIdx.x; i < nr * N; i += blockDim.x) {
+        const int rr = i / N, q = i - rr * N;
+        cp_async4(xs + rr * NP + kPbPad + q, xsrc + (size_t)r0 * N + i);
+      }
     }
     asm volatile("cp.async.wait_all;" ::: "memory");
     __syncthreads();
@@ -102,29 +119,27 @@ __global__ void __launch_bounds__(512) k_pb_forward(const PbGeom g, const float 
       const float fr0 = (float)(csd - cfl);
       const int ci0 = (int)cfl;
       const float tn = (float)tanf_;
+      // candidate columns are clamped into the zero padding once the ray
+      // has left the image (their chord weights then multiply zeros)
       if (axis) {  // uniform per view: a ray on a pixel edge goes to the positive side
+#pragma unroll 4
         for (int rr = 0; rr < nr; ++rr) {
           const float u = fmaf(-(float)rr, tn, fr0);
-          const float kf = floorf(u + 0.5f);       // the one pixel with -1/2 <= c* - cc < 1/2
-          const int cc = ci0 + (int)kf;
-          if (cc >= 0 && cc < N) zf += xs[rr * N + cc];
+          const int cc = min(max(ci0 + __float2int_rd(u + 0.5f), -1), N);  // -1/2 <= c* - cc < 1/2
+          zf += xs[rr * NP + kPbPad + cc];
         }
       } else {
-        const float p1 = 0.5f * (a_ - b_), p2 = 0.5f * (a_ + b_);
+#pragma unroll 4
         for (int rr = 0; rr < nr; ++rr) {
           const float u = fmaf(-(float)rr, tn, fr0);
-          const float kf = floorf(u);
-          const float fr = u - kf;
-          const int j_lo = (int)ceilf(fr - w);  // candidates ci + j_lo .. ci + j_lo + 2
-          const int cc0 = ci0 + (int)kf + j_lo;
-          const float sd0 = fr - (float)j_lo;    // c* - cc0
-          const float *xr = xs + rr * N;
+          const int ki = __float2int_rd(u);
+          const float fr = u - (float)ki;
+          const int j_lo = __float2int_ru(fr - w);  // candidates ci + j_lo .. ci + j_lo + 2
+          const int cc0 = min(max(ci0 + ki + j_lo, -3), N);
+          const float sd0 = fr - (float)j_lo;  // c* - cc0 (unclamped)
+          const float *xr = xs + rr * NP + kPbPad + cc0;
 #pragma unroll
-          for (int j = 0; j < 3; ++j) {
-            const int cc = cc0 + j;
-            const float l = chord(fabsf(sd0 - (float)j), a_, p1, p2, inv_a, inv_ab);
-            if (cc >= 0 && cc < N) zf = fmaf(l, xr[cc], zf);
-          }
+          for (int j = 0; j < 3; ++j) zf = fmaf(chord(fabsf(sd0 - (float)j), inv_a, kd, kp), xr[j], zf);
         }
       }
       z += (double)zf;  // fp32 partial per chunk, fp64 across chunks
@@ -160,105 +175,129 @@ __global__ void __launch_bounds__(512) k_pb_forward(const PbGeom g, const float 
   pdl_trigger();
 }
 
-constexpr int kPbViews = 32;  // residual views staged per chunk in the backward
+constexpr int kPbViews = 32;  // views staged per chunk in the backward
 constexpr int kPbTile = 16;   // backward blocks cover 16 x 16 pixel tiles
+constexpr int kPbPx = 4;      // consecutive pixels of a tile row per thread
+constexpr int kPbWin = 32;    // bins staged per view: every bin a tile's pixels can reach
+constexpr int kPbParts = 4;   // view ranges, one block each (partials added in order)
 
 // Per-view record of the backward, built once per chunk: the bin coordinate
-// of the tile's corner pixel in fp64 split into an integer and an fp32
-// fraction, so that a pixel's own coordinate is base_f + dc cos + dr sin with
-// |dc|, |dr| < 16 (fp32 error ~1e-6 bins).
+// b* of the tile's corner pixel relative to the start wlo of the view's
+// staged bin window (fp64 arithmetic, fp32 result in [1, 24)), so that a
+// pixel's own coordinate is base_f + dc cos + dr sin with dc, dr < 16.
 struct PbView {
-  float cs, sn, base_f, wb;   // cos, sin, fraction at the tile corner, footprint half-width
-  float p1, inv_max, inv_ab;  // plateau half-width, plateau and ramp scales
-  int base_i;                 // integer part at the tile corner
+  float cs, sn, base_f, wb;     // cos, sin, corner b* - wlo, footprint half-width
+  float inv_max, kd, kp;        // chord scales (chord(); kd = 0: axis-aligned view)
+  int wlo;                      // first staged bin
 };
 
-// g_pixel = Σ_views Σ_bins L r: one thread per (pixel, half of the views).
-// Block = one 16 x 16 tile; half h covers views [h*ceil(nv/2), ...);
-// out2[h*d + pixel] (fp64).
-__global__ void __launch_bounds__(256) k_pb_backward(const PbGeom g, const float *__restrict__ r,
-                                                     double *__restrict__ out2) {
-  extern __shared__ __align__(16) float rs[];  // [kPbViews][B]
+// g_pixel = Σ_views Σ_bins L r: one thread per kPbPx pixels of a tile row and
+// one range of views (blockIdx.y of kPbParts); out[part*d + pixel] (fp64).
+// Per chunk of views a tile stages only the 32-bin window of r each view's
+// rays can reach inside the tile (zeros outside [0, B): no bounds checks).
+__global__ void __launch_bounds__(kPbTile * kPbTile / kPbPx) k_pb_backward(const PbGeom g,
+                                                                          const float *__restrict__ r,
+                                                                          double *__restrict__ out) {
+  __shared__ __align__(16) float rs[kPbViews][kPbWin];
   __shared__ PbView vw[kPbViews];
+  constexpr int TPR = kPbTile / kPbPx;  // threads per tile row
   const int N = g.N, B = g.B;
   const int64_t d = (int64_t)N * N;
-  const int half = blockIdx.y;
-  const int vh = (g.nv + 1) / 2;
-  const int va = half * vh, vb = min(g.nv, va + vh);
+  const int part = blockIdx.y;
+  const int vh = (g.nv + kPbParts - 1) / kPbParts;
+  const int va = part * vh, vb = min(g.nv, va + vh);
   const int tiles_c = (N + kPbTile - 1) / kPbTile;
   const int tr0 = (blockIdx.x / tiles_c) * kPbTile, tc0 = (blockIdx.x % tiles_c) * kPbTile;
-  const int dr = threadIdx.x / kPbTile, dc = threadIdx.x % kPbTile;
-  const int pr = tr0 + dr, pc = tc0 + dc;
-  const bool own = pr < N && pc < N;
+  const int dr = threadIdx.x / TPR, dc0 = (threadIdx.x % TPR) * kPbPx;
+  const int pr = tr0 + dr;
   pdl_wait();  // r is written by the forward pass
-  double acc = 0.0;
+  float accf[kPbPx];
+  double acc[kPbPx];
+#pragma unroll
+  for (int q = 0; q < kPbPx; ++q) acc[q] = 0.0;
   for (int v0 = va; v0 < vb; v0 += kPbViews) {
     const int nv = min(kPbViews, vb - v0);
-    __syncthreads();
-    for (int i = threadIdx.x; i < nv * B; i += blockDim.x) cp_async4(rs + i, r + (int64_t)v0 * B + i);
-    if (threadIdx.x < nv) {
+    __syncthreads();  // previous chunk consumed
+    if ((int)threadIdx.x < nv) {
       const int k = g.v0 + v0 + threadIdx.x;
       const double cs = g.trig[2 * k], sn = g.trig[2 * k + 1];
       const bool axis = fabs(cs) < 1e-12 || fabs(sn) < 1e-12;
       const float a_ = axis ? (fabs(cs) < 1e-12 ? 0.0f : 1.0f) : (float)fabs(cs);
       const float b_ = axis ? (fabs(sn) < 1e-12 ? 0.0f : 1.0f) : (float)fabs(sn);
       const float amax = fmaxf(a_, b_), amin = fminf(a_, b_);
-      // b* of the tile corner: (X cos + Y sin) N + (B-1)/2, X N = tc0 - N/2
-      const double bsd = fma((double)(tc0 - N / 2), cs, (double)(tr0 - N / 2) * sn) + 0.5 * (B - 1);
-      const double bfl = floor(bsd);
+      const double csr = axis ? (fabs(cs) < 1e-12 ? 0.0 : cs) : cs, snr = axis ? (fabs(sn) < 1e-12 ? 0.0 : sn) : sn;
+      // b* of the tile corner: (X cos + Y sin) N + (B-1)/2, X N = tc0 - N/2;
+      // the tile's b* span [lo, hi] sets the window (candidates floor(b*) - 1 .. + 1)
+      const double bsd = fma((double)(tc0 - N / 2), csr, (double)(tr0 - N / 2) * snr) + 0.5 * (B - 1);
+      const double e = (double)(kPbTile - 1);
+      const double lo = bsd + fmin(0.0, e * csr) + fmin(0.0, e * snr);
+      const int wlo = (int)floor(lo) - 1;
       PbView v;
-      v.cs = axis ? (fabs(cs) < 1e-12 ? 0.0f : (float)cs) : (float)cs;
-      v.sn = axis ? (fabs(sn) < 1e-12 ? 0.0f : (float)sn) : (float)sn;
-      v.base_f = (float)(bsd - bfl);
+      v.cs = (float)csr;
+      v.sn = (float)snr;
+      v.base_f = (float)(bsd - (double)wlo);
       v.wb = 0.5f * (a_ + b_);
-      v.p1 = 0.5f * (amax - amin);
       v.inv_max = 1.0f / amax;
-      v.inv_ab = amin > 0.0f ? 1.0f / (a_ * b_) : 0.0f;
-      v.base_i = (int)bfl;  // may be negative; axis views are the ones with inv_ab == 0
+      v.kd = amin > 0.0f ? 1.0f / (a_ * b_) : 0.0f;
+      v.kp = v.wb * v.kd;
+      v.wlo = wlo;
       vw[threadIdx.x] = v;
     }
-    asm volatile("cp.async.wait_all;" ::: "memory");
     __syncthreads();
-    if (own) {
-      float accf = 0.0f;
-      for (int vv = 0; vv < nv; ++vv) {
-        const PbView v = vw[vv];
-        const bool axis = v.inv_ab == 0.0f;
-        const int base_i = v.base_i;
-        const float u = fmaf((float)dc, v.cs, fmaf((float)dr, v.sn, v.base_f));
-        const float *rv = rs + vv * B;
-        if (axis) {  // the one bin with -1/2 < b* - b <= 1/2
-          const int bb = base_i + (int)ceilf(u - 0.5f);
-          if (bb >= 0 && bb < B) accf += rv[bb];
-        } else {
-          const float kf = floorf(u);
-          const float fr = u - kf;
-          const int j_lo = (int)ceilf(fr - v.wb);
-          const int bb0 = base_i + (int)kf + j_lo;
-          const float sd0 = fr - (float)j_lo;  // b* - bb0
+    for (int i = threadIdx.x; i < nv * kPbWin; i += blockDim.x) {
+      const int vv = i / kPbWin, j = i - vv * kPbWin;
+      const int bb = vw[vv].wlo + j;
+      rs[vv][j] = (bb >= 0 && bb < B) ? __ldg(r + (int64_t)(v0 + vv) * B + bb) : 0.0f;
+    }
+    __syncthreads();
 #pragma unroll
-          for (int j = 0; j < 2; ++j) {
-            const int bb = bb0 + j;
-            const float dd = fabsf(sd0 - (float)j);
-            const float l = dd <= v.p1 ? v.inv_max : fmaxf(0.0f, (v.wb - dd) * v.inv_ab);
-            if (bb >= 0 && bb < B) accf = fmaf(l, rv[bb], accf);
-          }
+    for (int q = 0; q < kPbPx; ++q) accf[q] = 0.0f;
+    for (int vv = 0; vv < nv; ++vv) {
+      const PbView v = vw[vv];
+      const float *rv = rs[vv];
+      const float u0 = fmaf((float)dc0, v.cs, fmaf((float)dr, v.sn, v.base_f));
+      if (v.kd == 0.0f) {  // axis-aligned (uniform): the one bin with -1/2 < b* - b <= 1/2
+#pragma unroll
+        for (int q = 0; q < kPbPx; ++q) {
+          const float u = fmaf((float)q, v.cs, u0);
+          accf[q] += rv[__float2int_ru(u - 0.5f)];
+        }
+      } else {
+#pragma unroll
+        for (int q = 0; q < kPbPx; ++q) {
+          const float u = fmaf((float)q, v.cs, u0);
+          const int ki = __float2int_rd(u);
+          const float fr = u - (float)ki;
+          const int j_lo = __float2int_ru(fr - v.wb);
+          const float sd0 = fr - (float)j_lo;  // b* - (bin ki + j_lo)
+          const float *rb = rv + ki + j_lo;
+          accf[q] = fmaf(chord(fabsf(sd0), v.inv_max, v.kd, v.kp), rb[0], accf[q]);
+          accf[q] = fmaf(chord(fabsf(sd0 - 1.0f), v.inv_max, v.kd, v.kp), rb[1], accf[q]);
         }
       }
-      acc += (double)accf;
     }
+#pragma unroll
+    for (int q = 0; q < kPbPx; ++q) acc[q] += (double)accf[q];  // fp32 per chunk, fp64 across chunks
   }
-  if (own) out2[half * d + (int64_t)pr * N + pc] = acc / (double)N;
+#pragma unroll
+  for (int q = 0; q < kPbPx; ++q) {
+    const int pc = tc0 + dc0 + q;
+    if (pr < N && pc < N) out[part * d + (int64_t)pr * N + pc] = acc[q] / (double)N;
+  }
   pdl_trigger();
 }
 
-// g = out2[0] + out2[1] (the two view halves, in order) into the partial row
-__global__ void k_pb_combine(const double *__restrict__ out2, int64_t d, double *__restrict__ g) {
+// g = out[0] + out[1] + ... (the view ranges, in order) into the partial row
+__global__ void k_pb_combine(const double *__restrict__ out, int64_t d, double *__restrict__ g) {
   pdl_wait();
   pdl_trigger();
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < d;
-       i += (int64_t)gridDim.x * blockDim.x)
-    g[i] = out2[i] + out2[d + i];
+       i += (int64_t)gridDim.x * blockDim.x) {
+    double v = out[i];
+#pragma unroll
+    for (int p = 1; p < kPbParts; ++p) v += out[p * d + i];
+    g[i] = v;
+  }
 }
 
 }  // namespace poly

@@ -384,10 +384,10 @@ int enqueue_pass(poly_handle *h, const double *x, bool loss) {
     a.mode = p.mode;
     const int thr = std::max(32, (p.pb_bins + 31) / 32 * 32);
     TRY(launch(h, loss ? (const void *)&k_pb_forward<true> : (const void *)&k_pb_forward<false>,
-               dim3(h->pb.nv), dim3(thr), (size_t)kPbRows * p.pb_side * 4, true, h->pb, x32, a));
+               dim3(h->pb.nv), dim3(thr), (size_t)kPbRows * (p.pb_side + 2 * kPbPad) * 4, true, h->pb, x32, a));
     const unsigned tiles = (unsigned)(((p.pb_side + kPbTile - 1) / kPbTile) * ((p.pb_side + kPbTile - 1) / kPbTile));
-    TRY(launch(h, (const void *)&k_pb_backward, dim3(tiles, 2), dim3(kPbTile * kPbTile),
-               (size_t)kPbViews * p.pb_bins * 4, true, h->pb, (const float *)h->rbuf, h->pb_out2));
+    TRY(launch(h, (const void *)&k_pb_backward, dim3(tiles, kPbParts), dim3(kPbTile * kPbTile / kPbPx), 0, true,
+               h->pb, (const float *)h->rbuf, h->pb_out2));
     return launch(h, (const void *)&k_pb_combine, dim3((unsigned)std::min<int64_t>(1024, (p.d + 255) / 256)),
                   dim3(256), 0, true, (const double *)h->pb_out2, (int64_t)p.d, h->partials);
   }
@@ -1176,17 +1176,14 @@ int poly_init(const poly_problem *pin, poly_handle **out) {
       if (cudaMemcpy(h->pb_trig, trig.data(), trig.size() * 8, cudaMemcpyHostToDevice) != cudaSuccess)
         return bail(fail(POLY_ECUDA, "geometry upload failed"));
       h->pb.trig = h->pb_trig;
-      if ((rc = dev_alloc(h, &h->pb_out2, (size_t)2 * p.d)) != POLY_OK) return bail(rc);
+      if ((rc = dev_alloc(h, &h->pb_out2, (size_t)kPbParts * p.d)) != POLY_OK) return bail(rc);
       h->k4_grid = h->pb.nv;
       for (int f = 0; f < 2; ++f) {
         const void *fn = f ? (const void *)&k_pb_forward<true> : (const void *)&k_pb_forward<false>;
         if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 kPbRows * p.pb_side * 4) != cudaSuccess)
+                                 kPbRows * (p.pb_side + 2 * kPbPad) * 4) != cudaSuccess)
           return bail(fail(POLY_EUNSUPPORTED, "parallel beam: image too wide for the row stage"));
       }
-      if (cudaFuncSetAttribute((const void *)&k_pb_backward, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               kPbViews * p.pb_bins * 4) != cudaSuccess)
-        return bail(fail(POLY_ECUDA, "parallel beam: backward attributes"));
     }
     if ((rc = dev_alloc(h, &h->loss_partials, (size_t)h->k4_grid)) != POLY_OK) return bail(rc);
     if ((rc = dev_alloc(h, &h->rbuf, (size_t)std::max<int64_t>(1, p.n_local))) != POLY_OK) return bail(rc);
