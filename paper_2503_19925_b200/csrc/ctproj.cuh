@@ -33,11 +33,18 @@
 
 namespace poly {
 
+#ifndef POLY_PB_ROWSPLIT
+#define POLY_PB_ROWSPLIT 2
+#endif
+constexpr int kPbRowSplit = POLY_PB_ROWSPLIT;  // forward blocks per view (row ranges)
+
 struct PbGeom {
   int32_t N, V, B;
   int32_t v0;          // first view of this handle's rows (row_offset / B)
   int32_t nv;          // views held (n_local / B)
   const double *trig;  // [2V]: cos θ_k, sin θ_k (host libm, θ_k = kπ/V)
+  double *zpart;       // [kPbRowSplit][n_local] forward partial sums per row range
+  int32_t *ticket;     // [nv] forward blocks finished per view (reset by the last)
 };
 
 // chord length / Δ for a pixel whose centre is dd (>= 0) pixel widths from
@@ -76,7 +83,7 @@ __global__ void __launch_bounds__(512) k_pb_forward(const PbGeom g, const float 
   const float inv_a = 1.0f / a_, inv_ab = b_ > 0.0f ? 1.0f / (a_ * b_) : 0.0f;
   const float w = 0.5f * (a_ + b_) * inv_a;  // footprint half-width in columns
   // chord in column units: distance dd columns = dd a perpendicular
-  const float kd = a_ * inv_ab, kp = 0.5f * (a_ + b_) * inv_ab;
+  const float kd = a_ * inv_ab, kp = 0.5f * (a_ + b_) * inv_ab, kp1 = kp - kd, kp2 = kp - 2.0f * kd;
   const int NP = N + 2 * kPbPad;
   for (int i = threadIdx.x; i < kPbRows * 2 * kPbPad; i += blockDim.x) {
     const int rr = i / (2 * kPbPad), q = i - rr * 2 * kPbPad;
@@ -87,12 +94,16 @@ __global__ void __launch_bounds__(512) k_pb_forward(const PbGeom g, const float 
   const double tanf_ = sf / cf;
   const double c0 = (double)(N / 2);  // centre pixel index (integer N/2, as gen/ct.py)
   const double C0 = c0 + tb * N / cf + c0 * tanf_;
+  // this block's row range (blockIdx.y of kPbRowSplit): the view's rays are
+  // split by rows so that the grid is several waves of blocks, not 2.4
+  const int rs = blockIdx.y;
+  const int rb = (int)((int64_t)N * rs / kPbRowSplit), re = (int)((int64_t)N * (rs + 1) / kPbRowSplit);
   pdl_wait();  // x is written by the previous kernel; r is read by the previous backward
   float zf = 0.0f;
   double z = 0.0;
-  for (int r0 = 0; r0 < N; r0 += kPbRows) {
+  for (int r0 = rb; r0 < re; r0 += kPbRows) {
     __syncthreads();  // previous chunk consumed
-    const int nr = min(kPbRows, N - r0);
+    const int nr = min(kPbRows, re - r0);
     // stage the chunk with async copies (many in flight; a load->store loop
     // serialises on L2 latency): 16-byte pieces when the rows allow it
     if ((N & 3) == 0) {
@@ -136,15 +147,32 @@ __global__ void __launch_bounds__(512) k_pb_forward(const PbGeom g, const float 
           const float fr = u - (float)ki;
           const int j_lo = __float2int_ru(fr - w);  // candidates ci + j_lo .. ci + j_lo + 2
           const int cc0 = min(max(ci0 + ki + j_lo, -3), N);
-          const float sd0 = fr - (float)j_lo;  // c* - cc0 (unclamped)
+          const float sd0 = fr - (float)j_lo;  // c* - cc0 (unclamped), in (w - 1, w]
           const float *xr = xs + rr * NP + kPbPad + cc0;
-#pragma unroll
-          for (int j = 0; j < 3; ++j) zf = fmaf(chord(fabsf(sd0 - (float)j), inv_a, kd, kp), xr[j], zf);
+          // |sd0 - j| = j - sd0 for j = 1, 2: the chord's argument folds into one FMA
+          zf = fmaf(chord(fabsf(sd0), inv_a, kd, kp), xr[0], zf);
+          zf = fmaf(fminf(inv_a, fmaxf(0.0f, fmaf(sd0, kd, kp1))), xr[1], zf);
+          zf = fmaf(fminf(inv_a, fmaxf(0.0f, fmaf(sd0, kd, kp2))), xr[2], zf);
         }
       }
       z += (double)zf;  // fp32 partial per chunk, fp64 across chunks
       zf = 0.0f;
     }
+  }
+  // partial sums of the row ranges; the view's last block adds them in order
+  __shared__ int last;
+  const int64_t nloc = (int64_t)g.nv * B;
+  if (b < B) g.zpart[rs * nloc + (int64_t)kl * B + b] = z;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) last = atomicAdd(g.ticket + kl, 1) == kPbRowSplit - 1;
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  if (threadIdx.x == 0) g.ticket[kl] = 0;  // ready for the next launch
+  if (b < B) {
+    z = 0.0;
+    for (int q = 0; q < kPbRowSplit; ++q) z += __ldcg(g.zpart + q * nloc + (int64_t)kl * B + b);
   }
   z /= (double)N;  // chord lengths in units of Δ
   double lacc = 0.0;
@@ -177,9 +205,15 @@ __global__ void __launch_bounds__(512) k_pb_forward(const PbGeom g, const float 
 
 constexpr int kPbViews = 32;  // views staged per chunk in the backward
 constexpr int kPbTile = 16;   // backward blocks cover 16 x 16 pixel tiles
-constexpr int kPbPx = 4;      // consecutive pixels of a tile row per thread
+#ifndef POLY_PB_PX
+#define POLY_PB_PX 4
+#endif
+#ifndef POLY_PB_PARTS
+#define POLY_PB_PARTS 16
+#endif
+constexpr int kPbPx = POLY_PB_PX;  // consecutive pixels of a tile row per thread
 constexpr int kPbWin = 32;    // bins staged per view: every bin a tile's pixels can reach
-constexpr int kPbParts = 4;   // view ranges, one block each (partials added in order)
+constexpr int kPbParts = POLY_PB_PARTS;  // view ranges, one block each (partials added in order)
 
 // Per-view record of the backward, built once per chunk: the bin coordinate
 // b* of the tile's corner pixel relative to the start wlo of the view's

@@ -240,7 +240,8 @@ struct poly_handle {
   bool sell16 = false;                 // both SELL copies in the 6-byte delta form
   // POLY_PARALLEL_BEAM
   PbGeom pb{};
-  double *pb_trig = nullptr, *pb_out2 = nullptr;
+  double *pb_trig = nullptr, *pb_out2 = nullptr, *pb_zpart = nullptr;
+  int32_t *pb_ticket = nullptr;
   int k4f16_grid = 0, k4b16_grid = 0;  // resident-slot grids (slices dealt grid-stride)
   // TV sets: Dykstra state, statistics, cluster launch shape
   double *tv_zk = nullptr, *tv_p = nullptr, *tv_q = nullptr;
@@ -384,7 +385,8 @@ int enqueue_pass(poly_handle *h, const double *x, bool loss) {
     a.mode = p.mode;
     const int thr = std::max(32, (p.pb_bins + 31) / 32 * 32);
     TRY(launch(h, loss ? (const void *)&k_pb_forward<true> : (const void *)&k_pb_forward<false>,
-               dim3(h->pb.nv), dim3(thr), (size_t)kPbRows * (p.pb_side + 2 * kPbPad) * 4, true, h->pb, x32, a));
+               dim3(h->pb.nv, kPbRowSplit), dim3(thr), (size_t)kPbRows * (p.pb_side + 2 * kPbPad) * 4, true, h->pb,
+               x32, a));
     const unsigned tiles = (unsigned)(((p.pb_side + kPbTile - 1) / kPbTile) * ((p.pb_side + kPbTile - 1) / kPbTile));
     TRY(launch(h, (const void *)&k_pb_backward, dim3(tiles, kPbParts), dim3(kPbTile * kPbTile / kPbPx), 0, true,
                h->pb, (const float *)h->rbuf, h->pb_out2));
@@ -1177,6 +1179,12 @@ int poly_init(const poly_problem *pin, poly_handle **out) {
         return bail(fail(POLY_ECUDA, "geometry upload failed"));
       h->pb.trig = h->pb_trig;
       if ((rc = dev_alloc(h, &h->pb_out2, (size_t)kPbParts * p.d)) != POLY_OK) return bail(rc);
+      if ((rc = dev_alloc(h, &h->pb_zpart, (size_t)kPbRowSplit * p.n_local)) != POLY_OK) return bail(rc);
+      if ((rc = dev_alloc(h, &h->pb_ticket, (size_t)h->pb.nv)) != POLY_OK) return bail(rc);
+      if (cudaMemset(h->pb_ticket, 0, sizeof(int32_t) * (size_t)h->pb.nv) != cudaSuccess)
+        return bail(fail(POLY_ECUDA, "parallel beam: ticket reset"));
+      h->pb.zpart = h->pb_zpart;
+      h->pb.ticket = h->pb_ticket;
       h->k4_grid = h->pb.nv;
       for (int f = 0; f < 2; ++f) {
         const void *fn = f ? (const void *)&k_pb_forward<true> : (const void *)&k_pb_forward<false>;
