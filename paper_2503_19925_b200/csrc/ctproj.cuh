@@ -22,11 +22,12 @@
 //                      most 3 pixels per row its footprint covers; then the
 //                      link and residual per ray (fp64) as K1, r stored fp32.
 //   K5b k_pb_backward  one thread per 4 pixels of a 16 x 16 tile row and a
-//                      quarter of the views: for every view the at most 2
+//                      16th of the views: for every view the at most 2
 //                      bins whose rays cross each pixel, from the 32-bin
 //                      window of residuals the tile can reach (staged per
-//                      view chunk in shared memory); the quarters are added
-//                      in order (deterministic).
+//                      view chunk in shared memory); the last of a tile's
+//                      16 view-range blocks adds their partials in order
+//                      (deterministic).
 #pragma once
 
 #include "dense.cuh"
@@ -45,6 +46,7 @@ struct PbGeom {
   const double *trig;  // [2V]: cos θ_k, sin θ_k (host libm, θ_k = kπ/V)
   double *zpart;       // [kPbRowSplit][n_local] forward partial sums per row range
   int32_t *ticket;     // [nv] forward blocks finished per view (reset by the last)
+  int32_t *tticket;    // [tiles] backward blocks finished per tile (reset by the last)
 };
 
 // chord length / Δ for a pixel whose centre is dd (>= 0) pixel widths from
@@ -94,6 +96,18 @@ __global__ void __launch_bounds__(512) k_pb_forward(const PbGeom g, const float 
   const double tanf_ = sf / cf;
   const double c0 = (double)(N / 2);  // centre pixel index (integer N/2, as gen/ct.py)
   const double C0 = c0 + tb * N / cf + c0 * tanf_;
+  // frame rows where the ray's footprint can touch the image: c*(r) within
+  // [-2, N + 1] (half-width <= 1 column); other rows add exact zeros, so the
+  // loops skip them (a ray outside the image skips everything)
+  int r_lo = 0, r_hi = N;
+  if (tanf_ == 0.0) {
+    if (!(C0 >= -2.0 && C0 <= N + 1.0)) r_lo = r_hi = 0;
+  } else {
+    const double ra = (C0 + 2.0) / tanf_, rb2 = (C0 - N - 1.0) / tanf_;
+    r_lo = (int)fmax(0.0, floor(fmin(ra, rb2)) - 1.0);
+    r_hi = (int)fmin((double)N, ceil(fmax(ra, rb2)) + 2.0);
+    if (r_hi < r_lo) r_hi = r_lo;
+  }
   // this block's row range (blockIdx.y of kPbRowSplit): the view's rays are
   // split by rows so that the grid is several waves of blocks, not 2.4
   const int rs = blockIdx.y;
@@ -133,15 +147,17 @@ __global__ void __launch_bounds__(512) k_pb_forward(const PbGeom g, const float 
       // candidate columns are clamped into the zero padding once the ray
       // has left the image (their chord weights then multiply zeros)
       if (axis) {  // uniform per view: a ray on a pixel edge goes to the positive side
+        const int ra = max(0, r_lo - r0), rz = min(nr, r_hi - r0);
 #pragma unroll 4
-        for (int rr = 0; rr < nr; ++rr) {
+        for (int rr = ra; rr < rz; ++rr) {
           const float u = fmaf(-(float)rr, tn, fr0);
           const int cc = min(max(ci0 + __float2int_rd(u + 0.5f), -1), N);  // -1/2 <= c* - cc < 1/2
           zf += xs[rr * NP + kPbPad + cc];
         }
       } else {
+        const int ra = max(0, r_lo - r0), rz = min(nr, r_hi - r0);
 #pragma unroll 4
-        for (int rr = 0; rr < nr; ++rr) {
+        for (int rr = ra; rr < rz; ++rr) {
           const float u = fmaf(-(float)rr, tn, fr0);
           const int ki = __float2int_rd(u);
           const float fr = u - (float)ki;
@@ -231,9 +247,11 @@ struct PbView {
 // rays can reach inside the tile (zeros outside [0, B): no bounds checks).
 __global__ void __launch_bounds__(kPbTile * kPbTile / kPbPx) k_pb_backward(const PbGeom g,
                                                                           const float *__restrict__ r,
-                                                                          double *__restrict__ out) {
+                                                                          double *__restrict__ out,
+                                                                          double *__restrict__ gout) {
   __shared__ __align__(16) float rs[kPbViews][kPbWin];
   __shared__ PbView vw[kPbViews];
+  __shared__ int last;
   constexpr int TPR = kPbTile / kPbPx;  // threads per tile row
   const int N = g.N, B = g.B;
   const int64_t d = (int64_t)N * N;
@@ -318,20 +336,25 @@ __global__ void __launch_bounds__(kPbTile * kPbTile / kPbPx) k_pb_backward(const
     const int pc = tc0 + dc0 + q;
     if (pr < N && pc < N) out[part * d + (int64_t)pr * N + pc] = acc[q] / (double)N;
   }
-  pdl_trigger();
-}
-
-// g = out[0] + out[1] + ... (the view ranges, in order) into the partial row
-__global__ void k_pb_combine(const double *__restrict__ out, int64_t d, double *__restrict__ g) {
-  pdl_wait();
-  pdl_trigger();
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < d;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    double v = out[i];
+  // the tile's last block adds the kPbParts partials in order into g
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) last = atomicAdd(g.tticket + blockIdx.x, 1) == kPbParts - 1;
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  if (threadIdx.x == 0) g.tticket[blockIdx.x] = 0;  // ready for the next launch
 #pragma unroll
-    for (int p = 1; p < kPbParts; ++p) v += out[p * d + i];
-    g[i] = v;
+  for (int q = 0; q < kPbPx; ++q) {
+    const int pc = tc0 + dc0 + q;
+    if (pr < N && pc < N) {
+      const int64_t i = (int64_t)pr * N + pc;
+      double v = __ldcg(out + i);
+      for (int p = 1; p < kPbParts; ++p) v += __ldcg(out + p * d + i);
+      gout[i] = v;
+    }
   }
+  pdl_trigger();
 }
 
 }  // namespace poly

@@ -241,7 +241,7 @@ struct poly_handle {
   // POLY_PARALLEL_BEAM
   PbGeom pb{};
   double *pb_trig = nullptr, *pb_out2 = nullptr, *pb_zpart = nullptr;
-  int32_t *pb_ticket = nullptr;
+  int32_t *pb_ticket = nullptr, *pb_tticket = nullptr;
   int k4f16_grid = 0, k4b16_grid = 0;  // resident-slot grids (slices dealt grid-stride)
   // TV sets: Dykstra state, statistics, cluster launch shape
   double *tv_zk = nullptr, *tv_p = nullptr, *tv_q = nullptr;
@@ -388,10 +388,8 @@ int enqueue_pass(poly_handle *h, const double *x, bool loss) {
                dim3(h->pb.nv, kPbRowSplit), dim3(thr), (size_t)kPbRows * (p.pb_side + 2 * kPbPad) * 4, true, h->pb,
                x32, a));
     const unsigned tiles = (unsigned)(((p.pb_side + kPbTile - 1) / kPbTile) * ((p.pb_side + kPbTile - 1) / kPbTile));
-    TRY(launch(h, (const void *)&k_pb_backward, dim3(tiles, kPbParts), dim3(kPbTile * kPbTile / kPbPx), 0, true,
-               h->pb, (const float *)h->rbuf, h->pb_out2));
-    return launch(h, (const void *)&k_pb_combine, dim3((unsigned)std::min<int64_t>(1024, (p.d + 255) / 256)),
-                  dim3(256), 0, true, (const double *)h->pb_out2, (int64_t)p.d, h->partials);
+    return launch(h, (const void *)&k_pb_backward, dim3(tiles, kPbParts), dim3(kPbTile * kPbTile / kPbPx), 0, true,
+                  h->pb, (const float *)h->rbuf, h->pb_out2, h->partials);
   }
   // fp32 copy of x for the gathers: written by the step kernel for the
   // internal iterates, converted here for a caller's x
@@ -1183,6 +1181,13 @@ int poly_init(const poly_problem *pin, poly_handle **out) {
       if ((rc = dev_alloc(h, &h->pb_ticket, (size_t)h->pb.nv)) != POLY_OK) return bail(rc);
       if (cudaMemset(h->pb_ticket, 0, sizeof(int32_t) * (size_t)h->pb.nv) != cudaSuccess)
         return bail(fail(POLY_ECUDA, "parallel beam: ticket reset"));
+      {
+        const int tc = (p.pb_side + kPbTile - 1) / kPbTile;
+        if ((rc = dev_alloc(h, &h->pb_tticket, (size_t)tc * tc)) != POLY_OK) return bail(rc);
+        if (cudaMemset(h->pb_tticket, 0, sizeof(int32_t) * (size_t)tc * tc) != cudaSuccess)
+          return bail(fail(POLY_ECUDA, "parallel beam: ticket reset"));
+        h->pb.tticket = h->pb_tticket;
+      }
       h->pb.zpart = h->pb_zpart;
       h->pb.ticket = h->pb_ticket;
       h->k4_grid = h->pb.nv;
