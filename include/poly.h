@@ -158,10 +158,12 @@ typedef struct poly_problem {
   double tv_dykstra_tol; /* [1e-4] Dykstra stops at ||z_{k+1} - z_k|| <= tol    */
   int32_t tv_max_it;     /* [5000] FISTA iterations per prox                                    */
   int32_t tv_max_outer;  /* [1000] Dykstra sweeps                                              */
-  /* POLY_PARALLEL_BEAM geometry: N = pb_side (d = N*N, N <= 4096), V = pb_views,
-   * B = pb_bins; this rank holds rows [row_offset, row_offset + n_local), both
-   * multiples of B (whole views).  fp32 chord lengths; mode EXACT, no per-row
-   * spectra.  A, row_ptr, col, val are unused. */
+  /* POLY_PARALLEL_BEAM geometry: N = pb_side (d = N*N, 2 <= N <= 4096; the
+   * forward's 32-row shared stage limits N to 1768 on sm_100a: larger sides
+   * return POLY_EUNSUPPORTED), V = pb_views, B = pb_bins <= 1024; this rank
+   * holds rows [row_offset, row_offset + n_local), both multiples of B (whole
+   * views).  fp32 chord lengths; mode EXACT, no per-row spectra.  A, row_ptr,
+   * col, val are unused. */
   int32_t pb_side, pb_views, pb_bins, pb_reserved;
 } poly_problem;
 
