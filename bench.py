@@ -177,7 +177,10 @@ def run_ours(args):
     cfg, row0, n_local, scaling = D.shard(cfg0, rank, world, strong=cfg0.name in STRONG)
     w = PW.build(cfg, row0=row0, n_local=n_local)
     nccl_id = D.exchange_id(P.poly_nccl_unique_id, rank, world)
-    poly = PW.make_poly(w, rank=rank, world=world, nccl_id=nccl_id)
+    p2p = args.p2p and world > 1
+    poly = PW.make_poly(w, rank=rank, world=world, nccl_id=nccl_id, flags=P.POLY_FLAG_P2P if p2p else 0)
+    if p2p:
+        poly.p2p_setup()   # K9: cross-rank sum over NVLink peer memory instead of ncclAllReduce
     gamma = gamma_for(cfg)
     x = torch.zeros(cfg.d, dtype=torch.float64, device="cuda")
 
@@ -248,7 +251,7 @@ def run_ours(args):
             "data": "synthetic (seeded Philox generators, BASELINE.json recipe)",
             "config": {"workload": WORKLOAD_DESC.get(args.config, args.config), "name": args.config,
                        "n_global": cfg.n, "n_local": n_local, "d": cfg.d, "W": cfg.W,
-                       "I_bar": cfg.I_bar, "parallelism": f"dp{world} (row shards + NCCL allreduce)",
+                       "I_bar": cfg.I_bar, "parallelism": f"dp{world} (row shards + " + ("K9 NVLink peer reduce)" if p2p else "NCCL allreduce)"),
                        "precision": "fp32 A, fp32 FMA dot/axpy; fp64 link, residual, reductions, iterate",
                        "l2": "inputs larger than L2 (A >> 126 MB), no flush" if ab > 4 * 126e6 else
                              "A may be L2-resident (small shard)",
@@ -386,6 +389,8 @@ def main():
     ap.add_argument("--config", default="c2", choices=sorted(WORKLOAD_DESC))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--p2p", action="store_true",
+                    help="N>1: sum over ranks with the K9 peer-reduce kernel instead of ncclAllReduce")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--e2e-steps", type=int, default=2)

@@ -47,7 +47,7 @@
 extern "C" {
 #endif
 
-#define POLY_ABI_VERSION 3
+#define POLY_ABI_VERSION 4
 
 /* status codes */
 #define POLY_OK 0
@@ -90,6 +90,9 @@ extern "C" {
                                     dense problems (poly_solve then replays the general graph) */
 #define POLY_FLAG_COMM 8u        /* use the NCCL path (reduce -> ncclAllReduce -> step) even when
                                     world == 1; needs nccl_id.  Exercises the collective path on one GPU */
+#define POLY_FLAG_P2P 32u        /* allocate a peer-reduce window (with world > 1 or POLY_FLAG_COMM);
+                                    after poly_p2p_open the cross-rank sum runs as one kernel over
+                                    NVLink peer memory (K9) instead of ncclAllReduce */
 
 /* poly_problem.mode: which per-row scalar the fused pass evaluates.  Every mode
  * streams A once and returns g = (1/n) Σ_i φ_i a_i and a scalar objective.   */
@@ -275,6 +278,20 @@ int poly_describe(poly_handle *h, int64_t *out, int32_t nout);
  * broadcast the bytes to all ranks before poly_init.  POLY_ENCCL if NCCL
  * cannot be loaded. */
 int poly_nccl_unique_id(void *out128);
+
+/* K9 peer reduce (step a6 without NCCL).  With
+ * POLY_FLAG_P2P every rank exports its window with poly_p2p_handle (64 bytes,
+ * a cudaIpcMemHandle_t), the caller all-gathers the world*64 bytes in rank
+ * order (e.g. torch.distributed.all_gather_object) and every rank calls
+ * poly_p2p_open with them; from then on each F evaluation's sum over ranks is
+ * one kernel that publishes this rank's unnormalised sums, waits for every
+ * rank's flag (system-scope acquire) and adds the ranks' windows in rank order
+ * over NVLink — identical bits on every rank.  All ranks must call
+ * poly_p2p_open before their next evaluation.  Errors: POLY_EINVAL (no
+ * POLY_FLAG_P2P, called twice), POLY_ECUDA (no peer access; the handle keeps
+ * the NCCL path). */
+int poly_p2p_handle(poly_handle *h, void *out64);
+int poly_p2p_open(poly_handle *h, const void *handles);
 
 /* Release everything the handle owns (workspaces, graphs, communicator). */
 void poly_free(poly_handle *h);

@@ -20,6 +20,7 @@ POLY_Y_I32, POLY_Y_F32, POLY_Y_F64 = 0, 1, 2
 POLY_SET_NONE, POLY_SET_BALL, POLY_SET_NONNEG, POLY_SET_NONNEG_BALL = 0, 1, 2, 3
 POLY_SET_TV_NONNEG, POLY_SET_TV = 4, 5
 POLY_FLAG_HOST_INPUTS, POLY_FLAG_NO_GRAPH, POLY_FLAG_NO_PDL, POLY_FLAG_COMM, POLY_FLAG_NO_SMALL = 1, 2, 4, 8, 16
+POLY_FLAG_P2P = 32
 POLY_SOLVE_PROFILE = 1
 POLY_MODE_EXACT, POLY_MODE_L2, POLY_MODE_L1, POLY_MODE_NLL = 0, 1, 2, 3
 POLY_METHOD_EXTRAGRADIENT, POLY_METHOD_GD = 0, 1
@@ -27,7 +28,7 @@ POLY_METHOD_EXTRAGRADIENT, POLY_METHOD_GD = 0, 1
 EXPORTED = ["poly_init", "poly_loss_grad", "poly_solve", "poly_forward", "poly_expected_counts",
             "poly_reparameterize", "poly_kernel_times", "poly_describe", "poly_nccl_unique_id",
             "poly_free", "poly_last_error", "poly_abi_version", "poly_solve_ex", "poly_project",
-            "poly_stream_probe"]
+            "poly_stream_probe", "poly_p2p_handle", "poly_p2p_open"]
 
 
 class PolyProblem(C.Structure):
@@ -88,6 +89,8 @@ def _load():
     lib.poly_kernel_times.argtypes = [vp, dp, i32]
     lib.poly_describe.argtypes = [vp, C.POINTER(C.c_int64), i32]
     lib.poly_nccl_unique_id.argtypes = [vp]
+    lib.poly_p2p_handle.argtypes = [vp, vp]
+    lib.poly_p2p_open.argtypes = [vp, vp]
     lib.poly_free.argtypes = [vp]
     lib.poly_free.restype = None
     lib.poly_last_error.restype = C.c_char_p
@@ -195,6 +198,20 @@ def poly_nccl_unique_id() -> bytes:
     buf = C.create_string_buffer(128)
     _check(_lib.poly_nccl_unique_id(buf))
     return buf.raw
+
+
+def poly_p2p_handle(h: int) -> bytes:
+    """This rank's 64-byte peer-reduce window handle (POLY_FLAG_P2P)."""
+    buf = C.create_string_buffer(64)
+    _check(_lib.poly_p2p_handle(h, buf))
+    return buf.raw
+
+
+def poly_p2p_open(h: int, handles: bytes):
+    """Map every rank's window (world * 64 bytes in rank order): K9 replaces
+    ncclAllReduce for this handle from the next evaluation on."""
+    buf = C.create_string_buffer(bytes(handles), len(handles))
+    _check(_lib.poly_p2p_open(h, buf))
 
 
 def poly_free(h: int):

@@ -96,6 +96,16 @@ class Poly:
         self.problem = p
         self.h = poly_init(p)
 
+    def p2p_setup(self):
+        """K9: exchange the peer-reduce window handles (all ranks, collective
+        over the default torch.distributed group) and switch this handle's
+        cross-rank sum from ncclAllReduce to the NVLink peer-reduce kernel.
+        Needs flags with POLY_FLAG_P2P."""
+        from . import dist as D
+        from . import poly_p2p_handle, poly_p2p_open
+        hs = D.gather_handles(poly_p2p_handle(self.h), int(self.problem.rank), int(self.problem.world))
+        poly_p2p_open(self.h, hs)
+
     def close(self):
         if getattr(self, "h", None):
             poly_free(self.h)

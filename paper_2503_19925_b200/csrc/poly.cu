@@ -32,6 +32,7 @@
 #include "tv.cuh"
 #include "small.cuh"
 #include "ctproj.cuh"
+#include "p2p.cuh"
 
 using namespace poly;
 
@@ -269,6 +270,12 @@ struct poly_handle {
   int graph_U = 8;
   ncclComm_t nccl = nullptr;
   bool comm_path = false;  // world > 1 or POLY_FLAG_COMM: reduce -> allreduce -> step
+  // K9 peer reduce (POLY_FLAG_P2P + poly_p2p_open): this rank's window, the
+  // peers' IPC mappings, the per-block evaluation counters
+  char *p2p_win = nullptr;
+  char *p2p_peer[kP2PMaxRanks] = {};
+  unsigned long long *p2p_epoch = nullptr;
+  bool p2p = false;
   // profiling
   bool prof = false;
   std::vector<cudaEvent_t> evpool;
@@ -571,6 +578,24 @@ int enqueue_allreduce(poly_handle *h) {
   return POLY_OK;
 }
 
+// K9: the cross-rank sum over NVLink peer memory (csrc/p2p.cuh)
+int enqueue_peer_reduce(poly_handle *h) {
+  ProfScope ps(h, 2);
+  PeerArgs a{};
+  a.comm = h->comm;
+  a.n = h->p.d + 1;
+  a.world = (int32_t)h->p.world;
+  a.rank = (int32_t)h->p.rank;
+  for (int r = 0; r < a.world; ++r) a.win[r] = h->p2p_peer[r];
+  a.epoch = h->p2p_epoch;
+  // the same grid on every rank (same d; the SM count of the GPU model)
+  const int grid = (int)std::min<int64_t>(std::min(h->sms, kP2PMaxBlocks), (a.n + 255) / 256);
+  // with PDL the blocks start while the reduce kernel drains and wait for it
+  // (griddepcontrol.wait); K9 never triggers early, so its dependents start
+  // after it exits and never compete with its waiting blocks for SMs
+  return launch(h, (const void *)&k_peer_reduce, dim3(grid), dim3(256), 0, true, a);
+}
+
 // F at x, then either g/loss (step == false) or x_out = P_X(anchor - γ F(x)).
 int enqueue_eval(poly_handle *h, const double *x, bool loss, bool step, const double *anchor,
                  double *x_out, double *g_out) {
@@ -588,7 +613,7 @@ int enqueue_eval(poly_handle *h, const double *x, bool loss, bool step, const do
   FinArgs r = f;
   r.mode = FIN_REDUCE;
   TRY(enqueue_fin(h, r));
-  TRY(enqueue_allreduce(h));
+  TRY(h->p2p ? enqueue_peer_reduce(h) : enqueue_allreduce(h));
   f.mode = step ? FIN_STEP_COMM : FIN_GRAD_COMM;
   return enqueue_fin(h, f);
 }
@@ -1036,8 +1061,55 @@ int poly_nccl_unique_id(void *out128) {
   return POLY_OK;
 }
 
+int poly_p2p_handle(poly_handle *h, void *out64) {
+  if (!h || !out64) return fail(POLY_EINVAL, "NULL handle or out");
+  if (!h->p2p_win) return fail(POLY_EINVAL, "handle was not created with POLY_FLAG_P2P");
+  cudaIpcMemHandle_t m;
+  CK(cudaIpcGetMemHandle(&m, h->p2p_win));
+  static_assert(sizeof(m) == 64, "cudaIpcMemHandle_t is 64 bytes");
+  memcpy(out64, &m, 64);
+  return POLY_OK;
+}
+
+int poly_p2p_open(poly_handle *h, const void *handles) {
+  if (!h || !handles) return fail(POLY_EINVAL, "NULL handle or handles");
+  if (!h->p2p_win) return fail(POLY_EINVAL, "handle was not created with POLY_FLAG_P2P");
+  if (h->p2p) return fail(POLY_EINVAL, "poly_p2p_open called twice");
+  const int P = (int)h->p.world;
+  for (int r = 0; r < P; ++r) {
+    if (r == h->p.rank) {
+      h->p2p_peer[r] = h->p2p_win;
+      continue;
+    }
+    cudaIpcMemHandle_t m;
+    memcpy(&m, (const char *)handles + 64 * r, 64);
+    void *ptr = nullptr;
+    if (cudaIpcOpenMemHandle(&ptr, m, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
+      cudaGetLastError();
+      for (int q = 0; q < r; ++q)
+        if (q != h->p.rank && h->p2p_peer[q]) cudaIpcCloseMemHandle(h->p2p_peer[q]);
+      for (auto &q : h->p2p_peer) q = nullptr;
+      return fail(POLY_ECUDA, "cudaIpcOpenMemHandle(rank %d) failed: no peer access to that GPU", r);
+    }
+    h->p2p_peer[r] = (char *)ptr;
+  }
+  // graphs captured so far hold the NCCL path
+  for (auto &a : h->gexec)
+    for (auto &g : a)
+      if (g) cudaGraphExecDestroy(g), g = nullptr;
+  for (auto &a : h->gexec_ex)
+    for (auto &b : a)
+      for (auto &g : b)
+        if (g) cudaGraphExecDestroy(g), g = nullptr;
+  h->p2p = true;
+  return POLY_OK;
+}
+
 void poly_free(poly_handle *h) {
   if (!h) return;
+  if (h->p2p)
+    for (int r = 0; r < (int)h->p.world; ++r)
+      if (r != h->p.rank && h->p2p_peer[r]) cudaIpcCloseMemHandle(h->p2p_peer[r]);
   if (h->work) cudaStreamSynchronize(h->work);
   for (auto &a : h->gexec)
     for (auto &g : a)
@@ -1289,6 +1361,16 @@ int poly_init(const poly_problem *pin, poly_handle **out) {
   }
 
   h->comm_path = p.world > 1 || (p.flags & POLY_FLAG_COMM);
+  if (p.flags & POLY_FLAG_P2P) {
+    if (!h->comm_path) return bail(fail(POLY_EINVAL, "POLY_FLAG_P2P needs world > 1 or POLY_FLAG_COMM"));
+    if (p.world > kP2PMaxRanks) return bail(fail(POLY_EUNSUPPORTED, "POLY_FLAG_P2P: world > %d", kP2PMaxRanks));
+    const size_t wb = kP2PFlagBytes + (size_t)2 * (p.d + 1) * 8;
+    if ((rc = dev_alloc(h, &h->p2p_win, wb)) || (rc = dev_alloc(h, &h->p2p_epoch, (size_t)kP2PMaxBlocks)))
+      return bail(rc);
+    if (cudaMemsetAsync(h->p2p_win, 0, wb, h->work) != cudaSuccess ||
+        cudaMemsetAsync(h->p2p_epoch, 0, 8 * (size_t)kP2PMaxBlocks, h->work) != cudaSuccess)
+      return bail(fail(POLY_ECUDA, "p2p window reset"));
+  }
   if (h->comm_path) {
     NcclApi *api = nccl_api();
     if (!api) return bail(fail(POLY_ENCCL, "world > 1 but libnccl.so.2 cannot be loaded"));

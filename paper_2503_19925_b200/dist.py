@@ -47,6 +47,21 @@ def exchange_id(make_id, rank: int, world: int) -> bytes | None:
     return box[0]
 
 
+def gather_handles(handle: bytes, rank: int, world: int) -> bytes:
+    """All ranks' 64-byte peer-reduce window handles (poly_p2p_handle), in
+    rank order, for poly_p2p_open (K9).  world == 1: the rank's own."""
+    if len(handle) != 64:
+        raise ValueError("a peer-reduce window handle is 64 bytes")
+    if world == 1:
+        return bytes(handle)
+    import torch.distributed as dist
+    out = [None] * world
+    dist.all_gather_object(out, bytes(handle))
+    if any(h is None or len(h) != 64 for h in out):
+        raise RuntimeError("peer-reduce handle exchange incomplete")
+    return b"".join(out)
+
+
 def _reduce(value: float, op, device) -> float:
     import torch
     import torch.distributed as dist

@@ -94,6 +94,8 @@ def _body(rank, world):
     out["max"] = D.max_over_ranks(1.0 + rank, world, device="cpu")
     out["sum"] = D.sum_over_ranks(10.0 * (rank + 1), world, device="cpu")
     out["id"] = D.exchange_id(lambda: b"\x07" * 128, rank, world)
+    # K9's window-handle exchange: 64 bytes per rank, concatenated in rank order
+    out["handles"] = D.gather_handles(bytes([rank + 1]) * 64, rank, world)
     return out
 
 
@@ -133,3 +135,4 @@ def test_gloo_world2_sharded_oracle_matches_full():
         assert o["weak"] == (1000, 500 * r, 500, "weak")
         assert o["max"] == 2.0 and o["sum"] == 30.0
         assert o["id"] == b"\x07" * 128
+        assert o["handles"] == b"\x01" * 64 + b"\x02" * 64

@@ -493,6 +493,40 @@ def test_comm_path_single_rank(kind):
     p1.close()
 
 
+@pytest.mark.parametrize("kind", ["dense", "csr"])
+def test_peer_reduce_single_rank(kind):
+    """K9 (POLY_FLAG_P2P + poly_p2p_open): the cross-rank sum as one kernel
+    over the ranks' peer-memory windows instead of ncclAllReduce.  On one
+    rank it publishes, waits for its own flag and adds one window: the same
+    bits as the NCCL path, per call and through graph-replayed solves whose
+    evaluation counter cycles the double-buffered slots many times."""
+    P = _P()
+    W = _W()
+    cfg = G.scaled(G.C2, 20_000) if kind == "dense" else G.C4
+    w = W.build(cfg)
+    p1 = W.make_poly(w, flags=P.POLY_FLAG_COMM, nccl_id=P.poly_nccl_unique_id())
+    p2 = W.make_poly(w, flags=P.POLY_FLAG_COMM | P.POLY_FLAG_P2P, nccl_id=P.poly_nccl_unique_id())
+    p2.p2p_setup()
+    with pytest.raises(P.PolyError):
+        p2.p2p_setup()   # once per handle
+    x = torch.linspace(-0.02, 0.02, cfg.d, dtype=torch.float64, device="cuda")
+    for _ in range(3):
+        g1, l1 = p1.loss_grad(x)
+        g2, l2 = p2.loss_grad(x)
+        assert torch.equal(g1, g2) and l1 == l2
+    lam_bound = 4e-5 if kind == "csr" else 1.5
+    gam = 1.0 / (4.0 * cfg.I_bar * lam_bound * float(np.dot(*cfg.spectrum)))
+    xa = torch.zeros(cfg.d, dtype=torch.float64, device="cuda")
+    xb = torch.zeros_like(xa)
+    p1.solve(xa, 25, gam)
+    p2.solve(xb, 25, gam)
+    assert torch.equal(xa, xb)
+    p1.close()
+    p2.close()
+    with pytest.raises(P.PolyError):   # P2P needs the comm path
+        W.make_poly(w, flags=P.POLY_FLAG_P2P)
+
+
 def test_c4_compact_and_wide_sell_agree(c4, monkeypatch):
     """K4 stores both SELL copies as int16 index deltas + values (6 B/entry)
     when every delta fits; POLY_NO_SELL16 keeps the 8-byte {index, value}
