@@ -19,7 +19,7 @@
 //                      staged through shared memory (for views with
 //                      |sin θ| > |cos θ| the rows of the transposed image, in
 //                      which the ray is again "steep"); each ray adds the at
-//                      most 3 pixels per row its footprint covers; then the
+//                      most 2 pixels per row its footprint covers; then the
 //                      link and residual per ray (fp64) as K1, r stored fp32.
 //   K5b k_pb_backward  one thread per 4 pixels of a 16 x 16 tile row and a
 //                      16th of the views: for every view the at most 2
@@ -85,7 +85,7 @@ __global__ void __launch_bounds__(512) k_pb_forward(const PbGeom g, const float 
   const float inv_a = 1.0f / a_, inv_ab = b_ > 0.0f ? 1.0f / (a_ * b_) : 0.0f;
   const float w = 0.5f * (a_ + b_) * inv_a;  // footprint half-width in columns
   // chord in column units: distance dd columns = dd a perpendicular
-  const float kd = a_ * inv_ab, kp = 0.5f * (a_ + b_) * inv_ab, kp1 = kp - kd, kp2 = kp - 2.0f * kd;
+  const float kd = a_ * inv_ab, kp = 0.5f * (a_ + b_) * inv_ab, kp1 = kp - kd;
   const int NP = N + 2 * kPbPad;
   for (int i = threadIdx.x; i < kPbRows * 2 * kPbPad; i += blockDim.x) {
     const int rr = i / (2 * kPbPad), q = i - rr * 2 * kPbPad;
@@ -161,14 +161,15 @@ __global__ void __launch_bounds__(512) k_pb_forward(const PbGeom g, const float 
           const float u = fmaf(-(float)rr, tn, fr0);
           const int ki = __float2int_rd(u);
           const float fr = u - (float)ki;
-          const int j_lo = __float2int_ru(fr - w);  // candidates ci + j_lo .. ci + j_lo + 2
-          const int cc0 = min(max(ci0 + ki + j_lo, -3), N);
+          // the footprint [c* - w, c* + w] (w <= 1) holds at most two pixel
+          // centres with a nonzero chord: cc0 = ceil(c* - w) and cc0 + 1
+          const int j_lo = __float2int_ru(fr - w);
+          const int cc0 = min(max(ci0 + ki + j_lo, -2), N);
           const float sd0 = fr - (float)j_lo;  // c* - cc0 (unclamped), in (w - 1, w]
           const float *xr = xs + rr * NP + kPbPad + cc0;
-          // |sd0 - j| = j - sd0 for j = 1, 2: the chord's argument folds into one FMA
+          // |sd0 - 1| = 1 - sd0: the second chord's argument folds into one FMA
           zf = fmaf(chord(fabsf(sd0), inv_a, kd, kp), xr[0], zf);
           zf = fmaf(fminf(inv_a, fmaxf(0.0f, fmaf(sd0, kd, kp1))), xr[1], zf);
-          zf = fmaf(fminf(inv_a, fmaxf(0.0f, fmaf(sd0, kd, kp2))), xr[2], zf);
         }
       }
       z += (double)zf;  // fp32 partial per chunk, fp64 across chunks
