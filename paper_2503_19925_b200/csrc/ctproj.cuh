@@ -324,8 +324,9 @@ __global__ void __launch_bounds__(kPbTile * kPbTile / kPbPx) k_pb_backward(const
           const int j_lo = __float2int_ru(fr - v.wb);
           const float sd0 = fr - (float)j_lo;  // b* - (bin ki + j_lo)
           const float *rb = rv + ki + j_lo;
+          // sd0 <= wb < 1, so |sd0 - 1| = 1 - sd0 folds into one FMA
           accf[q] = fmaf(chord(fabsf(sd0), v.inv_max, v.kd, v.kp), rb[0], accf[q]);
-          accf[q] = fmaf(chord(fabsf(sd0 - 1.0f), v.inv_max, v.kd, v.kp), rb[1], accf[q]);
+          accf[q] = fmaf(fminf(v.inv_max, fmaxf(0.0f, fmaf(sd0, v.kd, v.kp - v.kd))), rb[1], accf[q]);
         }
       }
     }
