@@ -59,7 +59,14 @@ __device__ __forceinline__ float chord(float dd, float plateau, float kd, float 
   return fminf(plateau, fmaxf(0.0f, fmaf(-dd, kd, kp)));
 }
 
-constexpr int kPbRows = 32;  // image rows staged per chunk in the forward
+#ifndef POLY_PB_ROWS
+#define POLY_PB_ROWS 32
+#endif
+constexpr int kPbRows = POLY_PB_ROWS;  // image rows per staged chunk in the forward
+#ifndef POLY_PB_NBUF
+#define POLY_PB_NBUF 1
+#endif
+constexpr int kPbBufs = POLY_PB_NBUF;  // stage buffers (1: no prefetch, more resident blocks)
 constexpr int kPbPad = 4;    // zero columns on either side of a staged row (no bounds checks)
 
 // z_i for the rays of one view, then the residual (mode EXACT).  x32 holds
@@ -67,7 +74,8 @@ constexpr int kPbPad = 4;    // zero columns on either side of a staged row (no 
 template <bool LOSS>
 __global__ void __launch_bounds__(512) k_pb_forward(const PbGeom g, const float *__restrict__ x32,
                                                     const CsrFwdArgs a) {
-  extern __shared__ __align__(16) float xs[];  // [kPbRows][N + 2 kPbPad], image columns at kPbPad
+  extern __shared__ __align__(16) float xs[];  // [kPbBufs][kPbRows][N + 2 kPbPad], image columns at kPbPad
+  __shared__ __align__(8) uint64_t mbar[2];
   __shared__ double sp[3 * kMaxW];
   __shared__ double wl[16];
   const int N = g.N, B = g.B;
@@ -87,7 +95,7 @@ __global__ void __launch_bounds__(512) k_pb_forward(const PbGeom g, const float 
   // chord in column units: distance dd columns = dd a perpendicular
   const float kd = a_ * inv_ab, kp = 0.5f * (a_ + b_) * inv_ab, kp1 = kp - kd;
   const int NP = N + 2 * kPbPad;
-  for (int i = threadIdx.x; i < kPbRows * 2 * kPbPad; i += blockDim.x) {
+  for (int i = threadIdx.x; i < kPbBufs * kPbRows * 2 * kPbPad; i += blockDim.x) {
     const int rr = i / (2 * kPbPad), q = i - rr * 2 * kPbPad;
     xs[rr * NP + (q < kPbPad ? q : N + q)] = 0.0f;
   }
@@ -112,29 +120,52 @@ __global__ void __launch_bounds__(512) k_pb_forward(const PbGeom g, const float 
   // split by rows so that the grid is several waves of blocks, not 2.4
   const int rs = blockIdx.y;
   const int rb = (int)((int64_t)N * rs / kPbRowSplit), re = (int)((int64_t)N * (rs + 1) / kPbRowSplit);
+  if (threadIdx.x == 0) {
+    mbar_init(&mbar[0], 1);
+    mbar_init(&mbar[1], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
   pdl_wait();  // x is written by the previous kernel; r is read by the previous backward
-  float zf = 0.0f;
-  double z = 0.0;
-  for (int r0 = rb; r0 < re; r0 += kPbRows) {
-    __syncthreads();  // previous chunk consumed
-    const int nr = min(kPbRows, re - r0);
-    // stage the chunk with async copies (many in flight; a load->store loop
-    // serialises on L2 latency): 16-byte pieces when the rows allow it
-    if ((N & 3) == 0) {
-      const float4 *src = reinterpret_cast<const float4 *>(xsrc + (size_t)r0 * N);
-      const int q4 = N / 4;
-      for (int i = threadIdx.x; i < nr * q4; i += blockDim.x) {
-        const int rr = i / q4, q = i - rr * q4;
-        cp_async16(xs + rr * NP + kPbPad + 4 * q, src + i);
+  // Rows are staged in chunks of kPbRows through kPbBufs buffers: chunk
+  // c + kPbBufs is requested as soon as chunk c is consumed.  Rows of 16-byte multiples go through the TMA engine (one bulk
+  // copy per row, lanes of warp 0, completion on the buffer's mbarrier); other
+  // widths through per-thread cp.async completing on the same mbarrier.
+  const bool tma = (N & 3) == 0;
+  const int nchunks = (re - rb + kPbRows - 1) / kPbRows;
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+  auto issue = [&](int c) {
+    const int buf = c % kPbBufs, r0 = rb + c * kPbRows, nr = min(kPbRows, re - r0);
+    float *dst = xs + buf * kPbRows * NP + kPbPad;
+    if (tma) {
+      if (threadIdx.x < 32) {
+        if (threadIdx.x == 0) mbar_arrive_expect_tx(&mbar[buf], (uint32_t)(nr * N * 4));
+        __syncwarp();
+        for (int rr = threadIdx.x; rr < nr; rr += 32)
+          bulk_g2s(dst + rr * NP, xsrc + (size_t)(r0 + rr) * N, (uint32_t)(N * 4), &mbar[buf], pol);
       }
     } else {
       for (int i = threadIdx.x; i < nr * N; i += blockDim.x) {
         const int rr = i / N, q = i - rr * N;
-        cp_async4(xs + rr * NP + kPbPad + q, xsrc + (size_t)r0 * N + i);
+        cp_async4(dst + rr * NP + q, xsrc + (size_t)r0 * N + i);
       }
+      cp_async_mbar_arrive(&mbar[buf]);  // (.noinc) one arrival per thread, counted below
     }
-    asm volatile("cp.async.wait_all;" ::: "memory");
-    __syncthreads();
+  };
+  if (!tma && threadIdx.x == 0) {  // per-thread arrivals: re-init with the thread count
+    mbar_init(&mbar[0], blockDim.x);
+    mbar_init(&mbar[1], blockDim.x);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  for (int c = 0; c < kPbBufs && c < nchunks; ++c) issue(c);
+  float zf = 0.0f;
+  double z = 0.0;
+  for (int c = 0; c < nchunks; ++c) {
+    const int buf = c % kPbBufs, r0 = rb + c * kPbRows, nr = min(kPbRows, re - r0);
+    mbar_wait(&mbar[buf], (uint32_t)((c / kPbBufs) & 1));
+    const float *xsb = xs + buf * kPbRows * NP;
     if (b < B) {
       // crossing column at the chunk's first row in fp64, split into an
       // integer and an fp32 fraction; within the chunk the fraction steps by
@@ -152,7 +183,7 @@ __global__ void __launch_bounds__(512) k_pb_forward(const PbGeom g, const float 
         for (int rr = ra; rr < rz; ++rr) {
           const float u = fmaf(-(float)rr, tn, fr0);
           const int cc = min(max(ci0 + __float2int_rd(u + 0.5f), -1), N);  // -1/2 <= c* - cc < 1/2
-          zf += xs[rr * NP + kPbPad + cc];
+          zf += xsb[rr * NP + kPbPad + cc];
         }
       } else {
         const int ra = max(0, r_lo - r0), rz = min(nr, r_hi - r0);
@@ -166,7 +197,7 @@ __global__ void __launch_bounds__(512) k_pb_forward(const PbGeom g, const float 
           const int j_lo = __float2int_ru(fr - w);
           const int cc0 = min(max(ci0 + ki + j_lo, -2), N);
           const float sd0 = fr - (float)j_lo;  // c* - cc0 (unclamped), in (w - 1, w]
-          const float *xr = xs + rr * NP + kPbPad + cc0;
+          const float *xr = xsb + rr * NP + kPbPad + cc0;
           // |sd0 - 1| = 1 - sd0: the second chord's argument folds into one FMA
           zf = fmaf(chord(fabsf(sd0), inv_a, kd, kp), xr[0], zf);
           zf = fmaf(fminf(inv_a, fmaxf(0.0f, fmaf(sd0, kd, kp1))), xr[1], zf);
@@ -175,6 +206,8 @@ __global__ void __launch_bounds__(512) k_pb_forward(const PbGeom g, const float 
       z += (double)zf;  // fp32 partial per chunk, fp64 across chunks
       zf = 0.0f;
     }
+    __syncthreads();  // buffer consumed: request chunk c + kPbBufs into it
+    if (c + kPbBufs < nchunks) issue(c + kPbBufs);
   }
   // partial sums of the row ranges; the view's last block adds them in order
   __shared__ int last;

@@ -392,7 +392,7 @@ int enqueue_pass(poly_handle *h, const double *x, bool loss) {
     a.mode = p.mode;
     const int thr = std::max(32, (p.pb_bins + 31) / 32 * 32);
     TRY(launch(h, loss ? (const void *)&k_pb_forward<true> : (const void *)&k_pb_forward<false>,
-               dim3(h->pb.nv, kPbRowSplit), dim3(thr), (size_t)kPbRows * (p.pb_side + 2 * kPbPad) * 4, true, h->pb,
+               dim3(h->pb.nv, kPbRowSplit), dim3(thr), (size_t)kPbBufs * kPbRows * (p.pb_side + 2 * kPbPad) * 4, true, h->pb,
                x32, a));
     const unsigned tiles = (unsigned)(((p.pb_side + kPbTile - 1) / kPbTile) * ((p.pb_side + kPbTile - 1) / kPbTile));
     return launch(h, (const void *)&k_pb_backward, dim3(tiles, kPbParts), dim3(kPbTile * kPbTile / kPbPx), 0, true,
@@ -1266,7 +1266,7 @@ int poly_init(const poly_problem *pin, poly_handle **out) {
       for (int f = 0; f < 2; ++f) {
         const void *fn = f ? (const void *)&k_pb_forward<true> : (const void *)&k_pb_forward<false>;
         if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 kPbRows * (p.pb_side + 2 * kPbPad) * 4) != cudaSuccess)
+                                 kPbBufs * kPbRows * (p.pb_side + 2 * kPbPad) * 4) != cudaSuccess)
           return bail(fail(POLY_EUNSUPPORTED, "parallel beam: image too wide for the row stage"));
       }
     }
