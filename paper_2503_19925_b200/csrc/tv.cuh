@@ -345,8 +345,10 @@ __device__ int tv_prox(cg::cluster_group &cl, TvBand &bref, double lam, double r
       if (full_rows) phase_a(std::true_type());
       else phase_a(std::false_type());
     }
-    // ||Δx||², ||x||² over the cluster: warps in order, then every CTA pushes
-    // its pair to every rank and sums the CL pairs in rank order
+    // ||Δx||², ||x||² over the cluster: lanes, then the CTA's warps, then the
+    // CL ranks, each by the same xor butterfly (a fixed pairwise tree, so every
+    // lane of every CTA ends with identical bits); every CTA pushes its pair to
+    // every rank and sums the CL pairs itself
     {
       const uint32_t q = b.n_red & 1;
 #pragma unroll
@@ -357,17 +359,27 @@ __device__ int tv_prox(cg::cluster_group &cl, TvBand &bref, double lam, double r
         if (lane == 0) b.wsum[(threadIdx.x >> 5) * 4 + k] = v;
       }
       __syncthreads();  // also: xw, x of every row group written
-      if ((int)threadIdx.x < b.CL) {
-        double p0 = 0.0, p1 = 0.0;
-        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) p0 += b.wsum[w * 4], p1 += b.wsum[w * 4 + 1];
-        st_async_v2f64(mapa_u32(red_o + 16u * (uint32_t)(q * kTvMaxCL + b.rank), threadIdx.x), p0, p1,
-                       mapa_u32(mb + 8 * q, threadIdx.x));
+      if (threadIdx.x < 32) {
+        const int NWp = (int)(blockDim.x >> 5);
+        double p0 = lane < NWp ? b.wsum[lane * 4] : 0.0, p1 = lane < NWp ? b.wsum[lane * 4 + 1] : 0.0;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          p0 += __shfl_xor_sync(0xffffffffu, p0, o);
+          p1 += __shfl_xor_sync(0xffffffffu, p1, o);
+        }
+        if (lane < b.CL)
+          st_async_v2f64(mapa_u32(red_o + 16u * (uint32_t)(q * kTvMaxCL + b.rank), lane), p0, p1,
+                         mapa_u32(mb + 8 * q, lane));
       }
       if (threadIdx.x == 0) mbar_expect_tx(mb + 8 * q, (uint32_t)b.CL * 16u);
       mbar_wait_cluster(mb + 8 * q, (b.n_red >> 1) & 1);
-      acc[0] = acc[1] = 0.0;
-      for (int r = 0; r < b.CL; ++r)
-        acc[0] += red_slots[(q * kTvMaxCL + r) * 2], acc[1] += red_slots[(q * kTvMaxCL + r) * 2 + 1];
+      acc[0] = lane < b.CL ? red_slots[(q * kTvMaxCL + lane) * 2] : 0.0;
+      acc[1] = lane < b.CL ? red_slots[(q * kTvMaxCL + lane) * 2 + 1] : 0.0;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        acc[0] += __shfl_xor_sync(0xffffffffu, acc[0], o);
+        acc[1] += __shfl_xor_sync(0xffffffffu, acc[1], o);
+      }
       ++b.n_red;
     }
     if ((it > 1 && sqrt(acc[0]) <= rtol * sqrt(acc[1])) || it > max_it) break;
