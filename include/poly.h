@@ -154,7 +154,9 @@ typedef struct poly_problem {
   int32_t windows;
   const double *I_win;
   /* TV sets (POLY_SET_TV_NONNEG, POLY_SET_TV): anisotropic TV of the s x s image
-   * (forward differences, R21).  Zero selects the default in brackets. */
+   * (forward differences, R21), 2 <= s <= 256 (the projection runs in
+   * one thread-block cluster; larger images return POLY_EUNSUPPORTED).  Zero
+   * selects the default in brackets. */
   double tv_tau;         /* TV radius τ >= 0 (the paper: the truth's TV)          */
   double tv_tol;         /* [0.01] bisection stop |TV(x̄) - τ| <= tv_tol          */
   double tv_rtol;        /* [1e-6] prox: FISTA stops at relative primal change <= tv_rtol         */
