@@ -251,7 +251,8 @@ def run_ours(args):
             "data": "synthetic (seeded Philox generators, BASELINE.json recipe)",
             "config": {"workload": WORKLOAD_DESC.get(args.config, args.config), "name": args.config,
                        "n_global": cfg.n, "n_local": n_local, "d": cfg.d, "W": cfg.W,
-                       "I_bar": cfg.I_bar, "parallelism": f"dp{world} (row shards + " + ("K9 NVLink peer reduce)" if p2p else "NCCL allreduce)"),
+                       "I_bar": cfg.I_bar, "parallelism": "dp1 (single GPU, no collective)" if world == 1 else
+                       f"dp{world} (row shards + " + ("K9 NVLink peer reduce)" if p2p else "NCCL allreduce)"),
                        "precision": "fp32 A, fp32 FMA dot/axpy; fp64 link, residual, reductions, iterate",
                        "l2": "inputs larger than L2 (A >> 126 MB), no flush" if ab > 4 * 126e6 else
                              "A may be L2-resident (small shard)",
