@@ -21,7 +21,7 @@
 //                      which the ray is again "steep"); each ray adds the at
 //                      most 2 pixels per row its footprint covers; then the
 //                      link and residual per ray (fp64) as K1, r stored fp32.
-//   K5b k_pb_backward  one thread per 4 pixels of a 16 x 16 tile row and a
+//   K5b k_pb_backward  one thread per 2 pixels of a 16 x 16 tile row and a
 //                      16th of the views: for every view the at most 2
 //                      bins whose rays cross each pixel, from the 32-bin
 //                      window of residuals the tile can reach (staged per
@@ -256,7 +256,7 @@ __global__ void __launch_bounds__(512) k_pb_forward(const PbGeom g, const float 
 constexpr int kPbViews = 32;  // views staged per chunk in the backward
 constexpr int kPbTile = 16;   // backward blocks cover 16 x 16 pixel tiles
 #ifndef POLY_PB_PX
-#define POLY_PB_PX 4
+#define POLY_PB_PX 2
 #endif
 #ifndef POLY_PB_PARTS
 #define POLY_PB_PARTS 16
