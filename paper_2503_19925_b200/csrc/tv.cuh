@@ -12,13 +12,15 @@
 //
 // B200 mapping: ONE thread-block cluster of CL CTAs does the whole projection
 // — Dykstra, bisection and every FISTA iteration — with the image split into
-// CL row bands (s <= 256).  Each CTA keeps its band's prox input z and primal
-// x in shared memory and the FISTA duals u, w (horizontal, vertical) and the
-// extrapolated primal xw in registers (tv_prox); band edges are read from the
-// neighbour CTAs' shared memory (DSMEM) and every reduction (||Δx||, ||x||,
-// TV) is summed over the cluster in a fixed order, so all CTAs take identical
-// branch decisions.  Dykstra's state (z_k, p, q) lives in global memory (L2).
-// Two cluster barriers per FISTA iteration; no kernel launches inside.
+// CL row bands (s <= 256).  Each CTA keeps its band's prox input z, primal x,
+// extrapolated primal xw and momentum duals w in shared memory (rows of pitch
+// SC) and the duals u in registers (tv_prox); inside the FISTA loop the band
+// edges and the reductions (||Δx||, ||x||) travel as st.async pushes that
+// complete on the receiver's mbarrier — no cluster barrier per iteration —
+// and every sum is a fixed tree, so all CTAs take identical branch decisions.
+// Outside the loop (TV norms, Dykstra) the reductions use cluster_sum.
+// Dykstra's state (z_k, p, q) lives in global memory (L2).  No kernel
+// launches inside.
 #pragma once
 
 #include <cooperative_groups.h>
@@ -179,16 +181,15 @@ __device__ double tv_norm_x(cg::cluster_group &cl, TvBand &b) {
 // TV prox of b.z with parameter lam (FISTA on the dual, oracle_prox_tv's
 // iteration); leaves x = z - Dᵀu in b.x.  Returns the FISTA iterations.
 //
-// Register-resident: thread t owns column c = t % SC (SC = s rounded up to
-// 32) of RPT consecutive band rows starting at h*RPT (h = t / SC), and keeps
-// its duals u, w (horizontal and vertical) and the extrapolated primal xw in
-// registers.  Horizontal neighbours are lanes of the same warp (shuffles; the
-// warp-edge columns go through small shared buffers), vertical neighbours the
-// thread's own next row, the row group above/below (shared edge rows) or the
-// neighbouring CTA's band (DSMEM).  Only z and x stay in shared memory
-// (row-major, lanes on consecutive columns: conflict-free).  Per pixel and
-// iteration that is 3 shared accesses instead of ~23 for a shared-array form,
-// whose FISTA iteration was bound by shared-memory bandwidth (6 µs at s=256).
+// Thread map: thread t owns column c = t % SC (SC = s rounded up to 32) of
+// RPT consecutive band rows starting at h*RPT (h = t / SC) and keeps its
+// duals u (horizontal, vertical) in registers; w, z, x and xw are band arrays
+// in shared memory (row pitch SC, lanes on consecutive columns:
+// conflict-free).  Horizontal neighbours of u and xw come from shuffles (the
+// warp-edge columns through small shared buffers), vertical ones from the
+// thread's own next row, the row group above/below or — for the band's edge
+// rows — the halo the neighbouring CTA pushed.  The boundary rules are data
+// (no per-pixel branches); see the loop.
 // the dynamic shared memory of k_tv_project
 extern __shared__ __align__(16) double tv_smem[];
 
