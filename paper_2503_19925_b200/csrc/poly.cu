@@ -2,10 +2,13 @@
 //
 // Per F evaluation the library enqueues, on its own work
 // stream (ordered after the caller's stream with events):
-//   K1 k_dense_loss_grad (or K4 k_csr_loss_grad)   one pass over A
-//   K2/K3 k_finalize                                fixed-order reduce, 1/n,
+//   K1 k_dense_loss_grad, or K4f/K4b k_sell16_forward/backward (CSR), or
+//   K5f/K5b k_pb_forward/backward (matrix-free parallel beam)   one pass over A
+//   K2/K3 k_finalize (+ k_fin_apply)                fixed-order reduce, 1/n,
 //                                                   step + projection
-//   (world > 1: k_finalize(REDUCE) -> ncclAllReduce(d+1 doubles) -> k_finalize)
+//   (k_tv_project for the TV sets, between the step and k_fin_apply)
+//   (world > 1: k_finalize(REDUCE) -> ncclAllReduce(d+1 doubles), or K9
+//    k_peer_reduce after poly_p2p_open -> k_finalize)
 // and poly_solve replays one CUDA graph per U EXACT iterations
 // (Eq. extragrad-method) with programmatic dependent launch
 // between the kernels so the next A stream starts while the step finishes.
