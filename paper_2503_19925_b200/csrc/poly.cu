@@ -504,7 +504,8 @@ int small_solve_config(poly_handle *h, int *cl, size_t *smem) {
   const int64_t ldd = (p.d + 1) & ~1;
   const size_t s = (size_t)rows * ldd * h->elsize + 8 + (size_t)rows * 8 + 3 * kMaxW * 8 +
                    3 * kSmallMaxD * 8 + 2 * (kSmallMaxD + 1) * 8 +
-                   (kSmallThreads / 32) * (kSmallMaxD + 1) * 8 + (kSmallThreads / 32) * 8;
+                   (kSmallThreads / 32) * (kSmallMaxD + 1) * 8 + (kSmallThreads / 32) * 8 +
+                   2 * 8 + (size_t)2 * C * (p.d + 1) * 8;  // mbarriers + pushed partials
   if (s > 200 * 1024) return POLY_EUNSUPPORTED;
   *cl = C;
   *smem = s;

@@ -10,12 +10,12 @@
 //   warps take rows round-robin: z_i = <a_i, x> (fp64 lane partials, warp
 //   sum), the link and per-row scalar (row_residual: the same quantities as
 //   K1), g_warp += r_i a_i in fp64 registers; the CTA's warps are combined in
-//   order into this CTA's partial; one cluster barrier; every CTA then sums
-//   the CL partials over DSMEM in rank order (identical bits in every CTA),
-//   scales by 1/n and applies the step and projection itself, so the iterate
-//   is replicated without another exchange.  Partials are double-buffered:
-//   evaluation e+2 rewrites buffer e&1 only after every CTA passed the barrier
-//   of evaluation e+1, i.e. after all reads of it.
+//   order into this CTA's partial, which is pushed (st.async) into slot row
+//   `rank` of every CTA, completing on that CTA's mbarrier; every CTA then
+//   sums the CL rows in rank order (identical bits in every CTA), scales by
+//   1/n and applies the step and projection itself, so the iterate is
+//   replicated without another exchange.  Slots are double-buffered by
+//   evaluation parity (see the loop).
 #pragma once
 
 #include <cooperative_groups.h>
@@ -23,6 +23,7 @@
 #include <type_traits>
 
 #include "dense.cuh"
+#include "tv.cuh"  // st.async / cluster mbarrier helpers
 
 namespace poly {
 
@@ -102,6 +103,8 @@ __global__ void __launch_bounds__(kSmallThreads, 1) k_small_solve(const SmallArg
   double *part = vv + kSmallMaxD;                // [2][d + 1] partial g and loss (double-buffered)
   double *wp = part + 2 * (kSmallMaxD + 1);      // [NWp][d + 1]
   double *red = wp + NWp * (kSmallMaxD + 1);     // [NWp]
+  uint64_t *mbar = reinterpret_cast<uint64_t *>(red + NWp);  // [2]
+  double *slots = reinterpret_cast<double *>(mbar + 2);       // [2][CL][d + 1] pushed partials
   // A block, y, spectrum, x_1 = P_X(x_in)
   for (int i = threadIdx.x; i < rows * d; i += blockDim.x) {
     const int r = i / d, c = i - r * d;
@@ -110,7 +113,12 @@ __global__ void __launch_bounds__(kSmallThreads, 1) k_small_solve(const SmallArg
   for (int i = threadIdx.x; i < rows; i += blockDim.x) ys[i] = load_y_global(a.y, a.ytype, r0 + i);
   for (int i = threadIdx.x; i < 3 * kMaxW; i += blockDim.x) sp[i] = a.spec[i];
   for (int c = threadIdx.x; c < d; c += blockDim.x) vv[c] = a.x[c];
-  __syncthreads();
+  if (threadIdx.x == 0) {
+    mbar_init(&mbar[0], 1);
+    mbar_init(&mbar[1], 1);
+    fence_mbar_init();
+  }
+  cl_bar();  // every CTA's mbarriers exist before the first push
   small_project(a, vv, xa, red);
   for (int c = threadIdx.x; c < d; c += blockDim.x) xe[c] = xa[c];
   __syncthreads();
@@ -178,28 +186,30 @@ __global__ void __launch_bounds__(kSmallThreads, 1) k_small_solve(const SmallArg
     }
     if (lane == 0) wrow[kSmallMaxD] = lacc;
     __syncthreads();
-    double *pb = part + (size_t)(e & 1) * (kSmallMaxD + 1);
+    // ---- this CTA's partial (warps in order), pushed to every CTA's slot row
+    // `rank` with st.async completing on the receiver's mbarrier (no cluster
+    // barrier); slots alternate by evaluation parity — a CTA can only push
+    // evaluation e+2 after every CTA pushed e+1, i.e. after it finished
+    // reading the slots of e
+    const int q = e & 1, D1 = d + 1;
+    const uint32_t sb = smem_u32(slots) + 8u * (uint32_t)((q * CL + rank) * D1), mb = smem_u32(&mbar[q]);
     for (int c = threadIdx.x; c <= kSmallMaxD; c += blockDim.x) {
       if (c < d || c == kSmallMaxD) {
         double s = 0.0;
         for (int w = 0; w < NWp; ++w) s += wp[(size_t)w * (kSmallMaxD + 1) + c];
-        pb[c] = s;
+        const uint32_t off = 8u * (uint32_t)(c < d ? c : d);
+        for (int r = 0; r < CL; ++r) st_async_f64(mapa_u32(sb + off, r), s, mapa_u32(mb, r));
       }
     }
-    cl_bar();  // every CTA's partial of evaluation e is complete
+    if (threadIdx.x == 0) mbar_expect_tx(mb, (uint32_t)(CL * D1 * 8));
+    mbar_wait_cluster(mb, (uint32_t)((e >> 1) & 1));
     // ---- sum over the cluster in rank order, step from the anchor, project
-    for (int c = threadIdx.x; c <= kSmallMaxD; c += blockDim.x) {
-      if (c < d || c == kSmallMaxD) {
-        // all CL remote loads in flight before the (rank-ordered) sum
-        double pr[kSmallMaxCL];
-#pragma unroll
-        for (int r = 0; r < kSmallMaxCL; ++r) pr[r] = r < CL ? cl.map_shared_rank(pb, r)[c] : 0.0;
-        double s = 0.0;
-#pragma unroll
-        for (int r = 0; r < kSmallMaxCL; ++r) s += pr[r];
-        if (c < d) vv[c] = xa[c] - a.gamma * (s * inv_n);
-        else if (LOSS && rank == 0 && a.trace) a.trace[e] = s * inv_n;
-      }
+    const double *sq = slots + (size_t)q * CL * D1;
+    for (int c = threadIdx.x; c <= d; c += blockDim.x) {
+      double s = 0.0;
+      for (int r = 0; r < CL; ++r) s += sq[(size_t)r * D1 + c];
+      if (c < d) vv[c] = xa[c] - a.gamma * (s * inv_n);
+      else if (LOSS && rank == 0 && a.trace) a.trace[e] = s * inv_n;
     }
     __syncthreads();
     const bool half = (e & 1) == 0;  // x_{t+1/2} from x_t, then x_{t+1} from x_t
