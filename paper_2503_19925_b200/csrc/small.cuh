@@ -94,9 +94,13 @@ __global__ void __launch_bounds__(kSmallThreads, 1) k_small_solve(const SmallArg
   const int r0 = (int)((int64_t)a.n * rank / CL), r1 = (int)((int64_t)a.n * (rank + 1) / CL);
   const int rows = r1 - r0;
   const int ldd = (d + 1) & ~1;  // smem row pitch (elements), 8-byte aligned rows for double
+  // every CTA lays out its shared memory for the largest block, ceil(n / CL)
+  // rows, so that the arrays sit at the same offsets in every CTA: remote
+  // pushes address the receiver's slots and mbarriers by the sender's offsets
+  const int rows_cap = (a.n + CL - 1) / CL;
   T *As = reinterpret_cast<T *>(ssm);
-  double *ys = reinterpret_cast<double *>(As + (size_t)rows * ldd + ((size_t)rows * ldd & 1));
-  double *sp = ys + rows;                        // [3*kMaxW]
+  double *ys = reinterpret_cast<double *>(As + (size_t)rows_cap * ldd + ((size_t)rows_cap * ldd & 1));
+  double *sp = ys + rows_cap;                    // [3*kMaxW]
   double *xa = sp + 3 * kMaxW;                   // [d] anchor x_t
   double *xe = xa + kSmallMaxD;                  // [d] evaluation point
   double *vv = xe + kSmallMaxD;                  // [d] step vector

@@ -650,3 +650,28 @@ def test_small_cluster_solve_matches_graph_path(cfg):
     x_ref, tr_ref, _ = wo["problem"].solve(50, gam, trace=True)
     assert rel(xa.cpu().numpy(), x_ref) <= (1e-10 if cfg.dtype == "f64" else 1e-3)
     assert rel(ta, tr_ref) <= (1e-10 if cfg.dtype == "f64" else 1e-4)
+
+
+@pytest.mark.parametrize("n,d", [(500, 32), (1000, 64), (100, 100), (37, 250), (3, 8)])
+def test_small_cluster_solve_uneven_row_blocks(n, d):
+    """Row counts that do not divide by the cluster size give the CTAs row
+    blocks of different lengths; the cluster-resident solve lays out every
+    CTA's shared memory for the largest block so that the partials pushed
+    between CTAs land in the receiver's slots.  Same iterates as the graph
+    path and the oracle."""
+    P = _P()
+    pb = _rand_problem(n, d, seed=11)
+    p, o = _both(pb, set=G.SET_BALL, R=0.9)
+    q = P.Poly(A=torch.tensor(pb["A"], device="cuda"), d=pb["d"], y=torch.tensor(pb["y"], device="cuda"),
+               s=pb["s"], mu=pb["mu"], I_bar=pb["I_bar"], relu=pb["relu"], set=G.SET_BALL, R=0.9,
+               flags=P.POLY_FLAG_NO_SMALL)
+    gam = 0.05
+    xa = torch.zeros(d, dtype=torch.float64, device="cuda")
+    xb = torch.zeros_like(xa)
+    p.solve(xa, 20, gam)
+    q.solve(xb, 20, gam)
+    x_ref, _, _ = o.solve(20, gam)
+    assert rel(xa.cpu().numpy(), xb.cpu().numpy()) <= 1e-6
+    assert rel(xa.cpu().numpy(), x_ref) <= 1e-4
+    p.close()
+    q.close()
