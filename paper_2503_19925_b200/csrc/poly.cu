@@ -674,6 +674,9 @@ int build_graph_ex(poly_handle *h, int method, bool average, int U, cudaGraphExe
   e = cudaGraphInstantiate(out, g, 0);
   cudaGraphDestroy(g);
   if (e != cudaSuccess) return fail(POLY_ECUDA, "graph instantiate: %s", cudaGetErrorString(e));
+  // upload now, not at the first launch (which would then carry the upload)
+  if (cudaGraphUpload(*out, h->work) != cudaSuccess)
+    return fail(POLY_ECUDA, "graph upload: %s", cudaGetErrorString(cudaGetLastError()));
   return POLY_OK;
 }
 
@@ -691,6 +694,9 @@ int build_graph(poly_handle *h, bool loss, int U, cudaGraphExec_t *out) {
   e = cudaGraphInstantiate(out, g, 0);
   cudaGraphDestroy(g);
   if (e != cudaSuccess) return fail(POLY_ECUDA, "graph instantiate: %s", cudaGetErrorString(e));
+  // upload now, not at the first launch (which would then carry the upload)
+  if (cudaGraphUpload(*out, h->work) != cudaSuccess)
+    return fail(POLY_ECUDA, "graph upload: %s", cudaGetErrorString(cudaGetLastError()));
   return POLY_OK;
 }
 
@@ -1625,14 +1631,16 @@ int poly_solve(poly_handle *h, double *x, int T, double gamma, uint32_t flags, d
     const int U = std::min(h->graph_U, T);
     int li = loss ? 1 : 0;
     int rc = POLY_OK;
-    if (T >= h->graph_U && !h->gexec[li][1]) rc = build_graph(h, loss, h->graph_U, &h->gexec[li][1]);
-    if (rc == POLY_OK && (T % h->graph_U) && !h->gexec[li][0]) rc = build_graph(h, loss, 1, &h->gexec[li][0]);
+    // both graphs (U iterations and 1) are built and uploaded at the first
+    // solve, whatever its T, so that a short warm-up call prepares a long one
+    if (!h->gexec[li][1]) rc = build_graph(h, loss, h->graph_U, &h->gexec[li][1]);
+    if (rc == POLY_OK && !h->gexec[li][0]) rc = build_graph(h, loss, 1, &h->gexec[li][0]);
     if (rc != POLY_OK && h->pdl) {  // retry capture without programmatic edges
       h->pdl = false;
       cudaGetLastError();
       rc = POLY_OK;
-      if (T >= h->graph_U && !h->gexec[li][1]) rc = build_graph(h, loss, h->graph_U, &h->gexec[li][1]);
-      if (rc == POLY_OK && (T % h->graph_U) && !h->gexec[li][0]) rc = build_graph(h, loss, 1, &h->gexec[li][0]);
+      if (!h->gexec[li][1]) rc = build_graph(h, loss, h->graph_U, &h->gexec[li][1]);
+      if (rc == POLY_OK && !h->gexec[li][0]) rc = build_graph(h, loss, 1, &h->gexec[li][0]);
     }
     if (rc != POLY_OK) return rc;
     (void)U;
