@@ -220,19 +220,20 @@ __global__ void k_to_f32(const double *x, int64_t d, int32_t tr_side, float *out
 }
 
 __global__ void __launch_bounds__(256) k_fin_apply(const FinArgs a) {
-  __shared__ double s_nr;
+  __shared__ double s_w[8];
   pdl_wait();
   pdl_trigger();
   const int tid = threadIdx.x;
   const int nb = (a.d + 31) / 32;  // k_finalize blocks
-  if (tid < 32) {
-    double nr = 0.0;
-    for (int b = tid; b < nb; b += 32) nr += a.block_norm[b];
-    nr = warp_sum(nr);
-    if (tid == 0) s_nr = nr;
-  }
+  // all 256 threads read the block norms (loads in flight together), then a
+  // fixed tree: per-thread strided sums, warp butterflies, warps in order —
+  // the same bits in every block
+  double nr = 0.0;
+  for (int b = tid; b < nb; b += 256) nr += a.block_norm[b];
+  nr = warp_sum(nr);
+  if ((tid & 31) == 0) s_w[tid >> 5] = nr;
   __syncthreads();
-  const double nrm = sqrt(s_nr);
+  const double nrm = sqrt(((s_w[0] + s_w[1]) + (s_w[2] + s_w[3])) + ((s_w[4] + s_w[5]) + (s_w[6] + s_w[7])));
   double scale = 1.0;
   if ((a.set == 1 || a.set == 3) && nrm > a.R) scale = a.R / nrm;
   for (int k = blockIdx.x * blockDim.x + tid; k < a.d; k += gridDim.x * blockDim.x) {
