@@ -71,6 +71,7 @@ __global__ void __launch_bounds__(256) k_finalize(const FinArgs a) {
   pdl_wait();
   pdl_trigger();
   const int tid = threadIdx.x, cl = tid & 31, sl = tid >> 5;
+  const int NWf = (int)(blockDim.x >> 5);  // 8, or 2 when there is at most one partial row
   const int c = blockIdx.x * 32 + cl;
   const int mode = a.mode;
   const bool from_comm = (mode == FIN_GRAD_COMM || mode == FIN_STEP_COMM);
@@ -88,15 +89,15 @@ __global__ void __launch_bounds__(256) k_finalize(const FinArgs a) {
         // in a fixed order: deterministic for a fixed G
         double q0 = 0.0, q1 = 0.0, q2 = 0.0, q3 = 0.0;
         const double *col = a.partials + c;
-        const size_t st = (size_t)8 * a.d;
+        const size_t st = (size_t)NWf * a.d;
         int i = sl;
-        for (; i + 24 < a.G; i += 32) {
+        for (; i + 3 * NWf < a.G; i += 4 * NWf) {
           q0 += col[(size_t)i * a.d];
           q1 += col[(size_t)i * a.d + st];
           q2 += col[(size_t)i * a.d + 2 * st];
           q3 += col[(size_t)i * a.d + 3 * st];
         }
-        for (; i < a.G; i += 8) q0 += col[(size_t)i * a.d];
+        for (; i < a.G; i += NWf) q0 += col[(size_t)i * a.d];
         acc = (q0 + q1) + (q2 + q3);
       }
     }
@@ -118,8 +119,7 @@ __global__ void __launch_bounds__(256) k_finalize(const FinArgs a) {
     if (mode == FIN_GRAD || mode == FIN_GRAD_COMM || mode == FIN_REDUCE) return;
   }
   if (sl == 0 && needs_g) {
-#pragma unroll
-    for (int k = 0; k < 8; ++k) tot += sm[k][cl];
+    for (int k = 0; k < NWf; ++k) tot += sm[k][cl];
   }
   if (mode == FIN_REDUCE) {
     if (c < a.d) a.comm[c] = tot;

@@ -559,7 +559,10 @@ int launch_small_solve(poly_handle *h, double *x_dev, int T, bool loss, int C, s
 
 int enqueue_fin(poly_handle *h, const FinArgs &f) {
   ProfScope ps(h, 1);
-  TRY(launch(h, (const void *)&k_finalize, dim3(h->fin_grid), dim3(256), 0, true, f));
+  // one partial row (CSR / matrix-free backward) or the comm buffer: warp 0
+  // sums the columns and warp 1 of block 0 the loss — two warps suffice
+  const bool one_row = f.G <= 1 || f.mode == FIN_GRAD_COMM || f.mode == FIN_STEP_COMM || f.mode == FIN_PROJECT;
+  TRY(launch(h, (const void *)&k_finalize, dim3(h->fin_grid), dim3(one_row ? 64 : 256), 0, true, f));
   const bool steps = f.mode == FIN_STEP || f.mode == FIN_STEP_COMM || f.mode == FIN_PROJECT;
   if (h->tv_cl && steps) TRY(enqueue_tv(h, f.v_scratch, f.v_scratch));
   if (f.split && steps) {
