@@ -1,7 +1,7 @@
 """C1 (fp32/fp64) EXACT iteration time through the cluster-resident solve."""
 import os, sys, json
 import torch
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from gen import configs as G
 from paper_2503_19925_b200 import workloads as PW
 out = {}

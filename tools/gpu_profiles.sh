@@ -13,6 +13,7 @@ python bench.py --impl reference --steps 2 --warmup 3 > gpurun_out/bench_ref_c2_
 python tools/time_tv.py > gpurun_out/time_tv_$TAG.json 2>&1; echo "tv rc=$?"
 python tools/time_pb.py > gpurun_out/time_pb_$TAG.json 2>&1; echo "pb rc=$?"
 python tools/k9_time.py > gpurun_out/k9_$TAG.json 2>&1; echo "k9 rc=$?"
+python tools/c1_time.py > gpurun_out/c1_$TAG.json 2>&1; echo "c1 rc=$?"
 for c in c2 c3 c4; do
   ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -c 400 --csv \
       --log-file gpurun_out/launches_${c}_$TAG.csv python bench.py --config $c --steps 20 --warmup 3 --no-cpu --no-e2e \
