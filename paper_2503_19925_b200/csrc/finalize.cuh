@@ -47,6 +47,7 @@ struct FinArgs {
   int32_t G;                 // number of partial rows
   int32_t GL;                // number of loss partials
   int32_t split;             // 1: skip the last-block tail; k_fin_apply finishes the step
+  int32_t need_loss;         // 0: the objective is not wanted (its partials are not summed)
   int32_t set;
   int64_t n_norm;            // the n of Eq.(operator)
   const double *partials;    // [G][d]
@@ -103,12 +104,14 @@ __global__ void __launch_bounds__(256) k_finalize(const FinArgs a) {
     }
     sm[sl][cl] = acc;
   }
-  // ---- loss (block 0, warp 1), fixed order
+  // ---- loss (block 0, warp 1; only block 0 uses s_loss), fixed order — the
+  // partial sums only when the objective is wanted: with one partial per
+  // forward block (CSR: 4129) they are a long serial tail
   if (blockIdx.x == 0 && sl == 1 && needs_g) {
     double l = 0.0;
     if (from_comm) {
       l = (cl == 0) ? a.comm[a.d] : 0.0;
-    } else {
+    } else if (a.need_loss) {
       for (int i = cl; i < a.GL; i += 32) l += a.loss_partials[i];
     }
     l = warp_sum(l);

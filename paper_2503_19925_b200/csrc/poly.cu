@@ -443,6 +443,7 @@ FinArgs fin_base(poly_handle *h, int mode) {
   f.G = h->G;
   f.GL = h->p.layout == POLY_CSR ? h->k4_grid : (h->p.layout == POLY_PARALLEL_BEAM ? h->pb.nv : h->G);
   f.split = h->fin_split;
+  f.need_loss = 1;
   f.set = h->p.set;
   f.n_norm = h->n_norm;
   f.partials = h->partials;
@@ -608,6 +609,7 @@ int enqueue_eval(poly_handle *h, const double *x, bool loss, bool step, const do
                  double *x_out, double *g_out) {
   TRY(enqueue_pass(h, x, loss));
   FinArgs f = fin_base(h, 0);
+  f.need_loss = loss ? 1 : 0;
   f.anchor = anchor;
   f.x_out = x_out;
   f.x32_out = x32_of(h, x_out);
