@@ -394,7 +394,7 @@ def main():
                     help="N>1: sum over ranks with the K9 peer-reduce kernel instead of ncclAllReduce")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
-    ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--e2e-steps", type=int, default=4)
     ap.add_argument("--e2e-T", type=int, default=0)
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
