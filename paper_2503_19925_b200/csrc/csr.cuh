@@ -27,6 +27,7 @@
 #pragma once
 
 #include "dense.cuh"
+#include "finalize.cuh"  // SolveState (the backward's optional step epilogue)
 
 namespace poly {
 
@@ -352,10 +353,26 @@ __global__ void __launch_bounds__(POLY_SELL_LB_F) k_sell16_forward(const Sell16 
   pdl_trigger();
 }
 
+// Optional epilogue of the backward for the plain EXACT step on the split
+// path (d > 8192, no objective wanted, one rank): each block owns 32 columns
+// of g — exactly one k_finalize block — so it forms v = anchor - γ g/n, the
+// orthant clamp and the block's ||v - c||² itself, with k_finalize's
+// arithmetic (same bits), and k_fin_apply follows directly.
+struct StepEpi {
+  int32_t on;
+  int32_t set;
+  double n_norm;
+  const double *anchor;
+  const double *center;
+  const SolveState *state;
+  double *v_scratch;
+  double *block_norm;
+};
+
 template <typename T>
 __global__ void __launch_bounds__(POLY_SELL_LB_B) k_sell16_backward(const Sell16 s, int64_t nslices,
                                                               int32_t d, const float *__restrict__ r,
-                                                              double *__restrict__ g) {
+                                                              double *__restrict__ g, const StepEpi e) {
   __shared__ double part[4][32];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   pdl_wait();  // r is written by the forward pass
@@ -365,7 +382,21 @@ __global__ void __launch_bounds__(POLY_SELL_LB_B) k_sell16_backward(const Sell16
     if (warp == 0) {
       const int64_t c = sl * 32 + lane;
       const double v = (part[0][lane] + part[1][lane]) + (part[2][lane] + part[3][lane]);
-      if (c < d) g[c] = v;
+      if (!e.on) {
+        if (c < d) g[c] = v;
+      } else {
+        double q = 0.0;
+        if (c < d) {
+          const double gc = v / e.n_norm;
+          double vv = e.anchor[c] - e.state->gamma * gc;
+          if (e.set == 2 || e.set == 3) vv = vv > 0.0 ? vv : 0.0;
+          const double df = (e.set == 1 && e.center) ? vv - e.center[c] : vv;
+          q = df * df;
+          e.v_scratch[c] = vv;
+        }
+        q = warp_sum(q);
+        if (lane == 0) e.block_norm[sl] = q;
+      }
     }
     __syncthreads();
   }

@@ -247,6 +247,7 @@ struct poly_handle {
   double *pb_trig = nullptr, *pb_out2 = nullptr, *pb_zpart = nullptr;
   int32_t *pb_ticket = nullptr, *pb_tticket = nullptr;
   int k4f16_grid = 0, k4b16_grid = 0;  // resident-slot grids (slices dealt grid-stride)
+  StepEpi epi{};                        // K4b's step epilogue for the next pass (on = 0: write g)
   // TV sets: Dykstra state, statistics, cluster launch shape
   double *tv_zk = nullptr, *tv_p = nullptr, *tv_q = nullptr;
   int32_t *tv_stats = nullptr;
@@ -418,7 +419,7 @@ int enqueue_pass(poly_handle *h, const double *x, bool loss) {
     TRY(launch(h, kSell16Fwd[p.dtype][loss ? 1 : 0], dim3(h->k4f16_grid), dim3(128), 0, true,
                h->fwd16, (int64_t)h->nrslices, a));
     return launch(h, kSell16Bwd[p.dtype], dim3(h->k4b16_grid), dim3(128), 0, true, h->bwd16,
-                  (int64_t)h->nslices, (int32_t)p.d, (const float *)h->rbuf, h->partials);
+                  (int64_t)h->nslices, (int32_t)p.d, (const float *)h->rbuf, h->partials, h->epi);
   }
   TRY(launch(h, kCsrFwd[p.dtype][loss ? 1 : 0], dim3(h->k4_grid), dim3(128), 0, true,
              (const void *)h->sell_rows, (const int64_t *)h->row_slice_off, a));
@@ -573,6 +574,15 @@ int enqueue_fin(poly_handle *h, const FinArgs &f) {
   return POLY_OK;
 }
 
+// the part of enqueue_fin after k_finalize, for a pass whose epilogue already
+// wrote v and the block norms (FIN_STEP on the split path)
+int enqueue_fin_tail(poly_handle *h, const FinArgs &f) {
+  ProfScope ps(h, 1);
+  if (h->tv_cl) TRY(enqueue_tv(h, f.v_scratch, f.v_scratch));
+  const int grid = (int)std::min<int64_t>(h->sms, (h->p.d + 255) / 256);
+  return launch(h, (const void *)&k_fin_apply, dim3(grid), dim3(256), 0, true, f);
+}
+
 int enqueue_allreduce(poly_handle *h) {
   ProfScope ps(h, 2);
   NcclApi *api = nccl_api();
@@ -607,7 +617,6 @@ int enqueue_peer_reduce(poly_handle *h) {
 // F at x, then either g/loss (step == false) or x_out = P_X(anchor - γ F(x)).
 int enqueue_eval(poly_handle *h, const double *x, bool loss, bool step, const double *anchor,
                  double *x_out, double *g_out) {
-  TRY(enqueue_pass(h, x, loss));
   FinArgs f = fin_base(h, 0);
   f.need_loss = loss ? 1 : 0;
   f.anchor = anchor;
@@ -615,8 +624,27 @@ int enqueue_eval(poly_handle *h, const double *x, bool loss, bool step, const do
   f.x32_out = x32_of(h, x_out);
   f.tr_side = h->tr_side;
   f.g_out = g_out;
+  // compact-SELL CSR on the split path, plain step, no objective, one rank:
+  // K4b's epilogue does k_finalize's work (same bits) and k_fin_apply follows
+  const bool fuse = h->sell16 && h->p.layout == POLY_CSR && !h->comm_path && step && !loss && !g_out &&
+                    f.split && !getenv("POLY_NO_EPI");
+  h->epi = StepEpi{};
+  if (fuse) {
+    h->epi.on = 1;
+    h->epi.set = f.set;
+    h->epi.n_norm = (double)f.n_norm;
+    h->epi.anchor = anchor;
+    h->epi.center = f.center;
+    h->epi.state = f.state;
+    h->epi.v_scratch = f.v_scratch;
+    h->epi.block_norm = f.block_norm;
+  }
+  const int prc = enqueue_pass(h, x, loss);
+  h->epi = StepEpi{};
+  TRY(prc);
   if (!h->comm_path) {
     f.mode = step ? FIN_STEP : FIN_GRAD;
+    if (fuse) return enqueue_fin_tail(h, f);
     return enqueue_fin(h, f);
   }
   FinArgs r = f;
