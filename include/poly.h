@@ -47,7 +47,7 @@
 extern "C" {
 #endif
 
-#define POLY_ABI_VERSION 4
+#define POLY_ABI_VERSION 5
 
 /* status codes */
 #define POLY_OK 0
@@ -93,6 +93,12 @@ extern "C" {
 #define POLY_FLAG_P2P 32u        /* allocate a peer-reduce window (with world > 1 or POLY_FLAG_COMM);
                                     after poly_p2p_open the cross-rank sum runs as one kernel over
                                     NVLink peer memory (K9) instead of ncclAllReduce */
+
+#define POLY_FLAG_NVLS 64u       /* allocate for K9-NVLS (with world > 1 or POLY_FLAG_COMM): after
+                                    poly_nvls_open the cross-rank sum runs as one kernel over an
+                                    NVLink multicast object — the NVSwitch adds the ranks' vectors
+                                    (multimem.ld_reduce) and broadcasts the sums (multimem.st) —
+                                    instead of ncclAllReduce.  Exclusive with POLY_FLAG_P2P. */
 
 /* poly_problem.mode: which per-row scalar the fused pass evaluates.  Every mode
  * streams A once and returns g = (1/n) Σ_i φ_i a_i and a scalar objective.   */
@@ -273,7 +279,12 @@ int poly_kernel_times(poly_handle *h, double *out, int32_t nout);
 
 /* Static description of the chosen configuration, for reports:
  * out[0] grid CTAs, out[1] threads/CTA, out[2] rows per stage, out[3] stages,
- * out[4] dynamic smem bytes, out[5] SM count.  nout <= 6. */
+ * out[4] dynamic smem bytes, out[5] SM count; dense handles also report the K1
+ * instantiation k_dense_loss_grad<T, V, WPR, NW, RPS, LOSS, FULL>: out[6] V,
+ * out[7] WPR, out[8] NW, out[9] FULL (1: d fills the tile exactly, no column
+ * masks); 0 for CSR / matrix-free handles.  out[10] ranks of the handle's
+ * NCCL communicator (ncclCommCount; 0 without one), out[11] 1 when the
+ * cross-rank sum runs as K9 (poly_p2p_open).  nout <= 12. */
 int poly_describe(poly_handle *h, int64_t *out, int32_t nout);
 
 /* Write a fresh 128-byte ncclUniqueId into out (host).  Call on rank 0 and
@@ -295,7 +306,37 @@ int poly_nccl_unique_id(void *out128);
 int poly_p2p_handle(poly_handle *h, void *out64);
 int poly_p2p_open(poly_handle *h, const void *handles);
 
-/* Release everything the handle owns (workspaces, graphs, communicator). */
+/* K9-NVLS setup (step a6 through the switch).
+ * Collective, in two calls on every rank of a handle made with POLY_FLAG_NVLS:
+ *   1. poly_nvls_handle: rank 0 creates an NVLink multicast object sized for
+ *      flags + 4 slots of d+1 doubles (CU_DEVICE_ATTRIBUTE_MULTICAST_SUPPORTED
+ *      required, else POLY_EUNSUPPORTED) and writes a 64-byte descriptor to
+ *      out64 (host); other ranks' output is unused.  The caller broadcasts rank
+ *      0's 64 bytes (e.g. torch.distributed.broadcast_object_list).
+ *   2. poly_nvls_open(desc64 = rank 0's descriptor, host): every rank receives
+ *      the object's file descriptor from rank 0 over an abstract unix socket
+ *      (poly_share_fd; the ranks must share a node), adds its device, binds a
+ *      physical copy of the window and maps the unicast and multicast views;
+ *      two barriers over the handle's communicator order the steps.  From the
+ *      next F evaluation on, every cross-rank sum is k_nvls_reduce.
+ * Every wait inside the kernel is bounded (POLY_COMM_TIMEOUT_S, default 300 s);
+ * on a timeout the solve returns POLY_ENCCL and the communicator is aborted.
+ * Errors: POLY_EINVAL (no flag, wrong order, foreign descriptor),
+ * POLY_EUNSUPPORTED (no multicast support), POLY_ECUDA / POLY_ENOMEM (driver
+ * calls), POLY_ENCCL (a rank did not join within the timeout). */
+int poly_nvls_handle(poly_handle *h, void *out64);
+int poly_nvls_open(poly_handle *h, const void *desc64);
+
+/* Same-node file-descriptor hand-off used by poly_nvls_open: rank 0 listens
+ * on the abstract unix socket `name` and passes fd_in (SCM_RIGHTS) to the
+ * world-1 other ranks, which connect (retrying up to timeout_s seconds) and
+ * receive a duplicate in *fd_out; on rank 0 *fd_out = fd_in.  Collective over
+ * the ranks of one node.  Errors: POLY_EINVAL, POLY_ENCCL (timeout). */
+int poly_share_fd(int32_t rank, int32_t world, const char *name, int fd_in, int *fd_out, double timeout_s);
+
+/* Release everything the handle owns (workspaces, graphs, communicator,
+ * peer / multicast windows).  With K9 or K9-NVLS every rank must have
+ * finished its last evaluation before any rank frees (e.g. a barrier). */
 void poly_free(poly_handle *h);
 
 /* Thread-local message for the last error of this thread ("" if none). */

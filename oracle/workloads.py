@@ -3,8 +3,11 @@
 Builds the oracle's copy of a BASELINE.json workload (or of a subset of its
 rows) from the seeded generators in gen/ plus the oracle's own arithmetic for
 the expected counts (Eq. model).  It never reads anything
-produced by the CUDA path; tests compare the two sides' independently built
-inputs bit for bit (counts, indices) instead.
+the CUDA path computes; tests compare the two sides' independently built
+inputs bit for bit (counts, indices) instead.  The one thing it may take from
+the device is the output of the shared seeded generator (the Gaussian rows of
+A drawn by its CUDA twin), verified against gen/rng on sampled rows — see
+`build(A=...)`.
 """
 from __future__ import annotations
 
@@ -47,10 +50,33 @@ def csr_matrix(cfg: G.Config):
     return row_ptr, col, val.astype(np.float32)
 
 
-def build(cfg: G.Config, rows=None, with_counts=True):
+def _shared_rows(cfg: G.Config, rows, M, d, stream):
+    """Accept rows of a generated matrix produced by the generators' CUDA twin
+    (libpolysynth, the seeded input generator shared by both sides — it holds
+    none of the method's arithmetic) instead of redrawing them
+    here with numpy (≈2M draws/s: 4 minutes for full C2).  Sampled rows are
+    redrawn from gen/rng and must match bit for bit before the bytes are used."""
+    M = np.ascontiguousarray(M[:, :d])
+    if M.shape[0] != rows.shape[0]:
+        raise ValueError("shared matrix has the wrong number of rows")
+    m = rows.shape[0]
+    pick = sorted({0, m // 3, m // 2, (2 * m) // 3, m - 1}) if m else []
+    ref = rng.gaussian_rows(cfg.seed, stream, rows[pick], d)
+    ref = ref.astype(np.float32) if (cfg.dtype == "f32" or stream == rng.STREAM_A_KNOWN) else ref
+    if not np.array_equal(M[pick], ref.astype(M.dtype)):
+        raise ValueError("shared generator bytes differ from gen/rng on sampled rows")
+    return M
+
+
+def build(cfg: G.Config, rows=None, with_counts=True, A=None, A_known=None):
     """Oracle-side inputs for `cfg` restricted to global row indices `rows`
     (default: all).  Returns a dict of numpy arrays + an oracle Problem with
-    n_norm = cfg.n (the full problem's n, reading R4)."""
+    n_norm = cfg.n (the full problem's n, reading R4).
+
+    A / A_known (optional, host arrays [len(rows), >= d]): the generated rows
+    of A (and, for C3, of [A^1 | A^2]) as drawn by the generators' CUDA twin;
+    checked against gen/rng on sampled rows (`_shared_rows`).  Everything the
+    method computes from them — λ, counts, s', Ī', F — is the oracle's own."""
     s, mu = cfg.spectrum
     xs = x_star(cfg)
     out = {"s": s, "mu": mu, "x_star": xs}
@@ -70,14 +96,15 @@ def build(cfg: G.Config, rows=None, with_counts=True):
         mat = dict(row_ptr=row_ptr, col=col, val=val)
     else:
         rows = np.arange(cfg.n, dtype=np.int64) if rows is None else np.asarray(rows, dtype=np.int64)
-        A = dense_rows(cfg, rows)
+        A = dense_rows(cfg, rows) if A is None else _shared_rows(cfg, rows, A, cfg.d, rng.STREAM_A)
         out["A"] = A
         mat = dict(A=A)
     out["rows"] = rows
     s_row = I_row = None
     if cfg.kind == "reparam":
         xk = known_images(cfg)
-        Ak = known_rows(cfg, rows)
+        Ak = known_rows(cfg, rows) if A_known is None else \
+            _shared_rows(cfg, rows, A_known, 2 * cfg.d, rng.STREAM_A_KNOWN)
         pk = Problem(A=Ak, y=np.zeros(rows.shape[0]), s=s, mu=mu, I_bar=1.0, d=2 * cfg.d)
         b = pk.forward(xk)
         from . import reparam

@@ -21,6 +21,7 @@ POLY_SET_NONE, POLY_SET_BALL, POLY_SET_NONNEG, POLY_SET_NONNEG_BALL = 0, 1, 2, 3
 POLY_SET_TV_NONNEG, POLY_SET_TV = 4, 5
 POLY_FLAG_HOST_INPUTS, POLY_FLAG_NO_GRAPH, POLY_FLAG_NO_PDL, POLY_FLAG_COMM, POLY_FLAG_NO_SMALL = 1, 2, 4, 8, 16
 POLY_FLAG_P2P = 32
+POLY_FLAG_NVLS = 64
 POLY_SOLVE_PROFILE = 1
 POLY_MODE_EXACT, POLY_MODE_L2, POLY_MODE_L1, POLY_MODE_NLL = 0, 1, 2, 3
 POLY_METHOD_EXTRAGRADIENT, POLY_METHOD_GD = 0, 1
@@ -28,7 +29,8 @@ POLY_METHOD_EXTRAGRADIENT, POLY_METHOD_GD = 0, 1
 EXPORTED = ["poly_init", "poly_loss_grad", "poly_solve", "poly_forward", "poly_expected_counts",
             "poly_reparameterize", "poly_kernel_times", "poly_describe", "poly_nccl_unique_id",
             "poly_free", "poly_last_error", "poly_abi_version", "poly_solve_ex", "poly_project",
-            "poly_stream_probe", "poly_p2p_handle", "poly_p2p_open"]
+            "poly_stream_probe", "poly_p2p_handle", "poly_p2p_open", "poly_nvls_handle",
+            "poly_nvls_open", "poly_share_fd"]
 
 
 class PolyProblem(C.Structure):
@@ -91,6 +93,9 @@ def _load():
     lib.poly_nccl_unique_id.argtypes = [vp]
     lib.poly_p2p_handle.argtypes = [vp, vp]
     lib.poly_p2p_open.argtypes = [vp, vp]
+    lib.poly_nvls_handle.argtypes = [vp, vp]
+    lib.poly_nvls_open.argtypes = [vp, vp]
+    lib.poly_share_fd.argtypes = [i32, i32, C.c_char_p, C.c_int, C.POINTER(C.c_int), dbl]
     lib.poly_free.argtypes = [vp]
     lib.poly_free.restype = None
     lib.poly_last_error.restype = C.c_char_p
@@ -189,9 +194,10 @@ def poly_kernel_times(h: int):
 
 
 def poly_describe(h: int):
-    out = (C.c_int64 * 6)()
-    _check(_lib.poly_describe(h, out, 6))
-    return dict(zip(["grid", "threads", "rows_per_stage", "stages", "smem", "sms"], list(out)))
+    out = (C.c_int64 * 12)()
+    _check(_lib.poly_describe(h, out, 12))
+    return dict(zip(["grid", "threads", "rows_per_stage", "stages", "smem", "sms", "V", "WPR", "NW",
+                     "full", "comm_ranks", "k9"], list(out)))
 
 
 def poly_nccl_unique_id() -> bytes:
@@ -212,6 +218,29 @@ def poly_p2p_open(h: int, handles: bytes):
     ncclAllReduce for this handle from the next evaluation on."""
     buf = C.create_string_buffer(bytes(handles), len(handles))
     _check(_lib.poly_p2p_open(h, buf))
+
+
+def poly_nvls_handle(h: int) -> bytes:
+    """Rank 0: create the NVLink multicast object; its 64-byte descriptor
+    (POLY_FLAG_NVLS).  Other ranks get bytes they pass on unused."""
+    buf = C.create_string_buffer(64)
+    _check(_lib.poly_nvls_handle(h, buf))
+    return buf.raw
+
+
+def poly_nvls_open(h: int, desc: bytes):
+    """Join rank 0's multicast object (desc = rank 0's descriptor, on every
+    rank): K9-NVLS replaces ncclAllReduce for this handle."""
+    buf = C.create_string_buffer(bytes(desc), 64)
+    _check(_lib.poly_nvls_open(h, buf))
+
+
+def poly_share_fd(rank: int, world: int, name: str, fd_in: int, timeout_s: float = 30.0) -> int:
+    """Same-node fd hand-off of poly_nvls_open (rank 0 -> the others)."""
+    out = C.c_int(-1)
+    _check(_lib.poly_share_fd(int(rank), int(world), name.encode(), int(fd_in), C.byref(out),
+                              float(timeout_s)))
+    return out.value
 
 
 def poly_free(h: int):

@@ -106,6 +106,20 @@ class Poly:
         hs = D.gather_handles(poly_p2p_handle(self.h), int(self.problem.rank), int(self.problem.world))
         poly_p2p_open(self.h, hs)
 
+    def nvls_setup(self):
+        """K9-NVLS: rank 0 creates the NVLink multicast object, its descriptor
+        is broadcast over the default torch.distributed group (world > 1),
+        and every rank joins; the cross-rank sum then runs in the switch.
+        Needs flags with POLY_FLAG_NVLS."""
+        from . import poly_nvls_handle, poly_nvls_open
+        desc = poly_nvls_handle(self.h)
+        if int(self.problem.world) > 1:
+            import torch.distributed as dist
+            box = [desc if int(self.problem.rank) == 0 else None]
+            dist.broadcast_object_list(box, src=0)
+            desc = box[0]
+        poly_nvls_open(self.h, desc)
+
     def close(self):
         if getattr(self, "h", None):
             poly_free(self.h)

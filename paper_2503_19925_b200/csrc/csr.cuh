@@ -364,7 +364,7 @@ struct StepEpi {
   double n_norm;
   const double *anchor;
   const double *center;
-  const SolveState *state;
+  SolveState *state;
   double *v_scratch;
   double *block_norm;
 };
@@ -396,6 +396,7 @@ __global__ void __launch_bounds__(POLY_SELL_LB_B) k_sell16_backward(const Sell16
         }
         q = warp_sum(q);
         if (lane == 0) e.block_norm[sl] = q;
+        if (sl == 0 && lane == 0) e.state->loss_cur = 0.0;  // as k_finalize without the objective
       }
     }
     __syncthreads();

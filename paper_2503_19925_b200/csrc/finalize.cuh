@@ -36,7 +36,7 @@ struct SolveState {
   int32_t k;           // index of the last iterate folded into the window sum
   int32_t stopped;     // 1 once ||x̄_k - x̄_{k-1}|| <= tol (k >= 2)
   int32_t k_stop;
-  int32_t pad;
+  int32_t comm_err;    // K9: a peer did not publish within the wait bound (set on the device)
   double tol;
   double move;
 };

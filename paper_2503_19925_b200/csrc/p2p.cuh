@@ -11,7 +11,8 @@
 //   1. copies its chunk of the local unnormalised sums (comm) into its own
 //      slot q, and after a block barrier publishes flags[q][b] = e with one
 //      system-scope release store;
-//   2. waits (system-scope acquire loads) until every rank's flags[q][b] == e,
+//   2. waits (system-scope acquire loads, bounded by timeout_ns) until every
+//      rank's flags[q][b] == e,
 //      then sums its chunk over ranks 0..P-1 in rank order straight from the
 //      ranks' slots (NVLink loads) into comm — the same bits on every rank,
 //      so the replicated iterates stay identical.
@@ -34,7 +35,15 @@ struct PeerArgs {
   int32_t world, rank;
   char *win[kP2PMaxRanks];         // every rank's window (own one local, peers IPC-mapped)
   unsigned long long *epoch;       // [kP2PMaxBlocks] local evaluation counters, one per block
+  int32_t *err;                    // set to 1 when a wait exceeds timeout_ns (SolveState.comm_err)
+  unsigned long long timeout_ns;   // bound on every wait for a peer (globaltimer ns)
 };
+
+__device__ __forceinline__ unsigned long long globaltimer_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
 
 __device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long *p) {
   unsigned long long v;
@@ -63,11 +72,24 @@ __global__ void __launch_bounds__(256) k_peer_reduce(const PeerArgs a) {
   for (int64_t i = c0 + threadIdx.x; i < c1; i += blockDim.x) own[i] = a.comm[i];
   __syncthreads();
   if (threadIdx.x == 0) st_release_sys(flag(a.rank), e);
-  // 2. wait for the namesake blocks of every rank, then the rank-ordered sum
-  if (threadIdx.x < a.world)
-    while (ld_acquire_sys(flag(threadIdx.x)) != e) {
-    }
+  // 2. wait (bounded) for the namesake blocks of every rank, then the
+  // rank-ordered sum; a peer that never publishes ends the wait with err set
+  // (the host aborts the communicator: no rank hangs)
+  __shared__ int s_ok;
+  if (threadIdx.x == 0) s_ok = 1;
   __syncthreads();
+  if (threadIdx.x < a.world) {
+    const unsigned long long t0 = globaltimer_ns();
+    while (ld_acquire_sys(flag(threadIdx.x)) != e) {
+      if (globaltimer_ns() - t0 > a.timeout_ns) {
+        s_ok = 0;
+        atomicExch(a.err, 1);
+        break;
+      }
+    }
+  }
+  __syncthreads();
+  if (!s_ok) return;
   for (int64_t i = c0 + threadIdx.x; i < c1; i += blockDim.x) {
     double v = 0.0;
     for (int r = 0; r < a.world; ++r) v += ld_relaxed_sys(slot(r) + i);

@@ -12,8 +12,13 @@
 // and poly_solve replays one CUDA graph per U EXACT iterations
 // (Eq. extragrad-method) with programmatic dependent launch
 // between the kernels so the next A stream starts while the step finishes.
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <dlfcn.h>
+#include <sys/socket.h>
+#include <sys/un.h>
+#include <poll.h>
+#include <unistd.h>
 #include <nccl.h>
 #include <stdarg.h>
 #include <stdio.h>
@@ -24,7 +29,9 @@
 #include <cub/device/device_scan.cuh>
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
+#include <thread>
 #include <vector>
 
 #include "../../include/poly.h"
@@ -36,6 +43,7 @@
 #include "small.cuh"
 #include "ctproj.cuh"
 #include "p2p.cuh"
+#include "nvls.cuh"
 
 using namespace poly;
 
@@ -74,6 +82,8 @@ struct NcclApi {
   decltype(&ncclCommDestroy) commDestroy = nullptr;
   decltype(&ncclCommAbort) commAbort = nullptr;
   decltype(&ncclGetErrorString) errStr = nullptr;
+  decltype(&ncclCommGetAsyncError) asyncErr = nullptr;
+  decltype(&ncclCommCount) count = nullptr;
 };
 
 NcclApi *nccl_api() {
@@ -93,8 +103,10 @@ NcclApi *nccl_api() {
   api.commDestroy = (decltype(api.commDestroy))dlsym(api.lib, "ncclCommDestroy");
   api.commAbort = (decltype(api.commAbort))dlsym(api.lib, "ncclCommAbort");
   api.errStr = (decltype(api.errStr))dlsym(api.lib, "ncclGetErrorString");
+  api.asyncErr = (decltype(api.asyncErr))dlsym(api.lib, "ncclCommGetAsyncError");
+  api.count = (decltype(api.count))dlsym(api.lib, "ncclCommCount");
   if (!api.getUniqueId || !api.commInitRank || !api.allReduce || !api.commDestroy ||
-      !api.commAbort || !api.errStr) {
+      !api.commAbort || !api.errStr || !api.asyncErr || !api.count) {
     api.lib = nullptr;
     return nullptr;
   }
@@ -274,12 +286,26 @@ struct poly_handle {
   int graph_U = 8;
   ncclComm_t nccl = nullptr;
   bool comm_path = false;  // world > 1 or POLY_FLAG_COMM: reduce -> allreduce -> step
+  double comm_timeout_s = 300.0;  // POLY_COMM_TIMEOUT_S: host watchdog on waits with a communicator
+  bool no_epi = false;            // POLY_NO_EPI (read once at init): no K4b step epilogue
+  cudaEvent_t ev_poll[2] = {nullptr, nullptr}, ev_sync = nullptr;
   // K9 peer reduce (POLY_FLAG_P2P + poly_p2p_open): this rank's window, the
   // peers' IPC mappings, the per-block evaluation counters
   char *p2p_win = nullptr;
   char *p2p_peer[kP2PMaxRanks] = {};
   unsigned long long *p2p_epoch = nullptr;
   bool p2p = false;
+  // K9-NVLS (POLY_FLAG_NVLS + poly_nvls_open): the multicast window
+  struct {
+    bool on = false;
+    CUmemGenericAllocationHandle mc = 0, mem = 0;
+    bool have_mc = false, have_mem = false, bound = false;
+    CUdeviceptr uc_va = 0, mc_va = 0;
+    bool uc_mapped = false, mc_mapped = false;
+    size_t size = 0;
+    int fd = -1, listen_fd = -1;
+    unsigned long long *epoch = nullptr;
+  } nv;
   // profiling
   bool prof = false;
   std::vector<cudaEvent_t> evpool;
@@ -606,6 +632,8 @@ int enqueue_peer_reduce(poly_handle *h) {
   a.rank = (int32_t)h->p.rank;
   for (int r = 0; r < a.world; ++r) a.win[r] = h->p2p_peer[r];
   a.epoch = h->p2p_epoch;
+  a.err = &h->state->comm_err;
+  a.timeout_ns = (unsigned long long)(h->comm_timeout_s * 1e9);
   // the same grid on every rank (same d; the SM count of the GPU model)
   const int grid = (int)std::min<int64_t>(std::min(h->sms, kP2PMaxBlocks), (a.n + 255) / 256);
   // with PDL the blocks start while the reduce kernel drains and wait for it
@@ -613,6 +641,8 @@ int enqueue_peer_reduce(poly_handle *h) {
   // after it exits and never compete with its waiting blocks for SMs
   return launch(h, (const void *)&k_peer_reduce, dim3(grid), dim3(256), 0, true, a);
 }
+
+int enqueue_nvls_reduce(poly_handle *h);
 
 // F at x, then either g/loss (step == false) or x_out = P_X(anchor - γ F(x)).
 int enqueue_eval(poly_handle *h, const double *x, bool loss, bool step, const double *anchor,
@@ -627,7 +657,7 @@ int enqueue_eval(poly_handle *h, const double *x, bool loss, bool step, const do
   // compact-SELL CSR on the split path, plain step, no objective, one rank:
   // K4b's epilogue does k_finalize's work (same bits) and k_fin_apply follows
   const bool fuse = h->sell16 && h->p.layout == POLY_CSR && !h->comm_path && step && !loss && !g_out &&
-                    f.split && !getenv("POLY_NO_EPI");
+                    f.split && !h->no_epi;
   h->epi = StepEpi{};
   if (fuse) {
     h->epi.on = 1;
@@ -650,7 +680,7 @@ int enqueue_eval(poly_handle *h, const double *x, bool loss, bool step, const do
   FinArgs r = f;
   r.mode = FIN_REDUCE;
   TRY(enqueue_fin(h, r));
-  TRY(h->p2p ? enqueue_peer_reduce(h) : enqueue_allreduce(h));
+  TRY(h->nv.on ? enqueue_nvls_reduce(h) : (h->p2p ? enqueue_peer_reduce(h) : enqueue_allreduce(h)));
   f.mode = step ? FIN_STEP_COMM : FIN_GRAD_COMM;
   return enqueue_fin(h, f);
 }
@@ -742,6 +772,58 @@ int sync_out(poly_handle *h) {
   CK(cudaEventRecord(h->ev_out, h->work));
   CK(cudaStreamWaitEvent(h->user, h->ev_out, 0));
   return POLY_OK;
+}
+
+// Poll the communicator for an asynchronous error (a failed peer, a network
+// error).  On one the communicator is aborted so that this rank returns
+// instead of hanging (poly.h: "a rank aborts its communicator").
+int check_comm(poly_handle *h) {
+  if (!h->comm_path) return POLY_OK;
+  if (!h->nccl) return fail(POLY_ENCCL, "the communicator was aborted by an earlier error");
+  NcclApi *api = nccl_api();
+  ncclResult_t st = ncclSuccess;
+  const ncclResult_t q = api->asyncErr(h->nccl, &st);
+  if (q != ncclSuccess || (st != ncclSuccess && st != ncclInProgress)) {
+    api->commAbort(h->nccl);
+    h->nccl = nullptr;
+    return fail(POLY_ENCCL, "NCCL asynchronous error: %s; communicator aborted",
+                api->errStr(q != ncclSuccess ? q : st));
+  }
+  return POLY_OK;
+}
+
+// Host wait for ev.  Without a communicator: cudaEventSynchronize.  With one,
+// the wait polls NCCL's asynchronous error state and gives up after
+// comm_timeout_s: the communicator is aborted (which also releases NCCL
+// kernels waiting on a dead peer) and POLY_ENCCL returned.
+int wait_event(poly_handle *h, cudaEvent_t ev) {
+  if (!h->comm_path) {
+    CK(cudaEventSynchronize(ev));
+    return POLY_OK;
+  }
+  const auto t0 = std::chrono::steady_clock::now();
+  for (;;) {
+    const cudaError_t q = cudaEventQuery(ev);
+    if (q == cudaSuccess) return POLY_OK;
+    if (q != cudaErrorNotReady) return fail(POLY_ECUDA, "stream failed: %s", cudaGetErrorString(q));
+    TRY(check_comm(h));
+    const double el = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    if (el > h->comm_timeout_s) {
+      NcclApi *api = nccl_api();
+      if (h->nccl) api->commAbort(h->nccl);
+      h->nccl = nullptr;
+      return fail(POLY_ENCCL, "no progress for %.0f s with a communicator (a peer stopped?); aborted",
+                  h->comm_timeout_s);
+    }
+    std::this_thread::sleep_for(std::chrono::microseconds(el < 0.01 ? 2 : 50));
+  }
+}
+
+// Drain the work stream (through wait_event, so a hung collective cannot
+// block the host forever).
+int sync_work(poly_handle *h) {
+  CK(cudaEventRecord(h->ev_sync, h->work));
+  return wait_event(h, h->ev_sync);
 }
 
 template <typename T>
@@ -1087,6 +1169,279 @@ int build_sell(poly_handle *h) {
 
 }  // namespace
 
+namespace {
+
+// ------------------------------------------------------------ K9-NVLS host side
+// Driver entry points through the runtime (cudaGetDriverEntryPoint), so the
+// library does not link libcuda and still loads on a CPU-only box.
+struct DrvApi {
+  bool ok = false;
+  CUresult (*mcCreate)(CUmemGenericAllocationHandle *, const CUmulticastObjectProp *) = nullptr;
+  CUresult (*mcAddDevice)(CUmemGenericAllocationHandle, CUdevice) = nullptr;
+  CUresult (*mcBindMem)(CUmemGenericAllocationHandle, size_t, CUmemGenericAllocationHandle, size_t, size_t,
+                        unsigned long long) = nullptr;
+  CUresult (*mcUnbind)(CUmemGenericAllocationHandle, CUdevice, size_t, size_t) = nullptr;
+  CUresult (*mcGranularity)(size_t *, const CUmulticastObjectProp *, CUmulticastGranularity_flags) = nullptr;
+  CUresult (*memCreate)(CUmemGenericAllocationHandle *, size_t, const CUmemAllocationProp *,
+                        unsigned long long) = nullptr;
+  CUresult (*memRelease)(CUmemGenericAllocationHandle) = nullptr;
+  CUresult (*addrReserve)(CUdeviceptr *, size_t, size_t, CUdeviceptr, unsigned long long) = nullptr;
+  CUresult (*addrFree)(CUdeviceptr, size_t) = nullptr;
+  CUresult (*memMap)(CUdeviceptr, size_t, size_t, CUmemGenericAllocationHandle, unsigned long long) = nullptr;
+  CUresult (*memUnmap)(CUdeviceptr, size_t) = nullptr;
+  CUresult (*setAccess)(CUdeviceptr, size_t, const CUmemAccessDesc *, size_t) = nullptr;
+  CUresult (*exportFd)(void *, CUmemGenericAllocationHandle, CUmemAllocationHandleType, unsigned long long) = nullptr;
+  CUresult (*importFd)(CUmemGenericAllocationHandle *, void *, CUmemAllocationHandleType) = nullptr;
+  CUresult (*devAttr)(int *, CUdevice_attribute, CUdevice) = nullptr;
+};
+
+DrvApi *drv_api() {
+  static DrvApi api;
+  static bool tried = false;
+  if (tried) return api.ok ? &api : nullptr;
+  tried = true;
+  auto get = [](const char *name, void **fn) {
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint(name, fn, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess || !*fn) {
+      cudaGetLastError();
+      return false;
+    }
+    return true;
+  };
+  api.ok = get("cuMulticastCreate", (void **)&api.mcCreate) && get("cuMulticastAddDevice", (void **)&api.mcAddDevice) &&
+           get("cuMulticastBindMem", (void **)&api.mcBindMem) && get("cuMulticastUnbind", (void **)&api.mcUnbind) &&
+           get("cuMulticastGetGranularity", (void **)&api.mcGranularity) &&
+           get("cuMemCreate", (void **)&api.memCreate) && get("cuMemRelease", (void **)&api.memRelease) &&
+           get("cuMemAddressReserve", (void **)&api.addrReserve) && get("cuMemAddressFree", (void **)&api.addrFree) &&
+           get("cuMemMap", (void **)&api.memMap) && get("cuMemUnmap", (void **)&api.memUnmap) &&
+           get("cuMemSetAccess", (void **)&api.setAccess) &&
+           get("cuMemExportToShareableHandle", (void **)&api.exportFd) &&
+           get("cuMemImportFromShareableHandle", (void **)&api.importFd) &&
+           get("cuDeviceGetAttribute", (void **)&api.devAttr);
+  return api.ok ? &api : nullptr;
+}
+
+#define DRV(call)                                                                            \
+  do {                                                                                       \
+    CUresult r_ = (call);                                                                    \
+    if (r_ != CUDA_SUCCESS) return fail(POLY_ECUDA, "%s failed: CUresult %d (%s:%d)", #call, \
+                                        (int)r_, __FILE__, __LINE__);                        \
+  } while (0)
+
+// The 64-byte descriptor rank 0 hands to every rank (poly_nvls_handle ->
+// caller's broadcast -> poly_nvls_open).
+struct NvlsDesc {
+  uint32_t magic;   // 'NVLS'
+  int32_t world;
+  uint64_t size;    // window bytes (multiple of the multicast granularity)
+  char name[48];    // abstract unix socket on which rank 0 serves the multicast fd
+};
+static_assert(sizeof(NvlsDesc) == 64, "descriptor is 64 bytes");
+constexpr uint32_t kNvlsMagic = 0x534c564eu;
+
+sockaddr_un abstract_addr(const char *name, socklen_t *len) {
+  sockaddr_un a{};
+  a.sun_family = AF_UNIX;
+  a.sun_path[0] = '\0';  // abstract namespace: nothing on the file system
+  const size_t n = strnlen(name, sizeof(a.sun_path) - 2);
+  memcpy(a.sun_path + 1, name, n);
+  *len = (socklen_t)(offsetof(sockaddr_un, sun_path) + 1 + n);
+  return a;
+}
+
+double now_s() {
+  return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+
+}  // namespace
+
+extern "C" {
+// File-descriptor exchange of poly_nvls_open (declared in poly.h): rank 0
+// listens on the abstract unix socket `name` and sends fd_in to world-1
+// connecting ranks with SCM_RIGHTS; the other ranks connect (retrying until
+// timeout_s) and receive a duplicate in *fd_out.  Rank 0's *fd_out = fd_in.
+int poly_share_fd(int32_t rank, int32_t world, const char *name, int fd_in, int *fd_out, double timeout_s) {
+  if (!name || !fd_out || world < 1 || rank < 0 || rank >= world) return fail(POLY_EINVAL, "bad arguments");
+  *fd_out = -1;
+  socklen_t len = 0;
+  const sockaddr_un addr = abstract_addr(name, &len);
+  const double t_end = now_s() + timeout_s;
+  if (rank == 0) {
+    *fd_out = fd_in;
+    if (world == 1) return POLY_OK;
+    const int ls = socket(AF_UNIX, SOCK_STREAM | SOCK_CLOEXEC, 0);
+    if (ls < 0) return fail(POLY_ECUDA, "fd exchange: socket() failed");
+    if (bind(ls, (const sockaddr *)&addr, len) != 0 || listen(ls, world) != 0) {
+      close(ls);
+      return fail(POLY_ECUDA, "fd exchange: cannot listen on @%s", name);
+    }
+    int served = 0;
+    while (served < world - 1) {
+      pollfd pf{ls, POLLIN, 0};
+      const int left_ms = (int)std::max(0.0, (t_end - now_s()) * 1e3);
+      if (left_ms == 0 || poll(&pf, 1, std::min(left_ms, 1000)) < 0) break;
+      if (!(pf.revents & POLLIN)) continue;
+      const int c = accept(ls, nullptr, nullptr);
+      if (c < 0) continue;
+      char byte = 'F';
+      iovec io{&byte, 1};
+      char ctrl[CMSG_SPACE(sizeof(int))] = {};
+      msghdr m{};
+      m.msg_iov = &io;
+      m.msg_iovlen = 1;
+      m.msg_control = ctrl;
+      m.msg_controllen = sizeof(ctrl);
+      cmsghdr *cm = CMSG_FIRSTHDR(&m);
+      cm->cmsg_level = SOL_SOCKET;
+      cm->cmsg_type = SCM_RIGHTS;
+      cm->cmsg_len = CMSG_LEN(sizeof(int));
+      memcpy(CMSG_DATA(cm), &fd_in, sizeof(int));
+      if (sendmsg(c, &m, 0) == 1) ++served;
+      close(c);
+    }
+    close(ls);
+    if (served < world - 1) return fail(POLY_ENCCL, "fd exchange: %d of %d ranks connected within %.0f s", served,
+                                        world - 1, timeout_s);
+    return POLY_OK;
+  }
+  for (;;) {
+    const int c = socket(AF_UNIX, SOCK_STREAM | SOCK_CLOEXEC, 0);
+    if (c < 0) return fail(POLY_ECUDA, "fd exchange: socket() failed");
+    if (connect(c, (const sockaddr *)&addr, len) == 0) {
+      char byte = 0;
+      iovec io{&byte, 1};
+      char ctrl[CMSG_SPACE(sizeof(int))] = {};
+      msghdr m{};
+      m.msg_iov = &io;
+      m.msg_iovlen = 1;
+      m.msg_control = ctrl;
+      m.msg_controllen = sizeof(ctrl);
+      const ssize_t r = recvmsg(c, &m, 0);
+      cmsghdr *cm = CMSG_FIRSTHDR(&m);
+      close(c);
+      if (r == 1 && cm && cm->cmsg_type == SCM_RIGHTS) {
+        memcpy(fd_out, CMSG_DATA(cm), sizeof(int));
+        return POLY_OK;
+      }
+      return fail(POLY_ENCCL, "fd exchange: no descriptor received from rank 0");
+    }
+    close(c);
+    if (now_s() > t_end) return fail(POLY_ENCCL, "fd exchange: rank 0 not reachable on @%s", name);
+    std::this_thread::sleep_for(std::chrono::milliseconds(2));
+  }
+}
+}  // extern "C"
+
+namespace {
+
+void nvls_release(poly_handle *h) {
+  DrvApi *api = drv_api();
+  auto &v = h->nv;
+  if (api) {
+    if (v.mc_mapped) api->memUnmap(v.mc_va, v.size);
+    if (v.uc_mapped) api->memUnmap(v.uc_va, v.size);
+    if (v.mc_va) api->addrFree(v.mc_va, v.size);
+    if (v.uc_va) api->addrFree(v.uc_va, v.size);
+    if (v.bound) api->mcUnbind(v.mc, h->dev, 0, v.size);
+    if (v.have_mem) api->memRelease(v.mem);
+    if (v.have_mc) api->memRelease(v.mc);
+  }
+  if (v.fd >= 0) close(v.fd);
+  if (v.listen_fd >= 0) close(v.listen_fd);
+  v = decltype(h->nv){};
+}
+
+// every rank's host: a barrier through the handle's communicator (one
+// allreduce of one double, drained) — all devices are added to the multicast
+// object before any binds, all bound before any kernel uses it
+int comm_barrier(poly_handle *h) {
+  if (!h->comm_path || h->p.world == 1) return POLY_OK;
+  NcclApi *api = nccl_api();
+  if (!h->nccl) return fail(POLY_ENCCL, "no communicator");
+  const ncclResult_t r = api->allReduce(h->comm, h->comm, 1, ncclFloat64, ncclSum, h->nccl, h->work);
+  if (r != ncclSuccess) return fail(POLY_ENCCL, "barrier: %s", api->errStr(r));
+  return sync_work(h);
+}
+
+// K9-NVLS: the cross-rank sum of one F evaluation (csrc/nvls.cuh)
+int enqueue_nvls_reduce(poly_handle *h) {
+  ProfScope ps(h, 2);
+  NvlsArgs a{};
+  a.comm = h->comm;
+  a.n = h->p.d + 1;
+  a.world = (int32_t)h->p.world;
+  a.rank = (int32_t)h->p.rank;
+  a.uc = (char *)h->nv.uc_va;
+  a.mc = (char *)h->nv.mc_va;
+  a.epoch = h->nv.epoch;
+  a.err = &h->state->comm_err;
+  a.timeout_ns = (unsigned long long)(h->comm_timeout_s * 1e9);
+  const int grid = (int)std::min<int64_t>(std::min(h->sms, kNvlsMaxBlocks), (a.n + 255) / 256);
+  return launch(h, (const void *)&k_nvls_reduce, dim3(grid), dim3(256), 0, true, a);
+}
+
+}  // namespace
+
+namespace {
+
+constexpr int kPollEvery = 4;          // poll the device state every 4 replays (32 iterations)
+
+// Enqueue a copy of the solver state to pinned host memory behind
+// ev_poll[k & 1] and check the copy made at the previous poll (one poll
+// behind, so the device always has work queued): a non-finite iterate
+// is then seen within ~2 polls instead of after all T
+// iterations, and with a communicator NCCL's async error state is checked.
+int poll_state(poly_handle *h, int k) {
+  if (k >= 1) TRY(wait_event(h, h->ev_poll[(k - 1) & 1]));
+  TRY(check_comm(h));
+  if (h->hstate->bad != 0 || h->hstate->comm_err != 0) return POLY_OK;
+  CK(cudaMemcpyAsync(h->hstate, h->state, sizeof(SolveState), cudaMemcpyDeviceToHost, h->work));
+  CK(cudaEventRecord(h->ev_poll[k & 1], h->work));
+  return POLY_OK;
+}
+
+// Replay the U-iteration graph (and the 1-iteration graph for the tail) for
+// T iterations, polling every kPollEvery replays; a non-finite iterate or a
+// K9 wait timeout stops further launches.
+int replay_solve(poly_handle *h, cudaGraphExec_t gU, cudaGraphExec_t g1, int T) {
+  const int U = h->graph_U;
+  int done = 0, replays = 0, polls = 0;
+  while (done < T) {
+    const int step = (T - done >= U) ? U : 1;
+    CK(cudaGraphLaunch(step == U ? gU : g1, h->work));
+    done += step;
+    if (++replays % kPollEvery == 0 && done < T) {
+      TRY(poll_state(h, polls++));
+      if (h->hstate->bad != 0 || h->hstate->comm_err != 0) break;
+    }
+  }
+  return POLY_OK;
+}
+
+void collect_profile(poly_handle *h) {
+  double sum[3] = {0, 0, 0};
+  int cnt[3] = {0, 0, 0};
+  const bool dbg = getenv("POLY_PROF_DEBUG") != nullptr;
+  for (auto &r : h->recs) {
+    float ms = 0.f;
+    const cudaError_t e = cudaEventElapsedTime(&ms, r.a, r.b);
+    if (dbg) fprintf(stderr, "prof rec kind %d: %s %.4f ms\n", r.kind, cudaGetErrorString(e), ms);
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      continue;
+    }
+    sum[r.kind] += ms;
+    cnt[r.kind]++;
+  }
+  for (int k = 0; k < 3; ++k) h->ktimes[k] = cnt[k] ? sum[k] / cnt[k] : 0.0;
+  h->ktimes[3] = cnt[0];
+  h->ktimes[4] = cnt[0] + cnt[1];
+  h->prof = false;
+}
+
+}  // namespace
+
 extern "C" {
 
 
@@ -1148,12 +1503,125 @@ int poly_p2p_open(poly_handle *h, const void *handles) {
   return POLY_OK;
 }
 
+int poly_nvls_handle(poly_handle *h, void *out64) {
+  if (!h || !out64) return fail(POLY_EINVAL, "NULL handle or out");
+  if (!(h->p.flags & POLY_FLAG_NVLS)) return fail(POLY_EINVAL, "handle was not created with POLY_FLAG_NVLS");
+  if (h->nv.have_mc) return fail(POLY_EINVAL, "poly_nvls_handle called twice");
+  NvlsDesc dsc{};
+  dsc.magic = kNvlsMagic;
+  dsc.world = (int32_t)h->p.world;
+  if (h->p.rank == 0) {
+    DrvApi *api = drv_api();
+    if (!api) return fail(POLY_EUNSUPPORTED, "NVLS: driver multicast entry points unavailable");
+    int mcs = 0;
+    if (api->devAttr(&mcs, CU_DEVICE_ATTRIBUTE_MULTICAST_SUPPORTED, h->dev) != CUDA_SUCCESS || !mcs)
+      return fail(POLY_EUNSUPPORTED, "NVLS: the device does not support multicast objects");
+    CUmulticastObjectProp mp{};
+    mp.numDevices = (unsigned)h->p.world;
+    mp.handleTypes = CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR;
+    mp.size = kNvlsHdr + (size_t)4 * (h->p.d + 1) * 8;
+    size_t gran = 0;
+    DRV(api->mcGranularity(&gran, &mp, CU_MULTICAST_GRANULARITY_RECOMMENDED));
+    mp.size = (mp.size + gran - 1) / gran * gran;
+    DRV(api->mcCreate(&h->nv.mc, &mp));
+    h->nv.have_mc = true;
+    h->nv.size = mp.size;
+    int fd = -1;
+    DRV(api->exportFd(&fd, h->nv.mc, CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR, 0));
+    h->nv.fd = fd;
+    dsc.size = mp.size;
+    static int counter = 0;
+    snprintf(dsc.name, sizeof(dsc.name), "poly-nvls-%d-%d", (int)getpid(), ++counter);
+  }
+  memcpy(out64, &dsc, 64);
+  return POLY_OK;
+}
+
+int poly_nvls_open(poly_handle *h, const void *desc64) {
+  if (!h || !desc64) return fail(POLY_EINVAL, "NULL handle or descriptor");
+  if (!(h->p.flags & POLY_FLAG_NVLS)) return fail(POLY_EINVAL, "handle was not created with POLY_FLAG_NVLS");
+  if (h->nv.on) return fail(POLY_EINVAL, "poly_nvls_open called twice");
+  NvlsDesc dsc;
+  memcpy(&dsc, desc64, 64);
+  if (dsc.magic != kNvlsMagic || dsc.world != h->p.world || dsc.size == 0)
+    return fail(POLY_EINVAL, "NVLS: not a descriptor of this communicator (poly_nvls_handle on rank 0)");
+  if (h->p.rank == 0 && !h->nv.have_mc) return fail(POLY_EINVAL, "NVLS: rank 0 must call poly_nvls_handle first");
+  DrvApi *api = drv_api();
+  if (!api) return fail(POLY_EUNSUPPORTED, "NVLS: driver multicast entry points unavailable");
+  auto bail = [&](int rc) {
+    nvls_release(h);
+    return rc;
+  };
+  int rc = POLY_OK;
+  // 1. every rank obtains the multicast object (rank 0 serves its fd)
+  int fd = -1;
+  if ((rc = poly_share_fd((int32_t)h->p.rank, (int32_t)h->p.world, dsc.name, h->nv.fd, &fd,
+                          std::min(h->comm_timeout_s, 120.0))) != POLY_OK)
+    return bail(rc);
+  if (h->p.rank != 0) {
+    h->nv.fd = fd;
+    h->nv.size = dsc.size;
+    CUresult r = api->importFd(&h->nv.mc, (void *)(intptr_t)fd, CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR);
+    if (r != CUDA_SUCCESS) return bail(fail(POLY_ECUDA, "NVLS: import of the multicast object failed (%d)", (int)r));
+    h->nv.have_mc = true;
+  }
+  CUresult r = api->mcAddDevice(h->nv.mc, h->dev);
+  if (r != CUDA_SUCCESS) return bail(fail(POLY_ECUDA, "NVLS: cuMulticastAddDevice failed (%d)", (int)r));
+  if ((rc = comm_barrier(h)) != POLY_OK) return bail(rc);
+  // 2. this rank's physical copy, bound to the object; unicast and multicast views
+  CUmemAllocationProp ap{};
+  ap.type = CU_MEM_ALLOCATION_TYPE_PINNED;
+  ap.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
+  ap.location.id = h->dev;
+  ap.requestedHandleTypes = CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR;
+  const size_t sz = h->nv.size;
+  if ((r = api->memCreate(&h->nv.mem, sz, &ap, 0)) != CUDA_SUCCESS)
+    return bail(fail(POLY_ENOMEM, "NVLS: cuMemCreate(%zu) failed (%d)", sz, (int)r));
+  h->nv.have_mem = true;
+  if ((r = api->mcBindMem(h->nv.mc, 0, h->nv.mem, 0, sz, 0)) != CUDA_SUCCESS)
+    return bail(fail(POLY_ECUDA, "NVLS: cuMulticastBindMem failed (%d)", (int)r));
+  h->nv.bound = true;
+  CUmemAccessDesc ad{};
+  ad.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
+  ad.location.id = h->dev;
+  ad.flags = CU_MEM_ACCESS_FLAGS_PROT_READWRITE;
+  if ((r = api->addrReserve(&h->nv.uc_va, sz, sz, 0, 0)) != CUDA_SUCCESS ||
+      (r = api->memMap(h->nv.uc_va, sz, 0, h->nv.mem, 0)) != CUDA_SUCCESS)
+    return bail(fail(POLY_ECUDA, "NVLS: unicast mapping failed (%d)", (int)r));
+  h->nv.uc_mapped = true;
+  if ((r = api->setAccess(h->nv.uc_va, sz, &ad, 1)) != CUDA_SUCCESS ||
+      (r = api->addrReserve(&h->nv.mc_va, sz, sz, 0, 0)) != CUDA_SUCCESS ||
+      (r = api->memMap(h->nv.mc_va, sz, 0, h->nv.mc, 0)) != CUDA_SUCCESS)
+    return bail(fail(POLY_ECUDA, "NVLS: multicast mapping failed (%d)", (int)r));
+  h->nv.mc_mapped = true;
+  if ((r = api->setAccess(h->nv.mc_va, sz, &ad, 1)) != CUDA_SUCCESS)
+    return bail(fail(POLY_ECUDA, "NVLS: multicast access failed (%d)", (int)r));
+  if (!h->nv.epoch && (rc = dev_alloc(h, &h->nv.epoch, (size_t)kNvlsMaxBlocks)) != POLY_OK) return bail(rc);
+  if (cudaMemsetAsync((void *)h->nv.uc_va, 0, sz, h->work) != cudaSuccess ||
+      cudaMemsetAsync(h->nv.epoch, 0, 8 * (size_t)kNvlsMaxBlocks, h->work) != cudaSuccess)
+    return bail(fail(POLY_ECUDA, "NVLS: window reset failed"));
+  if ((rc = sync_work(h)) != POLY_OK || (rc = comm_barrier(h)) != POLY_OK) return bail(rc);
+  // graphs captured so far hold the NCCL path
+  for (auto &a : h->gexec)
+    for (auto &g : a)
+      if (g) cudaGraphExecDestroy(g), g = nullptr;
+  for (auto &a : h->gexec_ex)
+    for (auto &b : a)
+      for (auto &g : b)
+        if (g) cudaGraphExecDestroy(g), g = nullptr;
+  h->nv.on = true;
+  return POLY_OK;
+}
+
 void poly_free(poly_handle *h) {
   if (!h) return;
+  // drain first: a K9 launch may still be reading the peers' windows (the
+  // caller must also barrier across ranks before freeing, poly.h)
+  if (h->work) cudaStreamSynchronize(h->work);
   if (h->p2p)
     for (int r = 0; r < (int)h->p.world; ++r)
       if (r != h->p.rank && h->p2p_peer[r]) cudaIpcCloseMemHandle(h->p2p_peer[r]);
-  if (h->work) cudaStreamSynchronize(h->work);
+  nvls_release(h);
   for (auto &a : h->gexec)
     for (auto &g : a)
       if (g) cudaGraphExecDestroy(g);
@@ -1170,6 +1638,8 @@ void poly_free(poly_handle *h) {
   for (cudaEvent_t e : h->evpool) cudaEventDestroy(e);
   if (h->ev_in) cudaEventDestroy(h->ev_in);
   if (h->ev_out) cudaEventDestroy(h->ev_out);
+  for (cudaEvent_t e : {h->ev_poll[0], h->ev_poll[1], h->ev_sync})
+    if (e) cudaEventDestroy(e);
   if (h->work) cudaStreamDestroy(h->work);
   delete h;
 }
@@ -1201,8 +1671,16 @@ int poly_init(const poly_problem *pin, poly_handle **out) {
   h->use_graph = !(p.flags & POLY_FLAG_NO_GRAPH);
   if (cudaStreamCreateWithFlags(&h->work, cudaStreamNonBlocking) != cudaSuccess ||
       cudaEventCreateWithFlags(&h->ev_in, cudaEventDisableTiming) != cudaSuccess ||
-      cudaEventCreateWithFlags(&h->ev_out, cudaEventDisableTiming) != cudaSuccess)
+      cudaEventCreateWithFlags(&h->ev_out, cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&h->ev_poll[0], cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&h->ev_poll[1], cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&h->ev_sync, cudaEventDisableTiming) != cudaSuccess)
     return bail(fail(POLY_ECUDA, "stream/event creation failed"));
+  h->no_epi = getenv("POLY_NO_EPI") != nullptr;
+  if (const char *t = getenv("POLY_COMM_TIMEOUT_S")) {
+    const double v = atof(t);
+    if (v > 0.0) h->comm_timeout_s = v;
+  }
   if ((rc = sync_in(h)) != POLY_OK) return bail(rc);
 
   // host inputs -> library-owned device copies
@@ -1404,6 +1882,10 @@ int poly_init(const poly_problem *pin, poly_handle **out) {
   }
 
   h->comm_path = p.world > 1 || (p.flags & POLY_FLAG_COMM);
+  if ((p.flags & POLY_FLAG_NVLS) && !h->comm_path)
+    return bail(fail(POLY_EINVAL, "POLY_FLAG_NVLS needs world > 1 or POLY_FLAG_COMM"));
+  if ((p.flags & POLY_FLAG_NVLS) && (p.flags & POLY_FLAG_P2P))
+    return bail(fail(POLY_EINVAL, "POLY_FLAG_NVLS and POLY_FLAG_P2P are exclusive"));
   if (p.flags & POLY_FLAG_P2P) {
     if (!h->comm_path) return bail(fail(POLY_EINVAL, "POLY_FLAG_P2P needs world > 1 or POLY_FLAG_COMM"));
     if (p.world > kP2PMaxRanks) return bail(fail(POLY_EUNSUPPORTED, "POLY_FLAG_P2P: world > %d", kP2PMaxRanks));
@@ -1436,6 +1918,7 @@ int poly_init(const poly_problem *pin, poly_handle **out) {
 int poly_loss_grad(poly_handle *h, const double *x, double *g, double *loss) {
   if (!h || !x) return fail(POLY_EINVAL, "NULL handle or x");
   TRY(sync_in(h));
+  TRY(check_comm(h));
   const double *xd = x;
   if (!is_device_ptr(x)) {
     CK(cudaMemcpyAsync(h->xin, x, h->p.d * 8, cudaMemcpyHostToDevice, h->work));
@@ -1448,10 +1931,10 @@ int poly_loss_grad(poly_handle *h, const double *x, double *g, double *loss) {
   if (g && !g_dev) CK(cudaMemcpyAsync(g, h->gbuf, h->p.d * 8, cudaMemcpyDeviceToHost, h->work));
   if (loss) {
     CK(cudaMemcpyAsync(&h->hstate->loss_cur, &h->state->loss_cur, 8, cudaMemcpyDeviceToHost, h->work));
-    CK(cudaStreamSynchronize(h->work));
+    TRY(sync_work(h));
     *loss = h->hstate->loss_cur;
   } else if (g && !g_dev) {
-    CK(cudaStreamSynchronize(h->work));
+    TRY(sync_work(h));
   }
   TRY(sync_out(h));
   CK(cudaGetLastError());
@@ -1484,7 +1967,12 @@ int poly_solve_ex(poly_handle *h, const poly_solve_opts *o, double *x, double *x
             cudaGraphExecDestroy(g);
             g = nullptr;
           }
+      double *old = h->hist;
       TRY(dev_alloc(h, &h->hist, (size_t)cap * d));
+      if (old) {  // no graph refers to it any more; the stream must drain first
+        TRY(sync_work(h));
+        dev_release(h, old);
+      }
       if (!h->Ssum) {
         TRY(dev_alloc(h, &h->Ssum, (size_t)d));
         TRY(dev_alloc(h, &h->xbar, (size_t)d));
@@ -1516,6 +2004,7 @@ int poly_solve_ex(poly_handle *h, const poly_solve_opts *o, double *x, double *x
   const int T = o->T_max;
   const bool poll = avg && o->tol > 0.0;
   int done = 0;
+  auto halted = [&]() { return h->hstate->bad != 0 || h->hstate->comm_err != 0 || (poll && h->hstate->stopped); };
   if (h->use_graph && !h->prof) {
     const int U = h->graph_U;
     cudaGraphExec_t *gU = &h->gexec_ex[method][avg ? 1 : 0][1];
@@ -1524,44 +2013,26 @@ int poly_solve_ex(poly_handle *h, const poly_solve_opts *o, double *x, double *x
     if (T >= U && !*gU) rc = build_graph_ex(h, method, avg, U, gU);
     if (rc == POLY_OK && (T % U) && !*g1) rc = build_graph_ex(h, method, avg, 1, g1);
     if (rc != POLY_OK) return rc;
-    SolveState *snap = h->hstate;  // pinned; copied after every launch, read one launch behind
-    cudaEvent_t ev[2] = {nullptr, nullptr};
-    if (poll)
-      for (auto &e : ev) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-    int launches = 0;
-    bool stop = false;
-    while (done < T && !stop) {
+    // the stop rule is polled after every replay (one replay behind), the
+    // non-finite / K9 flags every kPollEvery replays otherwise
+    int replays = 0, polls = 0;
+    while (done < T && !halted()) {
       const int step = (T - done >= U) ? U : 1;
       CK(cudaGraphLaunch(step == U ? *gU : *g1, h->work));
       done += step;
-      if (poll) {
-        if (launches >= 1) {
-          CK(cudaEventSynchronize(ev[(launches - 1) & 1]));
-          if (snap->stopped) stop = true;
-        }
-        CK(cudaMemcpyAsync(snap, h->state, sizeof(SolveState), cudaMemcpyDeviceToHost, h->work));
-        CK(cudaEventRecord(ev[launches & 1], h->work));
-        ++launches;
-      }
+      if ((poll || ++replays % kPollEvery == 0) && done < T) TRY(poll_state(h, polls++));
     }
-    CK(cudaStreamSynchronize(h->work));
-    for (auto &e : ev)
-      if (e) cudaEventDestroy(e);
   } else {
-    for (; done < T; ++done) {
+    for (; done < T && !halted(); ++done) {
       TRY(enqueue_iteration_ex(h, method, avg));
-      if (poll && (done % 64) == 63) {
+      if (!h->prof && (done % 64) == 63) {
         CK(cudaMemcpyAsync(h->hstate, h->state, sizeof(SolveState), cudaMemcpyDeviceToHost, h->work));
-        CK(cudaStreamSynchronize(h->work));
-        if (h->hstate->stopped) {
-          ++done;
-          break;
-        }
+        TRY(sync_work(h));
       }
     }
   }
   CK(cudaMemcpyAsync(h->hstate, h->state, sizeof(SolveState), cudaMemcpyDeviceToHost, h->work));
-  CK(cudaStreamSynchronize(h->work));
+  TRY(sync_work(h));
   const SolveState fin = *h->hstate;
   const bool stopped = avg && fin.stopped;
   const double *last = stopped ? h->hist + (size_t)(fin.k_stop % h->avg_cap) * d : h->xa;
@@ -1571,24 +2042,16 @@ int poly_solve_ex(poly_handle *h, const poly_solve_opts *o, double *x, double *x
   if (x_last)
     CK(cudaMemcpyAsync(x_last, last, (size_t)d * 8,
                        is_device_ptr(x_last) ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, h->work));
-  CK(cudaStreamSynchronize(h->work));
-  if (h->prof) {
-    double sum[3] = {0, 0, 0};
-    int cnt[3] = {0, 0, 0};
-    for (auto &r : h->recs) {
-      float ms = 0.f;
-      cudaEventElapsedTime(&ms, r.a, r.b);
-      sum[r.kind] += ms;
-      cnt[r.kind]++;
-    }
-    for (int k = 0; k < 3; ++k) h->ktimes[k] = cnt[k] ? sum[k] / cnt[k] : 0.0;
-    h->ktimes[3] = cnt[0];
-    h->ktimes[4] = cnt[0] + cnt[1];
-    h->prof = false;
-  }
+  TRY(sync_work(h));
+  if (h->prof) collect_profile(h);
   TRY(sync_out(h));
   CK(cudaGetLastError());
   const int per = method == POLY_METHOD_EXTRAGRADIENT ? 2 : 1;
+  if (fin.comm_err) {
+    if (h->nccl) nccl_api()->commAbort(h->nccl);
+    h->nccl = nullptr;
+    return fail(POLY_ENCCL, "peer reduce: a peer did not publish within the wait bound; communicator aborted");
+  }
   if (info) {
     info->stopped = stopped ? 1 : 0;
     info->iters = stopped ? fin.k_stop - 1 : done;
@@ -1609,6 +2072,7 @@ int poly_solve(poly_handle *h, double *x, int T, double gamma, uint32_t flags, d
   if (!(gamma > 0.0) || !std::isfinite(gamma)) return fail(POLY_EINVAL, "gamma must be > 0");
   if (bad_iter) *bad_iter = 0;
   TRY(sync_in(h));
+  TRY(check_comm(h));
   const bool x_dev = is_device_ptr(x);
   CK(cudaMemcpyAsync(h->xa, x, h->p.d * 8, x_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice,
                      h->work));
@@ -1616,6 +2080,12 @@ int poly_solve(poly_handle *h, double *x, int T, double gamma, uint32_t flags, d
   if (want_trace && h->trace_cap < 2 * T) {
     double *nt = nullptr;
     TRY(dev_alloc(h, &nt, (size_t)2 * T));
+    // graphs hold the old trace pointer only through SolveState (read on the
+    // device), so the old buffer can go once the stream has drained
+    if (h->trace) {
+      TRY(sync_work(h));
+      dev_release(h, h->trace);
+    }
     h->trace = nt;
     h->trace_cap = 2 * T;
   }
@@ -1636,7 +2106,7 @@ int poly_solve(poly_handle *h, double *x, int T, double gamma, uint32_t flags, d
       if (want_trace)
         CK(cudaMemcpyAsync(trace, h->trace, (size_t)2 * T * 8, cudaMemcpyDeviceToHost, h->work));
       CK(cudaMemcpyAsync(h->hstate, h->state, sizeof(SolveState), cudaMemcpyDeviceToHost, h->work));
-      CK(cudaStreamSynchronize(h->work));
+      TRY(sync_work(h));
       TRY(sync_out(h));
       CK(cudaGetLastError());
       if (h->hstate->bad != 0) {
@@ -1660,10 +2130,9 @@ int poly_solve(poly_handle *h, double *x, int T, double gamma, uint32_t flags, d
     TRY(enqueue_fin(h, f));
   }
   const bool loss = want_trace;
+  int rc = POLY_OK;
   if (h->use_graph && !h->prof && T > 0) {
-    const int U = std::min(h->graph_U, T);
     int li = loss ? 1 : 0;
-    int rc = POLY_OK;
     // both graphs (U iterations and 1) are built and uploaded at the first
     // solve, whatever its T, so that a short warm-up call prepares a long one
     if (!h->gexec[li][1]) rc = build_graph(h, loss, h->graph_U, &h->gexec[li][1]);
@@ -1675,34 +2144,32 @@ int poly_solve(poly_handle *h, double *x, int T, double gamma, uint32_t flags, d
       if (!h->gexec[li][1]) rc = build_graph(h, loss, h->graph_U, &h->gexec[li][1]);
       if (rc == POLY_OK && !h->gexec[li][0]) rc = build_graph(h, loss, 1, &h->gexec[li][0]);
     }
-    if (rc != POLY_OK) return rc;
-    (void)U;
-    for (int t = 0; t + h->graph_U <= T; t += h->graph_U) CK(cudaGraphLaunch(h->gexec[li][1], h->work));
-    for (int t = 0; t < T % h->graph_U; ++t) CK(cudaGraphLaunch(h->gexec[li][0], h->work));
+    if (rc == POLY_OK) rc = replay_solve(h, h->gexec[li][1], h->gexec[li][0], T);
   } else {
-    for (int t = 0; t < T; ++t) TRY(enqueue_iteration(h, loss));
+    for (int t = 0; t < T && rc == POLY_OK; ++t) {
+      rc = enqueue_iteration(h, loss);
+      if (rc == POLY_OK && !h->prof && (t % kPollEvery) == kPollEvery - 1) rc = poll_state(h, t / kPollEvery);
+      if (rc == POLY_OK && h->hstate->bad) break;
+    }
+  }
+  if (rc != POLY_OK) {
+    h->prof = false;
+    sync_work(h);
+    return rc;
   }
   CK(cudaMemcpyAsync(x, h->xa, h->p.d * 8, x_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost,
                      h->work));
   if (want_trace) CK(cudaMemcpyAsync(trace, h->trace, (size_t)2 * T * 8, cudaMemcpyDeviceToHost, h->work));
   CK(cudaMemcpyAsync(h->hstate, h->state, sizeof(SolveState), cudaMemcpyDeviceToHost, h->work));
-  CK(cudaStreamSynchronize(h->work));
-  if (h->prof) {
-    double sum[3] = {0, 0, 0};
-    int cnt[3] = {0, 0, 0};
-    for (auto &r : h->recs) {
-      float ms = 0.f;
-      cudaEventElapsedTime(&ms, r.a, r.b);
-      sum[r.kind] += ms;
-      cnt[r.kind]++;
-    }
-    for (int k = 0; k < 3; ++k) h->ktimes[k] = cnt[k] ? sum[k] / cnt[k] : 0.0;
-    h->ktimes[3] = cnt[0];
-    h->ktimes[4] = cnt[0] + cnt[1];
-    h->prof = false;
-  }
+  TRY(sync_work(h));
+  if (h->prof) collect_profile(h);
   TRY(sync_out(h));
   CK(cudaGetLastError());
+  if (h->hstate->comm_err) {
+    if (h->nccl) nccl_api()->commAbort(h->nccl);
+    h->nccl = nullptr;
+    return fail(POLY_ENCCL, "peer reduce: a peer did not publish within the wait bound; communicator aborted");
+  }
   if (h->hstate->bad != 0) {
     const int b = h->hstate->bad;
     if (bad_iter) *bad_iter = b > 0 ? (b + 1) / 2 : 0;
@@ -1843,14 +2310,23 @@ int poly_kernel_times(poly_handle *h, double *out, int32_t nout) {
 }
 
 int poly_describe(poly_handle *h, int64_t *out, int32_t nout) {
-  if (!h || !out || nout < 0 || nout > 6) return fail(POLY_EINVAL, "bad arguments");
-  int64_t v[6];
+  if (!h || !out || nout < 0 || nout > 12) return fail(POLY_EINVAL, "bad arguments");
+  int64_t v[12] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+  if (h->nccl) {
+    int c = 0;
+    if (nccl_api()->count(h->nccl, &c) == ncclSuccess) v[10] = c;
+  }
+  v[11] = h->nv.on ? 2 : (h->p2p ? 1 : 0);
   if (h->p.layout == POLY_DENSE) {
     v[0] = h->k1_grid;
     v[1] = h->k1_threads;
     v[2] = h->dv->RPS;
     v[3] = h->k1_stages;
     v[4] = (int64_t)h->k1_smem;
+    v[6] = h->dv->V;     // K1 template <T, V, WPR, NW, RPS, LOSS, FULL>
+    v[7] = h->dv->WPR;
+    v[8] = h->dv->NW;
+    v[9] = h->full;
   } else {
     v[0] = h->k4_grid;   // K4f blocks (32-row slices); K4b: one block per 32-column slice
     v[1] = 128;

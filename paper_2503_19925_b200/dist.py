@@ -30,7 +30,7 @@ def shard(cfg, rank: int, world: int, strong: bool):
     larger (rows are keyed by global index, so the global problem is the same
     recipe with n*world rows)."""
     if world == 1:
-        return cfg, 0, cfg.n, "weak"
+        return cfg, 0, cfg.n, "strong" if strong else "weak"
     if strong:
         a, b = row_block(cfg.n, rank, world)
         return cfg, a, b - a, "strong"

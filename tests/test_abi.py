@@ -131,7 +131,7 @@ def test_reparameterize_validation(built):
 
 def test_abi_version_and_null_handle(built):
     import paper_2503_19925_b200 as P
-    assert P.poly_abi_version() == 4
+    assert P.poly_abi_version() == 5
     assert P.lib().poly_loss_grad(None, None, None, None) == P.POLY_EINVAL
     assert P.lib().poly_solve_ex(None, None, None, None, None) == P.POLY_EINVAL
     assert P.lib().poly_solve(None, None, 1, 1.0, 0, None, None) == P.POLY_EINVAL

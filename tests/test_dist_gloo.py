@@ -136,3 +136,55 @@ def test_gloo_world2_sharded_oracle_matches_full():
         assert o["max"] == 2.0 and o["sum"] == 30.0
         assert o["id"] == b"\x07" * 128
         assert o["handles"] == b"\x01" * 64 + b"\x02" * 64
+
+
+def _fd_worker(rank, world, port, name, path, q):
+    """poly_share_fd, the same-node hand-off poly_nvls_open uses for the
+    multicast object's descriptor: rank 0 shares an open file, the other ranks
+    read the shared content through the descriptor they receive."""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank),
+                      WORLD_SIZE=str(world))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import paper_2503_19925_b200 as P
+        fd = os.open(path, os.O_RDONLY) if rank == 0 else -1
+        got = P.poly_share_fd(rank, world, name, fd, timeout_s=30.0)
+        os.lseek(got, 0, os.SEEK_SET)
+        data = os.read(got, 64)
+        if rank != 0:
+            os.close(got)
+        dist.barrier()
+        q.put((rank, data.decode()))
+    except Exception as e:  # pragma: no cover
+        q.put((rank, repr(e)))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_share_fd_world(tmp_path, world):
+    path = tmp_path / "payload.txt"
+    path.write_text("multicast-object")
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    name = f"poly-test-{os.getpid()}-{world}"
+    ps = [ctx.Process(target=_fd_worker, args=(r, world, PORTS[world], name,
+                                               str(path), q)) for r in range(world)]
+    for p in ps:
+        p.start()
+    res = dict(q.get(timeout=120) for _ in range(world))
+    for p in ps:
+        p.join(timeout=60)
+    assert all(v == "multicast-object" for v in res.values()), res
+
+
+PORTS = {2: _free_port(), 3: _free_port()}
+
+
+def test_share_fd_timeout():
+    """A rank whose peer never shows up returns POLY_ENCCL after the timeout
+    instead of blocking (the 'abort instead of hang' rule)."""
+    import paper_2503_19925_b200 as P
+    with pytest.raises(P.PolyError) as ei:
+        P.poly_share_fd(1, 2, f"poly-nobody-{os.getpid()}", -1, timeout_s=0.3)
+    assert ei.value.code == P.POLY_ENCCL

@@ -181,20 +181,6 @@ def test_c2_full_size_properties(c2_gpu):
     assert rel(g, fbar) <= 3 * 1.1 * math.sqrt(cfg.d / cfg.n)
 
 
-def test_c2_reduced_solve_parity():
-    """C2 recipe on its first 20000 rows (own problem, n = 20000), T = 200."""
-    cfg = G.scaled(G.C2, 20_000)
-    W = _W()
-    wg = W.build(cfg)
-    wo = OW.build(cfg)
-    prob = wo["problem"]
-    gam, _ = OW.step_size(prob, wo["s"], wo["mu"], cfg.I_bar)
-    x_ref, _, _ = prob.solve(cfg.T, gam)
-    x = torch.zeros(cfg.d, dtype=torch.float64, device="cuda")
-    W.make_poly(wg).solve(x, cfg.T, gam)
-    assert rel(x.cpu().numpy(), x_ref) <= 1e-3
-
-
 # ------------------------------------------------------------------ C3
 def test_c3_reparam_rows_and_parity():
     cfg = G.C3
@@ -253,14 +239,17 @@ def test_c4_full_size_parity(c4):
 
 
 def test_c4_solve_parity(c4):
+    """C4 (CT CSR, BASELINE configs[3]) at its own T = 100 (reading R14) on
+    the compact-SELL path the bench runs: final iterate within 1e-3."""
     wg, wo = c4
     prob = wo["problem"]
     lam, _ = prob.lambda_max(max_it=30, tol=1e-6)
     gam = 1.0 / (4.0 * G.C4.I_bar * lam * float(np.dot(wo["s"], wo["mu"])))
-    x_ref, _, _ = prob.solve(20, gam)
+    x_ref, _, bad = prob.solve(G.C4.T, gam)
+    assert bad == 0
     x = torch.zeros(G.C4.d, dtype=torch.float64, device="cuda")
-    _W().make_poly(wg).solve(x, 20, gam)
-    assert rel(x.cpu().numpy(), x_ref) <= 1e-3
+    _W().make_poly(wg).solve(x, G.C4.T, gam)
+    assert rel(x.cpu().numpy(), x_ref) <= 1e-3, rel(x.cpu().numpy(), x_ref)
     assert x.min().item() >= 0.0 and x.norm().item() <= wo["R"] * (1 + 1e-12)
 
 
@@ -416,6 +405,31 @@ def test_nonfinite_is_reported():
     assert ei.value.code == P.POLY_ENONFINITE
 
 
+@pytest.mark.parametrize("ex", [False, True])
+def test_nonfinite_stops_early(ex):
+    """SPEC.md:320 / SURVEY §3.3: the non-finite flag is polled every few graph
+    replays, so a diverging solve of a million iterations returns within a
+    few replays with the first bad iteration, instead of running to T."""
+    import re
+    import time
+    P = _P()
+    pb = _rand_problem(20_000, 256, seed=4)
+    p, _ = _both(pb, set=G.SET_NONE)
+    p.solve(torch.zeros(256, dtype=torch.float64, device="cuda"), 16, 1e-6)   # graphs built first
+    x = torch.full((256,), 1e150, dtype=torch.float64, device="cuda")   # finite norm; the step overflows
+    t0 = time.perf_counter()
+    with pytest.raises(P.PolyError) as ei:
+        if ex:
+            p.solve_ex(x, 1_000_000, 1e300)
+        else:
+            p.solve(x, 1_000_000, 1e300)
+    dt = time.perf_counter() - t0
+    assert ei.value.code == P.POLY_ENONFINITE
+    bad = int(re.search(r"bad_iter=(\d+)", str(ei.value)).group(1))
+    assert 1 <= bad <= 2, str(ei.value)
+    assert dt < 2.0, dt                    # the full run would take ~20 s
+
+
 def test_negative_counts_rejected():
     P = _P()
     A = torch.zeros((4, 4), dtype=torch.float32, device="cuda")
@@ -527,6 +541,53 @@ def test_peer_reduce_single_rank(kind):
         W.make_poly(w, flags=P.POLY_FLAG_P2P)
 
 
+@pytest.mark.parametrize("kind", ["dense", "csr"])
+def test_nvls_reduce_single_rank(kind):
+    """K9-NVLS (POLY_FLAG_NVLS + poly_nvls_open): the cross-rank sum through
+    an NVLink multicast object — multimem.ld_reduce in the switch, broadcast by
+    multimem.st, multimem.red barriers.  On one rank the switch sums one copy:
+    the same bits as the NCCL path, and the oracle's F (Eq. operator,
+    PAPER.md:895) and EXACT iterates (Eq. extragrad-method, :915-923)."""
+    P = _P()
+    W = _W()
+    cfg = G.scaled(G.C2, 20_000) if kind == "dense" else G.C4
+    w = W.build(cfg)
+    wo = OW.build(cfg) if kind == "csr" else OW.build(cfg, rows=np.arange(cfg.n),
+                                                        A=w["A"][:, :cfg.d].cpu().numpy())
+    p1 = W.make_poly(w, flags=P.POLY_FLAG_COMM, nccl_id=P.poly_nccl_unique_id())
+    p3 = W.make_poly(w, flags=P.POLY_FLAG_COMM | P.POLY_FLAG_NVLS, nccl_id=P.poly_nccl_unique_id())
+    try:
+        p3.nvls_setup()
+    except P.PolyError as e:
+        if e.code in (P.POLY_EUNSUPPORTED, P.POLY_ECUDA):
+            pytest.skip(f"no NVLink multicast on this box: {e}")
+        raise
+    assert p3.describe()["k9"] == 2
+    with pytest.raises(P.PolyError):
+        p3.nvls_setup()   # once per handle
+    x = 0.5 * wo["x_star"]
+    g_ref, l_ref = wo["problem"].F(x)
+    xt = torch.tensor(x, device="cuda")
+    for _ in range(3):   # evaluation parities cycle the double-buffered slots
+        g1, l1 = p1.loss_grad(xt)
+        g3, l3 = p3.loss_grad(xt)
+        assert torch.equal(g1, g3) and l1 == l3
+    assert rel(g3.cpu().numpy(), g_ref) <= TOL32 and abs(l3 - l_ref) <= TOL32 * abs(l_ref)
+    lam_bound = 4e-5 if kind == "csr" else 1.5
+    gam = 1.0 / (4.0 * cfg.I_bar * lam_bound * float(np.dot(*cfg.spectrum)))
+    xa = torch.zeros(cfg.d, dtype=torch.float64, device="cuda")
+    xb = torch.zeros_like(xa)
+    p1.solve(xa, 25, gam)
+    p3.solve(xb, 25, gam)
+    assert torch.equal(xa, xb)
+    x_ref, _, _ = wo["problem"].solve(25, gam)
+    assert rel(xb.cpu().numpy(), x_ref) <= 1e-3
+    p1.close()
+    p3.close()
+    with pytest.raises(P.PolyError):   # NVLS needs the comm path
+        W.make_poly(w, flags=P.POLY_FLAG_NVLS)
+
+
 def test_c4_compact_and_wide_sell_agree(c4, monkeypatch):
     """K4 stores both SELL copies as int16 index deltas + values (6 B/entry)
     when every delta fits; POLY_NO_SELL16 keeps the 8-byte {index, value}
@@ -609,6 +670,45 @@ def test_c5_full_size_parity(c5_gpu):
         a = float(np.clip(a - gam * Fbar(ah), -cfg.radius, cfg.radius))
     assert abs(np.dot(xt, u) - a) <= band and np.linalg.norm(xt - np.dot(xt, u) * u) <= band
     p.close()
+
+
+def test_c5_full_size_streamed_oracle(c5_gpu):
+    """C5 per call at full size (8e6 rows, 148 CTAs accumulating ~54k rows
+    each in fp32 registers) against the oracle evaluated over the whole
+    matrix: F is a sum over rows (Eq. operator), so the oracle
+    takes the rows in blocks of 500k — each block's generated bytes copied to
+    the host and checked against gen/rng on sampled rows — computes that
+    block's λ, counts and (1/n) Σ_i terms itself, and adds the blocks in
+    order.  Counts bit-exact over all 8e6 rows; F ≤ 1e-4 at three points."""
+    import psutil
+    cfg = G.C5
+    w = c5_gpu
+    blk = 500_000
+    if psutil.virtual_memory().available < 4 * blk * cfg.d * 4:
+        pytest.skip("host memory too small for 8 GB oracle blocks")
+    xs = w["x_star"].cpu().numpy()
+    r = np.random.default_rng(17)
+    u = r.standard_normal(cfg.d)
+    x_r = r.standard_normal(cfg.d)
+    pts = [xs.copy(), 0.6 * x_r / np.linalg.norm(x_r),
+           (xs + 0.3 * u / np.linalg.norm(u)) / max(1.0, np.linalg.norm(xs + 0.3 * u / np.linalg.norm(u)))]
+    p = _W().make_poly(w)
+    got = [gpu_F(p, x) for x in pts]
+    p.close()
+    acc = [np.zeros(cfg.d) for _ in pts]
+    lacc = [0.0 for _ in pts]
+    for a in range(0, cfg.n, blk):
+        b = min(cfg.n, a + blk)
+        wo = OW.build(cfg, rows=np.arange(a, b), A=w["A"][a:b, :cfg.d].cpu().numpy())
+        assert np.array_equal(w["counts"][a:b].cpu().numpy(), wo["counts"]), (a, b)
+        for k, x in enumerate(pts):
+            g_c, l_c = wo["problem"].F(x)
+            acc[k] += g_c
+            lacc[k] += l_c
+        del wo
+    for (g, l), g_ref, l_ref in zip(got, acc, lacc):
+        assert rel(g, g_ref) <= TOL32, rel(g, g_ref)
+        assert abs(l - l_ref) <= TOL32 * abs(l_ref)
 
 
 def test_stream_probe_is_the_read_ceiling(c2_gpu):
