@@ -254,6 +254,7 @@ struct poly_handle {
   int tr_side = 0;                     // CSR, d = s²: fp32 copies also hold x transposed at [d, 2d)
   int64_t tr_slices = 0;               // K4f slices that gather from the transposed copy
   bool sell16 = false;                 // both SELL copies in the 6-byte delta form
+  bool sell_ring = false;              // fp32 SELL16 through the per-warp cp.async ring kernels
   // POLY_PARALLEL_BEAM
   PbGeom pb{};
   double *pb_trig = nullptr, *pb_out2 = nullptr, *pb_zpart = nullptr;
@@ -441,6 +442,12 @@ int enqueue_pass(poly_handle *h, const double *x, bool loss) {
   a.r = h->rbuf;
   a.mode = p.mode;
   a.loss_partials = h->loss_partials;
+  if (h->sell16 && h->sell_ring) {  // fp32 values: the cp.async-ring kernels
+    TRY(launch(h, loss ? (const void *)&k_sell16r_forward<true> : (const void *)&k_sell16r_forward<false>,
+               dim3(h->k4f16_grid), dim3(128), (size_t)kRingSmem, true, h->fwd16, (int64_t)h->nrslices, a));
+    return launch(h, (const void *)&k_sell16r_backward, dim3(h->k4b16_grid), dim3(128), (size_t)kRingSmem, true,
+                  h->bwd16, (int64_t)h->nslices, (int32_t)p.d, (const float *)h->rbuf, h->partials, h->epi);
+  }
   if (h->sell16) {
     TRY(launch(h, kSell16Fwd[p.dtype][loss ? 1 : 0], dim3(h->k4f16_grid), dim3(128), 0, true,
                h->fwd16, (int64_t)h->nrslices, a));
@@ -535,6 +542,33 @@ int small_solve_config(poly_handle *h, int *cl, size_t *smem) {
                    (kSmallThreads / 32) * (kSmallMaxD + 1) * 8 + (kSmallThreads / 32) * 8 +
                    2 * 8 + (size_t)2 * C * (p.d + 1) * 8;  // mbarriers + pushed partials
   if (s > 200 * 1024) return POLY_EUNSUPPORTED;
+  // a non-portable cluster of C CTAs with this much shared memory must be
+  // schedulable on this part (MIG slices, smaller GPCs): else the general path
+  {
+    const void *fn = p.dtype == POLY_F32 ? (const void *)&k_small_solve<float, false>
+                                         : (const void *)&k_small_solve<double, false>;
+    if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s) != cudaSuccess ||
+        cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess) {
+      cudaGetLastError();
+      return POLY_EUNSUPPORTED;
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(C);
+    cfg.blockDim = dim3(kSmallThreads);
+    cfg.dynamicSmemBytes = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = C;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    int nclusters = 0;
+    if (cudaOccupancyMaxActiveClusters(&nclusters, fn, &cfg) != cudaSuccess || nclusters < 1) {
+      cudaGetLastError();
+      return POLY_EUNSUPPORTED;
+    }
+  }
   *cl = C;
   *smem = s;
   return POLY_OK;
@@ -1142,6 +1176,7 @@ int build_sell_t(poly_handle *h) {
       return done(fail(POLY_ECUDA, "SELL16 pack: %s", cudaGetErrorString(cudaGetLastError())));
     if (!hov) {
       h->sell16 = true;
+      h->sell_ring = p.dtype == POLY_F32 && !getenv("POLY_NO_RING");
       // one block per slice: the block scheduler balances the uneven slices
       // (a grid-stride deal over the resident slots measured 12 % slower)
       h->k4f16_grid = (int)nrs;

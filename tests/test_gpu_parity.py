@@ -588,6 +588,30 @@ def test_nvls_reduce_single_rank(kind):
         W.make_poly(w, flags=P.POLY_FLAG_NVLS)
 
 
+@pytest.mark.parametrize("st,center", [(G.SET_BALL, "c"), (G.SET_NONNEG, None), (G.SET_NONNEG_BALL, None)])
+def test_c4_step_epilogue_same_bits(c4, monkeypatch, st, center):
+    """K4b's step epilogue (v = x_t - γ g/n, clamp and block norms inside the
+    backward on the plain-step path) gives the same bits as the separate
+    k_finalize step (POLY_NO_EPI), for a ball with a centre, the orthant and
+    orthant ∩ ball, over a graph-replayed C4 solve."""
+    P = _P()
+    wg, wo = c4
+    c = 0.3 * wo["x_star"] if center else None
+    R = 0.9 * wo["R"]
+    gam = 1.0 / (4.0 * G.C4.I_bar * 4e-5 * float(np.dot(wo["s"], wo["mu"])))
+    xs = []
+    for no_epi in (False, True):
+        if no_epi:
+            monkeypatch.setenv("POLY_NO_EPI", "1")
+        p = P.Poly(row_ptr=wg["row_ptr"], col=wg["col"], val=wg["val"], d=G.C4.d, y=wg["y"],
+                   s=wg["s"], mu=wg["mu"], I_bar=G.C4.I_bar, set=st, R=R, center=c)
+        x = torch.zeros(G.C4.d, dtype=torch.float64, device="cuda")
+        p.solve(x, 12, gam)
+        xs.append(x)
+        p.close()
+    assert torch.equal(xs[0], xs[1])
+
+
 def test_c4_compact_and_wide_sell_agree(c4, monkeypatch):
     """K4 stores both SELL copies as int16 index deltas + values (6 B/entry)
     when every delta fits; POLY_NO_SELL16 keeps the 8-byte {index, value}
