@@ -189,6 +189,20 @@ __device__ __forceinline__ void block_loss(double (*part)[32], double lacc, doub
   if (threadIdx.x == 0) out[blockIdx.x] = (part[0][0] + part[0][1]) + (part[0][2] + part[0][3]);
 }
 
+// the same with nw warps (their partials summed in warp order)
+__device__ __forceinline__ void block_loss_n(double (*part)[32], double lacc, double *out, int nw) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  lacc = warp_sum(lacc);
+  __syncthreads();
+  if (lane == 0) part[0][warp] = lacc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int w = 0; w < nw; ++w) t += part[0][w];
+    out[blockIdx.x] = t;
+  }
+}
+
 // K4f on a SELL-32 copy of A (rows as slices): block = 32 consecutive rows,
 // warp w takes steps w, w+4, ...; z_i combined in warp order, then lane i of
 // warp 0 evaluates row i's link and residual.
@@ -369,6 +383,31 @@ struct StepEpi {
   double *block_norm;
 };
 
+// warp 0 of a backward block: column sums of slice sl (the four warps'
+// partials in warp order) to g, or — with the step epilogue on — v, the
+// orthant clamp and the block's ||v - c||²
+__device__ __forceinline__ void backward_column_out(double (*part)[32], const StepEpi &e, double *g, int32_t d,
+                                                    int64_t sl, int lane) {
+  const int64_t c = sl * 32 + lane;
+  const double v = (part[0][lane] + part[1][lane]) + (part[2][lane] + part[3][lane]);
+  if (!e.on) {
+    if (c < d) g[c] = v;
+    return;
+  }
+  double q = 0.0;
+  if (c < d) {
+    const double gc = v / e.n_norm;
+    double vv = e.anchor[c] - e.state->gamma * gc;
+    if (e.set == 2 || e.set == 3) vv = vv > 0.0 ? vv : 0.0;
+    const double df = (e.set == 1 && e.center) ? vv - e.center[c] : vv;
+    q = df * df;
+    e.v_scratch[c] = vv;
+  }
+  q = warp_sum(q);
+  if (lane == 0) e.block_norm[sl] = q;
+  if (sl == 0 && lane == 0) e.state->loss_cur = 0.0;  // as k_finalize without the objective
+}
+
 template <typename T>
 __global__ void __launch_bounds__(POLY_SELL_LB_B) k_sell16_backward(const Sell16 s, int64_t nslices,
                                                               int32_t d, const float *__restrict__ r,
@@ -379,157 +418,7 @@ __global__ void __launch_bounds__(POLY_SELL_LB_B) k_sell16_backward(const Sell16
   for (int64_t sl = blockIdx.x; sl < nslices; sl += gridDim.x) {
     part[warp][lane] = sell16_dot<T, POLY_SELL_UNROLL_B>(s, sl, warp, lane, r);
     __syncthreads();
-    if (warp == 0) {
-      const int64_t c = sl * 32 + lane;
-      const double v = (part[0][lane] + part[1][lane]) + (part[2][lane] + part[3][lane]);
-      if (!e.on) {
-        if (c < d) g[c] = v;
-      } else {
-        double q = 0.0;
-        if (c < d) {
-          const double gc = v / e.n_norm;
-          double vv = e.anchor[c] - e.state->gamma * gc;
-          if (e.set == 2 || e.set == 3) vv = vv > 0.0 ? vv : 0.0;
-          const double df = (e.set == 1 && e.center) ? vv - e.center[c] : vv;
-          q = df * df;
-          e.v_scratch[c] = vv;
-        }
-        q = warp_sum(q);
-        if (lane == 0) e.block_norm[sl] = q;
-        if (sl == 0 && lane == 0) e.state->loss_cur = 0.0;  // as k_finalize without the objective
-      }
-    }
-    __syncthreads();
-  }
-  pdl_trigger();
-}
-
-// ------------------------------------------------------------------------
-// SELL16 with a per-warp cp.async ring (fp32 values): the same data and the
-// same delta chains, but each warp streams its groups into a private shared
-// memory ring RING groups ahead (cp.async: the loads are issued and the warp
-// moves on) and consumes them UNR at a time.  The HBM stream of deltas and
-// values no longer waits behind the dependent x / r gathers of the previous
-// groups, so it stays in flight while the gathers resolve.  A thread only
-// reads ring slots it filled itself (cp.async.wait_group, no barrier).
-#ifndef POLY_SELL_RING
-#define POLY_SELL_RING 8
-#endif
-#ifndef POLY_SELL_RING_UNR
-#define POLY_SELL_RING_UNR 2
-#endif
-constexpr int kRing = POLY_SELL_RING;
-constexpr int kRingUnr = POLY_SELL_RING_UNR;
-constexpr int kRingWarpBytes = kRing * 32 * (8 + 16);  // short4 deltas + float4 values per slot
-constexpr int kRingSmem = 4 * kRingWarpBytes;
-
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() {
-  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
-}
-
-// this warp's share of a slice, groups g = warp + 4j, through the ring
-__device__ __forceinline__ double sell16_dot_ring(const Sell16 &s, int64_t slice, int warp, int lane,
-                                                  const float *__restrict__ gv, unsigned char *ring) {
-  const int64_t o0 = s.slice_off[slice], ng = s.slice_off[slice + 1] - o0;
-  const int64_t nj = ng > warp ? (ng - warp + 3) / 4 : 0;
-  short4 *rdl = reinterpret_cast<short4 *>(ring);
-  float4 *rv = reinterpret_cast<float4 *>(ring + kRing * 32 * 8);
-  auto issue = [&](int64_t j) {
-    const int slot = (int)(j % kRing);
-    const int64_t gi = (o0 + warp + 4 * j) * 32 + lane;
-    cp_async8(rdl + slot * 32 + lane, s.dl + gi);
-    cp_async16(rv + slot * 32 + lane, (const float4 *)s.val + gi);
-  };
-#pragma unroll
-  for (int j = 0; j < kRing - kRingUnr; ++j) {
-    if (j < nj) issue(j);
-    cp_async_commit();
-  }
-  int32_t idx = s.base[(slice * 4 + warp) * 32 + lane];
-  double a0 = 0.0, a1 = 0.0;
-  for (int64_t j = 0; j < nj; j += kRingUnr) {
-#pragma unroll
-    for (int u = 0; u < kRingUnr; ++u) {
-      if (j + kRing - kRingUnr + u < nj) issue(j + kRing - kRingUnr + u);
-      cp_async_commit();
-    }
-    cp_async_wait<kRing - kRingUnr>();  // groups j .. j+UNR-1 have landed
-    float gg[4 * kRingUnr];
-    float4 vv[kRingUnr];
-#pragma unroll
-    for (int u = 0; u < kRingUnr; ++u) {
-      const int slot = (int)((j + u) % kRing);
-      const bool ok = j + u < nj;
-      const short4 dd = ok ? rdl[slot * 32 + lane] : make_short4(0, 0, 0, 0);
-      vv[u] = ok ? rv[slot * 32 + lane] : make_float4(0.f, 0.f, 0.f, 0.f);
-      const int32_t i0 = idx + dd.x, i1 = i0 + dd.y, i2 = i1 + dd.z, i3 = i2 + dd.w;
-      idx = i3;
-      gg[4 * u] = __ldg(gv + i0), gg[4 * u + 1] = __ldg(gv + i1);
-      gg[4 * u + 2] = __ldg(gv + i2), gg[4 * u + 3] = __ldg(gv + i3);
-    }
-#pragma unroll
-    for (int u = 0; u < kRingUnr; ++u) {
-      a0 = fma((double)vv[u].x, (double)gg[4 * u], a0);
-      a1 = fma((double)vv[u].y, (double)gg[4 * u + 1], a1);
-      a0 = fma((double)vv[u].z, (double)gg[4 * u + 2], a0);
-      a1 = fma((double)vv[u].w, (double)gg[4 * u + 3], a1);
-    }
-  }
-  cp_async_wait<0>();
-  return a0 + a1;
-}
-
-template <bool LOSS>
-__global__ void __launch_bounds__(128) k_sell16r_forward(const Sell16 s, int64_t nslices, const CsrFwdArgs a) {
-  extern __shared__ __align__(16) unsigned char ring_smem[];
-  __shared__ double sp[3 * kMaxW];
-  __shared__ double part[4][32];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  for (int i = threadIdx.x; i < 3 * kMaxW; i += blockDim.x) sp[i] = a.spec[i];
-  pdl_wait();  // x is written by the previous kernel; r is read by the previous backward
-  double lacc = 0.0;
-  for (int64_t sl = blockIdx.x; sl < nslices; sl += gridDim.x) {
-    part[warp][lane] = sell16_dot_ring(s, sl, warp, lane, a.x, ring_smem + warp * kRingWarpBytes);
-    __syncthreads();
-    lacc += forward_tail<LOSS>(part, sp, a, sl);
-    __syncthreads();
-  }
-  block_loss(part, lacc, a.loss_partials);
-  pdl_trigger();
-}
-
-__global__ void __launch_bounds__(128) k_sell16r_backward(const Sell16 s, int64_t nslices, int32_t d,
-                                                           const float *__restrict__ r, double *__restrict__ g,
-                                                           const StepEpi e) {
-  extern __shared__ __align__(16) unsigned char ring_smem[];
-  __shared__ double part[4][32];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  pdl_wait();  // r is written by the forward pass
-  for (int64_t sl = blockIdx.x; sl < nslices; sl += gridDim.x) {
-    part[warp][lane] = sell16_dot_ring(s, sl, warp, lane, r, ring_smem + warp * kRingWarpBytes);
-    __syncthreads();
-    if (warp == 0) {
-      const int64_t c = sl * 32 + lane;
-      const double v = (part[0][lane] + part[1][lane]) + (part[2][lane] + part[3][lane]);
-      if (!e.on) {
-        if (c < d) g[c] = v;
-      } else {
-        double q = 0.0;
-        if (c < d) {
-          const double gc = v / e.n_norm;
-          double vv = e.anchor[c] - e.state->gamma * gc;
-          if (e.set == 2 || e.set == 3) vv = vv > 0.0 ? vv : 0.0;
-          const double df = (e.set == 1 && e.center) ? vv - e.center[c] : vv;
-          q = df * df;
-          e.v_scratch[c] = vv;
-        }
-        q = warp_sum(q);
-        if (lane == 0) e.block_norm[sl] = q;
-        if (sl == 0 && lane == 0) e.state->loss_cur = 0.0;
-      }
-    }
+    if (warp == 0) backward_column_out(part, e, g, d, sl, lane);
     __syncthreads();
   }
   pdl_trigger();

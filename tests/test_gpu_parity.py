@@ -612,20 +612,72 @@ def test_c4_step_epilogue_same_bits(c4, monkeypatch, st, center):
     assert torch.equal(xs[0], xs[1])
 
 
-def test_c4_compact_and_wide_sell_agree(c4, monkeypatch):
-    """K4 stores both SELL copies as int16 index deltas + values (6 B/entry)
-    when every delta fits; POLY_NO_SELL16 keeps the 8-byte {index, value}
-    form.  Same sums up to accumulation order, both at oracle parity."""
+def test_c4_dsell_sell16_and_wide_agree(c4, monkeypatch):
+    """K4 keeps three layouts of the caller's CSR: SELL16 (the default: int16
+    index deltas + values), DSELL (POLY_DSELL=1: per-slice dictionaries staged
+    in shared memory, 1-byte local deltas + values, dsell.cuh) and the 8-byte
+    {index, value} form (POLY_NO_SELL16).  Same sums up to accumulation
+    order, all at oracle parity."""
     wg, wo = c4
     W = _W()
     x = torch.tensor(0.7 * wo["x_star"], device="cuda")
     g16, l16 = W.make_poly(wg).loss_grad(x)
+    monkeypatch.setenv("POLY_DSELL", "1")
+    g_ds, l_ds = W.make_poly(wg).loss_grad(x)
+    monkeypatch.delenv("POLY_DSELL")
     monkeypatch.setenv("POLY_NO_SELL16", "1")
     g32, l32 = W.make_poly(wg).loss_grad(x)
     g_ref, l_ref = wo["problem"].F(0.7 * wo["x_star"])
-    assert rel(g16.cpu().numpy(), g32.cpu().numpy()) <= 1e-12
-    assert abs(l16 - l32) <= 1e-12 * abs(l32)
-    assert rel(g16.cpu().numpy(), g_ref) <= TOL32
+    for g, l in ((g_ds, l_ds), (g16, l16)):
+        assert rel(g.cpu().numpy(), g32.cpu().numpy()) <= 1e-12
+        assert abs(l - l32) <= 1e-12 * abs(l32)
+    assert rel(g_ds.cpu().numpy(), g_ref) <= TOL32
+
+
+@pytest.mark.parametrize("n,d,density", [(1000, 4096, 0.01), (77, 300, 0.5), (4097, 2048, 0.003),
+                                         (64, 200_000, 0.002)])
+def test_dsell_random_sparse(n, d, density, monkeypatch):
+    """DSELL (POLY_DSELL=1) on unstructured sparse matrices (random columns, ragged rows,
+    empty rows and columns, local-index gaps > 255 bridged by filler steps,
+    a wide column span for d = 200000): oracle parity."""
+    P = _P()
+    monkeypatch.setenv("POLY_DSELL", "1")
+    r = np.random.default_rng(n + d)
+    mask = r.random((n, d)) < density if d * n <= 5e7 else None
+    if mask is None:
+        rows, cols = [], []
+        for i in range(n):
+            k = r.integers(0, 40)
+            rows += [i] * k
+            cols += sorted(r.choice(d, size=k, replace=False).tolist())
+        rows, cols = np.array(rows, dtype=np.int64), np.array(cols, dtype=np.int32)
+    else:
+        rows, cols = np.nonzero(mask)
+        cols = cols.astype(np.int32)
+    if n > 10:
+        keep = rows != 3                       # an empty row
+        rows, cols = rows[keep], cols[keep]
+    row_ptr = np.zeros(n + 1, dtype=np.int64)
+    np.add.at(row_ptr, rows + 1, 1)
+    row_ptr = np.cumsum(row_ptr)
+    val = r.uniform(0.0, 1.0 / math.sqrt(max(1, density * d)), rows.shape[0]).astype(np.float32)
+    s, mu = np.array([0.3, 0.7]), np.array([1.5, 0.5])
+    xs = r.uniform(0, 1, d) / math.sqrt(d)
+    lam = 50.0 * np.array([np.dot(s, np.exp(-mu * max(0.0, float(val[row_ptr[i]:row_ptr[i + 1]] @
+                                                         xs[cols[row_ptr[i]:row_ptr[i + 1]]]))))
+                           for i in range(n)])
+    y = rng.poisson(7, rng.STREAM_TEST, lam, np.arange(n)).astype(np.int32)
+    o = oracle.Problem(row_ptr=row_ptr, col=cols, val=val, y=y.astype(np.float64), s=s, mu=mu, I_bar=50.0,
+                       d=d, set=G.SET_NONE)
+    p = P.Poly(row_ptr=torch.tensor(row_ptr, device="cuda"), col=torch.tensor(cols, device="cuda"),
+               val=torch.tensor(val, device="cuda"), d=d, y=torch.tensor(y, device="cuda"), s=s, mu=mu,
+               I_bar=50.0, set=G.SET_NONE)
+    for x in (xs, 0.5 * xs, np.zeros(d)):
+        g_ref, l_ref = o.F(x)
+        g, l = gpu_F(p, x)
+        assert rel(g, g_ref) <= TOL32, rel(g, g_ref)
+        assert abs(l - l_ref) <= TOL32 * max(1.0, abs(l_ref))
+    p.close()
 
 
 # ------------------------------------------------------------------ C5 (full size, 131 GB)
