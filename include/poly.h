@@ -176,6 +176,15 @@ typedef struct poly_problem {
    * views).  fp32 chord lengths; mode EXACT, no per-row spectra.  A, row_ptr,
    * col, val are unused. */
   int32_t pb_side, pb_views, pb_bins, pb_reserved;
+  /* TV sets: λ values evaluated per round of the TV-prox search, one
+   * thread-block cluster each (reading R22; 1 = the paper's bisection);
+   * 0 = as many clusters as can be resident (at most 16).  More than can be
+   * resident: POLY_EUNSUPPORTED. */
+  int32_t tv_k;
+  /* TV sets: 0 (default) = each TV prox of one projection starts FISTA from
+   * the dual solution of the previous prox (same cluster; the first from 0),
+   * clipped to the new λ's box (reading R23); 1 = every prox from 0. */
+  int32_t tv_cold;
 } poly_problem;
 
 /* Validate *p, copy host parameters, pick the kernel configuration for

@@ -40,7 +40,7 @@ class _Problem(C.Structure):
         ("relu", C.c_int), ("set", C.c_int), ("R", C.c_double), ("center", C.c_void_p),
         ("tv_side", C.c_int), ("tv_tau", C.c_double), ("tv_tol", C.c_double),
         ("tv_rtol", C.c_double), ("tv_dtol", C.c_double), ("tv_max_it", C.c_int),
-        ("tv_max_outer", C.c_int),
+        ("tv_max_outer", C.c_int), ("tv_k", C.c_int), ("tv_warm", C.c_int),
     ]
 
 
@@ -87,6 +87,20 @@ def lib():
         _lib.oracle_project_tv_nonneg.restype = C.c_int
         _lib.oracle_project_tv_nonneg.argtypes = [C.c_int, dp, C.c_double, C.c_double, C.c_double,
                                                   C.c_int, C.c_double, C.c_int, dp]
+        _lib.oracle_project_tv_k.restype = C.c_int
+        _lib.oracle_project_tv_k.argtypes = [C.c_int, dp, C.c_double, C.c_double, C.c_double,
+                                             C.c_int, C.c_int, dp]
+        _lib.oracle_project_tv_nonneg_kw.restype = C.c_int
+        _lib.oracle_project_tv_nonneg_kw.argtypes = [C.c_int, dp, C.c_double, C.c_double, C.c_double,
+                                                     C.c_int, C.c_double, C.c_int, C.c_int, C.c_int, dp]
+        _lib.oracle_project_tv_k_warm.restype = C.c_int
+        _lib.oracle_project_tv_k_warm.argtypes = [C.c_int, dp, C.c_double, C.c_double, C.c_double,
+                                                  C.c_int, C.c_int, dp, dp]
+        _lib.oracle_fista_iterations.restype = C.c_longlong
+        _lib.oracle_fista_iterations.argtypes = [C.c_int]
+        _lib.oracle_project_tv_nonneg_k.restype = C.c_int
+        _lib.oracle_project_tv_nonneg_k.argtypes = [C.c_int, dp, C.c_double, C.c_double, C.c_double,
+                                                    C.c_int, C.c_double, C.c_int, C.c_int, dp]
         _lib.oracle_set_threads.argtypes = [C.c_int]
         _lib.oracle_max_threads.restype = C.c_int
     return _lib
@@ -170,6 +184,8 @@ class Problem:
             st.tv_dtol = float(tv.get("dykstra_tol", 1e-4))
             st.tv_max_it = int(tv.get("max_it", 5000))
             st.tv_max_outer = int(tv.get("max_outer", 1000))
+            st.tv_k = int(tv.get("k", 1))
+            st.tv_warm = int(tv.get("warm", 0))
         self._st = st
 
     @property
@@ -304,19 +320,34 @@ def prox_tv(z, lam, rtol=1e-6, max_it=5000):
     return x, u[:2 * side * (side - 1)], int(it)
 
 
-def project_tv(z, tau, tv_tol=0.01, rtol=1e-6, max_it=5000):
+def fista_iterations(reset=True) -> int:
+    """FISTA iterations run by the TV proxes since the last reset."""
+    return int(lib().oracle_fista_iterations(1 if reset else 0))
+
+
+def project_tv(z, tau, tv_tol=0.01, rtol=1e-6, max_it=5000, k=1, warm=False):
+    """P onto {||x||_TV <= tau} as the paper computes it; k λ values per search
+    round (reading R22; k = 1: the binary search), proxes warm-started from the
+    previous prox of the same λ slot (reading R23) if warm.  (x, rounds)."""
     z, side = _side(np.ravel(z))
     x = np.zeros_like(z)
-    steps = lib().oracle_project_tv(side, _dp(z), float(tau), float(tv_tol), float(rtol),
-                                    int(max_it), _dp(x))
+    if warm:
+        ust = np.zeros(max(1, int(k)) * 2 * side * (side - 1) + 1)
+        steps = lib().oracle_project_tv_k_warm(side, _dp(z), float(tau), float(tv_tol), float(rtol),
+                                               int(max_it), int(k), _dp(ust), _dp(x))
+    else:
+        steps = lib().oracle_project_tv_k(side, _dp(z), float(tau), float(tv_tol), float(rtol),
+                                          int(max_it), int(k), _dp(x))
     return x, int(steps)
 
 
-def project_tv_nonneg(z, tau, tv_tol=0.01, rtol=1e-6, max_it=5000, tol=1e-4, max_outer=100000):
+def project_tv_nonneg(z, tau, tv_tol=0.01, rtol=1e-6, max_it=5000, tol=1e-4, max_outer=100000, k=1,
+                      warm=False):
     z, side = _side(np.ravel(z))
     x = np.zeros_like(z)
-    it = lib().oracle_project_tv_nonneg(side, _dp(z), float(tau), float(tv_tol), float(rtol),
-                                        int(max_it), float(tol), int(max_outer), _dp(x))
+    it = lib().oracle_project_tv_nonneg_kw(side, _dp(z), float(tau), float(tv_tol), float(rtol),
+                                           int(max_it), float(tol), int(max_outer), int(k), int(bool(warm)),
+                                           _dp(x))
     return x, int(it)
 
 

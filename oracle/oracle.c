@@ -53,6 +53,8 @@ typedef struct {
   int tv_side;
   double tv_tau, tv_tol, tv_rtol, tv_dtol;
   int tv_max_it, tv_max_outer;
+  int tv_k;                 /* λ evaluations per search round (reading R22); <= 1: binary */
+  int tv_warm;              /* 1: warm-started proxes within a projection (reading R23) */
 } oracle_problem;
 
 void oracle_set_threads(int t) {
@@ -225,8 +227,18 @@ void oracle_project(int set, int64_t d, double R, const double *c, const double 
 
 int oracle_project_tv(int side, const double *z, double tau, double tv_tol, double rtol,
                       int max_it, double *x);
+int oracle_project_tv_k(int side, const double *z, double tau, double tv_tol, double rtol,
+                        int max_it, int K, double *x);
+int oracle_project_tv_nonneg_k(int side, const double *z, double tau, double tv_tol, double rtol,
+                               int max_it, double tol, int max_outer, int K, double *out);
 int oracle_project_tv_nonneg(int side, const double *z, double tau, double tv_tol, double rtol,
                              int max_it, double tol, int max_outer, double *out);
+int oracle_project_tv_nonneg_kw(int side, const double *z, double tau, double tv_tol, double rtol,
+                                int max_it, double tol, int max_outer, int K, int warm, double *out);
+int oracle_project_tv_k_warm(int side, const double *z, double tau, double tv_tol, double rtol,
+                             int max_it, int K, double *ustate, double *x);
+int oracle_prox_tv_from(int side, const double *z, double lam, double rtol, int max_it, double *x,
+                        double *u_out, const double *u_in);
 
 /* P_X for the problem's set: the closed forms above, or the TV sets of
  * NEXT-2.  out may alias v. */
@@ -234,11 +246,17 @@ static void project_p(const oracle_problem *p, const double *v, double *out) {
   if (p->set == OR_SET_TV_NONNEG || p->set == OR_SET_TV) {
     const int64_t d = p->d;
     double *t = (double *)malloc((size_t)d * sizeof(double));
-    if (p->set == OR_SET_TV_NONNEG)
-      oracle_project_tv_nonneg(p->tv_side, v, p->tv_tau, p->tv_tol, p->tv_rtol, p->tv_max_it,
-                               p->tv_dtol, p->tv_max_outer, t);
-    else
-      oracle_project_tv(p->tv_side, v, p->tv_tau, p->tv_tol, p->tv_rtol, p->tv_max_it, t);
+    if (p->set == OR_SET_TV_NONNEG) {
+      oracle_project_tv_nonneg_kw(p->tv_side, v, p->tv_tau, p->tv_tol, p->tv_rtol, p->tv_max_it,
+                                  p->tv_dtol, p->tv_max_outer, p->tv_k, p->tv_warm, t);
+    } else {
+      const int K = p->tv_k < 1 ? 1 : p->tv_k;
+      double *ust = p->tv_warm ? (double *)calloc((size_t)K * 2 * p->tv_side * (p->tv_side - 1) + 1,
+                                                  sizeof(double))
+                               : NULL;
+      oracle_project_tv_k_warm(p->tv_side, v, p->tv_tau, p->tv_tol, p->tv_rtol, p->tv_max_it, K, ust, t);
+      free(ust);
+    }
     memcpy(out, t, (size_t)d * sizeof(double));
     free(t);
     return;
@@ -567,18 +585,42 @@ double oracle_tv_norm(int side, const double *x) {
  * stop when the primal x(u) = z - D^T u moves by <= rtol ||x(u)|| or after
  * max_it iterations.  u_out (may be NULL) receives u [2 side (side-1)].
  * Returns the iterations used. */
+int oracle_prox_tv_from(int side, const double *z, double lam, double rtol, int max_it, double *x,
+                        double *u_out, const double *u_in);
+
 int oracle_prox_tv(int side, const double *z, double lam, double rtol, int max_it, double *x,
                    double *u_out) {
+  return oracle_prox_tv_from(side, z, lam, rtol, max_it, x, u_out, NULL);
+}
+
+/* FISTA iterations run by all proxes since the last reset (statistics only). */
+static long long g_fista_iters = 0;
+long long oracle_fista_iterations(int reset) {
+  const long long v = g_fista_iters;
+  if (reset) g_fista_iters = 0;
+  return v;
+}
+
+/* The same FISTA started from the dual point clip(u_in, ±λ/2) (u_in NULL: 0). */
+int oracle_prox_tv_from(int side, const double *z, double lam, double rtol, int max_it, double *x,
+                        double *u_out, const double *u_in) {
   const int d = side * side, m = 2 * side * (side - 1);
   double *u = (double *)calloc((size_t)(m > 0 ? m : 1), sizeof(double));
   double *w = (double *)calloc((size_t)(m > 0 ? m : 1), sizeof(double));
+  if (u_in)
+    for (int k = 0; k < m; ++k) {
+      const double v = u_in[k];
+      u[k] = w[k] = v > lam / 2.0 ? lam / 2.0 : (v < -lam / 2.0 ? -lam / 2.0 : v);
+    }
   double *un = (double *)malloc((size_t)(m > 0 ? m : 1) * sizeof(double));
   double *dx = (double *)malloc((size_t)(m > 0 ? m : 1) * sizeof(double));
   double *xw = (double *)malloc((size_t)d * sizeof(double));
   double *xp = (double *)malloc((size_t)d * sizeof(double));
   double t = 1.0;
   int it = 0;
-  for (int k = 0; k < d; ++k) x[k] = z[k];
+  /* the primal of the starting dual: x(u0) = z - Dᵀu0 (= z from u0 = 0) */
+  tv_Dt(side, u, x);
+  for (int k = 0; k < d; ++k) x[k] = z[k] - x[k];
   if (lam > 0.0 && m > 0) {
     for (it = 1; it <= max_it; ++it) {
       tv_Dt(side, w, xw);
@@ -606,6 +648,7 @@ int oracle_prox_tv(int side, const double *z, double lam, double rtol, int max_i
     }
     if (it > max_it) it = max_it;
   }
+  g_fista_iters += it;
   if (u_out)
     for (int k = 0; k < m; ++k) u_out[k] = u[k];
   free(u);
@@ -622,31 +665,114 @@ int oracle_prox_tv(int side, const double *z, double lam, double rtol, int max_i
  * "tuned via a binary search" until | ||x̄||_TV - τ | <= tv_tol (0.01 in the
  * paper).  Bracket: λ_hi = 1, doubled while ||prox(z, λ_hi)||_TV
  * > τ; bisection of [λ_lo, λ_hi] for at most 60 steps.  Returns the bisection
- * steps used (0 if z ∈ X1). */
-int oracle_project_tv(int side, const double *z, double tau, double tv_tol, double rtol,
-                      int max_it, double *x) {
+ * steps used (0 if z ∈ X1).
+ *
+ * Reading R22: the search may evaluate K values of λ per round
+ * (the GPU evaluates them at once, one thread-block cluster each).  With
+ * K = 1 this is exactly the search above.  For K > 1:
+ *   bracket round g: λ = 2^(gK + k), k = 0..K-1; the first k with TV <= τ
+ *     gives hi = 2^(gK + k), lo = 2^(gK + k - 1) (0 when gK + k = 0);
+ *     at most 200 values, as the doubling loop;
+ *   search round: λ_k = lo + (hi - lo)(k + 1)/(K + 1) (K = 1: (lo + hi)/2);
+ *     stop at the smallest k with |TV_k - τ| <= tv_tol (its prox is the
+ *     result); else, with k* the smallest k with TV_k <= τ, the new bracket
+ *     is [λ_{k*-1} (lo if k* = 0), λ_{k*}], or [λ_{K-1}, hi] if there is none;
+ *     at most 60 rounds, after which the result is the prox at λ_{k*} (at
+ *     λ_{K-1} if there is none).
+ * Returns the rounds used. */
+static int project_tv_core(int side, const double *z, double tau, double tv_tol, double rtol, int max_it,
+                           int K, double *ustate, double *x);
+
+int oracle_project_tv_k(int side, const double *z, double tau, double tv_tol, double rtol,
+                        int max_it, int K, double *x) {
+  return project_tv_core(side, z, tau, tv_tol, rtol, max_it, K, NULL, x);
+}
+
+/* The same with warm-started proxes (reading R23): ustate [K][2 side (side-1)]
+ * holds, per λ slot k, the dual solution of the slot's last prox; each prox
+ * starts from it (clipped to the new box by oracle_prox_tv_from) and leaves
+ * its own solution there.  ustate all zeros = cold starts for the first
+ * round.  NULL: every prox starts from 0 (the search above). */
+int oracle_project_tv_k_warm(int side, const double *z, double tau, double tv_tol, double rtol,
+                             int max_it, int K, double *ustate, double *x) {
+  return project_tv_core(side, z, tau, tv_tol, rtol, max_it, K, ustate, x);
+}
+
+static int project_tv_core(int side, const double *z, double tau, double tv_tol, double rtol, int max_it,
+                           int K, double *ustate, double *x) {
   const int d = side * side;
+  const size_t m = (size_t)2 * side * (side - 1);
+  if (K < 1) K = 1;
   if (oracle_tv_norm(side, z) <= tau) {
     for (int k = 0; k < d; ++k) x[k] = z[k];
     return 0;
   }
+  double *xs = (double *)malloc((size_t)K * d * sizeof(double));
+  double *tv = (double *)malloc((size_t)K * sizeof(double));
+  double *lam = (double *)malloc((size_t)K * sizeof(double));
   double lo = 0.0, hi = 1.0;
-  for (int g = 0; g < 200; ++g) {
-    oracle_prox_tv(side, z, hi, rtol, max_it, x, NULL);
-    if (oracle_tv_norm(side, x) <= tau) break;
-    lo = hi;
-    hi *= 2.0;
+  int found = 0;
+  for (int g = 0; g * K < 200 && !found; ++g) {
+    for (int k = 0; k < K; ++k) {
+      const int e = g * K + k;
+      if (e >= 200) { tv[k] = INFINITY; continue; }
+      lam[k] = ldexp(1.0, e);
+      oracle_prox_tv_from(side, z, lam[k], rtol, max_it, xs + (size_t)k * d, ustate ? ustate + k * m : NULL,
+                          ustate ? ustate + k * m : NULL);
+      tv[k] = oracle_tv_norm(side, xs + (size_t)k * d);
+    }
+    for (int k = 0; k < K; ++k) {
+      const int e = g * K + k;
+      if (e < 200 && tv[k] <= tau) {
+        hi = lam[k];
+        lo = e == 0 ? 0.0 : ldexp(1.0, e - 1);
+        found = 1;
+        break;
+      }
+    }
+    if (!found) {
+      const int e = (g + 1) * K - 1 < 199 ? (g + 1) * K - 1 : 199;
+      lo = ldexp(1.0, e);
+      hi = 2.0 * lo;
+    }
   }
-  int steps = 0;
-  for (steps = 1; steps <= 60; ++steps) {
-    const double lam = 0.5 * (lo + hi);
-    oracle_prox_tv(side, z, lam, rtol, max_it, x, NULL);
-    const double tv = oracle_tv_norm(side, x);
-    if (fabs(tv - tau) <= tv_tol) break;
-    if (tv > tau) lo = lam;
-    else hi = lam;
+  int rounds, sel = K - 1;
+  for (rounds = 1; rounds <= 60; ++rounds) {
+    for (int k = 0; k < K; ++k) {
+      lam[k] = K == 1 ? 0.5 * (lo + hi) : lo + (hi - lo) * (double)(k + 1) / (double)(K + 1);
+      oracle_prox_tv_from(side, z, lam[k], rtol, max_it, xs + (size_t)k * d, ustate ? ustate + k * m : NULL,
+                          ustate ? ustate + k * m : NULL);
+      tv[k] = oracle_tv_norm(side, xs + (size_t)k * d);
+    }
+    int hit = -1, ks = -1;
+    for (int k = 0; k < K && hit < 0; ++k)
+      if (fabs(tv[k] - tau) <= tv_tol) hit = k;
+    for (int k = 0; k < K && ks < 0; ++k)
+      if (tv[k] <= tau) ks = k;
+    if (hit >= 0) {
+      sel = hit;
+      break;
+    }
+    sel = ks >= 0 ? ks : K - 1;
+    if (ks >= 0) {
+      const double nlo = ks > 0 ? lam[ks - 1] : lo;
+      hi = lam[ks];
+      lo = nlo;
+    } else {
+      lo = lam[K - 1];
+    }
   }
-  return steps;
+  if (rounds > 60) rounds = 60;
+  for (int k = 0; k < d; ++k) x[k] = xs[(size_t)sel * d + k];
+  free(xs);
+  free(tv);
+  free(lam);
+  return rounds;
+}
+
+int oracle_project_tv(int side, const double *z, double tau, double tv_tol, double rtol,
+                      int max_it, double *x) {
+  return oracle_project_tv_k(side, z, tau, tv_tol, rtol, max_it, 1, x);
 }
 
 /* Dykstra's algorithm for X1 ∩ X2, Eq.(projection-intersection)
@@ -655,9 +781,18 @@ int oracle_project_tv(int side, const double *z, double tau, double tv_tol, doub
  *   z_{k+1} = P_X2(y_k + q_k),  q_{k+1} = y_k + q_k - z_{k+1},
  * stopping at ||z_{k+1} - z_k||_2 <= tol (1e-4 in the paper) or max_outer.
  * P_X2 keeps the positive entries.  Returns the sweeps. */
-int oracle_project_tv_nonneg(int side, const double *z, double tau, double tv_tol, double rtol,
-                             int max_it, double tol, int max_outer, double *out) {
+int oracle_project_tv_nonneg_k(int side, const double *z, double tau, double tv_tol, double rtol,
+                               int max_it, double tol, int max_outer, int K, double *out) {
+  return oracle_project_tv_nonneg_kw(side, z, tau, tv_tol, rtol, max_it, tol, max_outer, K, 0, out);
+}
+
+/* warm = 1: the proxes of the whole projection — all Dykstra sweeps — share
+ * one warm-start state per λ slot (reading R23), zero at the start. */
+int oracle_project_tv_nonneg_kw(int side, const double *z, double tau, double tv_tol, double rtol,
+                                int max_it, double tol, int max_outer, int K, int warm, double *out) {
   const int d = side * side;
+  double *ust = warm ? (double *)calloc((size_t)(K < 1 ? 1 : K) * 2 * side * (side - 1) + 1, sizeof(double))
+                     : NULL;
   double *zk = (double *)malloc((size_t)d * sizeof(double));
   double *p = (double *)calloc((size_t)d, sizeof(double));
   double *q = (double *)calloc((size_t)d, sizeof(double));
@@ -667,7 +802,7 @@ int oracle_project_tv_nonneg(int side, const double *z, double tau, double tv_to
   int it;
   for (it = 1; it <= max_outer; ++it) {
     for (int k = 0; k < d; ++k) v[k] = zk[k] + p[k];
-    oracle_project_tv(side, v, tau, tv_tol, rtol, max_it, y);
+    project_tv_core(side, v, tau, tv_tol, rtol, max_it, K, ust, y);
     for (int k = 0; k < d; ++k) p[k] = zk[k] + p[k] - y[k];
     double dn = 0.0;
     for (int k = 0; k < d; ++k) {
@@ -686,5 +821,11 @@ int oracle_project_tv_nonneg(int side, const double *z, double tau, double tv_to
   free(q);
   free(y);
   free(v);
+  free(ust);
   return it;
+}
+
+int oracle_project_tv_nonneg(int side, const double *z, double tau, double tv_tol, double rtol,
+                             int max_it, double tol, int max_outer, double *out) {
+  return oracle_project_tv_nonneg_k(side, z, tau, tv_tol, rtol, max_it, tol, max_outer, 1, out);
 }

@@ -50,7 +50,7 @@ class PolyProblem(C.Structure):
         ("tv_tau", C.c_double), ("tv_tol", C.c_double), ("tv_rtol", C.c_double),
         ("tv_dykstra_tol", C.c_double), ("tv_max_it", C.c_int32), ("tv_max_outer", C.c_int32),
         ("pb_side", C.c_int32), ("pb_views", C.c_int32), ("pb_bins", C.c_int32),
-        ("pb_reserved", C.c_int32),
+        ("pb_reserved", C.c_int32), ("tv_k", C.c_int32), ("tv_cold", C.c_int32),
     ]
 
 

@@ -269,9 +269,13 @@ struct poly_handle {
   int k4f16_grid = 0, k4b16_grid = 0;  // resident-slot grids (slices dealt grid-stride)
   StepEpi epi{};                        // K4b's step epilogue for the next pass (on = 0: write g)
   // TV sets: Dykstra state, statistics, cluster launch shape
-  double *tv_zk = nullptr, *tv_p = nullptr, *tv_q = nullptr;
-  int32_t *tv_stats = nullptr;
+  double *tv_zk = nullptr, *tv_p = nullptr, *tv_q = nullptr;  // [tv_k][d] each
+  int32_t *tv_stats = nullptr;         // [4]
   int tv_cl = 0;
+  int tv_k = 1;                        // clusters = λ values per search round (reading R22)
+  double *tv_vals = nullptr, *tv_xsel = nullptr;
+  double *tv_ustate = nullptr;         // [tv_k][2][d] warm-start duals (reading R23), NULL when cold
+  unsigned int *tv_gbar = nullptr;
   size_t tv_smem = 0;
   Sell16 fwd16{}, bwd16{};
   int64_t sell_steps = 0;              // slice_off[nslices]
@@ -517,8 +521,16 @@ int enqueue_tv(poly_handle *h, const double *v, double *out) {
   a.max_it = h->p.tv_max_it > 0 ? h->p.tv_max_it : 5000;
   a.max_outer = h->p.tv_max_outer > 0 ? h->p.tv_max_outer : 1000;
   a.stats = h->tv_stats;
+  a.K = h->tv_k;
+  a.tv_vals = h->tv_vals;
+  a.gbar = h->tv_gbar;
+  a.xsel = h->tv_xsel;
+  a.timeout_ns = 20ull * 1000000000ull;
+  a.warm = h->tv_ustate ? 1 : 0;
+  a.u_state = h->tv_ustate;
+  if (h->tv_k > 1) CK(cudaMemsetAsync(h->tv_gbar, 0, 4, h->work));
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(h->tv_cl);
+  cfg.gridDim = dim3(h->tv_cl * h->tv_k);
   cfg.blockDim = dim3(kTvThreads);
   cfg.dynamicSmemBytes = h->tv_smem;
   cfg.stream = h->work;
@@ -860,6 +872,15 @@ int wait_event(poly_handle *h, cudaEvent_t ev) {
     }
     std::this_thread::sleep_for(std::chrono::microseconds(el < 0.01 ? 2 : 50));
   }
+}
+
+// The TV projection's clusters flag stats[3] when they failed to meet.
+int check_tv_meet(poly_handle *h) {
+  if (!h->tv_stats || h->tv_k <= 1) return POLY_OK;
+  int32_t f = 0;
+  CK(cudaMemcpy(&f, h->tv_stats + 3, 4, cudaMemcpyDeviceToHost));
+  if (f) return fail(POLY_ECUDA, "TV projection: the %d clusters did not meet (not co-resident)", h->tv_k);
+  return POLY_OK;
 }
 
 // Drain the work stream (through wait_event, so a hung collective cannot
@@ -1992,15 +2013,41 @@ int poly_init(const poly_problem *pin, poly_handle **out) {
     h->tv_smem = ((size_t)5 * cap + tv_edge_doubles(s) + 8 + 4 + (kTvThreads / 32) * 4) * 8 + tv_xchg_bytes(s);
     if (s > 256 || h->tv_smem > kSmemLimit)
       return bail(fail(POLY_EUNSUPPORTED, "TV image side %d too large for one cluster", s));
-    if ((rc = dev_alloc(h, &h->tv_zk, (size_t)p.d)) || (rc = dev_alloc(h, &h->tv_p, (size_t)p.d)) ||
-        (rc = dev_alloc(h, &h->tv_q, (size_t)p.d)) || (rc = dev_alloc(h, &h->tv_stats, 3)))
-      return bail(rc);
-    if (cudaMemsetAsync(h->tv_stats, 0, 12, h->work) != cudaSuccess) return bail(fail(POLY_ECUDA, "memset"));
     if (cudaFuncSetAttribute((const void *)&k_tv_project, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)h->tv_smem) != cudaSuccess ||
         cudaFuncSetAttribute((const void *)&k_tv_project, cudaFuncAttributeNonPortableClusterSizeAllowed,
                              1) != cudaSuccess)
       return bail(fail(POLY_ECUDA, "TV kernel attributes: %s", cudaGetErrorString(cudaGetLastError())));
+    {  // λ values per round: as many clusters as can be resident at once (or the caller's tv_k)
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3(h->tv_cl);
+      cfg.blockDim = dim3(kTvThreads);
+      cfg.dynamicSmemBytes = h->tv_smem;
+      cudaLaunchAttribute attr[1];
+      attr[0].id = cudaLaunchAttributeClusterDimension;
+      attr[0].val.clusterDim.x = h->tv_cl;
+      attr[0].val.clusterDim.y = 1;
+      attr[0].val.clusterDim.z = 1;
+      cfg.attrs = attr;
+      cfg.numAttrs = 1;
+      int maxc = 0;
+      if (cudaOccupancyMaxActiveClusters(&maxc, (const void *)&k_tv_project, &cfg) != cudaSuccess || maxc < 1) {
+        cudaGetLastError();
+        return bail(fail(POLY_EUNSUPPORTED, "TV: a %d-CTA cluster cannot be resident", h->tv_cl));
+      }
+      const int want = p.tv_k > 0 ? p.tv_k : std::min(maxc, kTvMaxK);
+      if (want > maxc || want > kTvMaxK)
+        return bail(fail(POLY_EUNSUPPORTED, "TV: tv_k = %d clusters requested, %d can be resident", want,
+                         std::min(maxc, kTvMaxK)));
+      h->tv_k = want;
+    }
+    const size_t kd = (size_t)h->tv_k * p.d;
+    if ((rc = dev_alloc(h, &h->tv_zk, kd)) || (rc = dev_alloc(h, &h->tv_p, kd)) || (rc = dev_alloc(h, &h->tv_q, kd)) ||
+        (rc = dev_alloc(h, &h->tv_stats, 4)) || (rc = dev_alloc(h, &h->tv_vals, (size_t)2 * h->tv_k)) ||
+        (rc = dev_alloc(h, &h->tv_gbar, 1)) || (rc = dev_alloc(h, &h->tv_xsel, (size_t)p.d)) ||
+        (!p.tv_cold && (rc = dev_alloc(h, &h->tv_ustate, 2 * kd))))
+      return bail(rc);
+    if (cudaMemsetAsync(h->tv_stats, 0, 16, h->work) != cudaSuccess) return bail(fail(POLY_ECUDA, "memset"));
   }
   if ((rc = dev_alloc(h, &h->comm, (size_t)p.d + 1)) != POLY_OK) return bail(rc);
   if ((rc = dev_alloc(h, &h->xa, (size_t)p.d)) != POLY_OK) return bail(rc);
@@ -2349,6 +2396,7 @@ int poly_solve(poly_handle *h, double *x, int T, double gamma, uint32_t flags, d
     h->nccl = nullptr;
     return fail(POLY_ENCCL, "peer reduce: a peer did not publish within the wait bound; communicator aborted");
   }
+  TRY(check_tv_meet(h));
   if (h->hstate->bad != 0) {
     const int b = h->hstate->bad;
     if (bad_iter) *bad_iter = b > 0 ? (b + 1) / 2 : 0;
@@ -2432,7 +2480,7 @@ int poly_reparameterize(int32_t W, const double *s, const double *mu, double I_b
 int poly_project(poly_handle *h, const double *v, double *x, int64_t *stats) {
   if (!h || !v || !x) return fail(POLY_EINVAL, "NULL argument");
   TRY(sync_in(h));
-  if (h->tv_stats) CK(cudaMemsetAsync(h->tv_stats, 0, 12, h->work));
+  if (h->tv_stats) CK(cudaMemsetAsync(h->tv_stats, 0, 16, h->work));
   if (h->tv_cl) {
     TRY(enqueue_tv(h, v, x));
   } else {
@@ -2443,13 +2491,14 @@ int poly_project(poly_handle *h, const double *v, double *x, int64_t *stats) {
     f.tr_side = 0;
     TRY(enqueue_fin(h, f));
   }
-  int32_t hs[3] = {0, 0, 0};
-  if (h->tv_stats) CK(cudaMemcpyAsync(hs, h->tv_stats, 12, cudaMemcpyDeviceToHost, h->work));
+  int32_t hs[4] = {0, 0, 0, 0};
+  if (h->tv_stats) CK(cudaMemcpyAsync(hs, h->tv_stats, 16, cudaMemcpyDeviceToHost, h->work));
   CK(cudaStreamSynchronize(h->work));
   if (stats)
     for (int k = 0; k < 3; ++k) stats[k] = hs[k];
   TRY(sync_out(h));
   CK(cudaGetLastError());
+  if (hs[3]) return fail(POLY_ECUDA, "TV projection: the %d clusters did not meet (not co-resident)", h->tv_k);
   return POLY_OK;
 }
 

@@ -10,8 +10,8 @@
 // FISTA on the dual (x = z - Dᵀu, |u| <= λ/2, step 1/8), stopped at a relative
 // primal change <= rtol; λ bracketed from 1 by doubling, then bisected.
 //
-// B200 mapping: ONE thread-block cluster of CL CTAs does the whole projection
-// — Dykstra, bisection and every FISTA iteration — with the image split into
+// B200 mapping: a thread-block cluster of CL CTAs does the whole projection
+// — Dykstra, the λ search and every FISTA iteration — with the image split into
 // CL row bands (s <= 256).  Each CTA keeps its band's prox input z, primal x,
 // extrapolated primal xw and momentum duals w in shared memory (rows of pitch
 // SC) and the duals u in registers (tv_prox); inside the FISTA loop the band
@@ -20,7 +20,13 @@
 // and every sum is a fixed tree, so all CTAs take identical branch decisions.
 // Outside the loop (TV norms, Dykstra) the reductions use cluster_sum.
 // Dykstra's state (z_k, p, q) lives in global memory (L2).  No kernel
-// launches inside.
+// launches inside.  K such clusters (one grid) run the λ search K values at a
+// time (reading R22: round of K evaluations, K = 1 the paper's bisection):
+// cluster c computes the prox at the c-th λ of the round, the clusters meet
+// at a global-memory barrier, read the K TV values in order and all take the
+// same decision; the selected cluster broadcasts its prox through global
+// memory.  Every cluster keeps its own copy of the Dykstra state and runs the
+// identical (deterministic) sweep, so no other exchange is needed.
 #pragma once
 
 #include <cooperative_groups.h>
@@ -35,6 +41,7 @@ namespace cg = cooperative_groups;
 
 constexpr int kTvThreads = 512;
 constexpr int kTvMaxCL = 16;
+constexpr int kTvMaxK = 16;  // λ values per search round (clusters)
 
 struct TvArgs {
   const double *v;     // [d] point to project
@@ -44,8 +51,17 @@ struct TvArgs {
   int32_t nonneg;      // 1: X1 ∩ X2 by Dykstra; 0: X1 only
   double tau, tv_tol, rtol, tol;
   int32_t max_it, max_outer;
-  int32_t *stats;      // optional [3]: Dykstra sweeps, bisection steps, FISTA iterations (totals)
+  int32_t *stats;      // optional [4]: Dykstra sweeps, search rounds, FISTA iterations (totals),
+                       // [3] set to 1 if the clusters failed to meet (not co-resident)
   SolveState *state;   // optional: non-finite flag (bad = -2) for the solver
+  // k-ary λ search (reading R22): K clusters evaluate K values of λ per round
+  int32_t K;
+  double *tv_vals;     // [2][K] TV of each cluster's prox, by round parity (global)
+  unsigned int *gbar;  // cross-cluster barrier counter (zeroed before every launch)
+  double *xsel;        // [d] the selected prox, broadcast to the other clusters
+  unsigned long long timeout_ns;  // bound on every cross-cluster wait
+  int32_t warm;        // 1: each prox starts FISTA from the previous prox's duals (reading R23)
+  double *u_state;     // [K][2][d] duals (horizontal, vertical) per pixel, per cluster (warm starts)
 };
 
 constexpr int kTvMaxRpt = 8;
@@ -77,6 +93,7 @@ struct TvBand {
   uint64_t *mbar;
   double *xs;
   uint32_t n_red, n_a, n_b;  // reductions, phase-A and phase-B executions (same in every CTA)
+  double *ush, *usv;         // warm starts: this cluster's duals per global pixel (NULL: cold)
 };
 
 // shared bytes of tv_prox's exchange area (after the reduction scratch)
@@ -243,7 +260,16 @@ __device__ int tv_prox(cg::cluster_group &cl, TvBand &bref, double lam, double r
   for (int i = threadIdx.x; i < b.H * SC; i += blockDim.x) BU.st(i, 0.0);
   for (int i = threadIdx.x; i < b.H * MR * NCW; i += blockDim.x) EU.st(i, 0.0);
   cl.sync();
-  if (!(lam > 0.0)) return 0;  // (no reductions yet: bref.parity unchanged)
+  if (!(lam > 0.0)) {  // x = z (no reductions yet: bref.parity unchanged); the duals become 0
+    if (bref.ush) {
+      for (int i = threadIdx.x; i < R * s; i += blockDim.x) {
+        bref.ush[(int64_t)b.r0 * s + i] = 0.0;
+        bref.usv[(int64_t)b.r0 * s + i] = 0.0;
+      }
+      cl.sync();
+    }
+    return 0;
+  }
   const double hl = 0.5 * lam;
   // Boundary rules as data, so the per-pixel code has no branches: a dual
   // that the oracle never updates (no right / lower neighbour, or a padding
@@ -279,6 +305,27 @@ __device__ int tv_prox(cg::cluster_group &cl, TvBand &bref, double lam, double r
   double uh[MR], uv[MR];
 #pragma unroll
   for (int k = 0; k < MR; ++k) uh[k] = uv[k] = 0.0;
+  // warm start (reading R23): u0 = the previous prox's duals clipped to this
+  // λ's box (a dual with no neighbour has the box [-0, 0]), w0 = u0; the
+  // edge buffers and the row above the band get the same starting values
+  const bool warm = bref.ush != nullptr;
+  if (warm) {
+    const int64_t g0 = (int64_t)b.r0 * s;
+    const double *ush = bref.ush, *usv = bref.usv;
+#pragma unroll
+    for (int k = 0; k < MR; ++k) {
+      if (!((pm >> k) & 1)) continue;
+      const int64_t pix = g0 + (int64_t)(lr0 + k) * s + c;
+      const double hlv = (vm >> k) & 1 ? hl : 0.0;
+      uh[k] = tv_clip(ush[pix], hlh);
+      uv[k] = tv_clip(usv[pix], hlv);
+      WH.st(i0 + k * SC, uh[k]);
+      WV.st(i0 + k * SC, uv[k]);
+      if (lane == 31 && k < nr) EU.st(eb + k * NCW, uh[k]);
+      if (k == nr - 1) BU.st(h * SC + c, uv[k]);
+    }
+    cl.sync();
+  }
   double t = 1.0;
   int it = 1;
   for (;; ++it) {
@@ -294,6 +341,8 @@ __device__ int tv_prox(cg::cluster_group &cl, TvBand &bref, double lam, double r
         const uint32_t q = (b.n_b - 1) & 1;
         mbar_wait_cluster(mb + 8 * (2 + q), ((b.n_b - 1) >> 1) & 1);
         if (up_halo) a_uv = halo_up[(q * SC + c) * 2], a_wv = halo_up[(q * SC + c) * 2 + 1];
+      } else if (it == 1 && up_halo && warm) {  // warm start: the starting duals of the row above (w0 = u0)
+        a_uv = a_wv = tv_clip(bref.usv[(int64_t)(b.r0 - 1) * s + c], hl);
       }
       auto phase_a = [&](auto full_t) {
         constexpr bool full = decltype(full_t)::value;
@@ -460,7 +509,18 @@ __device__ int tv_prox(cg::cluster_group &cl, TvBand &bref, double lam, double r
   // the band below pushed this (last) iteration's xw halo: consume its phase
   if (has_dn) mbar_wait_cluster(mb + 8 * (4 + (b.n_a & 1)), (b.n_a >> 1) & 1);
   ++b.n_a;
-  cl.sync();  // x final everywhere (callers read the neighbours' x)
+  if (warm) {  // this prox's duals: the next prox's starting point
+    const int64_t g0 = (int64_t)b.r0 * s;
+    double *ush = bref.ush, *usv = bref.usv;
+#pragma unroll
+    for (int k = 0; k < MR; ++k) {
+      if (!((pm >> k) & 1)) continue;
+      const int64_t pix = g0 + (int64_t)(lr0 + k) * s + c;
+      ush[pix] = uh[k];
+      usv[pix] = uv[k];
+    }
+  }
+  cl.sync();  // x final everywhere (callers read the neighbours' x); duals stored
   bref.parity = b.parity;
   bref.n_red = b.n_red, bref.n_a = b.n_a, bref.n_b = b.n_b;
   return it - 1;
@@ -482,32 +542,133 @@ __device__ int tv_prox_any(cg::cluster_group &cl, TvBand &b, double lam, double 
   }
 }
 
-__device__ void tv_project_ball(cg::cluster_group &cl, TvBand &b, const TvArgs &a,
-                                int *n_bis, int *n_fista) {
-  for (int i = threadIdx.x; i < (b.r1 - b.r0) * b.SC; i += blockDim.x) b.x[i] = b.z[i];
+__device__ __forceinline__ unsigned tv_ld_acquire(const unsigned *p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ unsigned long long tv_clock() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+
+// The K clusters meet (every thread of every CTA calls it; epoch counts the
+// meetings of this launch, the same in all CTAs).  A cluster that waits past
+// timeout_ns flags stats[3] and from then on no barrier waits again.
+__device__ void tv_grid_sync(cg::cluster_group &cl, const TvArgs &a, unsigned &epoch) {
+  ++epoch;
+  if (a.K <= 1) return;
+  __threadfence();  // this CTA's global writes (TV values, the selected prox) before the arrival
+  cl.sync();
+  if (cl.block_rank() == 0 && threadIdx.x == 0) {
+    atomicAdd(a.gbar, 1u);
+    const unsigned target = (unsigned)a.K * epoch;
+    const unsigned long long t0 = tv_clock();
+    while (tv_ld_acquire(a.gbar) < target) {
+      if (*(volatile int32_t *)(a.stats + 3) || tv_clock() - t0 > a.timeout_ns) {
+        atomicExch(a.stats + 3, 1);
+        break;
+      }
+    }
+    __threadfence();
+  }
+  cl.sync();
+}
+
+// P_X1(b.z) into b.x: the λ search of reading R22 (oracle_project_tv_k), this
+// cluster evaluating value c of every round.  *n_bis counts rounds.
+__device__ void tv_project_ball(cg::cluster_group &cl, TvBand &b, const TvArgs &a, int c, unsigned &epoch,
+                                unsigned &round, int *n_bis, int *n_fista) {
+  const int K = a.K > 1 ? a.K : 1;
+  const int nb = (b.r1 - b.r0) * b.SC;
+  for (int i = threadIdx.x; i < nb; i += blockDim.x) b.x[i] = b.z[i];
   cl.sync();
   if (tv_norm_x(cl, b) <= a.tau) return;
+  // every cluster publishes its TV for the round and reads all K in order
+  auto exchange = [&](double tv, double *all) {
+    const int slot = (int)(round & 1u) * K;
+    ++round;
+    if (K > 1 && cl.block_rank() == 0 && threadIdx.x == 0) a.tv_vals[slot + c] = tv;
+    tv_grid_sync(cl, a, epoch);
+    for (int k = 0; k < K; ++k) all[k] = (K == 1) ? tv : __ldcg(a.tv_vals + slot + k);
+  };
+  double all[kTvMaxK], lam[kTvMaxK];
   double lo = 0.0, hi = 1.0;
-  for (int g = 0; g < 200; ++g) {
-    *n_fista += tv_prox_any(cl, b, hi, a.rtol, a.max_it);
-    if (tv_norm_x(cl, b) <= a.tau) break;
-    lo = hi;
-    hi *= 2.0;
+  bool found = false;
+  for (int g = 0; g * K < 200 && !found; ++g) {
+    const int e = g * K + c;
+    double tv = INFINITY;
+    if (e < 200) {
+      *n_fista += tv_prox_any(cl, b, ldexp(1.0, e), a.rtol, a.max_it);
+      tv = tv_norm_x(cl, b);
+    }
+    exchange(tv, all);
+    for (int k = 0; k < K; ++k) {
+      const int ek = g * K + k;
+      if (ek < 200 && all[k] <= a.tau) {
+        hi = ldexp(1.0, ek);
+        lo = ek == 0 ? 0.0 : ldexp(1.0, ek - 1);
+        found = true;
+        break;
+      }
+    }
+    if (!found) {
+      const int ek = (g + 1) * K - 1 < 199 ? (g + 1) * K - 1 : 199;
+      lo = ldexp(1.0, ek);
+      hi = 2.0 * lo;
+    }
   }
+  int sel = K - 1;
   for (int st = 1; st <= 60; ++st) {
-    const double lam = 0.5 * (lo + hi);
-    *n_fista += tv_prox_any(cl, b, lam, a.rtol, a.max_it);
+    for (int k = 0; k < K; ++k)
+      lam[k] = K == 1 ? 0.5 * (lo + hi) : lo + (hi - lo) * (double)(k + 1) / (double)(K + 1);
+    *n_fista += tv_prox_any(cl, b, lam[c], a.rtol, a.max_it);
     ++*n_bis;
-    const double tv = tv_norm_x(cl, b);
-    if (fabs(tv - a.tau) <= a.tv_tol) break;
-    if (tv > a.tau) lo = lam;
-    else hi = lam;
+    exchange(tv_norm_x(cl, b), all);
+    int hit = -1, ks = -1;
+    for (int k = 0; k < K && hit < 0; ++k)
+      if (fabs(all[k] - a.tau) <= a.tv_tol) hit = k;
+    for (int k = 0; k < K && ks < 0; ++k)
+      if (all[k] <= a.tau) ks = k;
+    if (hit >= 0) {
+      sel = hit;
+      break;
+    }
+    sel = ks >= 0 ? ks : K - 1;
+    if (ks >= 0) {
+      const double nlo = ks > 0 ? lam[ks - 1] : lo;
+      hi = lam[ks];
+      lo = nlo;
+    } else {
+      lo = lam[K - 1];
+    }
+  }
+  if (K > 1) {  // the selected cluster's prox becomes everyone's b.x
+    const int64_t g0 = (int64_t)b.r0 * b.s;
+    if (c == sel)
+      for (int i = threadIdx.x; i < nb; i += blockDim.x) {
+        const int lr = i / b.SC, cc = i - lr * b.SC;
+        if (cc < b.s) a.xsel[g0 + (int64_t)lr * b.s + cc] = b.x[i];
+      }
+    tv_grid_sync(cl, a, epoch);
+    if (c != sel)
+      for (int i = threadIdx.x; i < nb; i += blockDim.x) {
+        const int lr = i / b.SC, cc = i - lr * b.SC;
+        if (cc < b.s) b.x[i] = __ldcg(a.xsel + g0 + (int64_t)lr * b.s + cc);
+      }
+    __syncthreads();
+    tv_grid_sync(cl, a, epoch);  // xsel is rewritten by the next selection only after everyone read it
   }
 }
 
 __global__ void __launch_bounds__(kTvThreads, 1) k_tv_project(const TvArgs a) {
   double *tsm = tv_smem;
   cg::cluster_group cl = cg::this_cluster();
+  const int c = (int)(blockIdx.x / cl.num_blocks());  // this cluster's λ slot of each round
+  const int64_t dd = (int64_t)a.s * a.s;
+  double *zk = a.zk + c * dd, *pp = a.p + c * dd, *qq = a.q + c * dd;  // private Dykstra state
+  unsigned epoch = 0, round = 0;
   TvBand b;
   b.s = a.s;
   b.CL = (int)cl.num_blocks();
@@ -532,13 +693,22 @@ __global__ void __launch_bounds__(kTvThreads, 1) k_tv_project(const TvArgs a) {
   b.mbar = reinterpret_cast<uint64_t *>(b.wsum + (kTvThreads / 32) * 4);
   b.xs = reinterpret_cast<double *>((reinterpret_cast<uintptr_t>(b.mbar + 6) + 15) & ~(uintptr_t)15);
   b.n_red = b.n_a = b.n_b = 0;
+  b.ush = b.usv = nullptr;
+  if (a.warm && a.u_state) {  // this cluster's duals start at 0 for every projection
+    b.ush = a.u_state + (int64_t)c * 2 * dd;
+    b.usv = b.ush + dd;
+    for (int64_t i = (int64_t)b.r0 * a.s + threadIdx.x; i < (int64_t)b.r1 * a.s; i += blockDim.x)
+      b.ush[i] = b.usv[i] = 0.0;
+  }
   if (threadIdx.x == 0) {
     for (int i = 0; i < 6; ++i) mbar_init(b.mbar + i, 1);
     fence_mbar_init();
   }
   cl.sync();
   pdl_wait();  // v is written by the previous kernel
-  pdl_trigger();
+  // with K > 1 the clusters wait for one another: a dependent launched early
+  // could hold the SMs a not-yet-placed cluster needs, so trigger at the end
+  if (a.K <= 1) pdl_trigger();
   const int64_t g0 = (int64_t)b.r0 * a.s;
   const int nb = (b.r1 - b.r0) * b.SC;  // band arrays incl. padding columns
   // band element i (pitch SC) <-> global pixel g0 + gi(i); padding columns have gi < 0
@@ -552,50 +722,53 @@ __global__ void __launch_bounds__(kTvThreads, 1) k_tv_project(const TvArgs a) {
       const int64_t j = gi(i);
       b.z[i] = j >= 0 ? a.v[g0 + j] : 0.0;
     }
-    tv_project_ball(cl, b, a, &n_bis, &n_fista);
-    for (int i = threadIdx.x; i < nb; i += blockDim.x) {
-      const int64_t j = gi(i);
-      if (j >= 0) a.out[g0 + j] = b.x[i];
-    }
+    tv_project_ball(cl, b, a, c, epoch, round, &n_bis, &n_fista);
+    if (c == 0)
+      for (int i = threadIdx.x; i < nb; i += blockDim.x) {
+        const int64_t j = gi(i);
+        if (j >= 0) a.out[g0 + j] = b.x[i];
+      }
   } else {
     // Dykstra: z_0 = v, p_0 = q_0 = 0
     for (int i = threadIdx.x; i < b.npx; i += blockDim.x) {
-      a.zk[g0 + i] = a.v[g0 + i];
-      a.p[g0 + i] = 0.0;
-      a.q[g0 + i] = 0.0;
+      zk[g0 + i] = a.v[g0 + i];
+      pp[g0 + i] = 0.0;
+      qq[g0 + i] = 0.0;
     }
     for (sweeps = 1; sweeps <= a.max_outer; ++sweeps) {
       for (int i = threadIdx.x; i < nb; i += blockDim.x) {
         const int64_t j = gi(i);
-        b.z[i] = j >= 0 ? a.zk[g0 + j] + a.p[g0 + j] : 0.0;
+        b.z[i] = j >= 0 ? zk[g0 + j] + pp[g0 + j] : 0.0;
       }
-      tv_project_ball(cl, b, a, &n_bis, &n_fista);  // y_k in b.x
+      tv_project_ball(cl, b, a, c, epoch, round, &n_bis, &n_fista);  // y_k in b.x
       double acc[1] = {0.0};
       for (int i = threadIdx.x; i < nb; i += blockDim.x) {
         const int64_t j = gi(i);
         if (j < 0) continue;
-        const double zk = a.zk[g0 + j], y = b.x[i];
-        const double pn = zk + a.p[g0 + j] - y;
-        const double sq = y + a.q[g0 + j];
+        const double z0 = zk[g0 + j], y = b.x[i];
+        const double pn = z0 + pp[g0 + j] - y;
+        const double sq = y + qq[g0 + j];
         const double zn = sq > 0.0 ? sq : 0.0;
-        a.p[g0 + j] = pn;
-        a.q[g0 + j] = sq - zn;
-        acc[0] += (zn - zk) * (zn - zk);
-        a.zk[g0 + j] = zn;
+        pp[g0 + j] = pn;
+        qq[g0 + j] = sq - zn;
+        acc[0] += (zn - z0) * (zn - z0);
+        zk[g0 + j] = zn;
       }
       cluster_sum<1>(cl, b, acc);
       if (sqrt(acc[0]) <= a.tol) break;
     }
     if (sweeps > a.max_outer) sweeps = a.max_outer;
-    for (int i = threadIdx.x; i < b.npx; i += blockDim.x) a.out[g0 + i] = a.zk[g0 + i];
+    if (c == 0)
+      for (int i = threadIdx.x; i < b.npx; i += blockDim.x) a.out[g0 + i] = zk[g0 + i];
   }
-  if (b.rank == 0 && threadIdx.x == 0) {
+  if (c == 0 && b.rank == 0 && threadIdx.x == 0) {
     if (a.stats) {
       a.stats[0] += sweeps;
       a.stats[1] += n_bis;
       a.stats[2] += n_fista;
     }
   }
+  if (a.K > 1) pdl_trigger();
 }
 
 }  // namespace poly

@@ -535,6 +535,13 @@ def test_peer_reduce_single_rank(kind):
     p1.solve(xa, 25, gam)
     p2.solve(xb, 25, gam)
     assert torch.equal(xa, xb)
+    # and against the oracle: F (Eq. operator) and the EXACT iterate
+    wo = OW.build(cfg) if kind == "csr" else OW.build(cfg, rows=np.arange(cfg.n),
+                                                        A=w["A"][:, :cfg.d].cpu().numpy())
+    g_ref, l_ref = wo["problem"].F(x.cpu().numpy())
+    assert rel(g2.cpu().numpy(), g_ref) <= TOL32 and abs(l2 - l_ref) <= TOL32 * abs(l_ref)
+    x_ref, _, _ = wo["problem"].solve(25, gam)
+    assert rel(xb.cpu().numpy(), x_ref) <= 1e-3
     p1.close()
     p2.close()
     with pytest.raises(P.PolyError):   # P2P needs the comm path

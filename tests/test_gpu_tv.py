@@ -47,12 +47,13 @@ def _image(side, seed):
     return x + 0.15 * r.standard_normal(side * side)
 
 
-@pytest.mark.parametrize("side", [7, 16, 40])
-def test_tv_ball_projection_matches_oracle(side):
+@pytest.mark.parametrize("side,k,warm", [(7, 1, 0), (16, 1, 0), (40, 1, 0), (16, 3, 0), (40, 4, 0),
+                                         (16, 1, 1), (40, 1, 1), (40, 3, 1)])
+def test_tv_ball_projection_matches_oracle(side, k, warm):
     z = _image(side, side)
     tau = 0.4 * oracle.tv_norm(z)
-    tv = dict(tau=tau, tol=1e-9, rtol=1e-12, max_it=100000)
-    x_ref, steps = oracle.project_tv(z, tau, tv_tol=1e-9, rtol=1e-12, max_it=100000)
+    tv = dict(tau=tau, tol=1e-9, rtol=1e-12, max_it=100000, k=k, cold=1 - warm)
+    x_ref, steps = oracle.project_tv(z, tau, tv_tol=1e-9, rtol=1e-12, max_it=100000, k=k, warm=bool(warm))
     p = _handle(side, _P().POLY_SET_TV, tv)
     x, st = p.project(torch.tensor(z, device="cuda"))
     x = x.cpu().numpy()
@@ -61,13 +62,14 @@ def test_tv_ball_projection_matches_oracle(side):
     p.close()
 
 
-@pytest.mark.parametrize("side", [12, 21])
-def test_tv_nonneg_projection_matches_oracle(side):
+@pytest.mark.parametrize("side,k,warm", [(12, 1, 0), (21, 1, 0), (21, 5, 0), (21, 1, 1), (12, 3, 1)])
+def test_tv_nonneg_projection_matches_oracle(side, k, warm):
     z = _image(side, 3 + side) - 0.1
     tau = 0.5 * oracle.tv_norm(np.maximum(z, 0))
-    tv = dict(tau=tau, tol=1e-8, rtol=1e-12, max_it=100000, dykstra_tol=1e-9, max_outer=100000)
+    tv = dict(tau=tau, tol=1e-8, rtol=1e-12, max_it=100000, dykstra_tol=1e-9, max_outer=100000, k=k,
+              cold=1 - warm)
     x_ref, it = oracle.project_tv_nonneg(z, tau, tv_tol=1e-8, rtol=1e-12, max_it=100000,
-                                         tol=1e-9, max_outer=100000)
+                                         tol=1e-9, max_outer=100000, k=k, warm=bool(warm))
     p = _handle(side, _P().POLY_SET_TV_NONNEG, tv)
     x, st = p.project(torch.tensor(z, device="cuda"))
     x = x.cpu().numpy()
@@ -113,7 +115,7 @@ def test_solve_with_tv_set_matches_oracle():
     y = oracle.Problem(row_ptr=rp, col=col, val=val, y=np.zeros(n), s=s, mu=mu, I_bar=1e3,
                        d=d).mean(xs)
     tv = dict(tau=0.1 * oracle.tv_norm(xs), tol=1e-8, rtol=1e-12, max_it=100000,
-              dykstra_tol=1e-9, max_outer=100000)
+              dykstra_tol=1e-9, max_outer=100000, k=2, warm=1, cold=0)
     o = oracle.Problem(row_ptr=rp, col=col, val=val, y=y, s=s, mu=mu, I_bar=1e3, d=d,
                        set=oracle.SET_TV_NONNEG, tv=tv)
     gam = 0.5
@@ -135,15 +137,21 @@ def test_solve_with_tv_set_matches_oracle():
 
 @pytest.mark.parametrize("side", [100, 200, 256])
 @pytest.mark.parametrize("max_it", [3, 50])
-def test_tv_ball_projection_fixed_iterations_matches_oracle(side, max_it):
+@pytest.mark.parametrize("k,warm", [(1, 0), (4, 0), (1, 1), (4, 1)])
+def test_tv_ball_projection_fixed_iterations_matches_oracle(side, max_it, k, warm):
     """With rtol below reach both sides run exactly max_it FISTA iterations
     per prox, so the cluster kernel must follow the oracle's iteration step
     for step: sides whose bands give the kernel partial row groups (100, 200)
-    and the full 16-row bands of 256, every bisection step included."""
+    and the full 16-row bands of 256, every search round included — one
+    cluster (the paper's bisection) and four clusters (reading R22: four λ per
+    round, the rounds' TV values exchanged through global memory), each with
+    cold and warm-started proxes (reading R23: the duals carried from prox to
+    prox through global memory, the band-edge row included)."""
     z = _image(side, side)
     tau = 0.4 * oracle.tv_norm(z)
-    x_ref, steps = oracle.project_tv(z, tau, tv_tol=1e-3, rtol=1e-30, max_it=max_it)
-    p = _handle(side, _P().POLY_SET_TV, dict(tau=tau, tol=1e-3, rtol=1e-30, max_it=max_it))
+    x_ref, steps = oracle.project_tv(z, tau, tv_tol=1e-3, rtol=1e-30, max_it=max_it, k=k, warm=bool(warm))
+    p = _handle(side, _P().POLY_SET_TV, dict(tau=tau, tol=1e-3, rtol=1e-30, max_it=max_it, k=k,
+                                             cold=1 - warm))
     x, st = p.project(torch.tensor(z, device="cuda"))
     x = x.cpu().numpy()
     assert st[1] == min(steps, 60) and st[2] % max_it == 0 and st[2] >= max_it * st[1]

@@ -9,6 +9,8 @@ optimality independent of the algorithm), closed-form limits (λ = 0, λ -> ∞,
 τ = 0), monotonicity of ||prox(z, λ)||_TV in λ, and scipy's SLSQP solution
 of the same projections written as smooth QPs (a library routine).
 """
+import math
+
 import numpy as np
 import pytest
 from scipy.optimize import minimize
@@ -149,3 +151,73 @@ def test_solve_with_tv_set_reduces_to_orthant_for_large_tau():
                              "dykstra_tol": 1e-9})
     xb, _, _ = p_b.solve(5, 1e-3, x1=np.linspace(-1, 1, d))
     assert xb.min() >= 0.0 and oracle.tv_norm(xb) <= tau + 1e-5
+
+
+@pytest.mark.parametrize("k", [2, 3, 8])
+def test_kary_search_matches_qp_and_binary(k):
+    """Reading R22: k λ values per search round.  The result is still a TV
+    prox of z whose TV is within tv_tol of τ, so at tight tolerances it is the
+    projection (SLSQP QP) like the binary search's; rounds shrink roughly by
+    log2(k + 1); k = 1 is exactly the binary search."""
+    r = np.random.default_rng(11)
+    z = r.standard_normal(16)
+    tau = 0.35 * oracle.tv_norm(z)
+    x1, st1 = oracle.project_tv(z, tau, tv_tol=1e-9, rtol=1e-13, max_it=200000, k=1)
+    xk, stk = oracle.project_tv(z, tau, tv_tol=1e-9, rtol=1e-13, max_it=200000, k=k)
+    assert abs(oracle.tv_norm(xk) - tau) <= 1e-8
+    assert np.allclose(xk, _slsqp(z, tau, nonneg=False), atol=1e-5)
+    assert np.allclose(xk, x1, atol=1e-6)
+    assert stk <= st1 and stk <= math.ceil(st1 / math.log2(k + 1)) + 2
+    xb, _ = oracle.project_tv(z, tau, tv_tol=1e-9, rtol=1e-13, max_it=200000)
+    assert np.array_equal(xb, x1)          # default k = 1: the binary search itself
+    # orthant ∩ TV ball by Dykstra with the k-ary inner search
+    zn = z + 0.3
+    taun = 0.5 * oracle.tv_norm(np.maximum(zn, 0))
+    xn, it = oracle.project_tv_nonneg(zn, taun, tv_tol=1e-10, rtol=1e-13, max_it=200000,
+                                      tol=1e-11, max_outer=100000, k=k)
+    assert xn.min() >= 0.0 and oracle.tv_norm(xn) <= taun + 1e-6
+    assert np.allclose(xn, _slsqp(zn, taun, nonneg=True), atol=1e-4)
+
+
+def test_kary_bracket_large_lambda():
+    """τ far below TV(z): the bracket doubles λ past 2^k; the k-ary bracket
+    (2^(gk + j)) lands on the same power-of-two bracket as the doubling loop."""
+    r = np.random.default_rng(12)
+    z = 40.0 * r.standard_normal(25)
+    tau = 1e-3 * oracle.tv_norm(z)
+    for k in (1, 3, 5):
+        x, st = oracle.project_tv(z, tau, tv_tol=1e-6, rtol=1e-12, max_it=400000, k=k)
+        assert abs(oracle.tv_norm(x) - tau) <= 1e-6, (k, oracle.tv_norm(x), tau)
+
+
+@pytest.mark.parametrize("k", [1, 3])
+def test_warm_started_proxes_match_qp(k):
+    """Reading R23: each prox of a projection starts FISTA from the previous
+    prox's dual solution (clipped to the new box).  The prox itself is the
+    same minimiser, so at tight tolerances the projection is unchanged (QP
+    certificate); at the paper's tolerances the TV bound still holds and the
+    proxes need fewer FISTA iterations than cold starts."""
+    r = np.random.default_rng(11)
+    z = r.standard_normal(16)
+    tau = 0.35 * oracle.tv_norm(z)
+    xw, _ = oracle.project_tv(z, tau, tv_tol=1e-9, rtol=1e-13, max_it=200000, k=k, warm=True)
+    assert abs(oracle.tv_norm(xw) - tau) <= 1e-8
+    assert np.allclose(xw, _slsqp(z, tau, nonneg=False), atol=1e-5)
+    zn = z + 0.3
+    taun = 0.5 * oracle.tv_norm(np.maximum(zn, 0))
+    xn, _ = oracle.project_tv_nonneg(zn, taun, tv_tol=1e-10, rtol=1e-13, max_it=200000, tol=1e-11,
+                                     max_outer=100000, k=k, warm=True)
+    assert xn.min() >= 0.0 and np.allclose(xn, _slsqp(zn, taun, nonneg=True), atol=1e-4)
+    # paper tolerances on a 48 x 48 phantom: fewer FISTA iterations, same guarantees
+    from gen import ct
+    img = ct.ellipse_phantom(5, 48, 6) + 0.2 * r.standard_normal(48 * 48)
+    t = oracle.tv_norm(ct.ellipse_phantom(5, 48, 6))
+    oracle.fista_iterations(True)
+    xc, _ = oracle.project_tv_nonneg(img, t, k=k)
+    n_cold = oracle.fista_iterations(True)
+    xh, _ = oracle.project_tv_nonneg(img, t, k=k, warm=True)
+    n_warm = oracle.fista_iterations(True)
+    assert n_warm < (0.8 if k == 1 else 1.0) * n_cold, (n_warm, n_cold)
+    for x in (xc, xh):
+        assert x.min() >= 0.0 and oracle.tv_norm(x) <= t + 0.05
+    assert np.linalg.norm(xh - xc) <= 1e-3 * np.linalg.norm(xc)

@@ -17,7 +17,7 @@ def tv_norm(x, s):
     return float(np.abs(np.diff(x, axis=1)).sum() + np.abs(np.diff(x, axis=0)).sum())
 
 
-def main(side=256, reps=3):
+def main(side=256, reps=3, k=1, cold=0):
     d = side * side
     xs = ct.ellipse_phantom(3, side, 10)
     z = xs + 0.2 * np.random.default_rng(0).standard_normal(d)
@@ -25,7 +25,7 @@ def main(side=256, reps=3):
     rp = torch.tensor([0, 1], dtype=torch.int64, device="cuda")
     p = P.Poly(row_ptr=rp, col=torch.zeros(1, dtype=torch.int32, device="cuda"),
                val=torch.zeros(1, device="cuda"), d=d, y=torch.zeros(1, dtype=torch.int32, device="cuda"),
-               s=[1.0], mu=[1.0], I_bar=1.0, set=P.POLY_SET_TV_NONNEG, tv=dict(tau=tau))
+               s=[1.0], mu=[1.0], I_bar=1.0, set=P.POLY_SET_TV_NONNEG, tv=dict(tau=tau, k=k, cold=cold))
     zt = torch.tensor(z, device="cuda")
     out = torch.empty_like(zt)
     p.project(zt, out)
@@ -39,11 +39,14 @@ def main(side=256, reps=3):
         times.append(e0.elapsed_time(e1))
     xo = out.cpu().numpy()
     print(json.dumps({"what": "P_X, X = TV ball ∩ orthant (paper tolerances 0.01 / 1e-6 / 1e-4)",
-                      "side": side, "ms": float(np.median(times)), "dykstra_sweeps": stats[0],
-                      "bisection_steps": stats[1], "fista_iterations": stats[2],
-                      "us_per_fista_iteration": 1e3 * float(np.median(times)) / max(stats[2], 1),
+                      "side": side, "lambda_per_round": k or "auto", "prox_start": "cold" if cold else "warm (R23)", "ms": float(np.median(times)),
+                      "dykstra_sweeps": stats[0], "search_rounds": stats[1], "fista_iterations": stats[2],
+                      "us_per_fista_iteration_per_cluster": 1e3 * float(np.median(times)) / max(stats[2], 1),
                       "tv_out": tv_norm(xo, side), "tau": tau, "min": float(xo.min())}))
 
 
 if __name__ == "__main__":
-    main()
+    # arguments: k:cold pairs, e.g. 1:1 1:0 4:0
+    for spec in sys.argv[1:] or ["1:1", "1:0"]:
+        k, cold = (int(v) for v in spec.split(":"))
+        main(k=k, cold=cold)
