@@ -229,7 +229,7 @@ __device__ __forceinline__ double tv_clip(double v, double h) {
 // rows per thread for pitch SC: bands of at most ceil(SC/16) rows over 512/SC row groups
 __host__ __device__ constexpr int tv_mr(int SC) { return ((SC + 15) / 16 + kTvThreads / SC - 1) / (kTvThreads / SC); }
 
-template <int SC>
+template <int SC, bool WARM>
 __device__ int tv_prox(cg::cluster_group &cl, TvBand &bref, double lam, double rtol, int max_it) {
   // a private copy of the band (registers): tv_prox is not inlined, and the
   // reductions' parity flips on the caller's (local-memory) copy would put a
@@ -308,7 +308,10 @@ __device__ int tv_prox(cg::cluster_group &cl, TvBand &bref, double lam, double r
   // warm start (reading R23): u0 = the previous prox's duals clipped to this
   // λ's box (a dual with no neighbour has the box [-0, 0]), w0 = u0; the
   // edge buffers and the row above the band get the same starting values
-  const bool warm = bref.ush != nullptr;
+#ifndef POLY_TV_WARM_CODE
+#define POLY_TV_WARM_CODE 1
+#endif
+  constexpr bool warm = POLY_TV_WARM_CODE && WARM;
   if (warm) {
     const int64_t g0 = (int64_t)b.r0 * s;
     const double *ush = bref.ush, *usv = bref.usv;
@@ -326,6 +329,18 @@ __device__ int tv_prox(cg::cluster_group &cl, TvBand &bref, double lam, double r
     }
     cl.sync();
   }
+  // the row above the band at iteration 1: (u_v, w_v) of its starting duals
+  // (0 cold, u0 warm) placed in the halo slot iteration 1 reads — the slot the
+  // band above last pushed into, consumed by the previous prox; its next push
+  // goes to the other slot, and the one after can only come after this CTA's
+  // iteration-1 phase A (it waits on a reduction this CTA joins after it)
+  if (up_halo) {
+    const uint32_t q = (b.n_b - 1) & 1;
+    const double v0 = warm ? tv_clip(bref.usv[(int64_t)(b.r0 - 1) * s + c], hl) : 0.0;
+    double *hu = const_cast<double *>(halo_up) + (q * SC + c) * 2;
+    hu[0] = v0;
+    hu[1] = v0;
+  }
   double t = 1.0;
   int it = 1;
   for (;; ++it) {
@@ -337,12 +352,10 @@ __device__ int tv_prox(cg::cluster_group &cl, TvBand &bref, double lam, double r
     if (nr > 0) {  // warp-uniform
       double a_uv = 0.0, a_wv = 0.0;  // row above
       if (up_local) a_uv = BU.ld((h - 1) * SC + c), a_wv = WV.ld(i0 - SC);
-      if (it > 1 && lr0 == 0 && has_up) {  // (u_v, w_v) halo pushed by the band above in its last phase B
+      if (lr0 == 0 && has_up) {  // (u_v, w_v) halo pushed by the band above in its last phase B
         const uint32_t q = (b.n_b - 1) & 1;
-        mbar_wait_cluster(mb + 8 * (2 + q), ((b.n_b - 1) >> 1) & 1);
+        if (it > 1) mbar_wait_cluster(mb + 8 * (2 + q), ((b.n_b - 1) >> 1) & 1);
         if (up_halo) a_uv = halo_up[(q * SC + c) * 2], a_wv = halo_up[(q * SC + c) * 2 + 1];
-      } else if (it == 1 && up_halo && warm) {  // warm start: the starting duals of the row above (w0 = u0)
-        a_uv = a_wv = tv_clip(bref.usv[(int64_t)(b.r0 - 1) * s + c], hl);
       }
       auto phase_a = [&](auto full_t) {
         constexpr bool full = decltype(full_t)::value;
@@ -509,9 +522,11 @@ __device__ int tv_prox(cg::cluster_group &cl, TvBand &bref, double lam, double r
   // the band below pushed this (last) iteration's xw halo: consume its phase
   if (has_dn) mbar_wait_cluster(mb + 8 * (4 + (b.n_a & 1)), (b.n_a >> 1) & 1);
   ++b.n_a;
-  if (warm) {  // this prox's duals: the next prox's starting point
+  // this prox's duals: the next prox's starting point (the pointers are
+  // re-read here, volatile, so that they are not kept live through the loop)
+  if (warm) {
+    double *ush = *(double *volatile *)&bref.ush, *usv = *(double *volatile *)&bref.usv;
     const int64_t g0 = (int64_t)b.r0 * s;
-    double *ush = bref.ush, *usv = bref.usv;
 #pragma unroll
     for (int k = 0; k < MR; ++k) {
       if (!((pm >> k) & 1)) continue;
@@ -530,15 +545,16 @@ __device__ int tv_prox(cg::cluster_group &cl, TvBand &bref, double lam, double r
 __noinline__
 #endif
 __device__ int tv_prox_any(cg::cluster_group &cl, TvBand &b, double lam, double rtol, int max_it) {
+  const bool w = b.ush != nullptr;
   switch (b.SC) {
-    case 32: return tv_prox<32>(cl, b, lam, rtol, max_it);
-    case 64: return tv_prox<64>(cl, b, lam, rtol, max_it);
-    case 96: return tv_prox<96>(cl, b, lam, rtol, max_it);
-    case 128: return tv_prox<128>(cl, b, lam, rtol, max_it);
-    case 160: return tv_prox<160>(cl, b, lam, rtol, max_it);
-    case 192: return tv_prox<192>(cl, b, lam, rtol, max_it);
-    case 224: return tv_prox<224>(cl, b, lam, rtol, max_it);
-    default: return tv_prox<256>(cl, b, lam, rtol, max_it);
+    case 32: return w ? tv_prox<32, true>(cl, b, lam, rtol, max_it) : tv_prox<32, false>(cl, b, lam, rtol, max_it);
+    case 64: return w ? tv_prox<64, true>(cl, b, lam, rtol, max_it) : tv_prox<64, false>(cl, b, lam, rtol, max_it);
+    case 96: return w ? tv_prox<96, true>(cl, b, lam, rtol, max_it) : tv_prox<96, false>(cl, b, lam, rtol, max_it);
+    case 128: return w ? tv_prox<128, true>(cl, b, lam, rtol, max_it) : tv_prox<128, false>(cl, b, lam, rtol, max_it);
+    case 160: return w ? tv_prox<160, true>(cl, b, lam, rtol, max_it) : tv_prox<160, false>(cl, b, lam, rtol, max_it);
+    case 192: return w ? tv_prox<192, true>(cl, b, lam, rtol, max_it) : tv_prox<192, false>(cl, b, lam, rtol, max_it);
+    case 224: return w ? tv_prox<224, true>(cl, b, lam, rtol, max_it) : tv_prox<224, false>(cl, b, lam, rtol, max_it);
+    default: return w ? tv_prox<256, true>(cl, b, lam, rtol, max_it) : tv_prox<256, false>(cl, b, lam, rtol, max_it);
   }
 }
 
