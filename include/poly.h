@@ -177,9 +177,8 @@ typedef struct poly_problem {
    * col, val are unused. */
   int32_t pb_side, pb_views, pb_bins, pb_reserved;
   /* TV sets: λ values evaluated per round of the TV-prox search, one
-   * thread-block cluster each (reading R22; 1 = the paper's bisection);
-   * 0 = as many clusters as can be resident (at most 16).  More than can be
-   * resident: POLY_EUNSUPPORTED. */
+   * thread-block cluster each (reading R22); 0 or 1 = the paper's bisection
+   * (the default), up to 16.  More than can be resident: POLY_EUNSUPPORTED. */
   int32_t tv_k;
   /* TV sets: 0 (default) = each TV prox of one projection starts FISTA from
    * the dual solution of the previous prox (same cluster; the first from 0),

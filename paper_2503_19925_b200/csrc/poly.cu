@@ -2018,7 +2018,7 @@ int poly_init(const poly_problem *pin, poly_handle **out) {
         cudaFuncSetAttribute((const void *)&k_tv_project, cudaFuncAttributeNonPortableClusterSizeAllowed,
                              1) != cudaSuccess)
       return bail(fail(POLY_ECUDA, "TV kernel attributes: %s", cudaGetErrorString(cudaGetLastError())));
-    {  // λ values per round: as many clusters as can be resident at once (or the caller's tv_k)
+    {  // λ values per round (clusters): the caller's tv_k, if that many can be resident
       cudaLaunchConfig_t cfg = {};
       cfg.gridDim = dim3(h->tv_cl);
       cfg.blockDim = dim3(kTvThreads);
@@ -2035,7 +2035,7 @@ int poly_init(const poly_problem *pin, poly_handle **out) {
         cudaGetLastError();
         return bail(fail(POLY_EUNSUPPORTED, "TV: a %d-CTA cluster cannot be resident", h->tv_cl));
       }
-      const int want = p.tv_k > 0 ? p.tv_k : std::min(maxc, kTvMaxK);
+      const int want = p.tv_k > 1 ? p.tv_k : 1;  // default: the paper's bisection (R22 measured slower)
       if (want > maxc || want > kTvMaxK)
         return bail(fail(POLY_EUNSUPPORTED, "TV: tv_k = %d clusters requested, %d can be resident", want,
                          std::min(maxc, kTvMaxK)));

@@ -39,7 +39,7 @@ def main(side=256, reps=3, k=1, cold=0):
         times.append(e0.elapsed_time(e1))
     xo = out.cpu().numpy()
     print(json.dumps({"what": "P_X, X = TV ball ∩ orthant (paper tolerances 0.01 / 1e-6 / 1e-4)",
-                      "side": side, "lambda_per_round": k or "auto", "prox_start": "cold" if cold else "warm (R23)", "ms": float(np.median(times)),
+                      "side": side, "lambda_per_round": max(k, 1), "prox_start": "cold" if cold else "warm (R23)", "ms": float(np.median(times)),
                       "dykstra_sweeps": stats[0], "search_rounds": stats[1], "fista_iterations": stats[2],
                       "us_per_fista_iteration_per_cluster": 1e3 * float(np.median(times)) / max(stats[2], 1),
                       "tv_out": tv_norm(xo, side), "tau": tau, "min": float(xo.min())}))
