@@ -62,7 +62,7 @@ template <typename T>
 __global__ void __launch_bounds__(128) k_csc_backward(const CscEnt<T> *__restrict__ ent,
                                                       const int64_t *__restrict__ slice_off,
                                                       int32_t d, const float *__restrict__ r,
-                                                      double *__restrict__ g) {
+                                                      double *__restrict__ g, const int32_t *colmap) {
   __shared__ double part[4][32];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t s0 = slice_off[blockIdx.x], s1 = slice_off[blockIdx.x + 1];
@@ -71,24 +71,26 @@ __global__ void __launch_bounds__(128) k_csc_backward(const CscEnt<T> *__restric
   pdl_wait();  // r is written by the forward pass
   double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
   int64_t k = warp;
+  // (a marked layout's padding entries carry row -1 and value 0)
+  auto rv = [&](int32_t row) { return row >= 0 ? (double)__ldg(r + row) : 0.0; };
   for (; k + 12 < len; k += 16) {
     const CscEnt<T> q0 = p[(k) * 32], q1 = p[(k + 4) * 32], q2 = p[(k + 8) * 32],
                     q3 = p[(k + 12) * 32];
-    a0 = fma((double)q0.val, (double)__ldg(r + q0.row), a0);
-    a1 = fma((double)q1.val, (double)__ldg(r + q1.row), a1);
-    a2 = fma((double)q2.val, (double)__ldg(r + q2.row), a2);
-    a3 = fma((double)q3.val, (double)__ldg(r + q3.row), a3);
+    a0 = fma((double)q0.val, rv(q0.row), a0);
+    a1 = fma((double)q1.val, rv(q1.row), a1);
+    a2 = fma((double)q2.val, rv(q2.row), a2);
+    a3 = fma((double)q3.val, rv(q3.row), a3);
   }
   for (; k < len; k += 4) {
     const CscEnt<T> q = p[k * 32];
-    a0 = fma((double)q.val, (double)__ldg(r + q.row), a0);
+    a0 = fma((double)q.val, rv(q.row), a0);
   }
   part[warp][lane] = (a0 + a1) + (a2 + a3);
   __syncthreads();
   if (warp == 0) {
-    const int c = blockIdx.x * 32 + lane;
+    const int c = colmap ? colmap[blockIdx.x * 32 + lane] : blockIdx.x * 32 + lane;
     const double v = (part[0][lane] + part[1][lane]) + (part[2][lane] + part[3][lane]);
-    if (c < d) g[c] = v;
+    if (c >= 0 && c < d) g[c] = v;
   }
   pdl_trigger();
 }
@@ -387,15 +389,17 @@ struct StepEpi {
 // partials in warp order) to g, or — with the step epilogue on — v, the
 // orthant clamp and the block's ||v - c||²
 __device__ __forceinline__ void backward_column_out(double (*part)[32], const StepEpi &e, double *g, int32_t d,
-                                                    int64_t sl, int lane) {
-  const int64_t c = sl * 32 + lane;
+                                                    int64_t sl, int lane, const int32_t *colmap = nullptr) {
+  // colmap (tiled slices): the column of each slot, -1 for an empty slot
+  const int64_t c = colmap ? (int64_t)colmap[sl * 32 + lane] : sl * 32 + lane;
   const double v = (part[0][lane] + part[1][lane]) + (part[2][lane] + part[3][lane]);
+  const bool ok = c >= 0 && c < d;
   if (!e.on) {
-    if (c < d) g[c] = v;
+    if (ok) g[c] = v;
     return;
   }
   double q = 0.0;
-  if (c < d) {
+  if (ok) {
     const double gc = v / e.n_norm;
     double vv = e.anchor[c] - e.state->gamma * gc;
     if (e.set == 2 || e.set == 3) vv = vv > 0.0 ? vv : 0.0;
@@ -411,14 +415,15 @@ __device__ __forceinline__ void backward_column_out(double (*part)[32], const St
 template <typename T>
 __global__ void __launch_bounds__(POLY_SELL_LB_B) k_sell16_backward(const Sell16 s, int64_t nslices,
                                                               int32_t d, const float *__restrict__ r,
-                                                              double *__restrict__ g, const StepEpi e) {
+                                                              double *__restrict__ g, const StepEpi e,
+                                                              const int32_t *colmap) {
   __shared__ double part[4][32];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   pdl_wait();  // r is written by the forward pass
   for (int64_t sl = blockIdx.x; sl < nslices; sl += gridDim.x) {
     part[warp][lane] = sell16_dot<T, POLY_SELL_UNROLL_B>(s, sl, warp, lane, r);
     __syncthreads();
-    if (warp == 0) backward_column_out(part, e, g, d, sl, lane);
+    if (warp == 0) backward_column_out(part, e, g, d, sl, lane, colmap);
     __syncthreads();
   }
   pdl_trigger();
@@ -437,8 +442,25 @@ __global__ void k_sell16_pack(const CscEnt<T> *ent, const int64_t *slice_off, in
     const int64_t o0 = slice_off[sl], len = slice_off[sl + 1] - o0;
     const int64_t g0 = off16[sl], ng = off16[sl + 1] - g0;
     const int64_t li = sl * 32 + lane;
-    const int64_t mylen = li < nlanes ? (row_ptr ? row_ptr[li + 1] - row_ptr[li] : (int64_t)cnt[li]) : 0;
-    int32_t prev = (4 * warp < min(mylen, len)) ? ent[(o0 + 4 * warp) * 32 + lane].row : 0;
+    // marked layout (row_ptr and cnt NULL): every lane spans the slice, padding
+    // entries carry row -1 (they become delta 0 / value 0); the chain starts at
+    // the warp's first real entry so that padding gathers stay in range
+    const bool marked = !row_ptr && !cnt;
+    const int64_t mylen = marked ? len : (li < nlanes ? (row_ptr ? row_ptr[li + 1] - row_ptr[li] : (int64_t)cnt[li]) : 0);
+    int32_t prev = 0;
+    if (marked) {
+      bool found = false;
+      for (int64_t g = warp; g < ng && !found; g += 4)
+        for (int j = 0; j < 4 && !found; ++j) {
+          const int64_t k = 4 * g + j;
+          if (k < len) {
+            const int32_t r = ent[(o0 + k) * 32 + lane].row;
+            if (r >= 0) prev = r, found = true;
+          }
+        }
+    } else if (4 * warp < min(mylen, len)) {
+      prev = ent[(o0 + 4 * warp) * 32 + lane].row;
+    }
     base[(sl * 4 + warp) * 32 + lane] = prev;
     for (int64_t g = warp; g < ng; g += 4) {
       int32_t dd[4];
@@ -450,6 +472,7 @@ __global__ void k_sell16_pack(const CscEnt<T> *ent, const int64_t *slice_off, in
         vv[j] = (T)0;
         if (k < mylen) {
           const CscEnt<T> e = ent[(o0 + k) * 32 + lane];
+          if (e.row < 0) continue;  // marked padding: delta 0, value 0
           const int64_t dlt = (int64_t)e.row - prev;
           if (dlt < -32768 || dlt > 32767) atomicOr(overflow, 1);
           dd[j] = (int32_t)dlt;
@@ -564,6 +587,79 @@ __global__ void k_slice_len(const int32_t *cnt, int32_t d, int32_t nslices, int6
   int32_t m = 0;
   for (int c = 32 * s; c < min(d, 32 * s + 32); ++c) m = max(m, cnt[c]);
   len[s] = m;
+}
+
+// ---- tiled, block-synchronised SELL-32 of Aᵀ (square images, poly_init only)
+// Slices are 4 x 8 pixel tiles (colmap: slot -> column), and the lanes' entry
+// chains are re-aligned at every row block of RB rows: within block b every
+// lane of slice s has boff[s][b] .. boff[s][b+1] steps (the slice's largest
+// count in that block), padded with marked entries (row -1).  For the CT
+// matrix a row block is ~15 views, so a warp's 32 gathers stay within a few
+// views of r (4.4 instead of 18.8 sectors per request) for
+// 12 % padding.
+__global__ void k_colblk_count(const int32_t *rows, const int32_t *col, int64_t nnz, int32_t RB, int32_t NBK,
+                               int32_t *blkcnt) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < nnz; e += (int64_t)gridDim.x * blockDim.x)
+    atomicAdd(blkcnt + (int64_t)col[e] * NBK + rows[e] / RB, 1);
+}
+
+// per column: exclusive prefix of its block counts (in place into bpre)
+__global__ void k_colblk_prefix(const int32_t *blkcnt, int32_t d, int32_t NBK, int32_t *bpre) {
+  for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < d; c += gridDim.x * blockDim.x) {
+    int32_t a = 0;
+    for (int b = 0; b < NBK; ++b) {
+      bpre[(int64_t)c * NBK + b] = a;
+      a += blkcnt[(int64_t)c * NBK + b];
+    }
+  }
+}
+
+// per slice: the step offset of each row block (max count over the lanes) and the length
+__global__ void k_slice_blocks(const int32_t *blkcnt, const int32_t *colmap, int32_t nslices, int32_t NBK,
+                               int32_t *boff, int64_t *slen) {
+  for (int s = blockIdx.x * blockDim.x + threadIdx.x; s < nslices; s += gridDim.x * blockDim.x) {
+    int64_t a = 0;
+    for (int b = 0; b < NBK; ++b) {
+      int32_t m = 0;
+      for (int l = 0; l < 32; ++l) {
+        const int32_t c = colmap[s * 32 + l];
+        if (c >= 0) m = max(m, blkcnt[(int64_t)c * NBK + b]);
+      }
+      boff[(int64_t)s * NBK + b] = (int32_t)a;
+      a += m;
+    }
+    slen[s] = a;
+  }
+}
+
+template <typename T>
+__global__ void k_sell_mark(CscEnt<T> *ent, int64_t count) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < count; i += (int64_t)gridDim.x * blockDim.x) {
+    CscEnt<T> q;
+    q.row = -1;
+    q.val = (T)0;
+    ent[i] = q;
+  }
+}
+
+template <typename T>
+__global__ void k_sell_fill_sync(const int32_t *sorted_col, const int32_t *perm, const int32_t *rows, const T *val,
+                                 const int64_t *colptr, const int32_t *bpre, const int32_t *boff,
+                                 const int32_t *slot_of, const int64_t *slice_off, int32_t RB, int32_t NBK,
+                                 int64_t nnz, CscEnt<T> *ent) {
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < nnz; k += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t c = sorted_col[k];
+    const int32_t e = perm[k];
+    const int32_t r = rows[e];
+    const int32_t b = r / RB;
+    const int64_t j = k - colptr[c] - bpre[(int64_t)c * NBK + b];
+    const int32_t slot = slot_of[c];
+    const int32_t s = slot >> 5;
+    CscEnt<T> q;
+    q.row = r;
+    q.val = val[e];
+    ent[(slice_off[s] + boff[(int64_t)s * NBK + b] + j) * 32 + (slot & 31)] = q;
+  }
 }
 
 // entry k of the column-sorted order (stable: ascending row within a column)

@@ -24,6 +24,13 @@
 
 namespace poly {
 
+#ifndef POLY_EXP_DEG32
+#define POLY_EXP_DEG32 9  // exp polynomial degree of the link for fp32 A (common.cuh exp_nonpos)
+#endif
+#ifndef POLY_K1_LINK_SPLIT
+#define POLY_K1_LINK_SPLIT 1  // WPR > 1: the row group's warps split the link's bins
+#endif
+
 struct DenseArgs {
   const void *A;
   int64_t lda;           // row pitch, elements
@@ -174,6 +181,34 @@ __device__ __forceinline__ double link_exact_pair(const double *sp, int W, int r
   return yv - Ii * hs;
 }
 
+// The mode-0 link of two rows split over the WPR warps of a row group (W <=
+// 32): warp w evaluates bins j = w + WPR l (l = lane & 15) of row q (lanes
+// 0-15) and row q+1 (lanes 16-31), so each exp is computed once per row
+// instead of once per warp; returns this half's partial sums Σ s_j e_j and
+// Σ (s_j/μ_j)(1 - e_j) (or s_j z under the ReLU) in *hs, *Hs.
+template <bool LOSS, int DEG, int WPR>
+__device__ __forceinline__ void link_partial_pair(const double *sp, int W, int relu, double z,
+                                                  const float *srow, int w, double *hs_out,
+                                                  double *Hs_out) {
+  const bool neg = relu && z < 0.0;
+  const double zc = neg ? 0.0 : z;
+  const int j = w + WPR * (threadIdx.x & 15);
+  double hs = 0.0, Hs = 0.0;
+  if (j < W) {
+    const double sj = srow ? (double)srow[j] : sp[j];
+    const double e = exp_nonpos<DEG>(-sp[kMaxW + j] * zc);
+    hs = sj * e;
+    if (LOSS) Hs = neg ? sj * z : sj * sp[2 * kMaxW + j] * (1.0 - e);
+  }
+#pragma unroll
+  for (int o = 8; o > 0; o >>= 1) {
+    hs += __shfl_xor_sync(0xffffffffu, hs, o);
+    if (LOSS) Hs += __shfl_xor_sync(0xffffffffu, Hs, o);
+  }
+  *hs_out = hs;
+  *Hs_out = Hs;
+}
+
 __device__ __forceinline__ double load_y(const unsigned char *yb, int ytype, int r) {
   if (ytype == 0) return (double)((const int32_t *)yb)[2 * r];
   if (ytype == 1) return (double)((const float *)yb)[2 * r];
@@ -248,7 +283,8 @@ __global__ void __launch_bounds__(32 * (NW + 1), 1) k_dense_loss_grad(const Dens
   T *ring = reinterpret_cast<T *>(smem);
   unsigned char *side = smem + (size_t)S * stage_elems * sizeof(T);
   double *red = reinterpret_cast<double *>(side + (size_t)S * a.side_stride);  // [2][G][RG][WPR]
-  double *sp = red + 2 * G * RG * WPR;                                         // [3*kMaxW]
+  double *hred = red + 2 * G * RG * WPR;                                       // [2][G][RG][WPR][2]
+  double *sp = hred + 4 * G * RG * WPR;                                        // [3*kMaxW]
   uint64_t *full = reinterpret_cast<uint64_t *>(sp + 3 * kMaxW);
   uint64_t *empty = full + S;
   double *lsum = reinterpret_cast<double *>(empty + S);  // [NW]
@@ -426,7 +462,28 @@ __global__ void __launch_bounds__(32 * (NW + 1), 1) k_dense_loss_grad(const Dens
     }
     // a2-a4
     if (PAIR && a.mode == 0 && a.W <= 32) {
-      // two rows per link: lanes 0-15 row q, lanes 16-31 row q+1
+      // two rows per link: lanes 0-15 row q, lanes 16-31 row q+1; with WPR > 1
+      // the group's warps split the bins (link_partial_pair) and exchange the
+      // partial sums through shared memory (a second named barrier)
+      constexpr int DEG = std::is_same<T, double>::value ? 13 : POLY_EXP_DEG32;
+      double *hb = hred + ((size_t)(buf ^ 1) * G + grp) * RG * WPR * 2;  // (buf flipped after the z exchange)
+      constexpr bool SPLIT = WPR > 1 && POLY_K1_LINK_SPLIT;
+      if (SPLIT) {
+#pragma unroll
+        for (int q = 0; q < RG; q += 2) {
+          const int h = lane >> 4;
+          const int lr = grp + G * (q + h);
+          const bool valid = lr < rows;
+          const float *srow = (valid && has_rowspec) ? (const float *)(sd + soff) + lr * a.W : nullptr;
+          double hs, Hs;
+          link_partial_pair<LOSS, DEG, WPR>(sp, a.W, a.relu, valid ? zh[q >> 1] : 0.0, srow, w, &hs, &Hs);
+          if ((lane & 15) == 0) {
+            hb[((q + h) * WPR + w) * 2] = hs;
+            if (LOSS) hb[((q + h) * WPR + w) * 2 + 1] = Hs;
+          }
+        }
+        named_bar_sync(1 + grp, 32 * WPR);
+      }
 #pragma unroll
       for (int q = 0; q < RG; q += 2) {
         const int h = lane >> 4;
@@ -435,8 +492,25 @@ __global__ void __launch_bounds__(32 * (NW + 1), 1) k_dense_loss_grad(const Dens
         const double yv = valid ? load_y(sd + yoff, a.ytype, lr) : 0.0;
         const double Ii = (valid && has_rowspec) ? (double)((const float *)(sd + ioff))[lr] : a.I_bar;
         const float *srow = (valid && has_rowspec) ? (const float *)(sd + soff) + lr * a.W : nullptr;
-        const double rh = link_exact_pair<LOSS, std::is_same<T, double>::value ? 13 : 9>(
-            sp, a.W, a.relu, valid ? zh[q >> 1] : 0.0, yv, Ii, srow, valid && w == 0, &lacc);
+        double rh;
+        if (SPLIT) {  // the row's partial sums over the group's warps, in warp order
+          double hs = 0.0, Hs = 0.0;
+#pragma unroll
+          for (int k = 0; k < WPR; ++k) {
+            hs += hb[((q + h) * WPR + k) * 2];
+            if (LOSS) Hs += hb[((q + h) * WPR + k) * 2 + 1];
+          }
+          const double zq = valid ? zh[q >> 1] : 0.0;
+          if (LOSS) {  // both halves' terms land on lane 0 (the lane whose lacc is kept)
+            const double lt = (valid && w == 0) ? yv * zq - Ii * Hs : 0.0;
+            const double lo = __shfl_sync(0xffffffffu, lt, 16);
+            if (lane == 0) lacc += lt + lo;
+          }
+          rh = yv - Ii * hs;
+        } else {
+          rh = link_exact_pair<LOSS, DEG>(sp, a.W, a.relu, valid ? zh[q >> 1] : 0.0, yv, Ii, srow, valid && w == 0,
+                                          &lacc);
+        }
         const T r2[2] = {(T)__shfl_sync(0xffffffffu, rh, 0), (T)__shfl_sync(0xffffffffu, rh, 16)};
 #pragma unroll
         for (int u = 0; u < 2; ++u) {
@@ -470,7 +544,7 @@ __global__ void __launch_bounds__(32 * (NW + 1), 1) k_dense_loss_grad(const Dens
         const float *srow = has_rowspec ? (const float *)(sd + soff) + lr * a.W : nullptr;
         const double r =
             a.mode == 0
-                ? link_exact<LOSS, std::is_same<T, double>::value ? 13 : 9>(sp, a.W, a.relu, zp[q], yv,
+                ? link_exact<LOSS, std::is_same<T, double>::value ? 13 : POLY_EXP_DEG32>(sp, a.W, a.relu, zp[q], yv,
                                                                            Ii, srow, w == 0, &lacc)
                 : row_residual<LOSS>(sp, a.W, a.relu, zp[q], yv, Ii, srow, w == 0, &lacc, a.mode);
         const T rt = (T)r;

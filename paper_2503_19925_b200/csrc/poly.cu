@@ -252,6 +252,7 @@ struct poly_handle {
   int nslices = 0;                     // K4b blocks: 32-column SELL slices of A^T
   void *sell = nullptr;                // CscEnt<T>[slice_off[nslices] * 32]
   int64_t *slice_off = nullptr;        // [nslices + 1] slice start, in 32-entry steps
+  int32_t *colmap = nullptr;           // tiled K4b slices: column of each slot (-1 empty), NULL = identity
   float *rbuf = nullptr;               // [n_local] residuals between K4f and K4b
   float *xa32 = nullptr, *xh32 = nullptr, *xin32 = nullptr;  // CSR: fp32 copies of xa, xh, a caller's x
   int tr_side = 0;                     // CSR, d = s²: fp32 copies also hold x transposed at [d, 2d)
@@ -465,18 +466,20 @@ int enqueue_pass(poly_handle *h, const double *x, bool loss) {
     TRY(launch(h, kSell16Fwd[p.dtype][loss ? 1 : 0], dim3(h->k4f16_grid), dim3(128), 0, true,
                h->fwd16, (int64_t)h->nrslices, a));
     return launch(h, kSell16Bwd[p.dtype], dim3(h->k4b16_grid), dim3(128), 0, true, h->bwd16,
-                  (int64_t)h->nslices, (int32_t)p.d, (const float *)h->rbuf, h->partials, h->epi);
+                  (int64_t)h->nslices, (int32_t)p.d, (const float *)h->rbuf, h->partials, h->epi,
+                  (const int32_t *)h->colmap);
   }
   TRY(launch(h, kCsrFwd[p.dtype][loss ? 1 : 0], dim3(h->k4_grid), dim3(128), 0, true,
              (const void *)h->sell_rows, (const int64_t *)h->row_slice_off, a));
   int32_t d32 = (int32_t)p.d;
   const float *rb = h->rbuf;
   double *gp = h->partials;
+  const int32_t *cmap = h->colmap;
   if (p.dtype == POLY_F32)
     return launch(h, kCscBwd[0], dim3(h->nslices), dim3(128), 0, true,
-                  (const CscEnt<float> *)h->sell, (const int64_t *)h->slice_off, d32, rb, gp);
+                  (const CscEnt<float> *)h->sell, (const int64_t *)h->slice_off, d32, rb, gp, cmap);
   return launch(h, kCscBwd[1], dim3(h->nslices), dim3(128), 0, true,
-                (const CscEnt<double> *)h->sell, (const int64_t *)h->slice_off, d32, rb, gp);
+                (const CscEnt<double> *)h->sell, (const int64_t *)h->slice_off, d32, rb, gp, cmap);
 }
 
 float *x32_of(poly_handle *h, const double *x) {
@@ -1026,7 +1029,8 @@ int setup_dense(poly_handle *h) {
   const int RG = dv->RPS / G;
   const size_t stage = (size_t)dv->RPS * p.lda * h->elsize;
   h->k1_side = (int)(((size_t)dv->RPS * (12 + 4 * p.W) + 15) / 16 * 16);
-  const size_t fixed = (size_t)2 * G * RG * dv->WPR * 8 + 3 * kMaxW * 8 + 2 * 8 * 8 + dv->NW * 8 + 256;
+  // z exchange [2][G][RG][WPR] + link partials [2][G][RG][WPR][2] + spectrum + mbarriers + loss
+  const size_t fixed = (size_t)6 * G * RG * dv->WPR * 8 + 3 * kMaxW * 8 + 2 * 8 * 8 + dv->NW * 8 + 256;
   int S = (int)(kRingBudget / (stage + h->k1_side));
   S = std::max(2, std::min(8, S));
   size_t ring = (size_t)S * stage;
@@ -1192,7 +1196,44 @@ int build_sell_t(poly_handle *h) {
   k_widen<<<(int)std::min<int64_t>(4096, (d + 256) / 256), 256, 0, st>>>(cnt, d, cnt64);
   size_t t2 = tb2;
   cub::DeviceScan::ExclusiveSum(tstore, t2, cnt64, colptr, (int)d + 1, st);
-  k_slice_len<<<(h->nslices + 255) / 256, 256, 0, st>>>(cnt, (int32_t)d, h->nslices, slen);
+  // opt-in (POLY_K4B_SYNC=1), square images (d = side², side % 8 == 0): 4 x 8
+  // pixel tiles as slices and lane chains re-aligned every row block (csr.cuh
+  // k_sell_fill_sync).  On C4 it cuts K4b's gather sectors per request from
+  // 16.9 to 7.2 but adds 9 % padding and runs slower (46 vs 40 us): the pass
+  // is latency-bound, not sector-bound
+  const int side = h->tr_side;
+  const bool synced = side > 0 && side % 8 == 0 && (int64_t)side * side == d && nnz > 0 &&
+                      getenv("POLY_K4B_SYNC") && !getenv("POLY_DSELL");
+  int32_t NBK = 24;
+  if (const char *e = getenv("POLY_K4B_BLOCKS")) NBK = std::max(1, atoi(e));
+  const int32_t RB = (int32_t)std::max<int64_t>(1, (p.n_local + NBK - 1) / NBK);
+  int32_t *blkoff = nullptr, *bpre = nullptr, *blkcnt = nullptr, *slot_of = nullptr;
+  if (synced) {
+    std::vector<int32_t> cm((size_t)h->nslices * 32, -1), so((size_t)d, -1);
+    const int tw = 8, th = 4, tpr = side / tw;
+    for (int t = 0; t < h->nslices; ++t) {
+      const int r0 = (t / tpr) * th, c0 = (t % tpr) * tw;
+      for (int l = 0; l < 32; ++l) {
+        const int r = r0 + l / tw, c = c0 + l % tw;
+        if (r < side) {
+          cm[(size_t)t * 32 + l] = r * side + c;
+          so[(size_t)r * side + c] = t * 32 + l;
+        }
+      }
+    }
+    if ((rc = dev_alloc(h, &h->colmap, cm.size())) || (rc = talloc((size_t)d * 4, (void **)&slot_of)) ||
+        (rc = talloc((size_t)d * NBK * 4, (void **)&blkcnt)) || (rc = talloc((size_t)d * NBK * 4, (void **)&bpre)) ||
+        (rc = talloc((size_t)h->nslices * NBK * 4, (void **)&blkoff)))
+      return done(rc);
+    cudaMemcpyAsync(h->colmap, cm.data(), cm.size() * 4, cudaMemcpyHostToDevice, st);
+    cudaMemcpyAsync(slot_of, so.data(), so.size() * 4, cudaMemcpyHostToDevice, st);
+    cudaMemsetAsync(blkcnt, 0, (size_t)d * NBK * 4, st);
+    k_colblk_count<<<g, 256, 0, st>>>(rows, p.col, nnz, RB, NBK, blkcnt);
+    k_colblk_prefix<<<(int)((d + 255) / 256), 256, 0, st>>>(blkcnt, (int32_t)d, NBK, bpre);
+    k_slice_blocks<<<(h->nslices + 127) / 128, 128, 0, st>>>(blkcnt, h->colmap, h->nslices, NBK, blkoff, slen);
+  } else {
+    k_slice_len<<<(h->nslices + 255) / 256, 256, 0, st>>>(cnt, (int32_t)d, h->nslices, slen);
+  }
   cudaMemsetAsync(slen + h->nslices, 0, 8, st);
   size_t t3 = tb3;
   cub::DeviceScan::ExclusiveSum(tstore, t3, slen, h->slice_off, h->nslices + 1, st);
@@ -1202,10 +1243,16 @@ int build_sell_t(poly_handle *h) {
     return done(fail(POLY_ECUDA, "SELL build: %s", cudaGetErrorString(cudaGetLastError())));
   CscEnt<T> *ent = nullptr;
   if ((rc = dev_alloc(h, &ent, (size_t)std::max<int64_t>(1, steps) * 32))) return done(rc);
-  cudaMemsetAsync(ent, 0, (size_t)std::max<int64_t>(1, steps) * 32 * sizeof(CscEnt<T>), st);
-  if (nnz > 0)
-    k_sell_fill<T><<<g, 256, 0, st>>>(keys, perm, rows, (const T *)p.val, colptr, h->slice_off,
-                                      nnz, ent);
+  if (synced) {
+    k_sell_mark<T><<<g, 256, 0, st>>>(ent, std::max<int64_t>(1, steps) * 32);
+    k_sell_fill_sync<T><<<g, 256, 0, st>>>(keys, perm, rows, (const T *)p.val, colptr, bpre, blkoff, slot_of,
+                                           h->slice_off, RB, NBK, nnz, ent);
+  } else {
+    cudaMemsetAsync(ent, 0, (size_t)std::max<int64_t>(1, steps) * 32 * sizeof(CscEnt<T>), st);
+    if (nnz > 0)
+      k_sell_fill<T><<<g, 256, 0, st>>>(keys, perm, rows, (const T *)p.val, colptr, h->slice_off,
+                                        nnz, ent);
+  }
   h->sell = ent;
   h->sell_steps = steps;
   // DSELL (fp32, dsell.cuh): the forward copy needs every row's entries ascending in
@@ -1335,7 +1382,7 @@ int build_sell_t(poly_handle *h) {
     k_sell16_pack<T><<<(int)std::min<int64_t>(65535, nrs), 128, 0, st>>>(
         rent, h->row_slice_off, nrs, p.row_ptr, nullptr, p.n_local, foff, fdl, fval, fbase, ovf);
     k_sell16_pack<T><<<(int)std::min<int64_t>(65535, h->nslices), 128, 0, st>>>(
-        ent, h->slice_off, h->nslices, nullptr, cnt, d, boff, bdl, bval, bbase, ovf);
+        ent, h->slice_off, h->nslices, nullptr, h->colmap ? nullptr : cnt, d, boff, bdl, bval, bbase, ovf);
     int32_t hov = 0;
     cudaMemcpyAsync(&hov, ovf, 4, cudaMemcpyDeviceToHost, st);
     if (cudaStreamSynchronize(st) != cudaSuccess)

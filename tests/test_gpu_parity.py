@@ -641,6 +641,27 @@ def test_c4_dsell_sell16_and_wide_agree(c4, monkeypatch):
     assert rel(g_ds.cpu().numpy(), g_ref) <= TOL32
 
 
+def test_c4_tiled_synced_backward(c4, monkeypatch):
+    """K4b's opt-in tiled, block-synchronised Aᵀ layout (POLY_K4B_SYNC=1: 4 x 8
+    pixel tiles as slices, lane chains re-aligned every row block with
+    marked padding, output columns through the tile map): oracle parity per
+    call and through a solve with the step epilogue."""
+    wg, wo = c4
+    W = _W()
+    monkeypatch.setenv("POLY_K4B_SYNC", "1")
+    p = W.make_poly(wg)
+    x0 = 0.7 * wo["x_star"]
+    g, l = gpu_F(p, x0)
+    g_ref, l_ref = wo["problem"].F(x0)
+    assert rel(g, g_ref) <= TOL32 and abs(l - l_ref) <= TOL32 * abs(l_ref)
+    gam = 1.0 / (4.0 * G.C4.I_bar * 4e-5 * float(np.dot(wo["s"], wo["mu"])))
+    x = torch.zeros(G.C4.d, dtype=torch.float64, device="cuda")
+    p.solve(x, 10, gam)
+    x_ref, _, _ = wo["problem"].solve(10, gam)
+    assert rel(x.cpu().numpy(), x_ref) <= 1e-3
+    p.close()
+
+
 @pytest.mark.parametrize("n,d,density", [(1000, 4096, 0.01), (77, 300, 0.5), (4097, 2048, 0.003),
                                          (64, 200_000, 0.002)])
 def test_dsell_random_sparse(n, d, density, monkeypatch):
