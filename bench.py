@@ -304,6 +304,7 @@ def run_ours(args):
             "read_ceiling_k8": read_ceiling,
             "frac_of_read_ceiling": (achieved / read_ceiling) if achieved and read_ceiling else None}
     desc = poly.describe()
+    launches = launches_per_step(w, cfg, world) * args.steps  # (before e2e releases the device copy of A)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
@@ -334,7 +335,7 @@ def run_ours(args):
             "roofline": roof,
             "cpu_baseline": cpu,
             "e2e": e2e,
-            "gpu_launches": launches_per_step(w, cfg, world) * args.steps,
+            "gpu_launches": launches,
             "clocks": clk.summary(),
         }
         if world > 1:
