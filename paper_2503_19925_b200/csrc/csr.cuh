@@ -350,61 +350,8 @@ __device__ __forceinline__ double sell16_dot(const Sell16 &s, int64_t slice, int
   return a0 + a1;
 }
 
-// The same sum with the next batch's stream loads issued before this batch's
-// gathers (register double-buffering): a warp's HBM latency and its gather
-// latency overlap instead of adding up.
-template <typename T, int UNR>
-__device__ __forceinline__ double sell16_dot_pf(const Sell16 &s, int64_t slice, int warp, int lane,
-                                                const float *__restrict__ gv) {
-  const int64_t o0 = s.slice_off[slice], ng = s.slice_off[slice + 1] - o0;
-  int32_t idx = s.base[(slice * 4 + warp) * 32 + lane];
-  double a0 = 0.0, a1 = 0.0;
-  using V4 = typename Val4<T>::type;
-  short4 dA[UNR], dB[UNR];
-  V4 vA[UNR], vB[UNR];
-  auto load = [&](int64_t g, short4 *dd, V4 *vv) {
-#pragma unroll
-    for (int u = 0; u < UNR; ++u) {
-      const bool ok = g + 4 * u < ng;
-      const int64_t gi = (o0 + (ok ? g + 4 * u : 0)) * 32 + lane;
-      dd[u] = ok ? __ldcs(s.dl + gi) : make_short4(0, 0, 0, 0);
-      vv[u] = ok ? Val4<T>::load(s.val, gi) : V4{};
-    }
-  };
-  auto consume = [&](const short4 *dd, const V4 *vv) {
-    float gg[4 * UNR];
-#pragma unroll
-    for (int u = 0; u < UNR; ++u) {
-      const int32_t i0 = idx + dd[u].x, i1 = i0 + dd[u].y, i2 = i1 + dd[u].z, i3 = i2 + dd[u].w;
-      idx = i3;
-      gg[4 * u] = __ldg(gv + i0), gg[4 * u + 1] = __ldg(gv + i1);
-      gg[4 * u + 2] = __ldg(gv + i2), gg[4 * u + 3] = __ldg(gv + i3);
-    }
-#pragma unroll
-    for (int u = 0; u < UNR; ++u) {
-      a0 = fma((double)vv[u].x, (double)gg[4 * u], a0);
-      a1 = fma((double)vv[u].y, (double)gg[4 * u + 1], a1);
-      a0 = fma((double)vv[u].z, (double)gg[4 * u + 2], a0);
-      a1 = fma((double)vv[u].w, (double)gg[4 * u + 3], a1);
-    }
-  };
-  // (padding groups past ng load as zero deltas and values: they add nothing)
-  int64_t g = warp;
-  if (g < ng) load(g, dA, vA);
-  for (; g < ng; g += 8 * UNR) {
-    const int64_t g2 = g + 4 * UNR;
-    if (g2 < ng) load(g2, dB, vB);
-    consume(dA, vA);
-    if (g2 >= ng) break;
-    const int64_t g3 = g2 + 4 * UNR;
-    if (g3 < ng) load(g3, dA, vA);
-    consume(dB, vB);
-  }
-  return a0 + a1;
-}
-
-template <typename T, bool LOSS, bool PF = false>
-__global__ void __launch_bounds__(128, PF ? 6 : POLY_SELL_MINB_F) k_sell16_forward(const Sell16 s, int64_t nslices,
+template <typename T, bool LOSS>
+__global__ void __launch_bounds__(POLY_SELL_LB_F) k_sell16_forward(const Sell16 s, int64_t nslices,
                                                              const CsrFwdArgs a) {
   __shared__ double sp[3 * kMaxW];
   __shared__ double part[4][32];
@@ -413,8 +360,7 @@ __global__ void __launch_bounds__(128, PF ? 6 : POLY_SELL_MINB_F) k_sell16_forwa
   pdl_wait();  // x is written by the previous kernel; r is read by the previous backward
   double lacc = 0.0;
   for (int64_t sl = blockIdx.x; sl < nslices; sl += gridDim.x) {  // fixed slice -> block map
-    part[warp][lane] = PF ? sell16_dot_pf<T, POLY_SELL_UNROLL_F>(s, sl, warp, lane, a.x)
-                          : sell16_dot<T, POLY_SELL_UNROLL_F>(s, sl, warp, lane, a.x);
+    part[warp][lane] = sell16_dot<T, POLY_SELL_UNROLL_F>(s, sl, warp, lane, a.x);
     __syncthreads();
     lacc += forward_tail<LOSS>(part, sp, a, sl);
     __syncthreads();  // part is rewritten by the next slice
@@ -466,8 +412,8 @@ __device__ __forceinline__ void backward_column_out(double (*part)[32], const St
   if (sl == 0 && lane == 0) e.state->loss_cur = 0.0;  // as k_finalize without the objective
 }
 
-template <typename T, bool PF = false>
-__global__ void __launch_bounds__(128, PF ? 6 : 16) k_sell16_backward(const Sell16 s, int64_t nslices,
+template <typename T>
+__global__ void __launch_bounds__(POLY_SELL_LB_B) k_sell16_backward(const Sell16 s, int64_t nslices,
                                                               int32_t d, const float *__restrict__ r,
                                                               double *__restrict__ g, const StepEpi e,
                                                               const int32_t *colmap) {
@@ -475,8 +421,7 @@ __global__ void __launch_bounds__(128, PF ? 6 : 16) k_sell16_backward(const Sell
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   pdl_wait();  // r is written by the forward pass
   for (int64_t sl = blockIdx.x; sl < nslices; sl += gridDim.x) {
-    part[warp][lane] = PF ? sell16_dot_pf<T, POLY_SELL_UNROLL_B>(s, sl, warp, lane, r)
-                          : sell16_dot<T, POLY_SELL_UNROLL_B>(s, sl, warp, lane, r);
+    part[warp][lane] = sell16_dot<T, POLY_SELL_UNROLL_B>(s, sl, warp, lane, r);
     __syncthreads();
     if (warp == 0) backward_column_out(part, e, g, d, sl, lane, colmap);
     __syncthreads();

@@ -155,16 +155,12 @@ const void *kCsrFwd[2][2] = {
 };
 const void *kCscBwd[2] = {(const void *)&k_csc_backward<float>,
                           (const void *)&k_csc_backward<double>};
-// [PF: next batch's stream loads issued before this batch's gathers][dtype][loss]
-const void *kSell16Fwd[2][2][2] = {
-    {{(const void *)&k_sell16_forward<float, false>, (const void *)&k_sell16_forward<float, true>},
-     {(const void *)&k_sell16_forward<double, false>, (const void *)&k_sell16_forward<double, true>}},
-    {{(const void *)&k_sell16_forward<float, false, true>, (const void *)&k_sell16_forward<float, true, true>},
-     {(const void *)&k_sell16_forward<double, false, true>, (const void *)&k_sell16_forward<double, true, true>}},
+const void *kSell16Fwd[2][2] = {
+    {(const void *)&k_sell16_forward<float, false>, (const void *)&k_sell16_forward<float, true>},
+    {(const void *)&k_sell16_forward<double, false>, (const void *)&k_sell16_forward<double, true>},
 };
-const void *kSell16Bwd[2][2] = {{(const void *)&k_sell16_backward<float>, (const void *)&k_sell16_backward<double>},
-                                {(const void *)&k_sell16_backward<float, true>,
-                                 (const void *)&k_sell16_backward<double, true>}};
+const void *kSell16Bwd[2] = {(const void *)&k_sell16_backward<float>,
+                             (const void *)&k_sell16_backward<double>};
 constexpr int kSplitFinD = 8192;  // d above which the step tail runs as k_fin_apply
 
 constexpr size_t kSmemLimit = 227 * 1024;
@@ -263,7 +259,6 @@ struct poly_handle {
   int64_t tr_slices = 0;               // K4f slices that gather from the transposed copy
   bool sell16 = false;                 // both SELL copies in the 6-byte delta form
   bool dsell = false;                  // fp32: both copies in the dictionary-staged 5-byte form (dsell.cuh)
-  int sell_pf = 0;                     // bit 0: K4f, bit 1: K4b with software-pipelined stream loads
   DSell dfwd{}, dbwd{};
   int32_t dfwd_cap = 0, dbwd_cap = 0;  // largest |F_s| per direction (shared-memory staging)
   size_t dfwd_smem = 0, dbwd_smem = 0;
@@ -468,9 +463,9 @@ int enqueue_pass(poly_handle *h, const double *x, bool loss) {
                   h->epi);
   }
   if (h->sell16) {
-    TRY(launch(h, kSell16Fwd[h->sell_pf & 1][p.dtype][loss ? 1 : 0], dim3(h->k4f16_grid), dim3(128), 0, true,
+    TRY(launch(h, kSell16Fwd[p.dtype][loss ? 1 : 0], dim3(h->k4f16_grid), dim3(128), 0, true,
                h->fwd16, (int64_t)h->nrslices, a));
-    return launch(h, kSell16Bwd[(h->sell_pf >> 1) & 1][p.dtype], dim3(h->k4b16_grid), dim3(128), 0, true, h->bwd16,
+    return launch(h, kSell16Bwd[p.dtype], dim3(h->k4b16_grid), dim3(128), 0, true, h->bwd16,
                   (int64_t)h->nslices, (int32_t)p.d, (const float *)h->rbuf, h->partials, h->epi,
                   (const int32_t *)h->colmap);
   }
@@ -1929,7 +1924,6 @@ int poly_init(const poly_problem *pin, poly_handle **out) {
       cudaEventCreateWithFlags(&h->ev_sync, cudaEventDisableTiming) != cudaSuccess)
     return bail(fail(POLY_ECUDA, "stream/event creation failed"));
   h->no_epi = getenv("POLY_NO_EPI") != nullptr;
-  if (const char *e = getenv("POLY_SELL_PF")) h->sell_pf = atoi(e) & 3;
   if (const char *t = getenv("POLY_COMM_TIMEOUT_S")) {
     const double v = atof(t);
     if (v > 0.0) h->comm_timeout_s = v;
