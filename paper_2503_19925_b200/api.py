@@ -122,6 +122,13 @@ class Poly:
 
     def close(self):
         if getattr(self, "h", None):
+            # K9 / K9-NVLS: a peer may still read this rank's window until it
+            # finished its last evaluation, so the ranks meet before freeing
+            from . import POLY_FLAG_NVLS, POLY_FLAG_P2P
+            if int(self.problem.world) > 1 and int(self.problem.flags) & (POLY_FLAG_P2P | POLY_FLAG_NVLS):
+                import torch.distributed as dist
+                if dist.is_available() and dist.is_initialized():
+                    dist.barrier()
             poly_free(self.h)
             self.h = None
 

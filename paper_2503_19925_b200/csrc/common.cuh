@@ -119,8 +119,22 @@ __host__ __device__ constexpr double inv_factorial(int n) {
   return 1.0 / f;
 }
 
+// DEG = 0: the fraction 2^f, |f| <= 1/2, by the SFU (ex2.approx.ftz.f32) on a
+// fp64 Cody-Waite reduction: relative error ~3e-7 (the fp32-A link's option
+// POLY_K1_MUFU_EXP; x >= -87 keeps 2^f·2^k inside the fp32 SFU's range).
+__device__ __forceinline__ double exp_nonpos_sfu(double x) {
+  x = fmax(x, -87.0);
+  const double k = rint(x * 1.4426950408889634);
+  double r = fma(-k, 6.93147180369123816490e-01, x);
+  r = fma(-k, 1.90821492927058770002e-10, r);
+  float e2;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e2) : "f"((float)(r * 1.4426950408889634)));
+  return (double)e2 * __longlong_as_double((long long)(1023 + (int)k) << 52);
+}
+
 template <int DEG = 13>
 __device__ __forceinline__ double exp_nonpos(double x) {
+  if (DEG == 0) return exp_nonpos_sfu(x);
   x = fmax(x, -708.0);
   const double k = rint(x * 1.4426950408889634);
   double r = fma(-k, 6.93147180369123816490e-01, x);

@@ -25,7 +25,7 @@
 namespace poly {
 
 #ifndef POLY_EXP_DEG32
-#define POLY_EXP_DEG32 9  // exp polynomial degree of the link for fp32 A (common.cuh exp_nonpos)
+#define POLY_EXP_DEG32 9  // exp polynomial degree of the link for fp32 A (common.cuh exp_nonpos; 0: SFU)
 #endif
 #ifndef POLY_K1_LINK_SPLIT
 #define POLY_K1_LINK_SPLIT 1  // WPR > 1: the row group's warps split the link's bins
@@ -447,16 +447,23 @@ __global__ void __launch_bounds__(32 * (NW + 1), 1) k_dense_loss_grad(const Dens
         for (int q = 0; q < RG; ++q) rb2[q * WPR + w] = zp[q];
       }
       named_bar_sync(1 + grp, 32 * WPR);
+      if (PAIR && a.mode == 0 && a.W <= 32) {  // the pair link: each half-warp needs only its row's z
 #pragma unroll
-      for (int q = 0; q < RG; ++q) {
-        double z = 0.0;
+        for (int q = 0; q < RG; q += 2) {
+          const int qq = q + (lane >> 4);
+          double z = 0.0;
 #pragma unroll
-        for (int k = 0; k < WPR; ++k) z += rb2[q * WPR + k];
-        zp[q] = z;
-      }
-      if (PAIR) {
+          for (int k = 0; k < WPR; ++k) z += rb2[qq * WPR + k];
+          zh[q >> 1] = z;
+        }
+      } else {
 #pragma unroll
-        for (int q = 0; q < RG; q += 2) zh[q >> 1] = (lane & 16) ? zp[q + 1] : zp[q];
+        for (int q = 0; q < RG; ++q) {
+          double z = 0.0;
+#pragma unroll
+          for (int k = 0; k < WPR; ++k) z += rb2[q * WPR + k];
+          zp[q] = z;
+        }
       }
       buf ^= 1;
     }
