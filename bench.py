@@ -312,8 +312,8 @@ def run_ours(args):
     poly.close()
     del poly   # drops the handle's references to A (C5: 131 GB that e2e needs back)
     e2e = None
-    if not args.no_e2e and world == 1:
-        e2e = run_e2e(P, w, cfg, gamma, args)
+    if not args.no_e2e:
+        e2e = run_e2e(P, D, w, cfg, gamma, args, rank, world)
 
     if rank == 0:
         line = {
@@ -346,20 +346,26 @@ def run_ours(args):
         dist.destroy_process_group()
 
 
-def run_e2e(P, w, cfg, gamma, args):
+def run_e2e(P, D, w, cfg, gamma, args, rank=0, world=1):
     """The same metric through the C ABI with HOST inputs: every step is
     poly_init(POLY_FLAG_HOST_INPUTS: A, y copied from pinned host memory into
-    library-owned HBM) + poly_solve(T iterations from a host x, x returned to
-    the host) + poly_free; the timed region covers all of it.  The device copy
-    of A made by the workload builder is released first (C5's 131 GB would not
-    fit twice)."""
+    library-owned HBM; with N ranks each its row block and a fresh
+    communicator) + poly_solve(T iterations from a host x, x returned to the
+    host) + poly_free; the timed region covers all of it (max over ranks).
+    The device copy of A made by the workload builder is released first (C5's
+    131 GB would not fit twice)."""
     import psutil
     import torch
     ab = a_bytes(w)
     need = ab + side_bytes(w)
-    if need * 1.15 + 8e9 > psutil.virtual_memory().available:
+    # every rank of the node stages its block: the node must hold them all;
+    # the decision is rank 0's, so that all ranks take the same path
+    skip = need * world * 1.15 + 8e9 > psutil.virtual_memory().available
+    if world > 1:
+        skip = D.max_over_ranks(1.0 if skip else 0.0, world) > 0.5
+    if skip:
         return {"value": None, "unit": "GB/s",
-                "skipped": f"host memory: {need / 1e9:.0f} GB of inputs, "
+                "skipped": f"host memory: {need * world / 1e9:.0f} GB of inputs, "
                            f"{psutil.virtual_memory().available / 1e9:.0f} GB available"}
     cudart = torch.cuda.cudart()
     registered = []
@@ -403,24 +409,30 @@ def run_e2e(P, w, cfg, gamma, args):
     steps = args.e2e_steps if ab < 20e9 else min(args.e2e_steps, 2)
     for rep in range(1 + steps):
         x_h = torch.zeros(cfg.d, dtype=torch.float64).pin_memory()
+        nid = D.exchange_id(P.poly_nccl_unique_id, rank, world)   # a communicator per init
+        if world > 1:
+            import torch.distributed as dist
+            dist.barrier()
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(st)
         p = P.Poly(d=cfg.d, y=y_h, s=w["s"], mu=w["mu"], I_bar=cfg.I_bar, set=cfg.set,
-                   R=w["R"], n_global=w["n_global"], flags=P.POLY_FLAG_HOST_INPUTS,
-                   stream=st.cuda_stream, **mat, **extra)
+                   R=w["R"], n_global=w["n_global"], row_offset=w["row0"], rank=rank, world=world,
+                   nccl_id=nid, flags=P.POLY_FLAG_HOST_INPUTS, stream=st.cuda_stream, **mat, **extra)
         p.solve(x_h, T, gamma)
         e1.record(st)
         torch.cuda.synchronize()
         p.close()
         if rep > 0:                                  # rep 0 warms the allocator/graph path
-            vals.append(e0.elapsed_time(e1))
+            vals.append(D.max_over_ranks(e0.elapsed_time(e1), world))
     ms = statistics.median(vals)
-    h2d = sum(v.numel() * v.element_size() for v in [y_h] + list(mat.values()) + list(extra.values()))
+    ab = D.sum_over_ranks(float(ab), world)
+    h2d = D.sum_over_ranks(float(sum(v.numel() * v.element_size()
+                                     for v in [y_h] + list(mat.values()) + list(extra.values()))), world)
     for h in registered:
         cudart.cudaHostUnregister(h.data_ptr())
     return {"value": 2.0 * T * ab / (ms * 1e-3) / 1e9, "unit": "GB/s",
-            "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": 8 * cfg.d,
+            "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": 8 * cfg.d * world,
             "iterations_per_step": T, "ms_per_step": ms, "steps_timed": len(vals),
             "host_prep_s": prep_s,
             "note": "step = poly_init(pinned host A or CSR, y) + poly_solve(T, host x) + poly_free"}
