@@ -47,6 +47,7 @@
 #include "p2p.cuh"
 #include "nvls.cuh"
 #include "dsell.cuh"
+#include "tiled.cuh"
 
 using namespace poly;
 
@@ -268,6 +269,15 @@ struct poly_handle {
   double *pb_trig = nullptr, *pb_out2 = nullptr, *pb_zpart = nullptr;
   int32_t *pb_ticket = nullptr, *pb_tticket = nullptr;
   int k4f16_grid = 0, k4b16_grid = 0;  // resident-slot grids (slices dealt grid-stride)
+  // K4t (tiled.cuh): strip forward + link + tile backward, the default for fp32 CSR
+  bool tiled = false;
+  StripFwd tfwd{};
+  TileBwd tbwd{};
+  int tf_grid = 0, tb_grid = 0;        // forward CTAs (2 per SM), backward CTAs (one per tile)
+  size_t tf_smem = 0, tb_smem = 0;
+  bool tile_epi = false;               // every warp of K4tb covers one k_finalize block
+  int32_t tb_lcap = 0;                 // K4tb ray-list capacity (floats, multiple of 4)
+  int64_t tf_groups = 0, tb_groups = 0;
   StepEpi epi{};                        // K4b's step epilogue for the next pass (on = 0: write g)
   // TV sets: Dykstra state, statistics, cluster launch shape
   double *tv_zk = nullptr, *tv_p = nullptr, *tv_q = nullptr;  // [tv_k][d] each
@@ -454,6 +464,14 @@ int enqueue_pass(poly_handle *h, const double *x, bool loss) {
   a.r = h->rbuf;
   a.mode = p.mode;
   a.loss_partials = h->loss_partials;
+  if (h->tiled) {
+    TRY(launch(h, (const void *)&k_strip_forward, dim3(h->tf_grid), dim3((kFwdWarps + 1) * 32), h->tf_smem, true,
+               h->tfwd, x32));
+    TRY(launch(h, loss ? (const void *)&k_strip_link<true> : (const void *)&k_strip_link<false>, dim3(h->k4_grid),
+               dim3(256), 0, true, a, (const double *)h->tfwd.pz, h->tfwd.NS, h->tfwd.ctr));
+    return launch(h, (const void *)&k_tile_backward, dim3(h->tb_grid), dim3((kBwdWarps + 1) * 32), h->tb_smem, true,
+                  h->tbwd, (const float *)h->rbuf, h->partials, (int32_t)p.d, h->epi, h->tb_lcap);
+  }
   if (h->dsell) {
     TRY(launch(h, loss ? (const void *)&k_dsell_forward<true> : (const void *)&k_dsell_forward<false>,
                dim3(h->k4_grid), dim3(kDsThreads), h->dfwd_smem, true, h->dfwd, (int64_t)h->nrslices,
@@ -714,7 +732,7 @@ int enqueue_eval(poly_handle *h, const double *x, bool loss, bool step, const do
   f.g_out = g_out;
   // compact-SELL CSR on the split path, plain step, no objective, one rank:
   // K4b's epilogue does k_finalize's work (same bits) and k_fin_apply follows
-  const bool fuse = (h->sell16 || h->dsell) && h->p.layout == POLY_CSR && !h->comm_path && step && !loss && !g_out &&
+  const bool fuse = (h->sell16 || h->dsell || (h->tiled && h->tile_epi)) && h->p.layout == POLY_CSR && !h->comm_path && step && !loss && !g_out &&
                     f.split && !h->no_epi;
   h->epi = StepEpi{};
   if (fuse) {
@@ -1410,7 +1428,240 @@ int build_sell_t(poly_handle *h) {
   return done(POLY_OK);
 }
 
+// K4t (tiled.cuh) from the caller's fp32 CSR (poly_init only): the strip
+// forward copy and the tile backward copy, both as 8-bit deltas + fp32
+// values.  Returns POLY_EUNSUPPORTED (message cleared) when the matrix does
+// not fit the format; build_sell then builds the SELL pair.
+int build_tiled(poly_handle *h) {
+  const poly_problem &p = h->p;
+  const int64_t nnz = p.nnz, d = p.d, n = p.n_local;
+  if (p.dtype != POLY_F32 || nnz < 1 || n < 1 || nnz >= ((int64_t)1 << 31) || n >= ((int64_t)1 << 31) ||
+      getenv("POLY_NO_TILED") || getenv("POLY_DSELL") || getenv("POLY_K4B_SYNC"))
+    return POLY_EUNSUPPORTED;
+  TiledGeom m{};
+  {
+    const int64_t s = (int64_t)llround(std::sqrt((double)d));
+    if (s * s == d && s > 1) m.rows_img = m.cols_img = (int32_t)s;
+    else m.rows_img = 1, m.cols_img = (int32_t)d;
+  }
+  // strips: the fewest with a strip of <= 100 KB (two forward CTAs per SM)
+  // and every ascending delta (< P + W) within 8 bits
+  const size_t kStripBytes = 100 * 1024;
+  for (m.NS = 1; m.NS <= kMaxStrips; ++m.NS) {
+    m.W = (m.cols_img + m.NS - 1) / m.NS;
+    m.P = m.rows_img > 1 ? (m.W | 1) : m.W;
+    if ((size_t)m.rows_img * m.P * 4 <= kStripBytes && (m.rows_img == 1 || m.P + m.W <= 256)) break;
+  }
+  if (m.NS > kMaxStrips || (int64_t)m.rows_img * m.P > 65535) return POLY_EUNSUPPORTED;
+  m.NS = (m.cols_img + m.W - 1) / m.W;
+  if (m.rows_img > 1) m.TW = 32, m.TH = 8;
+  else m.TW = kTileSlots, m.TH = 1;
+  m.tiles_x = (m.cols_img + m.TW - 1) / m.TW;
+  const int64_t ntiles = (int64_t)((m.rows_img + m.TH - 1) / m.TH) * m.tiles_x;
+  if (ntiles >= ((int64_t)1 << 23)) return POLY_EUNSUPPORTED;
+  const int64_t nwarps = ntiles * 8;
+  cudaStream_t st = h->work;
+  std::vector<void *> tmp;
+  std::vector<void *> mine;  // persistent buffers, released on failure
+  auto talloc = [&](size_t bytes, void **ptr) -> int {
+    if (cudaMalloc(ptr, std::max<size_t>(bytes, 16)) != cudaSuccess) {
+      cudaGetLastError();
+      return fail(POLY_ENOMEM, "tiled build: cudaMalloc(%zu) failed", bytes);
+    }
+    tmp.push_back(*ptr);
+    return POLY_OK;
+  };
+  auto palloc = [&](size_t bytes, void **ptr) -> int {
+    unsigned char *q = nullptr;
+    TRY(dev_alloc(h, &q, bytes));
+    mine.push_back(q);
+    *ptr = q;
+    return POLY_OK;
+  };
+  auto done = [&](int code) {
+    cudaStreamSynchronize(st);
+    for (void *q : tmp) cudaFree(q);
+    if (code != POLY_OK)
+      for (void *q : mine) dev_release(h, q);
+    if (code == POLY_EUNSUPPORTED) g_err[0] = 0;
+    return code;
+  };
+  const int g = 148 * 8;
+  int rc;
+  // ---- forward: sort by (strip, row, local index)
+  int32_t *rows = nullptr, *perm_in = nullptr, *perm = nullptr, *seglen = nullptr, *nz = nullptr, *ovf = nullptr;
+  uint64_t *kin = nullptr, *ks = nullptr;
+  int64_t *segstart = nullptr;
+  const int64_t nsn = (int64_t)m.NS * n;
+  if ((rc = talloc(nnz * 4, (void **)&rows)) || (rc = talloc(nnz * 4, (void **)&perm_in)) ||
+      (rc = talloc(nnz * 4, (void **)&perm)) || (rc = talloc(nnz * 8, (void **)&kin)) ||
+      (rc = talloc(nnz * 8, (void **)&ks)) || (rc = talloc(nsn * 4, (void **)&seglen)) ||
+      (rc = talloc(nsn * 8, (void **)&segstart)) || (rc = talloc(kMaxStrips * 4, (void **)&nz)) ||
+      (rc = talloc(4, (void **)&ovf)))
+    return done(rc);
+  cudaMemsetAsync(seglen, 0, nsn * 4, st);
+  cudaMemsetAsync(nz, 0, kMaxStrips * 4, st);
+  cudaMemsetAsync(ovf, 0, 4, st);
+  k_entry_rows<<<g, 256, 0, st>>>(p.row_ptr, n, rows);
+  k_tf_keys<<<g, 256, 0, st>>>(rows, p.col, nnz, n, m, kin, perm_in, seglen);
+  const int sbits = 32 - __builtin_clz((unsigned)std::max(1, m.NS - 1));
+  // 64-bit key radix sorts (temporary storage sized per call)
+  auto sort64 = [&](const uint64_t *ki, uint64_t *ko, const int32_t *vi, int32_t *vo, int64_t items, int bits) -> int {
+    size_t tb = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, tb, ki, ko, vi, vo, (int)items, 0, bits, st);
+    void *ts = nullptr;
+    TRY(talloc(tb, &ts));
+    if (cub::DeviceRadixSort::SortPairs(ts, tb, ki, ko, vi, vo, (int)items, 0, bits, st) != cudaSuccess)
+      return fail(POLY_ECUDA, "tiled build: radix sort failed");
+    return POLY_OK;
+  };
+  if ((rc = sort64(kin, ks, perm_in, perm, nnz, 48 + sbits))) return done(rc);
+  k_tf_segstart<<<g, 256, 0, st>>>(ks, nnz, n, segstart);
+  // segments of each strip longest first
+  uint64_t *okin = nullptr, *oks = nullptr;
+  int32_t *orin = nullptr, *srow = nullptr;
+  if ((rc = talloc(nsn * 8, (void **)&okin)) || (rc = talloc(nsn * 8, (void **)&oks)) ||
+      (rc = talloc(nsn * 4, (void **)&orin)) || (rc = talloc(nsn * 4, (void **)&srow)))
+    return done(rc);
+  k_tf_order_keys<<<g, 256, 0, st>>>(seglen, n, m.NS, okin, orin, nz);
+  if ((rc = sort64(okin, oks, orin, srow, nsn, 32 + sbits))) return done(rc);
+  std::vector<int32_t> hnz(m.NS);
+  cudaMemcpyAsync(hnz.data(), nz, m.NS * 4, cudaMemcpyDeviceToHost, st);
+  if (cudaStreamSynchronize(st) != cudaSuccess)
+    return done(fail(POLY_ECUDA, "tiled build: %s", cudaGetErrorString(cudaGetLastError())));
+  std::vector<int32_t> ustart(m.NS + 1, 0);
+  for (int s = 0; s < m.NS; ++s) ustart[s + 1] = ustart[s] + (hnz[s] + kFwdWarps * 32 - 1) / (kFwdWarps * 32);
+  const int64_t units = ustart[m.NS];
+  int32_t *d_ustart = nullptr, *d_ctr = nullptr;
+  int64_t *ulen = nullptr, *uoff = nullptr;
+  uint8_t *fhdr = nullptr;
+  double *pz = nullptr;
+  if ((rc = palloc((m.NS + 1) * 4, (void **)&d_ustart)) || (rc = palloc(m.NS * 4, (void **)&d_ctr)) ||
+      (rc = palloc((units + 1) * 8, (void **)&uoff)) || (rc = palloc(std::max<int64_t>(1, units) * kFwdHdr, (void **)&fhdr)) ||
+      (rc = palloc(nsn * 8, (void **)&pz)) || (rc = talloc((units + 1) * 8, (void **)&ulen)))
+    return done(rc);
+  cudaMemcpyAsync(d_ustart, ustart.data(), (m.NS + 1) * 4, cudaMemcpyHostToDevice, st);
+  cudaMemsetAsync(d_ctr, 0, m.NS * 4, st);
+  cudaMemsetAsync(pz, 0, nsn * 8, st);
+  k_tf_unitlen<<<(int)std::min<int64_t>(4096, (units + 256) / 256), 256, 0, st>>>(d_ustart, m.NS, srow, seglen, n,
+                                                                                 units, ulen);
+  size_t tb3 = 0;
+  cub::DeviceScan::ExclusiveSum(nullptr, tb3, ulen, uoff, (int)units + 1, st);
+  void *ts3 = nullptr;
+  if ((rc = talloc(tb3, &ts3))) return done(rc);
+  cub::DeviceScan::ExclusiveSum(ts3, tb3, ulen, uoff, (int)units + 1, st);
+  int64_t frows = 0;
+  cudaMemcpyAsync(&frows, uoff + units, 8, cudaMemcpyDeviceToHost, st);
+  if (cudaStreamSynchronize(st) != cudaSuccess)
+    return done(fail(POLY_ECUDA, "tiled build: %s", cudaGetErrorString(cudaGetLastError())));
+  uint8_t *frec = nullptr;
+  if ((rc = palloc((size_t)std::max<int64_t>(1, frows) * kFwdWarps * kRecBytes, (void **)&frec))) return done(rc);
+  k_tf_pack<<<(int)std::min<int64_t>(65535, (units * kFwdWarps + 7) / 8), 256, 0, st>>>(
+      d_ustart, m.NS, srow, seglen, nz, segstart, ks, perm, (const float *)p.val, n, units, uoff, frec, fhdr, ovf);
+  // ---- backward: sort by (tile, row, slot), ray lists, then by (tile, slot, list position)
+  int32_t *flag = nullptr, *pidx = nullptr, *tcnt = nullptr, *list = nullptr;
+  int64_t *tcnt64 = nullptr, *pstart = nullptr, *loff = nullptr;
+  if ((rc = talloc(nnz * 4, (void **)&flag)) || (rc = talloc(nnz * 4, (void **)&pidx)) ||
+      (rc = talloc(ntiles * 4, (void **)&tcnt)) || (rc = talloc((ntiles + 1) * 8, (void **)&tcnt64)) ||
+      (rc = talloc((ntiles + 1) * 8, (void **)&pstart)) || (rc = palloc((ntiles + 1) * 8, (void **)&loff)))
+    return done(rc);
+  cudaMemsetAsync(tcnt, 0, ntiles * 4, st);
+  k_tb_keys<<<g, 256, 0, st>>>(rows, p.col, nnz, m, kin, perm_in);
+  const int tbits = 32 - __builtin_clz((unsigned)std::max<int64_t>(1, ntiles - 1));
+  if ((rc = sort64(kin, ks, perm_in, perm, nnz, 40 + tbits))) return done(rc);
+  k_tb_pairs<<<g, 256, 0, st>>>(ks, nnz, flag, tcnt);
+  size_t tb4 = 0, tb5 = 0;
+  cub::DeviceScan::InclusiveSum(nullptr, tb4, flag, pidx, (int)nnz, st);
+  cub::DeviceScan::ExclusiveSum(nullptr, tb5, tcnt64, loff, (int)ntiles + 1, st);
+  void *ts4 = nullptr;
+  if ((rc = talloc(std::max(tb4, tb5), &ts4))) return done(rc);
+  cub::DeviceScan::InclusiveSum(ts4, tb4, flag, pidx, (int)nnz, st);
+  // pair starts per tile (unpadded) and list offsets (each list padded to a multiple of 4: 16-byte copies)
+  k_widen<<<(int)std::min<int64_t>(4096, (ntiles + 256) / 256), 256, 0, st>>>(tcnt, ntiles, tcnt64);
+  cub::DeviceScan::ExclusiveSum(ts4, tb5, tcnt64, pstart, (int)ntiles + 1, st);
+  k_round4<<<(int)std::min<int64_t>(4096, (ntiles + 256) / 256), 256, 0, st>>>(tcnt64, ntiles);
+  cub::DeviceScan::ExclusiveSum(ts4, tb5, tcnt64, loff, (int)ntiles + 1, st);
+  int64_t nlist = 0;
+  cudaMemcpyAsync(&nlist, loff + ntiles, 8, cudaMemcpyDeviceToHost, st);
+  std::vector<int32_t> htc(ntiles);
+  cudaMemcpyAsync(htc.data(), tcnt, ntiles * 4, cudaMemcpyDeviceToHost, st);
+  if (cudaStreamSynchronize(st) != cudaSuccess)
+    return done(fail(POLY_ECUDA, "tiled build: %s", cudaGetErrorString(cudaGetLastError())));
+  int32_t lmax = 0;
+  for (int32_t v : htc) lmax = std::max(lmax, v);
+  const int32_t lcap = (std::max(1, lmax) + 3) & ~3;
+  const size_t bwd_smem = (size_t)kBwdStages * kBwdStageBytes + (size_t)lcap * 4 + 2 * kBwdStages * 8;
+  const size_t fwd_smem = (((size_t)m.rows_img * m.P * 4 + 127) & ~(size_t)127) + (size_t)kFwdStages * kFwdStageBytes +
+                          2 * kFwdStages * 8 + kFwdStages * 16;
+  if (bwd_smem + 2048 > 227 * 1024 || fwd_smem > 227 * 1024) return done(POLY_EUNSUPPORTED);
+  if ((rc = palloc((size_t)(nlist + 4) * 4, (void **)&list))) return done(rc);
+  cudaMemsetAsync(list, 0, (size_t)(nlist + 4) * 4, st);
+  k_tb_list<<<g, 256, 0, st>>>(ks, pidx, flag, pstart, loff, nnz, list, kin);
+  const int qbits = 32 + 32 - __builtin_clz((unsigned)std::max<int64_t>(1, ntiles * kTileSlots - 1));
+  if ((rc = sort64(kin, ks, perm, perm_in, nnz, qbits))) return done(rc);
+  // perm_in now maps the (tile, slot, position) order to the caller's entries
+  int32_t *scnt = nullptr, *tcol = nullptr;
+  int64_t *sstart = nullptr, *wlen = nullptr, *tlen = nullptr, *toff = nullptr;
+  uint16_t *bbase = nullptr;
+  const int64_t nslot = ntiles * kTileSlots;
+  if ((rc = talloc(nslot * 4, (void **)&scnt)) || (rc = talloc(nslot * 8, (void **)&sstart)) ||
+      (rc = talloc(nwarps * 8, (void **)&wlen)) || (rc = talloc((ntiles + 1) * 8, (void **)&tlen)) ||
+      (rc = palloc((ntiles + 1) * 8, (void **)&toff)) || (rc = palloc(nslot * 2 * 2, (void **)&bbase)) ||
+      (rc = palloc(nslot * 4, (void **)&tcol)))
+    return done(rc);
+  cudaMemsetAsync(scnt, 0, nslot * 4, st);
+  k_tb_slots<<<g, 256, 0, st>>>(ks, nnz, scnt, sstart);
+  k_tb_warplen<<<(int)std::min<int64_t>(4096, (nwarps + 255) / 256), 256, 0, st>>>(scnt, nwarps, wlen);
+  k_tb_tilelen<<<(int)std::min<int64_t>(4096, (ntiles + 256) / 256), 256, 0, st>>>(wlen, ntiles, tlen);
+  size_t tb6 = 0;
+  cub::DeviceScan::ExclusiveSum(nullptr, tb6, tlen, toff, (int)ntiles + 1, st);
+  void *ts6 = nullptr;
+  if ((rc = talloc(tb6, &ts6))) return done(rc);
+  cub::DeviceScan::ExclusiveSum(ts6, tb6, tlen, toff, (int)ntiles + 1, st);
+  int64_t brows = 0;
+  cudaMemcpyAsync(&brows, toff + ntiles, 8, cudaMemcpyDeviceToHost, st);
+  if (cudaStreamSynchronize(st) != cudaSuccess)
+    return done(fail(POLY_ECUDA, "tiled build: %s", cudaGetErrorString(cudaGetLastError())));
+  uint8_t *brec = nullptr;
+  const size_t bbytes = (size_t)std::max<int64_t>(1, brows) * kBwdStageBytes;
+  if ((rc = palloc(bbytes, (void **)&brec))) return done(rc);
+  cudaMemsetAsync(brec, 0, bbytes, st);  // the shorter halves' padding records
+  k_tb_pack<<<(int)std::min<int64_t>(65535, (nwarps + 7) / 8), 256, 0, st>>>(
+      ks, perm_in, (const float *)p.val, scnt, sstart, wlen, toff, nwarps, m, (int32_t)d, brec, bbase, tcol, ovf);
+  int32_t hov = 0;
+  cudaMemcpyAsync(&hov, ovf, 4, cudaMemcpyDeviceToHost, st);
+  if (cudaStreamSynchronize(st) != cudaSuccess)
+    return done(fail(POLY_ECUDA, "tiled build: %s", cudaGetErrorString(cudaGetLastError())));
+  if (hov) return done(POLY_EUNSUPPORTED);
+  h->tf_smem = fwd_smem;
+  h->tb_smem = bwd_smem;
+  h->tb_lcap = lcap;
+  if (cudaFuncSetAttribute((const void *)&k_strip_forward, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)h->tf_smem) != cudaSuccess ||
+      cudaFuncSetAttribute((const void *)&k_tile_backward, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)h->tb_smem) != cudaSuccess) {
+    cudaGetLastError();
+    return done(POLY_EUNSUPPORTED);
+  }
+  h->tfwd = StripFwd{frec, fhdr, uoff, d_ustart, d_ctr, pz, n, m.NS, m.rows_img, m.cols_img, m.W, m.P};
+  h->tbwd = TileBwd{brec, toff, bbase, list, loff, tcol, (int32_t)ntiles};
+  h->tf_grid = (int)std::max<int64_t>(m.NS, (int64_t)h->sms / m.NS * m.NS);
+  h->tb_grid = (int)ntiles;
+  h->tf_groups = frows * kFwdWarps;
+  h->tb_groups = brows * kBwdWarps;
+  // the fused step epilogue needs every warp's 32 columns to be one k_finalize block
+  h->tile_epi = m.rows_img == 1 || m.cols_img % 32 == 0;
+  // link blocks = loss partials (allocated for nrslices >= this grid)
+  h->k4_grid = (int)std::min<int64_t>((n + 255) / 256, (int64_t)h->sms * 8);
+  h->tiled = true;
+  h->tr_side = 0;  // the forward stages x itself: no transposed copy
+  h->tr_slices = 0;
+  return done(POLY_OK);
+}
+
 int build_sell(poly_handle *h) {
+  const int rt = build_tiled(h);
+  if (rt != POLY_EUNSUPPORTED) return rt;
   return h->p.dtype == POLY_F32 ? build_sell_t<float>(h) : build_sell_t<double>(h);
 }
 

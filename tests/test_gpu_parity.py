@@ -620,14 +620,20 @@ def test_c4_step_epilogue_same_bits(c4, monkeypatch, st, center):
 
 
 def test_c4_dsell_sell16_and_wide_agree(c4, monkeypatch):
-    """K4 keeps three layouts of the caller's CSR: SELL16 (the default: int16
-    index deltas + values), DSELL (POLY_DSELL=1: per-slice dictionaries staged
-    in shared memory, 1-byte local deltas + values, dsell.cuh) and the 8-byte
-    {index, value} form (POLY_NO_SELL16).  Same sums up to accumulation
-    order, all at oracle parity."""
+    """K4 keeps four layouts of the caller's CSR: K4t (the default for fp32:
+    strip forward + tile backward, 8-bit local deltas + values, gathers from
+    shared memory, tiled.cuh), SELL16 (POLY_NO_TILED=1: int16 index deltas +
+    values), DSELL (POLY_DSELL=1: per-slice dictionaries staged in shared
+    memory, dsell.cuh) and the 8-byte {index, value} form (POLY_NO_TILED=1
+    POLY_NO_SELL16=1).  SELL16 and DSELL form every product in fp64 (same
+    sums as the wide form up to accumulation order: 1e-12); K4t sums four
+    products in fp32 before its fp64 accumulator (POLY_TILE_CHAIN, relative
+    rounding ~1e-7 per group: 1e-6); all at oracle parity."""
     wg, wo = c4
     W = _W()
     x = torch.tensor(0.7 * wo["x_star"], device="cuda")
+    gt, lt = W.make_poly(wg).loss_grad(x)
+    monkeypatch.setenv("POLY_NO_TILED", "1")
     g16, l16 = W.make_poly(wg).loss_grad(x)
     monkeypatch.setenv("POLY_DSELL", "1")
     g_ds, l_ds = W.make_poly(wg).loss_grad(x)
@@ -638,7 +644,11 @@ def test_c4_dsell_sell16_and_wide_agree(c4, monkeypatch):
     for g, l in ((g_ds, l_ds), (g16, l16)):
         assert rel(g.cpu().numpy(), g32.cpu().numpy()) <= 1e-12
         assert abs(l - l32) <= 1e-12 * abs(l32)
-    assert rel(g_ds.cpu().numpy(), g_ref) <= TOL32
+    assert rel(gt.cpu().numpy(), g32.cpu().numpy()) <= 1e-6
+    assert abs(lt - l32) <= 1e-6 * abs(l32)
+    for g, l in ((g_ds, l_ds), (gt, lt)):
+        assert rel(g.cpu().numpy(), g_ref) <= TOL32
+        assert abs(l - l_ref) <= TOL32 * abs(l_ref)
 
 
 def test_c4_tiled_synced_backward(c4, monkeypatch):
