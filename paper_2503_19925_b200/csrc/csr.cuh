@@ -54,6 +54,7 @@ struct CsrFwdArgs {
   float *r;               // [n] residuals r_i (output)
   int32_t mode;
   double *loss_partials;  // [gridDim.x]
+  double mu_step;         // != 0: μ_j = μ_0 + j·mu_step (K4tl's geometric bins)
 };
 
 // 4 warps per 32-column slice; warp w takes steps w, w+4, w+8, ...; the four

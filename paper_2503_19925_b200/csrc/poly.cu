@@ -277,6 +277,7 @@ struct poly_handle {
   size_t tf_smem = 0, tb_smem = 0;
   bool tile_epi = false;               // every warp of K4tb covers one k_finalize block
   int32_t tb_lcap = 0;                 // K4tb ray-list capacity (floats, multiple of 4)
+  double mu_step = 0.0;                // != 0: μ is an arithmetic progression (geometric bins in K4tl)
   int64_t tf_groups = 0, tb_groups = 0;
   StepEpi epi{};                        // K4b's step epilogue for the next pass (on = 0: write g)
   // TV sets: Dykstra state, statistics, cluster launch shape
@@ -464,6 +465,7 @@ int enqueue_pass(poly_handle *h, const double *x, bool loss) {
   a.r = h->rbuf;
   a.mode = p.mode;
   a.loss_partials = h->loss_partials;
+  a.mu_step = h->mu_step;
   if (h->tiled) {
     TRY(launch(h, (const void *)&k_strip_forward, dim3(h->tf_grid), dim3((kFwdWarps + 1) * 32), h->tf_smem, true,
                h->tfwd, x32));
@@ -1444,9 +1446,9 @@ int build_tiled(poly_handle *h) {
     if (s * s == d && s > 1) m.rows_img = m.cols_img = (int32_t)s;
     else m.rows_img = 1, m.cols_img = (int32_t)d;
   }
-  // strips: the fewest with a strip of <= 100 KB (two forward CTAs per SM)
+  // strips: the fewest with a strip of <= POLY_STRIP_KB (the rest of the SM holds the ring)
   // and every ascending delta (< P + W) within 8 bits
-  const size_t kStripBytes = 100 * 1024;
+  const size_t kStripBytes = (size_t)POLY_STRIP_KB * 1024;
   for (m.NS = 1; m.NS <= kMaxStrips; ++m.NS) {
     m.W = (m.cols_img + m.NS - 1) / m.NS;
     m.P = m.rows_img > 1 ? (m.W | 1) : m.W;
@@ -1623,7 +1625,7 @@ int build_tiled(poly_handle *h) {
   if (cudaStreamSynchronize(st) != cudaSuccess)
     return done(fail(POLY_ECUDA, "tiled build: %s", cudaGetErrorString(cudaGetLastError())));
   uint8_t *brec = nullptr;
-  const size_t bbytes = (size_t)std::max<int64_t>(1, brows) * kBwdStageBytes;
+  const size_t bbytes = (size_t)std::max<int64_t>(1, brows) * kBwdWarps * kRecBytes;
   if ((rc = palloc(bbytes, (void **)&brec))) return done(rc);
   cudaMemsetAsync(brec, 0, bbytes, st);  // the shorter halves' padding records
   k_tb_pack<<<(int)std::min<int64_t>(65535, (nwarps + 7) / 8), 256, 0, st>>>(
@@ -2224,6 +2226,17 @@ int poly_init(const poly_problem *pin, poly_handle **out) {
     spec[j] = s_eff[j];
     spec[kMaxW + j] = p.mu[j];
     spec[2 * kMaxW + j] = 1.0 / p.mu[j];
+  }
+  // μ an arithmetic progression (e.g. linspace): the CSR link walks the bins
+  // geometrically (tiled.cuh row_residual_serial); tolerance 8 ulp of max μ
+  if (p.W >= 3 && !getenv("POLY_NO_GEO_MU")) {
+    const double st = (p.mu[p.W - 1] - p.mu[0]) / (double)(p.W - 1);
+    double mx = 0.0, dev = 0.0;
+    for (int j = 0; j < p.W; ++j) mx = std::max(mx, std::fabs(p.mu[j]));
+    for (int j = 0; j < p.W; ++j) dev = std::max(dev, std::fabs(p.mu[0] + j * st - p.mu[j]));
+    bool pos = true;
+    for (int j = 0; j < p.W; ++j) pos = pos && p.mu[j] > 0.0;
+    if (st != 0.0 && pos && dev <= 8.0 * 2.220446049250313e-16 * mx) h->mu_step = st;
   }
   if ((rc = dev_alloc(h, &h->spec, 3 * kMaxW)) != POLY_OK) return bail(rc);
   if (cudaMemcpy(h->spec, spec.data(), spec.size() * 8, cudaMemcpyHostToDevice) != cudaSuccess)

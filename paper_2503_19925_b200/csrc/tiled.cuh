@@ -51,14 +51,33 @@ namespace poly {
 constexpr int kTileSlots = 256;      // pixels per backward tile (32 x 8)
 constexpr int kMaxStrips = 64;
 constexpr int kRecBytes = 640;       // one warp-group: 32 x 4 B deltas + 32 x 16 B values
-constexpr int kFwdWarps = 8;         // forward consumer warps (+1 producer warp)
-constexpr int kFwdCG = 4;            // group-rows per forward stage
-constexpr int kFwdStages = 5;
+#ifndef POLY_FWD_WARPS
+#define POLY_FWD_WARPS 8
+#endif
+#ifndef POLY_FWD_CG
+#define POLY_FWD_CG 4
+#endif
+#ifndef POLY_BWD_CG
+#define POLY_BWD_CG 1
+#endif
+constexpr int kFwdWarps = POLY_FWD_WARPS;  // forward consumer warps (+1 producer warp)
+constexpr int kFwdCG = POLY_FWD_CG;        // group-rows per forward stage (units padded to a multiple)
+#ifndef POLY_FWD_STAGES
+#define POLY_FWD_STAGES 8             // ~176 KB of the forward's records in flight per SM
+#endif
+#ifndef POLY_BWD_STAGES
+#define POLY_BWD_STAGES 6
+#endif
+#ifndef POLY_STRIP_KB
+#define POLY_STRIP_KB 48              // largest iterate strip (shared memory), KB
+#endif
+constexpr int kFwdStages = POLY_FWD_STAGES;
 constexpr int kFwdHdr = kFwdWarps * 32 * 6;  // per unit: uint16 base[256], then int32 row[256]
 constexpr int kFwdStageBytes = kFwdHdr + kFwdCG * kFwdWarps * kRecBytes;
 constexpr int kBwdWarps = 16;        // backward consumer warps: 8 pixel rows x 2 halves (+1 producer)
-constexpr int kBwdStages = 6;
-constexpr int kBwdStageBytes = kBwdWarps * kRecBytes;
+constexpr int kBwdStages = POLY_BWD_STAGES;
+constexpr int kBwdCG = POLY_BWD_CG;        // group-rows per backward stage (tiles padded to a multiple)
+constexpr int kBwdStageBytes = kBwdCG * kBwdWarps * kRecBytes;
 #ifndef POLY_TILE_CHAIN
 #define POLY_TILE_CHAIN 4             // entries summed in fp32 before the fp64 accumulator (1: exact fp64 products)
 #endif
@@ -118,6 +137,84 @@ __device__ __forceinline__ void rec_group(const uint8_t *rec, int lane, int &idx
 #endif
 }
 
+// the link and per-row scalar of one row in this lane (group8_residual's
+// quantities), four bins in flight, partial sums combined in a fixed order
+// mu_step != 0: μ_j = μ_0 + j·mu_step (an arithmetic progression, checked at
+// poly_init): e^{-μ_j z} from the smallest-μ bin by a ratio e^{-|mu_step| z}
+// (exact algebra; rounding grows by one ulp per bin), two exponentials per
+// row instead of W.
+template <bool LOSS>
+__device__ __forceinline__ double row_residual_serial(const double *sp, int W, int relu, double z, double yv,
+                                                      double Ii, const float *srow, double *l_out, int mode,
+                                                      double mu_step = 0.0) {
+  const bool neg = relu && z < 0.0;
+  const double zc = neg ? 0.0 : z;
+  double hs[4] = {0.0, 0.0, 0.0, 0.0}, Hs[4] = {0.0, 0.0, 0.0, 0.0}, hp[4] = {0.0, 0.0, 0.0, 0.0};
+  const bool geo = mu_step != 0.0 && (relu || mode == 0);
+  double eg = 0.0, rg = 1.0;  // geometric: the current bin's exponential and the ratio
+  if (geo) {
+    const int j0 = mu_step < 0.0 ? W - 1 : 0;  // the smallest μ
+    eg = exp_nonpos<POLY_EXP_DEG32>(-sp[kMaxW + j0] * zc);
+    rg = exp_nonpos<POLY_EXP_DEG32>(-fabs(mu_step) * zc);
+  }
+  auto bin = [&](int j, int q) {
+    const double sj = srow ? (double)srow[j] : sp[j];
+    double e;
+    if (geo) {
+      e = eg;
+      eg *= rg;
+    } else {
+      e = (relu || mode == 0) ? exp_nonpos<POLY_EXP_DEG32>(-sp[kMaxW + j] * zc) : exp(-sp[kMaxW + j] * z);
+    }
+    hs[q] = fma(sj, e, hs[q]);
+    if (mode == 0) {
+      if (LOSS) Hs[q] += neg ? sj * z : sj * sp[2 * kMaxW + j] * (1.0 - e);
+    } else {
+      hp[q] = fma(sj * sp[kMaxW + j], e, hp[q]);
+    }
+  };
+  if (geo && mu_step < 0.0) {
+    // smallest μ last: walk the bins downwards (accumulators as in the upward walk)
+    int j = W - 1;
+    for (; j >= 3; j -= 4) {
+#pragma unroll
+      for (int q = 0; q < 4; ++q) bin(j - q, q);
+    }
+    for (; j >= 0; --j) bin(j, 0);
+  } else {
+    int j = 0;
+    for (; j + 4 <= W; j += 4) {
+#pragma unroll
+      for (int q = 0; q < 4; ++q) bin(j + q, q);
+    }
+    for (; j < W; ++j) bin(j, 0);
+  }
+  const double hst = (hs[0] + hs[1]) + (hs[2] + hs[3]);
+  const double Hst = (Hs[0] + Hs[1]) + (Hs[2] + Hs[3]);
+  double hpt = (hp[0] + hp[1]) + (hp[2] + hp[3]);
+  double phi, l;
+  if (mode == 0) {
+    phi = yv - Ii * hst;
+    l = yv * z - Ii * Hst;
+  } else {
+    hpt = (relu && !(z > 0.0)) ? 0.0 : -hpt;
+    const double m = Ii * hst;
+    if (mode == 1) {
+      phi = 2.0 * (m - yv) * Ii * hpt;
+      l = (m - yv) * (m - yv);
+    } else if (mode == 2) {
+      const double rr = m - yv;
+      phi = (rr > 0.0 ? 1.0 : (rr < 0.0 ? -1.0 : 0.0)) * Ii * hpt;
+      l = fabs(rr);
+    } else {
+      phi = (Ii - yv / hst) * hpt;
+      l = m - yv * log(m);
+    }
+  }
+  *l_out = LOSS ? l : 0.0;
+  return phi;
+}
+
 // K4tf: grid = one CTA per SM (rounded to a multiple of NS), CTA b serves strip b % NS.
 __global__ void __launch_bounds__((kFwdWarps + 1) * 32, 1) k_strip_forward(const StripFwd f,
                                                                            const float *__restrict__ x) {
@@ -153,7 +250,7 @@ __global__ void __launch_bounds__((kFwdWarps + 1) * 32, 1) k_strip_forward(const
         for (int64_t k = 0; k < ng; k += kFwdCG) {
           const int st = it % kFwdStages;
           if (it >= kFwdStages) mbar_wait(empty + st, ((it / kFwdStages) - 1) & 1);
-          const int c = done ? 0 : (int)(ng - k < kFwdCG ? ng - k : kFwdCG);
+          const int c = done ? 0 : kFwdCG;  // units are padded to a multiple of kFwdCG group-rows
           desc[st] = make_int4(done ? -1 : u, (int)k, c, (k == 0 ? 1 : 0) | (k + c >= ng ? 2 : 0));
           uint8_t *sb = stg + st * kFwdStageBytes;
           if (done) {
@@ -201,62 +298,11 @@ __global__ void __launch_bounds__((kFwdWarps + 1) * 32, 1) k_strip_forward(const
     }
     const uint8_t *rb = sb + kFwdHdr + warp * kRecBytes;
 #pragma unroll
-    for (int k = 0; k < kFwdCG; ++k)
-      if (k < dsc.z) rec_group(rb + k * kFwdWarps * kRecBytes, lane, idx, sx, (k & 1) ? a1 : a0);
+    for (int k = 0; k < kFwdCG; ++k) rec_group(rb + k * kFwdWarps * kRecBytes, lane, idx, sx, (k & 1) ? a1 : a0);
     __syncwarp();
     if (lane == 0) mbar_arrive(empty + st);
     if ((dsc.w & 2) && row >= 0) f.pz[(int64_t)strip * f.n + row] = a0 + a1;
   }
-}
-
-// the link and per-row scalar of one row in this lane (group8_residual's
-// quantities), four bins in flight, partial sums combined in a fixed order
-template <bool LOSS>
-__device__ __forceinline__ double row_residual_serial(const double *sp, int W, int relu, double z, double yv,
-                                                      double Ii, const float *srow, double *l_out, int mode) {
-  const bool neg = relu && z < 0.0;
-  const double zc = neg ? 0.0 : z;
-  double hs[4] = {0.0, 0.0, 0.0, 0.0}, Hs[4] = {0.0, 0.0, 0.0, 0.0}, hp[4] = {0.0, 0.0, 0.0, 0.0};
-  auto bin = [&](int j, int q) {
-    const double sj = srow ? (double)srow[j] : sp[j];
-    const double e = (relu || mode == 0) ? exp_nonpos<POLY_EXP_DEG32>(-sp[kMaxW + j] * zc) : exp(-sp[kMaxW + j] * z);
-    hs[q] = fma(sj, e, hs[q]);
-    if (mode == 0) {
-      if (LOSS) Hs[q] += neg ? sj * z : sj * sp[2 * kMaxW + j] * (1.0 - e);
-    } else {
-      hp[q] = fma(sj * sp[kMaxW + j], e, hp[q]);
-    }
-  };
-  int j = 0;
-  for (; j + 4 <= W; j += 4) {
-#pragma unroll
-    for (int q = 0; q < 4; ++q) bin(j + q, q);
-  }
-  for (; j < W; ++j) bin(j, 0);
-  const double hst = (hs[0] + hs[1]) + (hs[2] + hs[3]);
-  const double Hst = (Hs[0] + Hs[1]) + (Hs[2] + Hs[3]);
-  double hpt = (hp[0] + hp[1]) + (hp[2] + hp[3]);
-  double phi, l;
-  if (mode == 0) {
-    phi = yv - Ii * hst;
-    l = yv * z - Ii * Hst;
-  } else {
-    hpt = (relu && !(z > 0.0)) ? 0.0 : -hpt;
-    const double m = Ii * hst;
-    if (mode == 1) {
-      phi = 2.0 * (m - yv) * Ii * hpt;
-      l = (m - yv) * (m - yv);
-    } else if (mode == 2) {
-      const double rr = m - yv;
-      phi = (rr > 0.0 ? 1.0 : (rr < 0.0 ? -1.0 : 0.0)) * Ii * hpt;
-      l = fabs(rr);
-    } else {
-      phi = (Ii - yv / hst) * hpt;
-      l = m - yv * log(m);
-    }
-  }
-  *l_out = LOSS ? l : 0.0;
-  return phi;
 }
 
 // K4tl: z_i from the strips' partials (strip order), the link and φ_i; one
@@ -285,7 +331,7 @@ __global__ void __launch_bounds__(256, 4) k_strip_link(const CsrFwdArgs a, const
       srow = a.s_row + row * a.W;
     }
     double l;
-    a.r[row] = (float)row_residual_serial<LOSS>(sp, a.W, a.relu, z, yv, Ii, srow, &l, a.mode);
+    a.r[row] = (float)row_residual_serial<LOSS>(sp, a.W, a.relu, z, yv, Ii, srow, &l, a.mode, a.mu_step);
     lacc += l;
   }
   block_loss_n(part, lacc, a.loss_partials, blockDim.x >> 5);
@@ -318,11 +364,12 @@ __global__ void __launch_bounds__((kBwdWarps + 1) * 32, 1)
     // producer: the tile's records are static — streaming starts before the wait
     if (lane == 0) {
       const uint64_t pol = l2_evict_first_policy();
-      for (int64_t k = 0; k < ng; ++k) {
+      for (int64_t k = 0; k < ng / kBwdCG; ++k) {
         const int st = (int)(k % kBwdStages);
         if (k >= kBwdStages) mbar_wait(empty + st, (uint32_t)((k / kBwdStages) - 1) & 1);
         mbar_arrive_expect_tx(full + st, kBwdStageBytes);
-        bulk_g2s(stg + st * kBwdStageBytes, t.rec + (G0 + k) * kBwdStageBytes, kBwdStageBytes, full + st, pol);
+        bulk_g2s(stg + st * kBwdStageBytes, t.rec + (G0 / kBwdCG + k) * kBwdStageBytes, kBwdStageBytes, full + st,
+                 pol);
       }
     }
     return;
@@ -340,10 +387,12 @@ __global__ void __launch_bounds__((kBwdWarps + 1) * 32, 1)
   cp_async_wait_all();
   named_bar(1, kBwdWarps * 32);
   double a0 = 0.0, a1 = 0.0;
-  for (int64_t k = 0; k < ng; ++k) {
+  for (int64_t k = 0; k < ng / kBwdCG; ++k) {
     const int st = (int)(k % kBwdStages);
     mbar_wait(full + st, (uint32_t)(k / kBwdStages) & 1);
-    rec_group(stg + st * kBwdStageBytes + warp * kRecBytes, lane, idx, sr, (k & 1) ? a1 : a0);
+#pragma unroll
+    for (int q = 0; q < kBwdCG; ++q)
+      rec_group(stg + st * kBwdStageBytes + (q * kBwdWarps + warp) * kRecBytes, lane, idx, sr, (q & 1) ? a1 : a0);
     __syncwarp();
     if (lane == 0) mbar_arrive(empty + st);
   }
@@ -446,7 +495,8 @@ __global__ void k_tf_unitlen(const int32_t *unit_start, int32_t NS, const int32_
     int s = 0;
     while (s + 1 < NS && unit_start[s + 1] <= U) ++s;
     const int64_t i = (int64_t)s * n + (U - unit_start[s]) * (kFwdWarps * 32);
-    ulen[U] = (seglen[(int64_t)s * n + srow[i]] + 3) / 4;
+    const int64_t g = (seglen[(int64_t)s * n + srow[i]] + 3) / 4;
+    ulen[U] = (g + kFwdCG - 1) / kFwdCG * kFwdCG;
   }
 }
 
@@ -559,7 +609,7 @@ __global__ void k_tb_tilelen(const int64_t *wlen, int64_t ntiles, int64_t *tlen)
     int64_t m = 0;
     if (t < ntiles)
       for (int w = 0; w < 8; ++w) m = max(m, (wlen[t * 8 + w] + 1) / 2);
-    tlen[t] = m;
+    tlen[t] = (m + kBwdCG - 1) / kBwdCG * kBwdCG;
   }
 }
 
