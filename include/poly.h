@@ -292,7 +292,12 @@ int poly_kernel_times(poly_handle *h, double *out, int32_t nout);
  * out[7] WPR, out[8] NW, out[9] FULL (1: d fills the tile exactly, no column
  * masks); 0 for CSR / matrix-free handles.  out[10] ranks of the handle's
  * NCCL communicator (ncclCommCount; 0 without one), out[11] 1 when the
- * cross-rank sum runs as K9 (poly_p2p_open).  nout <= 12. */
+ * cross-rank sum runs as K9 (poly_p2p_open), out[12] the CSR layout poly_init
+ * built: 3 K4t (strip forward + tile backward, the default for fp32 A when
+ * every local index delta fits 8 bits; then out[0] forward CTAs, out[1] its
+ * threads, out[2] column strips, out[3] backward tiles, out[4] forward smem),
+ * 1 SELL16, 2 DSELL, 0 the 8-byte SELL; -1 for dense / matrix-free handles.
+ * nout <= 13. */
 int poly_describe(poly_handle *h, int64_t *out, int32_t nout);
 
 /* Write a fresh 128-byte ncclUniqueId into out (host).  Call on rank 0 and

@@ -194,10 +194,10 @@ def poly_kernel_times(h: int):
 
 
 def poly_describe(h: int):
-    out = (C.c_int64 * 12)()
-    _check(_lib.poly_describe(h, out, 12))
+    out = (C.c_int64 * 13)()
+    _check(_lib.poly_describe(h, out, 13))
     return dict(zip(["grid", "threads", "rows_per_stage", "stages", "smem", "sms", "V", "WPR", "NW",
-                     "full", "comm_ranks", "k9"], list(out)))
+                     "full", "comm_ranks", "k9", "csr_layout"], list(out)))
 
 
 def poly_nccl_unique_id() -> bytes:

@@ -467,10 +467,22 @@ int enqueue_pass(poly_handle *h, const double *x, bool loss) {
   a.loss_partials = h->loss_partials;
   a.mu_step = h->mu_step;
   if (h->tiled) {
+#ifdef POLY_DEV_SKIP
+    // (dev timing builds only: leave one kernel out of the pass; results are wrong)
+    static const char *skip = getenv("POLY_DEV_SKIP");
+    const bool sf = skip && strchr(skip, 'f'), sl = skip && strchr(skip, 'l'), sb = skip && strchr(skip, 'b');
+    if (!sf)
+#endif
     TRY(launch(h, (const void *)&k_strip_forward, dim3(h->tf_grid), dim3((kFwdWarps + 1) * 32), h->tf_smem, true,
                h->tfwd, x32));
+#ifdef POLY_DEV_SKIP
+    if (!sl)
+#endif
     TRY(launch(h, loss ? (const void *)&k_strip_link<true> : (const void *)&k_strip_link<false>, dim3(h->k4_grid),
                dim3(256), 0, true, a, (const double *)h->tfwd.pz, h->tfwd.NS, h->tfwd.ctr));
+#ifdef POLY_DEV_SKIP
+    if (sb) return POLY_OK;
+#endif
     return launch(h, (const void *)&k_tile_backward, dim3(h->tb_grid), dim3((kBwdWarps + 1) * 32), h->tb_smem, true,
                   h->tbwd, (const float *)h->rbuf, h->partials, (int32_t)p.d, h->epi, h->tb_lcap);
   }
@@ -1448,7 +1460,9 @@ int build_tiled(poly_handle *h) {
   }
   // strips: the fewest with a strip of <= POLY_STRIP_KB (the rest of the SM holds the ring)
   // and every ascending delta (< P + W) within 8 bits
-  const size_t kStripBytes = (size_t)POLY_STRIP_KB * 1024;
+  // (and the strip plus the forward's ring within one SM's 227 KB)
+  const size_t kStripBytes = std::min<size_t>((size_t)POLY_STRIP_KB * 1024,
+                                              227 * 1024 - (size_t)kFwdStages * kFwdStageBytes - 512);
   for (m.NS = 1; m.NS <= kMaxStrips; ++m.NS) {
     m.W = (m.cols_img + m.NS - 1) / m.NS;
     m.P = m.rows_img > 1 ? (m.W | 1) : m.W;
@@ -1463,9 +1477,38 @@ int build_tiled(poly_handle *h) {
   if (ntiles >= ((int64_t)1 << 23)) return POLY_EUNSUPPORTED;
   const int64_t nwarps = ntiles * 8;
   cudaStream_t st = h->work;
+  // POLY_BUILD_TIMING=1: per-phase build times on stderr (syncs the stream)
+  static const bool btime = getenv("POLY_BUILD_TIMING") != nullptr;
+  auto t_last = std::chrono::steady_clock::now();
+  auto mark = [&](const char *what) {
+    if (!btime) return;
+    cudaStreamSynchronize(st);
+    const auto t = std::chrono::steady_clock::now();
+    fprintf(stderr, "[tiled build] %-28s %8.3f ms\n", what, std::chrono::duration<double, std::milli>(t - t_last).count());
+    t_last = t;
+  };
   std::vector<void *> tmp;
   std::vector<void *> mine;  // persistent buffers, released on failure
+  // temporaries come from one arena (one cudaMalloc / cudaFree instead of ~25:
+  // poly_init is inside the end-to-end measurement), overflow from cudaMalloc
+  const int64_t nsn_est = (int64_t)m.NS * n;
+  size_t arena_cap = (size_t)nnz * 40 + (size_t)nsn_est * 40 + (size_t)ntiles * kTileSlots * 16 + ((size_t)64 << 20);
+  char *arena = nullptr;
+  size_t arena_used = 0;
+  if (cudaMalloc((void **)&arena, arena_cap) != cudaSuccess) {
+    cudaGetLastError();
+    arena = nullptr;
+    arena_cap = 0;
+  } else {
+    tmp.push_back(arena);
+  }
   auto talloc = [&](size_t bytes, void **ptr) -> int {
+    const size_t need = (std::max<size_t>(bytes, 16) + 255) & ~(size_t)255;
+    if (arena && arena_used + need <= arena_cap) {
+      *ptr = arena + arena_used;
+      arena_used += need;
+      return POLY_OK;
+    }
     if (cudaMalloc(ptr, std::max<size_t>(bytes, 16)) != cudaSuccess) {
       cudaGetLastError();
       return fail(POLY_ENOMEM, "tiled build: cudaMalloc(%zu) failed", bytes);
@@ -1504,9 +1547,13 @@ int build_tiled(poly_handle *h) {
   cudaMemsetAsync(seglen, 0, nsn * 4, st);
   cudaMemsetAsync(nz, 0, kMaxStrips * 4, st);
   cudaMemsetAsync(ovf, 0, 4, st);
+  mark("alloc fwd temps (before rows)");
   k_entry_rows<<<g, 256, 0, st>>>(p.row_ptr, n, rows);
-  k_tf_keys<<<g, 256, 0, st>>>(rows, p.col, nnz, n, m, kin, perm_in, seglen);
   const int sbits = 32 - __builtin_clz((unsigned)std::max(1, m.NS - 1));
+  auto nbits = [](int64_t v) { int b = 1; while (b < 62 && ((int64_t)1 << b) <= v) ++b; return b; };  // bits of v >= 0
+  m.lb = nbits((int64_t)m.rows_img * m.P - 1);
+  m.rb = nbits(n - 1);
+  k_tf_keys<<<g, 256, 0, st>>>(rows, p.col, nnz, n, m, kin, perm_in, seglen);
   // 64-bit key radix sorts (temporary storage sized per call)
   auto sort64 = [&](const uint64_t *ki, uint64_t *ko, const int32_t *vi, int32_t *vo, int64_t items, int bits) -> int {
     size_t tb = 0;
@@ -1517,14 +1564,16 @@ int build_tiled(poly_handle *h) {
       return fail(POLY_ECUDA, "tiled build: radix sort failed");
     return POLY_OK;
   };
-  if ((rc = sort64(kin, ks, perm_in, perm, nnz, 48 + sbits))) return done(rc);
-  k_tf_segstart<<<g, 256, 0, st>>>(ks, nnz, n, segstart);
+  if ((rc = sort64(kin, ks, perm_in, perm, nnz, sbits + m.rb + m.lb))) return done(rc);
+  mark("fwd keys + sort");
+  k_tf_segstart<<<g, 256, 0, st>>>(ks, nnz, n, m, segstart);
   // segments of each strip longest first
   uint64_t *okin = nullptr, *oks = nullptr;
   int32_t *orin = nullptr, *srow = nullptr;
   if ((rc = talloc(nsn * 8, (void **)&okin)) || (rc = talloc(nsn * 8, (void **)&oks)) ||
       (rc = talloc(nsn * 4, (void **)&orin)) || (rc = talloc(nsn * 4, (void **)&srow)))
     return done(rc);
+  mark("segstart/order alloc");
   k_tf_order_keys<<<g, 256, 0, st>>>(seglen, n, m.NS, okin, orin, nz);
   if ((rc = sort64(okin, oks, orin, srow, nsn, 32 + sbits))) return done(rc);
   std::vector<int32_t> hnz(m.NS);
@@ -1559,7 +1608,8 @@ int build_tiled(poly_handle *h) {
   uint8_t *frec = nullptr;
   if ((rc = palloc((size_t)std::max<int64_t>(1, frows) * kFwdWarps * kRecBytes, (void **)&frec))) return done(rc);
   k_tf_pack<<<(int)std::min<int64_t>(65535, (units * kFwdWarps + 7) / 8), 256, 0, st>>>(
-      d_ustart, m.NS, srow, seglen, nz, segstart, ks, perm, (const float *)p.val, n, units, uoff, frec, fhdr, ovf);
+      d_ustart, m.NS, srow, seglen, nz, segstart, ks, perm, (const float *)p.val, n, units, uoff, m, frec, fhdr, ovf);
+  mark("fwd order sort + units + pack");
   // ---- backward: sort by (tile, row, slot), ray lists, then by (tile, slot, list position)
   int32_t *flag = nullptr, *pidx = nullptr, *tcnt = nullptr, *list = nullptr;
   int64_t *tcnt64 = nullptr, *pstart = nullptr, *loff = nullptr;
@@ -1570,8 +1620,9 @@ int build_tiled(poly_handle *h) {
   cudaMemsetAsync(tcnt, 0, ntiles * 4, st);
   k_tb_keys<<<g, 256, 0, st>>>(rows, p.col, nnz, m, kin, perm_in);
   const int tbits = 32 - __builtin_clz((unsigned)std::max<int64_t>(1, ntiles - 1));
-  if ((rc = sort64(kin, ks, perm_in, perm, nnz, 40 + tbits))) return done(rc);
-  k_tb_pairs<<<g, 256, 0, st>>>(ks, nnz, flag, tcnt);
+  if ((rc = sort64(kin, ks, perm_in, perm, nnz, tbits + m.rb + 8))) return done(rc);
+  mark("bwd keys + sort");
+  k_tb_pairs<<<g, 256, 0, st>>>(ks, nnz, m, flag, tcnt);
   size_t tb4 = 0, tb5 = 0;
   cub::DeviceScan::InclusiveSum(nullptr, tb4, flag, pidx, (int)nnz, st);
   cub::DeviceScan::ExclusiveSum(nullptr, tb5, tcnt64, loff, (int)ntiles + 1, st);
@@ -1595,11 +1646,16 @@ int build_tiled(poly_handle *h) {
   const size_t bwd_smem = (size_t)kBwdStages * kBwdStageBytes + (size_t)lcap * 4 + 2 * kBwdStages * 8;
   const size_t fwd_smem = (((size_t)m.rows_img * m.P * 4 + 127) & ~(size_t)127) + (size_t)kFwdStages * kFwdStageBytes +
                           2 * kFwdStages * 8 + kFwdStages * 16;
-  if (bwd_smem + 2048 > 227 * 1024 || fwd_smem > 227 * 1024) return done(POLY_EUNSUPPORTED);
+  if (bwd_smem + 2048 > 227 * 1024 || fwd_smem > 227 * 1024) {
+    if (btime) fprintf(stderr, "[tiled build] unsupported: smem fwd %zu bwd %zu\n", fwd_smem, bwd_smem);
+    return done(POLY_EUNSUPPORTED);
+  }
   if ((rc = palloc((size_t)(nlist + 4) * 4, (void **)&list))) return done(rc);
   cudaMemsetAsync(list, 0, (size_t)(nlist + 4) * 4, st);
-  k_tb_list<<<g, 256, 0, st>>>(ks, pidx, flag, pstart, loff, nnz, list, kin);
-  const int qbits = 32 + 32 - __builtin_clz((unsigned)std::max<int64_t>(1, ntiles * kTileSlots - 1));
+  mark("bwd pairs/scans/list alloc");
+  m.pb = nbits(std::max(1, lmax) - 1);
+  k_tb_list<<<g, 256, 0, st>>>(ks, pidx, flag, pstart, loff, nnz, m, list, kin);
+  const int qbits = m.pb + 32 - __builtin_clz((unsigned)std::max<int64_t>(1, ntiles * kTileSlots - 1));
   if ((rc = sort64(kin, ks, perm, perm_in, nnz, qbits))) return done(rc);
   // perm_in now maps the (tile, slot, position) order to the caller's entries
   int32_t *scnt = nullptr, *tcol = nullptr;
@@ -1611,8 +1667,9 @@ int build_tiled(poly_handle *h) {
       (rc = palloc((ntiles + 1) * 8, (void **)&toff)) || (rc = palloc(nslot * 2 * 2, (void **)&bbase)) ||
       (rc = palloc(nslot * 4, (void **)&tcol)))
     return done(rc);
+  mark("bwd list + sort2 + allocs");
   cudaMemsetAsync(scnt, 0, nslot * 4, st);
-  k_tb_slots<<<g, 256, 0, st>>>(ks, nnz, scnt, sstart);
+  k_tb_slots<<<g, 256, 0, st>>>(ks, nnz, m, scnt, sstart);
   k_tb_warplen<<<(int)std::min<int64_t>(4096, (nwarps + 255) / 256), 256, 0, st>>>(scnt, nwarps, wlen);
   k_tb_tilelen<<<(int)std::min<int64_t>(4096, (ntiles + 256) / 256), 256, 0, st>>>(wlen, ntiles, tlen);
   size_t tb6 = 0;
@@ -1622,19 +1679,30 @@ int build_tiled(poly_handle *h) {
   cub::DeviceScan::ExclusiveSum(ts6, tb6, tlen, toff, (int)ntiles + 1, st);
   int64_t brows = 0;
   cudaMemcpyAsync(&brows, toff + ntiles, 8, cudaMemcpyDeviceToHost, st);
+  std::vector<int64_t> htl(ntiles);
+  cudaMemcpyAsync(htl.data(), tlen, ntiles * 8, cudaMemcpyDeviceToHost, st);
   if (cudaStreamSynchronize(st) != cudaSuccess)
     return done(fail(POLY_ECUDA, "tiled build: %s", cudaGetErrorString(cudaGetLastError())));
+  int64_t tmax = 0;
+  for (int64_t v : htl) tmax = std::max(tmax, v);
+  // stage-interleaved tiles ([stage][tile]) unless the tiles' lengths differ by more than 1/8
+  const int32_t inter = getenv("POLY_BWD_TILE_MAJOR") ? 0 : (tmax * ntiles <= brows + brows / 8 ? 1 : 0);
   uint8_t *brec = nullptr;
-  const size_t bbytes = (size_t)std::max<int64_t>(1, brows) * kBwdWarps * kRecBytes;
+  const size_t bbytes = (size_t)std::max<int64_t>(1, inter ? tmax * ntiles : brows) * kBwdWarps * kRecBytes;
   if ((rc = palloc(bbytes, (void **)&brec))) return done(rc);
   cudaMemsetAsync(brec, 0, bbytes, st);  // the shorter halves' padding records
   k_tb_pack<<<(int)std::min<int64_t>(65535, (nwarps + 7) / 8), 256, 0, st>>>(
-      ks, perm_in, (const float *)p.val, scnt, sstart, wlen, toff, nwarps, m, (int32_t)d, brec, bbase, tcol, ovf);
+      ks, perm_in, (const float *)p.val, scnt, sstart, wlen, toff, nwarps, m, (int32_t)d, brec, bbase, tcol, ovf,
+      inter);
+  mark("bwd slots/scan/pack");
   int32_t hov = 0;
   cudaMemcpyAsync(&hov, ovf, 4, cudaMemcpyDeviceToHost, st);
   if (cudaStreamSynchronize(st) != cudaSuccess)
     return done(fail(POLY_ECUDA, "tiled build: %s", cudaGetErrorString(cudaGetLastError())));
-  if (hov) return done(POLY_EUNSUPPORTED);
+  if (hov) {
+    if (btime) fprintf(stderr, "[tiled build] unsupported: a local delta does not fit 8 bits (code %d)\n", hov);
+    return done(POLY_EUNSUPPORTED);
+  }
   h->tf_smem = fwd_smem;
   h->tb_smem = bwd_smem;
   h->tb_lcap = lcap;
@@ -1646,7 +1714,7 @@ int build_tiled(poly_handle *h) {
     return done(POLY_EUNSUPPORTED);
   }
   h->tfwd = StripFwd{frec, fhdr, uoff, d_ustart, d_ctr, pz, n, m.NS, m.rows_img, m.cols_img, m.W, m.P};
-  h->tbwd = TileBwd{brec, toff, bbase, list, loff, tcol, (int32_t)ntiles};
+  h->tbwd = TileBwd{brec, toff, bbase, list, loff, tcol, (int32_t)ntiles, inter};
   h->tf_grid = (int)std::max<int64_t>(m.NS, (int64_t)h->sms / m.NS * m.NS);
   h->tb_grid = (int)ntiles;
   h->tf_groups = frows * kFwdWarps;
@@ -2849,8 +2917,8 @@ int poly_kernel_times(poly_handle *h, double *out, int32_t nout) {
 }
 
 int poly_describe(poly_handle *h, int64_t *out, int32_t nout) {
-  if (!h || !out || nout < 0 || nout > 12) return fail(POLY_EINVAL, "bad arguments");
-  int64_t v[12] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+  if (!h || !out || nout < 0 || nout > 13) return fail(POLY_EINVAL, "bad arguments");
+  int64_t v[13] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
   if (h->nccl) {
     int c = 0;
     if (nccl_api()->count(h->nccl, &c) == ncclSuccess) v[10] = c;
@@ -2866,6 +2934,12 @@ int poly_describe(poly_handle *h, int64_t *out, int32_t nout) {
     v[7] = h->dv->WPR;
     v[8] = h->dv->NW;
     v[9] = h->full;
+  } else if (h->tiled) {
+    v[0] = h->tf_grid;   // K4tf CTAs (one per SM), K4tb: one CTA per 32 x 8 tile
+    v[1] = (kFwdWarps + 1) * 32;
+    v[2] = h->tfwd.NS;   // column strips
+    v[3] = h->tb_grid;
+    v[4] = (int64_t)h->tf_smem;
   } else {
     v[0] = h->k4_grid;   // K4f blocks (32-row slices); K4b: one block per 32-column slice
     v[1] = 128;
@@ -2873,6 +2947,8 @@ int poly_describe(poly_handle *h, int64_t *out, int32_t nout) {
     v[3] = h->sell_steps;
     v[4] = 0;
   }
+  // CSR layout: 0 wide SELL-32, 1 compact SELL16, 2 DSELL, 3 K4t (tiled.cuh); -1 dense / matrix-free
+  v[12] = h->p.layout != POLY_CSR ? -1 : (h->tiled ? 3 : (h->dsell ? 2 : (h->sell16 ? 1 : 0)));
   v[5] = h->sms;
   for (int i = 0; i < nout; ++i) out[i] = v[i];
   return POLY_OK;

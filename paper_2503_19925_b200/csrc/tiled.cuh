@@ -52,10 +52,10 @@ constexpr int kTileSlots = 256;      // pixels per backward tile (32 x 8)
 constexpr int kMaxStrips = 64;
 constexpr int kRecBytes = 640;       // one warp-group: 32 x 4 B deltas + 32 x 16 B values
 #ifndef POLY_FWD_WARPS
-#define POLY_FWD_WARPS 8
+#define POLY_FWD_WARPS 12
 #endif
 #ifndef POLY_FWD_CG
-#define POLY_FWD_CG 4
+#define POLY_FWD_CG 2
 #endif
 #ifndef POLY_BWD_CG
 #define POLY_BWD_CG 1
@@ -63,13 +63,19 @@ constexpr int kRecBytes = 640;       // one warp-group: 32 x 4 B deltas + 32 x 1
 constexpr int kFwdWarps = POLY_FWD_WARPS;  // forward consumer warps (+1 producer warp)
 constexpr int kFwdCG = POLY_FWD_CG;        // group-rows per forward stage (units padded to a multiple)
 #ifndef POLY_FWD_STAGES
-#define POLY_FWD_STAGES 8             // ~176 KB of the forward's records in flight per SM
+#define POLY_FWD_STAGES 8             // 141 KB of the forward's records in flight per SM
 #endif
 #ifndef POLY_BWD_STAGES
 #define POLY_BWD_STAGES 6
 #endif
+#ifndef POLY_FWD_PF
+#define POLY_FWD_PF 0                 // L2 prefetch of the next unit
+#endif
+#ifndef POLY_BWD_PF
+#define POLY_BWD_PF 0                // L2 prefetch this many stages ahead (<= stages: off)
+#endif
 #ifndef POLY_STRIP_KB
-#define POLY_STRIP_KB 48              // largest iterate strip (shared memory), KB
+#define POLY_STRIP_KB 100              // largest iterate strip (shared memory), KB
 #endif
 constexpr int kFwdStages = POLY_FWD_STAGES;
 constexpr int kFwdHdr = kFwdWarps * 32 * 6;  // per unit: uint16 base[256], then int32 row[256]
@@ -103,7 +109,20 @@ struct TileBwd {
   const int64_t *list_off;   // [ntiles + 1]
   const int32_t *tcol;       // [ntiles * 256] column of each slot, -1: none
   int32_t ntiles;
+  int32_t interleave;        // 1: stage k of every tile stored together ([k][tile]: the CTAs' bulk
+                             // copies walk one contiguous region), 0: tile-major
 };
+
+// byte offset of stage k of tile t (first group-row G0 in the tile-major form)
+__device__ __forceinline__ int64_t bwd_stage_off(const TileBwd &t, int tile, int64_t G0, int64_t k) {
+  return (t.interleave ? k * t.ntiles + tile : G0 / kBwdCG + k) * (int64_t)kBwdStageBytes;
+}
+
+// L2 prefetch of a contiguous range through the TMA engine (no shared memory):
+// the ring's bulk copies then find their bytes in L2
+__device__ __forceinline__ void bulk_prefetch_l2(const void *p, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+}
 
 __device__ __forceinline__ void cp_async_wait_all() {
   asm volatile("cp.async.commit_group;" ::: "memory");
@@ -241,15 +260,25 @@ __global__ void __launch_bounds__((kFwdWarps + 1) * 32, 1) k_strip_forward(const
     if (lane == 0) {
       const uint64_t pol = l2_evict_first_policy();
       pdl_wait();  // the counter is reset by the previous link kernel
-      int it = 0;
+      int it = 0, st = 0;
+      uint32_t eph = 0;  // stage index and the ring's pass parity (incremental: no division)
+      int u = atomicAdd(f.ctr + strip, 1);
+      auto prefetch_unit = [&](int uu) {
+        if (POLY_FWD_PF && uu < nu) {
+          const int64_t UU = (int64_t)u0 + uu, a0 = f.unit_off[UU], a1 = f.unit_off[UU + 1];
+          bulk_prefetch_l2(f.hdr + UU * kFwdHdr, kFwdHdr);
+          bulk_prefetch_l2(f.rec + a0 * kFwdWarps * kRecBytes, (uint32_t)((a1 - a0) * kFwdWarps * kRecBytes));
+        }
+      };
+      prefetch_unit(u);
       for (;;) {
-        const int u = atomicAdd(f.ctr + strip, 1);
         const bool done = u >= nu;
+        const int un = done ? nu : atomicAdd(f.ctr + strip, 1);  // the next unit, prefetched while this one streams
         const int64_t U = (int64_t)u0 + u;
         const int64_t g0 = done ? 0 : f.unit_off[U], ng = done ? 1 : f.unit_off[U + 1] - g0;
         for (int64_t k = 0; k < ng; k += kFwdCG) {
-          const int st = it % kFwdStages;
-          if (it >= kFwdStages) mbar_wait(empty + st, ((it / kFwdStages) - 1) & 1);
+          if (k == kFwdCG) prefetch_unit(un);
+          if (it >= kFwdStages) mbar_wait(empty + st, eph ^ 1);
           const int c = done ? 0 : kFwdCG;  // units are padded to a multiple of kFwdCG group-rows
           desc[st] = make_int4(done ? -1 : u, (int)k, c, (k == 0 ? 1 : 0) | (k + c >= ng ? 2 : 0));
           uint8_t *sb = stg + st * kFwdStageBytes;
@@ -262,8 +291,11 @@ __global__ void __launch_bounds__((kFwdWarps + 1) * 32, 1) k_strip_forward(const
             bulk_g2s(sb + kFwdHdr, f.rec + (g0 + k) * kFwdWarps * kRecBytes, data, full + st, pol);
           }
           ++it;
+          if (++st == kFwdStages) st = 0, eph ^= 1;
         }
         if (done) break;
+        if (ng <= kFwdCG) prefetch_unit(un);
+        u = un;
       }
     }
     return;
@@ -285,9 +317,10 @@ __global__ void __launch_bounds__((kFwdWarps + 1) * 32, 1) k_strip_forward(const
   pdl_trigger();
   int idx = 0, row = -1;
   double a0 = 0.0, a1 = 0.0;
-  for (int it = 0;; ++it) {
-    const int st = it % kFwdStages;
-    mbar_wait(full + st, (it / kFwdStages) & 1);
+  int st = 0;
+  uint32_t ph = 0;
+  for (;; st = st + 1 == kFwdStages ? 0 : st + 1, ph ^= st == 0 ? 1u : 0u) {
+    mbar_wait(full + st, ph);
     const int4 dsc = desc[st];
     if (dsc.x < 0) break;
     const uint8_t *sb = stg + st * kFwdStageBytes;
@@ -364,12 +397,18 @@ __global__ void __launch_bounds__((kBwdWarps + 1) * 32, 1)
     // producer: the tile's records are static — streaming starts before the wait
     if (lane == 0) {
       const uint64_t pol = l2_evict_first_policy();
-      for (int64_t k = 0; k < ng / kBwdCG; ++k) {
-        const int st = (int)(k % kBwdStages);
-        if (k >= kBwdStages) mbar_wait(empty + st, (uint32_t)((k / kBwdStages) - 1) & 1);
+      const int64_t ns = ng / kBwdCG;
+      if (POLY_BWD_PF > kBwdStages && ns > kBwdStages)
+        for (int64_t q = kBwdStages; q < min(ns, (int64_t)POLY_BWD_PF); ++q)
+          bulk_prefetch_l2(t.rec + bwd_stage_off(t, tile, G0, q), kBwdStageBytes);
+      int st = 0;
+      uint32_t eph = 0;
+      for (int64_t k = 0; k < ns; ++k, st = st + 1 == kBwdStages ? 0 : st + 1, eph ^= st == 0 ? 1u : 0u) {
+        if (POLY_BWD_PF > kBwdStages && k + POLY_BWD_PF < ns)
+          bulk_prefetch_l2(t.rec + bwd_stage_off(t, tile, G0, k + POLY_BWD_PF), kBwdStageBytes);
+        if (k >= kBwdStages) mbar_wait(empty + st, eph ^ 1);
         mbar_arrive_expect_tx(full + st, kBwdStageBytes);
-        bulk_g2s(stg + st * kBwdStageBytes, t.rec + (G0 / kBwdCG + k) * kBwdStageBytes, kBwdStageBytes, full + st,
-                 pol);
+        bulk_g2s(stg + st * kBwdStageBytes, t.rec + bwd_stage_off(t, tile, G0, k), kBwdStageBytes, full + st, pol);
       }
     }
     return;
@@ -387,9 +426,11 @@ __global__ void __launch_bounds__((kBwdWarps + 1) * 32, 1)
   cp_async_wait_all();
   named_bar(1, kBwdWarps * 32);
   double a0 = 0.0, a1 = 0.0;
-  for (int64_t k = 0; k < ng / kBwdCG; ++k) {
-    const int st = (int)(k % kBwdStages);
-    mbar_wait(full + st, (uint32_t)(k / kBwdStages) & 1);
+  const int nst = (int)(ng / kBwdCG);
+  int st = 0;
+  uint32_t ph = 0;
+  for (int k = 0; k < nst; ++k, st = st + 1 == kBwdStages ? 0 : st + 1, ph ^= st == 0 ? 1u : 0u) {
+    mbar_wait(full + st, ph);
 #pragma unroll
     for (int q = 0; q < kBwdCG; ++q)
       rec_group(stg + st * kBwdStageBytes + (q * kBwdWarps + warp) * kRecBytes, lane, idx, sr, (q & 1) ? a1 : a0);
@@ -436,6 +477,7 @@ struct TiledGeom {
   int32_t rows_img, cols_img;
   int32_t NS, W, P;          // strips
   int32_t TW, TH, tiles_x;   // tiles: TW x TH pixels (32 x 8, or 256 x 1 for one image row)
+  int32_t lb, rb, pb;        // sort-key field widths: strip-local index, row, ray-list position
 };
 
 __device__ __forceinline__ void strip_of(const TiledGeom &m, int32_t col, int32_t &strip, int32_t &loc) {
@@ -457,17 +499,18 @@ __global__ void k_tf_keys(const int32_t *rows, const int32_t *col, int64_t nnz, 
     int32_t s, loc;
     strip_of(m, col[e], s, loc);
     const uint32_t r = (uint32_t)rows[e];
-    key[e] = ((uint64_t)s << 48) | ((uint64_t)r << 16) | (uint64_t)loc;
+    key[e] = ((uint64_t)s << (m.rb + m.lb)) | ((uint64_t)r << m.lb) | (uint64_t)loc;
     perm[e] = (int32_t)e;
     atomicAdd(seglen + (int64_t)s * n + r, 1);
   }
 }
 
 // first sorted position of every segment
-__global__ void k_tf_segstart(const uint64_t *ks, int64_t nnz, int64_t n, int64_t *segstart) {
+__global__ void k_tf_segstart(const uint64_t *ks, int64_t nnz, int64_t n, TiledGeom m, int64_t *segstart) {
   for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < nnz; k += (int64_t)gridDim.x * blockDim.x) {
-    const uint64_t q = ks[k] >> 16;
-    if (k == 0 || (ks[k - 1] >> 16) != q) segstart[(int64_t)(q >> 32) * n + (q & 0xffffffffu)] = k;
+    const uint64_t q = ks[k] >> m.lb;
+    if (k == 0 || (ks[k - 1] >> m.lb) != q)
+      segstart[(int64_t)(q >> m.rb) * n + (int64_t)(q & ((1ull << m.rb) - 1))] = k;
   }
 }
 
@@ -503,8 +546,8 @@ __global__ void k_tf_unitlen(const int32_t *unit_start, int32_t NS, const int32_
 // one warp per (unit, warp), lane = segment: header and records
 __global__ void k_tf_pack(const int32_t *unit_start, int32_t NS, const int32_t *srow, const int32_t *seglen,
                           const int32_t *nz, const int64_t *segstart, const uint64_t *ks, const int32_t *perm,
-                          const float *val, int64_t n, int64_t units, const int64_t *unit_off, uint8_t *rec,
-                          uint8_t *hdr, int32_t *overflow) {
+                          const float *val, int64_t n, int64_t units, const int64_t *unit_off, TiledGeom m,
+                          uint8_t *rec, uint8_t *hdr, int32_t *overflow) {
   const int lane = threadIdx.x & 31;
   const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
   for (int64_t q = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); q < units * kFwdWarps; q += nw) {
@@ -520,7 +563,8 @@ __global__ void k_tf_pack(const int32_t *unit_start, int32_t NS, const int32_t *
       len = seglen[(int64_t)s * n + row];
       st = segstart[(int64_t)s * n + row];
     }
-    int32_t prev = len > 0 ? (int32_t)(ks[st] & 0xffffu) : 0;
+    const uint64_t lmask = (1ull << m.lb) - 1;
+    int32_t prev = len > 0 ? (int32_t)(ks[st] & lmask) : 0;
     ((uint16_t *)(hdr + U * kFwdHdr))[w * 32 + lane] = (uint16_t)prev;
     ((int32_t *)(hdr + U * kFwdHdr + kFwdWarps * 32 * 2))[w * 32 + lane] = row;
     const int64_t g0 = unit_off[U], ng = unit_off[U + 1] - g0;
@@ -532,7 +576,7 @@ __global__ void k_tf_pack(const int32_t *unit_start, int32_t NS, const int32_t *
         const int64_t k = 4 * g + qq;
         v4[qq] = 0.f;
         if (k < len) {
-          const int32_t loc = (int32_t)(ks[st + k] & 0xffffu);
+          const int32_t loc = (int32_t)(ks[st + k] & lmask);
           const int32_t dlt = loc - prev;
           if (dlt < 0 || dlt > 255) atomicOr(overflow, 1);
           dd |= (uint32_t)(dlt & 0xff) << (8 * qq);
@@ -553,29 +597,29 @@ __global__ void k_tb_keys(const int32_t *rows, const int32_t *col, int64_t nnz, 
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < nnz; e += (int64_t)gridDim.x * blockDim.x) {
     int32_t t, sl;
     tile_of(m, col[e], t, sl);
-    key[e] = ((uint64_t)t << 40) | ((uint64_t)(uint32_t)rows[e] << 8) | (uint64_t)sl;
+    key[e] = ((uint64_t)t << (m.rb + 8)) | ((uint64_t)(uint32_t)rows[e] << 8) | (uint64_t)sl;
     perm[e] = (int32_t)e;
   }
 }
 
 // first entry of every (tile, row) pair; pairs per tile
-__global__ void k_tb_pairs(const uint64_t *ks, int64_t nnz, int32_t *flag, int32_t *tcnt) {
+__global__ void k_tb_pairs(const uint64_t *ks, int64_t nnz, TiledGeom m, int32_t *flag, int32_t *tcnt) {
   for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < nnz; k += (int64_t)gridDim.x * blockDim.x) {
     const bool f = k == 0 || (ks[k - 1] >> 8) != (ks[k] >> 8);
     flag[k] = f ? 1 : 0;
-    if (f) atomicAdd(tcnt + (int64_t)(ks[k] >> 40), 1);
+    if (f) atomicAdd(tcnt + (int64_t)(ks[k] >> (m.rb + 8)), 1);
   }
 }
 
 // ray lists and the second sort's keys (tile*256 + slot | list position)
 __global__ void k_tb_list(const uint64_t *ks, const int32_t *pidx, const int32_t *flag, const int64_t *pstart,
-                          const int64_t *list_off, int64_t nnz, int32_t *list, uint64_t *key2) {
+                          const int64_t *list_off, int64_t nnz, TiledGeom m, int32_t *list, uint64_t *key2) {
   for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < nnz; k += (int64_t)gridDim.x * blockDim.x) {
     const uint64_t q = ks[k];
-    const int64_t t = (int64_t)(q >> 40);
+    const int64_t t = (int64_t)(q >> (m.rb + 8));
     const int64_t pos = (int64_t)pidx[k] - 1 - pstart[t];  // inclusive scan of flag
-    if (flag[k]) list[list_off[t] + pos] = (int32_t)((q >> 8) & 0xffffffffu);
-    key2[k] = ((uint64_t)(t * kTileSlots + (int64_t)(q & 0xffu)) << 32) | (uint64_t)pos;
+    if (flag[k]) list[list_off[t] + pos] = (int32_t)((q >> 8) & ((1ull << m.rb) - 1));
+    key2[k] = ((uint64_t)(t * kTileSlots + (int64_t)(q & 0xffu)) << m.pb) | (uint64_t)pos;
   }
 }
 
@@ -586,11 +630,11 @@ __global__ void k_round4(int64_t *c, int64_t n) {
 }
 
 // entries and first position per (tile, slot)
-__global__ void k_tb_slots(const uint64_t *ks2, int64_t nnz, int32_t *cnt, int64_t *start) {
+__global__ void k_tb_slots(const uint64_t *ks2, int64_t nnz, TiledGeom m, int32_t *cnt, int64_t *start) {
   for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < nnz; k += (int64_t)gridDim.x * blockDim.x) {
-    const uint64_t q = ks2[k] >> 32;
+    const uint64_t q = ks2[k] >> m.pb;
     atomicAdd(cnt + q, 1);
-    if (k == 0 || (ks2[k - 1] >> 32) != q) start[q] = k;
+    if (k == 0 || (ks2[k - 1] >> m.pb) != q) start[q] = k;
   }
 }
 
@@ -617,7 +661,8 @@ __global__ void k_tb_tilelen(const int64_t *wlen, int64_t ntiles, int64_t *tlen)
 // halves' bases; also the slot -> column map
 __global__ void k_tb_pack(const uint64_t *ks2, const int32_t *perm2, const float *val, const int32_t *cnt,
                           const int64_t *start, const int64_t *wlen, const int64_t *tile_off, int64_t nwarps,
-                          TiledGeom m, int32_t d, uint8_t *rec, uint16_t *base, int32_t *tcol, int32_t *overflow) {
+                          TiledGeom m, int32_t d, uint8_t *rec, uint16_t *base, int32_t *tcol, int32_t *overflow,
+                          int32_t interleave) {
   const int lane = threadIdx.x & 31;
   const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
   for (int64_t w = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); w < nwarps; w += nw) {
@@ -630,8 +675,9 @@ __global__ void k_tb_pack(const uint64_t *ks2, const int32_t *perm2, const float
     tcol[q] = (r < m.rows_img && c < m.cols_img && col < d) ? (int32_t)col : -1;
     const int32_t len = cnt[q];
     const int64_t st = len > 0 ? start[q] : 0;
-    int32_t prev = len > 0 ? (int32_t)(ks2[st] & 0xffffffffu) : 0;
-    if (prev > 65535) atomicOr(overflow, 1);
+    const uint64_t pmask = (1ull << m.pb) - 1;
+    int32_t prev = len > 0 ? (int32_t)(ks2[st] & pmask) : 0;
+    if (prev > 65535) atomicOr(overflow, 4);
     const int64_t ng = wlen[w], per = (ng + 1) / 2;  // half 0: groups [0, per), half 1: [per, ng)
     base[q * 2] = (uint16_t)prev;
     base[q * 2 + 1] = (uint16_t)prev;  // (ng <= per: the second half is all padding)
@@ -645,15 +691,18 @@ __global__ void k_tb_pack(const uint64_t *ks2, const int32_t *perm2, const float
         const int64_t e = 4 * g + j;
         v4[j] = 0.f;
         if (e < len) {
-          const int32_t pos = (int32_t)(ks2[st + e] & 0xffffffffu);
+          const int32_t pos = (int32_t)(ks2[st + e] & pmask);
           const int32_t dlt = pos - prev;
-          if (dlt < 0 || dlt > 255) atomicOr(overflow, 1);
+          if (dlt < 0 || dlt > 255) atomicOr(overflow, 2);
           dd |= (uint32_t)(dlt & 0xff) << (8 * j);
           prev = pos;
           v4[j] = val[perm2[st + e]];
         }
       }
-      uint8_t *rp = rec + ((tile_off[t] + k) * kBwdWarps + hh * 8 + pw) * kRecBytes;
+      const int64_t ntl = nwarps / 8;
+      const int64_t ri = interleave ? ((k / kBwdCG) * ntl + t) * (kBwdCG * kBwdWarps) + (k % kBwdCG) * kBwdWarps
+                                    : (tile_off[t] + k) * kBwdWarps;
+      uint8_t *rp = rec + (ri + hh * 8 + pw) * kRecBytes;
       ((uint32_t *)rp)[lane] = dd;
       ((float4 *)(rp + 128))[lane] = make_float4(v4[0], v4[1], v4[2], v4[3]);
     }
