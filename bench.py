@@ -217,6 +217,15 @@ def side_bytes(w):
     return b
 
 
+def kernel_label(w, poly):
+    """The kernels of one loss+grad pass, by the layout poly_init chose."""
+    if "A" in w:
+        return "k_dense_loss_grad"
+    lay = poly.describe().get("csr_layout", 1)
+    return {3: "k_strip_forward+k_strip_link+k_tile_backward", 2: "k_dsell_forward+k_dsell_backward",
+            1: "k_sell16_forward+k_sell16_backward"}.get(lay, "k_sell_forward+k_csc_backward")
+
+
 def read_traffic(name):
     tpath = os.path.join(ROOT, "profiles", f"traffic_{name}.json")
     try:
@@ -294,7 +303,7 @@ def run_ours(args):
             "frac": (achieved / peak) if achieved else None, "traffic": read_traffic(args.config),
             "peak_source": peak_src,
             "nominal_peak": NOMINAL_HBM, "frac_nominal": (achieved / NOMINAL_HBM) if achieved else None,
-            "kernel": "k_dense_loss_grad" if "A" in w else "k_sell16_forward+k_sell16_backward",
+            "kernel": kernel_label(w, poly),
             "kernel_ms": kt[0], "finalize_ms": kt[1], "allreduce_ms": kt[2],
             "bytes_per_launch": per_launch,
             "timing": "CUDA events around every kernel of K iterations launched one by one on the solve's "

@@ -501,7 +501,10 @@ __global__ void k_tf_keys(const int32_t *rows, const int32_t *col, int64_t nnz, 
     const uint32_t r = (uint32_t)rows[e];
     key[e] = ((uint64_t)s << (m.rb + m.lb)) | ((uint64_t)r << m.lb) | (uint64_t)loc;
     perm[e] = (int32_t)e;
-    atomicAdd(seglen + (int64_t)s * n + r, 1);
+    // one atomic per (warp, segment): a row's entries are adjacent in the CSR
+    const int64_t sg = (int64_t)s * n + r;
+    const unsigned peers = __match_any_sync(__activemask(), sg);
+    if ((__ffs(peers) - 1) == (int)(threadIdx.x & 31)) atomicAdd(seglen + sg, __popc(peers));
   }
 }
 
@@ -607,7 +610,12 @@ __global__ void k_tb_pairs(const uint64_t *ks, int64_t nnz, TiledGeom m, int32_t
   for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < nnz; k += (int64_t)gridDim.x * blockDim.x) {
     const bool f = k == 0 || (ks[k - 1] >> 8) != (ks[k] >> 8);
     flag[k] = f ? 1 : 0;
-    if (f) atomicAdd(tcnt + (int64_t)(ks[k] >> (m.rb + 8)), 1);
+    // one atomic per (warp, tile): sorted neighbours share the tile
+    const int64_t t = (int64_t)(ks[k] >> (m.rb + 8));
+    const unsigned act = __activemask();
+    const unsigned peers = __match_any_sync(act, f ? t : (int64_t)-1);
+    const int c = __popc(peers & __ballot_sync(act, f));
+    if (f && (__ffs(peers & __ballot_sync(act, f)) - 1) == (int)(threadIdx.x & 31)) atomicAdd(tcnt + t, c);
   }
 }
 
