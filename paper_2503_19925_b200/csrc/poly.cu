@@ -483,7 +483,7 @@ int enqueue_pass(poly_handle *h, const double *x, bool loss) {
 #ifdef POLY_DEV_SKIP
     if (sb) return POLY_OK;
 #endif
-    return launch(h, (const void *)&k_tile_backward, dim3(h->tb_grid), dim3((kBwdWarps + 1) * 32), h->tb_smem, true,
+    return launch(h, (const void *)&k_tile_backward, dim3(h->tb_grid), dim3((2 * h->tbwd.npw + 1) * 32), h->tb_smem, true,
                   h->tbwd, (const float *)h->rbuf, h->partials, (int32_t)p.d, h->epi, h->tb_lcap);
   }
   if (h->dsell) {
@@ -1470,8 +1470,23 @@ int build_tiled(poly_handle *h) {
   }
   if (m.NS > kMaxStrips || (int64_t)m.rows_img * m.P > 65535) return POLY_EUNSUPPORTED;
   m.NS = (m.cols_img + m.W - 1) / m.W;
-  if (m.rows_img > 1) m.TW = 32, m.TH = 8;
-  else m.TW = kTileSlots, m.TH = 1;
+  if (m.rows_img > 1) {
+    // 32 x TH tiles, TH in 4..8 chosen so that the busiest SM (two backward
+    // CTAs each) holds the fewest pixel rows: C4 (256 rows) takes TH = 7,
+    // 296 tiles = 2 per SM, instead of 256 tiles of 8 rows (two on 108 SMs,
+    // one on 40)
+    m.TW = 32;
+    int64_t best = INT64_MAX;
+    for (int th = 8; th >= 4; --th) {
+      const int64_t nt = (int64_t)((m.rows_img + th - 1) / th) * ((m.cols_img + 31) / 32);
+      const int64_t cost = (nt + 2 * h->sms - 1) / (2 * h->sms) * th;
+      if (cost < best) best = cost, m.TH = th;
+    }
+    if (getenv("POLY_TILE_TH")) m.TH = std::max(1, std::min(8, atoi(getenv("POLY_TILE_TH"))));
+  } else {
+    m.TW = kTileSlots, m.TH = 1;
+  }
+  const int32_t npw = m.TW * m.TH / 32;
   m.tiles_x = (m.cols_img + m.TW - 1) / m.TW;
   const int64_t ntiles = (int64_t)((m.rows_img + m.TH - 1) / m.TH) * m.tiles_x;
   if (ntiles >= ((int64_t)1 << 23)) return POLY_EUNSUPPORTED;
@@ -1643,7 +1658,7 @@ int build_tiled(poly_handle *h) {
   int32_t lmax = 0;
   for (int32_t v : htc) lmax = std::max(lmax, v);
   const int32_t lcap = (std::max(1, lmax) + 3) & ~3;
-  const size_t bwd_smem = (size_t)kBwdStages * kBwdStageBytes + (size_t)lcap * 4 + 2 * kBwdStages * 8;
+  const size_t bwd_smem = (size_t)kBwdStages * kBwdCG * 2 * npw * kRecBytes + (size_t)lcap * 4 + 2 * kBwdStages * 8;
   const size_t fwd_smem = (((size_t)m.rows_img * m.P * 4 + 127) & ~(size_t)127) + (size_t)kFwdStages * kFwdStageBytes +
                           2 * kFwdStages * 8 + kFwdStages * 16;
   if (bwd_smem + 2048 > 227 * 1024 || fwd_smem > 227 * 1024) {
@@ -1688,12 +1703,12 @@ int build_tiled(poly_handle *h) {
   // stage-interleaved tiles ([stage][tile]) unless the tiles' lengths differ by more than 1/8
   const int32_t inter = getenv("POLY_BWD_TILE_MAJOR") ? 0 : (tmax * ntiles <= brows + brows / 8 ? 1 : 0);
   uint8_t *brec = nullptr;
-  const size_t bbytes = (size_t)std::max<int64_t>(1, inter ? tmax * ntiles : brows) * kBwdWarps * kRecBytes;
+  const size_t bbytes = (size_t)std::max<int64_t>(1, inter ? tmax * ntiles : brows) * 2 * npw * kRecBytes;
   if ((rc = palloc(bbytes, (void **)&brec))) return done(rc);
   cudaMemsetAsync(brec, 0, bbytes, st);  // the shorter halves' padding records
   k_tb_pack<<<(int)std::min<int64_t>(65535, (nwarps + 7) / 8), 256, 0, st>>>(
       ks, perm_in, (const float *)p.val, scnt, sstart, wlen, toff, nwarps, m, (int32_t)d, brec, bbase, tcol, ovf,
-      inter);
+      inter, npw);
   mark("bwd slots/scan/pack");
   int32_t hov = 0;
   cudaMemcpyAsync(&hov, ovf, 4, cudaMemcpyDeviceToHost, st);
@@ -1714,11 +1729,11 @@ int build_tiled(poly_handle *h) {
     return done(POLY_EUNSUPPORTED);
   }
   h->tfwd = StripFwd{frec, fhdr, uoff, d_ustart, d_ctr, pz, n, m.NS, m.rows_img, m.cols_img, m.W, m.P};
-  h->tbwd = TileBwd{brec, toff, bbase, list, loff, tcol, (int32_t)ntiles, inter};
+  h->tbwd = TileBwd{brec, toff, bbase, list, loff, tcol, (int32_t)ntiles, npw, inter};
   h->tf_grid = (int)std::max<int64_t>(m.NS, (int64_t)h->sms / m.NS * m.NS);
   h->tb_grid = (int)ntiles;
   h->tf_groups = frows * kFwdWarps;
-  h->tb_groups = brows * kBwdWarps;
+  h->tb_groups = brows * 2 * npw;
   // the fused step epilogue needs every warp's 32 columns to be one k_finalize block
   h->tile_epi = m.rows_img == 1 || m.cols_img % 32 == 0;
   // link blocks = loss partials (allocated for nrslices >= this grid)

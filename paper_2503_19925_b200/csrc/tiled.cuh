@@ -102,20 +102,21 @@ struct StripFwd {
 
 struct TileBwd {
   const uint8_t *rec;        // tile t's group-row k of warp w (= half * 8 + pixel row): record
-                             // ((tile_off[t] + k) * kBwdWarps + w); zero records pad the shorter halves
+                             // ((tile_off[t] + k) * 2 * npw + w); zero records pad the shorter halves
   const int64_t *tile_off;   // [ntiles + 1] first group-row of each tile
   const uint16_t *base;      // [ntiles * 256][2] list position before each half's first entry
   const int32_t *list;       // concatenated ray lists (rows ascending), each starting at a multiple of 4
   const int64_t *list_off;   // [ntiles + 1]
   const int32_t *tcol;       // [ntiles * 256] column of each slot, -1: none
   int32_t ntiles;
+  int32_t npw;               // pixel warps per tile (TW * TH / 32); 2 * npw consumer warps
   int32_t interleave;        // 1: stage k of every tile stored together ([k][tile]: the CTAs' bulk
                              // copies walk one contiguous region), 0: tile-major
 };
 
 // byte offset of stage k of tile t (first group-row G0 in the tile-major form)
 __device__ __forceinline__ int64_t bwd_stage_off(const TileBwd &t, int tile, int64_t G0, int64_t k) {
-  return (t.interleave ? k * t.ntiles + tile : G0 / kBwdCG + k) * (int64_t)kBwdStageBytes;
+  return (t.interleave ? k * t.ntiles + tile : G0 / kBwdCG + k) * ((int64_t)kBwdCG * 2 * t.npw * kRecBytes);
 }
 
 // L2 prefetch of a contiguous range through the TMA engine (no shared memory):
@@ -377,8 +378,10 @@ __global__ void __launch_bounds__((kBwdWarps + 1) * 32, 1)
                     const StepEpi e, int32_t lcap) {
   extern __shared__ __align__(128) uint8_t smem[];
   __shared__ double part[8 * 32];
+  const int ncw = 2 * t.npw;                       // consumer warps
+  const int sbytes = kBwdCG * ncw * kRecBytes;     // one stage
   uint8_t *stg = smem;
-  float *sr = (float *)(smem + kBwdStages * kBwdStageBytes);
+  float *sr = (float *)(smem + kBwdStages * sbytes);
   int32_t *sl = (int32_t *)sr;
   uint64_t *full = (uint64_t *)(sr + lcap);
   uint64_t *empty = full + kBwdStages;
@@ -388,43 +391,43 @@ __global__ void __launch_bounds__((kBwdWarps + 1) * 32, 1)
   if (tid == 0) {
     for (int s = 0; s < kBwdStages; ++s) {
       mbar_init(full + s, 1);
-      mbar_init(empty + s, kBwdWarps);
+      mbar_init(empty + s, ncw);
     }
     fence_mbar_init();
   }
   __syncthreads();
-  if (warp == kBwdWarps) {
+  if (warp == ncw) {
     // producer: the tile's records are static — streaming starts before the wait
     if (lane == 0) {
       const uint64_t pol = l2_evict_first_policy();
       const int64_t ns = ng / kBwdCG;
       if (POLY_BWD_PF > kBwdStages && ns > kBwdStages)
         for (int64_t q = kBwdStages; q < min(ns, (int64_t)POLY_BWD_PF); ++q)
-          bulk_prefetch_l2(t.rec + bwd_stage_off(t, tile, G0, q), kBwdStageBytes);
+          bulk_prefetch_l2(t.rec + bwd_stage_off(t, tile, G0, q), sbytes);
       int st = 0;
       uint32_t eph = 0;
       for (int64_t k = 0; k < ns; ++k, st = st + 1 == kBwdStages ? 0 : st + 1, eph ^= st == 0 ? 1u : 0u) {
         if (POLY_BWD_PF > kBwdStages && k + POLY_BWD_PF < ns)
-          bulk_prefetch_l2(t.rec + bwd_stage_off(t, tile, G0, k + POLY_BWD_PF), kBwdStageBytes);
+          bulk_prefetch_l2(t.rec + bwd_stage_off(t, tile, G0, k + POLY_BWD_PF), sbytes);
         if (k >= kBwdStages) mbar_wait(empty + st, eph ^ 1);
-        mbar_arrive_expect_tx(full + st, kBwdStageBytes);
-        bulk_g2s(stg + st * kBwdStageBytes, t.rec + bwd_stage_off(t, tile, G0, k), kBwdStageBytes, full + st, pol);
+        mbar_arrive_expect_tx(full + st, sbytes);
+        bulk_g2s(stg + st * sbytes, t.rec + bwd_stage_off(t, tile, G0, k), sbytes, full + st, pol);
       }
     }
     return;
   }
-  const int pw = warp & 7, h = warp >> 3;
+  const int pw = warp % t.npw, h = warp / t.npw;
   const int64_t L0 = t.list_off[tile];
   const int L = (int)(t.list_off[tile + 1] - L0);
-  for (int i = 4 * tid; i < L; i += 4 * kBwdWarps * 32) cp_async16(sl + i, t.list + L0 + i);  // static
+  for (int i = 4 * tid; i < L; i += 4 * ncw * 32) cp_async16(sl + i, t.list + L0 + i);  // static
   const int slot = tile * kTileSlots + pw * 32 + lane;
   int idx = (int)t.base[(int64_t)slot * 2 + h];
   cp_async_wait_all();
-  named_bar(1, kBwdWarps * 32);
+  named_bar(1, ncw * 32);
   pdl_wait();  // r is written by the link kernel
-  for (int i = tid; i < L; i += kBwdWarps * 32) cp_async4(sr + i, r + sl[i]);  // in place, own slots only
+  for (int i = tid; i < L; i += ncw * 32) cp_async4(sr + i, r + sl[i]);  // in place, own slots only
   cp_async_wait_all();
-  named_bar(1, kBwdWarps * 32);
+  named_bar(1, ncw * 32);
   double a0 = 0.0, a1 = 0.0;
   const int nst = (int)(ng / kBwdCG);
   int st = 0;
@@ -433,13 +436,13 @@ __global__ void __launch_bounds__((kBwdWarps + 1) * 32, 1)
     mbar_wait(full + st, ph);
 #pragma unroll
     for (int q = 0; q < kBwdCG; ++q)
-      rec_group(stg + st * kBwdStageBytes + (q * kBwdWarps + warp) * kRecBytes, lane, idx, sr, (q & 1) ? a1 : a0);
+      rec_group(stg + st * sbytes + (q * ncw + warp) * kRecBytes, lane, idx, sr, (q & 1) ? a1 : a0);
     __syncwarp();
     if (lane == 0) mbar_arrive(empty + st);
   }
   const double v = a0 + a1;
   if (h > 0) part[pw * 32 + lane] = v;
-  named_bar(1, kBwdWarps * 32);
+  named_bar(1, ncw * 32);
   if (h > 0) {
     pdl_trigger();
     return;
@@ -670,7 +673,7 @@ __global__ void k_tb_tilelen(const int64_t *wlen, int64_t ntiles, int64_t *tlen)
 __global__ void k_tb_pack(const uint64_t *ks2, const int32_t *perm2, const float *val, const int32_t *cnt,
                           const int64_t *start, const int64_t *wlen, const int64_t *tile_off, int64_t nwarps,
                           TiledGeom m, int32_t d, uint8_t *rec, uint16_t *base, int32_t *tcol, int32_t *overflow,
-                          int32_t interleave) {
+                          int32_t interleave, int32_t npw) {
   const int lane = threadIdx.x & 31;
   const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
   for (int64_t w = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); w < nwarps; w += nw) {
@@ -708,9 +711,10 @@ __global__ void k_tb_pack(const uint64_t *ks2, const int32_t *perm2, const float
         }
       }
       const int64_t ntl = nwarps / 8;
-      const int64_t ri = interleave ? ((k / kBwdCG) * ntl + t) * (kBwdCG * kBwdWarps) + (k % kBwdCG) * kBwdWarps
-                                    : (tile_off[t] + k) * kBwdWarps;
-      uint8_t *rp = rec + (ri + hh * 8 + pw) * kRecBytes;
+      const int64_t ncw = 2 * npw;
+      const int64_t ri = interleave ? ((k / kBwdCG) * ntl + t) * (kBwdCG * ncw) + (k % kBwdCG) * ncw
+                                    : (tile_off[t] + k) * ncw;
+      uint8_t *rp = rec + (ri + hh * npw + pw) * kRecBytes;
       ((uint32_t *)rp)[lane] = dd;
       ((float4 *)(rp + 128))[lane] = make_float4(v4[0], v4[1], v4[2], v4[3]);
     }
