@@ -467,22 +467,10 @@ int enqueue_pass(poly_handle *h, const double *x, bool loss) {
   a.loss_partials = h->loss_partials;
   a.mu_step = h->mu_step;
   if (h->tiled) {
-#ifdef POLY_DEV_SKIP
-    // (dev timing builds only: leave one kernel out of the pass; results are wrong)
-    static const char *skip = getenv("POLY_DEV_SKIP");
-    const bool sf = skip && strchr(skip, 'f'), sl = skip && strchr(skip, 'l'), sb = skip && strchr(skip, 'b');
-    if (!sf)
-#endif
     TRY(launch(h, (const void *)&k_strip_forward, dim3(h->tf_grid), dim3((kFwdWarps + 1) * 32), h->tf_smem, true,
                h->tfwd, x32));
-#ifdef POLY_DEV_SKIP
-    if (!sl)
-#endif
     TRY(launch(h, loss ? (const void *)&k_strip_link<true> : (const void *)&k_strip_link<false>, dim3(h->k4_grid),
                dim3(256), 0, true, a, (const double *)h->tfwd.pz, h->tfwd.NS, h->tfwd.ctr));
-#ifdef POLY_DEV_SKIP
-    if (sb) return POLY_OK;
-#endif
     return launch(h, (const void *)&k_tile_backward, dim3(h->tb_grid), dim3((2 * h->tbwd.npw + 1) * 32), h->tb_smem, true,
                   h->tbwd, (const float *)h->rbuf, h->partials, (int32_t)p.d, h->epi, h->tb_lcap);
   }
