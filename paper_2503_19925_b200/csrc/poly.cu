@@ -48,6 +48,7 @@
 #include "nvls.cuh"
 #include "dsell.cuh"
 #include "tiled.cuh"
+#include "pass.cuh"
 
 using namespace poly;
 
@@ -277,6 +278,10 @@ struct poly_handle {
   size_t tf_smem = 0, tb_smem = 0;
   bool tile_epi = false;               // every warp of K4tb covers one k_finalize block
   int32_t tb_lcap = 0;                 // K4tb ray-list capacity (floats, multiple of 4)
+  int persist = 0;                     // K4p (pass.cuh): 1 link + backward persistent, 2 the whole pass
+  PassSync psync{};
+  int pass_grid = 0;
+  size_t pass_smem = 0;
   double mu_step = 0.0;                // != 0: μ is an arithmetic progression (geometric bins in K4tl)
   int64_t tf_groups = 0, tb_groups = 0;
   StepEpi epi{};                        // K4b's step epilogue for the next pass (on = 0: write g)
@@ -466,6 +471,19 @@ int enqueue_pass(poly_handle *h, const double *x, bool loss) {
   a.mode = p.mode;
   a.loss_partials = h->loss_partials;
   a.mu_step = h->mu_step;
+  if (h->tiled && h->persist) {
+    PassSync ps = h->psync;
+    ps.err = &h->state->comm_err;
+    if (h->persist == 2)
+      return launch(h, loss ? (const void *)&k_ct_pass<true> : (const void *)&k_ct_pass<false>, dim3(h->pass_grid),
+                    dim3(kPassWarps * 32), h->pass_smem, true, h->tfwd, h->tbwd, a, x32, h->partials, (int32_t)p.d,
+                    h->epi, ps);
+    TRY(launch(h, (const void *)&k_strip_forward, dim3(h->tf_grid), dim3((kFwdWarps + 1) * 32), h->tf_smem, true,
+               h->tfwd, x32));
+    return launch(h, loss ? (const void *)&k_ct_linkbwd<true> : (const void *)&k_ct_linkbwd<false>,
+                  dim3(h->pass_grid), dim3(kPassWarps * 32), h->pass_smem, true, h->tfwd, h->tbwd, a, h->partials,
+                  (int32_t)p.d, h->epi, ps);
+  }
   if (h->tiled) {
     TRY(launch(h, (const void *)&k_strip_forward, dim3(h->tf_grid), dim3((kFwdWarps + 1) * 32), h->tf_smem, true,
                h->tfwd, x32));
@@ -1728,6 +1746,55 @@ int build_tiled(poly_handle *h) {
   // row per thread (two CTAs per SM, each thread looping over rows, measured
   // slower: 127.9 vs 117.9 us per C4 step)
   h->k4_grid = (int)std::min<int64_t>((n + 255) / 256, (int64_t)h->sms * 8);
+  // K4p (pass.cuh, opt-in): the link and the backward as one persistent
+  // kernel after the strip forward (POLY_PERSIST=linkbwd), or the whole pass
+  // as one (POLY_PERSIST=full); one CTA per SM, grid barrier(s).  Measured
+  // slower than the three kernels at C4 (68.1 / 71.7 vs 62.9 us per pass: the
+  // link on 15 warps per SM and the grid barriers cost more than the kernel
+  // boundaries they remove)
+  const char *pm = getenv("POLY_PERSIST");
+  if (2 * npw <= 14 && pm && (!strcmp(pm, "full") || !strcmp(pm, "linkbwd"))) {
+    const int mode = !strcmp(pm, "full") ? 2 : 1;
+    const int sb = kBwdCG * 2 * npw * kRecBytes;
+    const size_t lists = ((size_t)2 * lcap * 4 + 127) & ~(size_t)127;
+    const size_t bars = (size_t)(2 * kPassFwdStages + 2 * kPassMaxBwdStages) * 8 + kPassFwdStages * 16;
+    size_t abytes, psm;
+    int nstb;
+    if (mode == 2) {
+      const size_t ringB = (size_t)kPassFwdStages * kFwdStageBytes;
+      abytes = std::max<size_t>(((size_t)m.rows_img * m.P * 4 + 127) & ~(size_t)127, lists);
+      psm = abytes + ringB + bars;
+      nstb = (int)std::min<size_t>(kPassMaxBwdStages, ringB / sb);
+    } else {
+      abytes = lists;
+      nstb = (int)std::min<size_t>(kPassMaxBwdStages, (212 * 1024 - lists - bars) / sb);
+      psm = abytes + (size_t)nstb * sb + bars;
+    }
+    const void *f0 = mode == 2 ? (const void *)&k_ct_pass<false> : (const void *)&k_ct_linkbwd<false>;
+    const void *f1 = mode == 2 ? (const void *)&k_ct_pass<true> : (const void *)&k_ct_linkbwd<true>;
+    int occ = 0;
+    uint32_t *gbar = nullptr;
+    bool ok = psm <= 220 * 1024 && nstb >= 2;
+    if (ok)
+      ok = cudaFuncSetAttribute(f0, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)psm) == cudaSuccess &&
+           cudaFuncSetAttribute(f1, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)psm) == cudaSuccess &&
+           cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, f0, kPassWarps * 32, psm) == cudaSuccess && occ >= 1;
+    cudaGetLastError();
+    if (ok && (rc = palloc(8, (void **)&gbar)) == POLY_OK) {
+      cudaMemsetAsync(gbar, 0, 8, st);
+      h->persist = mode;
+      h->pass_grid = h->sms;  // one CTA per SM: every CTA resident for the grid barriers
+      h->pass_smem = psm;
+      h->psync = PassSync{gbar, nullptr, nstb, (int32_t)abytes, lcap};
+      if (h->pass_grid > h->nrslices) {
+        double *lp = nullptr;
+        if ((rc = dev_alloc(h, &lp, (size_t)h->pass_grid))) return done(rc);
+        dev_release(h, h->loss_partials);
+        h->loss_partials = lp;
+      }
+      h->k4_grid = h->pass_grid;  // loss partials: one per CTA
+    }
+  }
   h->tiled = true;
   h->tr_side = 0;  // the forward stages x itself: no transposed copy
   h->tr_slices = 0;
@@ -2657,6 +2724,7 @@ int poly_solve_ex(poly_handle *h, const poly_solve_opts *o, double *x, double *x
   TRY(sync_out(h));
   CK(cudaGetLastError());
   const int per = method == POLY_METHOD_EXTRAGRADIENT ? 2 : 1;
+  if (fin.comm_err == 2) return fail(POLY_ECUDA, "K4p: grid barrier timed out (CTAs not co-resident)");
   if (fin.comm_err) {
     if (h->nccl) nccl_api()->commAbort(h->nccl);
     h->nccl = nullptr;
@@ -2775,6 +2843,7 @@ int poly_solve(poly_handle *h, double *x, int T, double gamma, uint32_t flags, d
   if (h->prof) collect_profile(h);
   TRY(sync_out(h));
   CK(cudaGetLastError());
+  if (h->hstate->comm_err == 2) return fail(POLY_ECUDA, "K4p: grid barrier timed out (CTAs not co-resident)");
   if (h->hstate->comm_err) {
     if (h->nccl) nccl_api()->commAbort(h->nccl);
     h->nccl = nullptr;
