@@ -41,6 +41,27 @@ struct SolveState {
   double move;
 };
 
+// K4t strip copies of the fp32 iterate (tiled.cuh): strip s of W image
+// columns stored as rows x P floats (the forward's shared-memory layout,
+// padding columns zero) at x32[off + s * SP], so the forward stages a strip
+// with one bulk copy.  W == 0: none.
+struct X32Strip {
+  int32_t W, P, rows, cols, SP;
+  int64_t off;
+};
+
+// the fp32 copies of x_k: row-major, the transposed image at [d, 2d)
+// (tr_side > 0), the strip copies (xs.W > 0)
+__device__ __forceinline__ void x32_store(float *o, int64_t d, int32_t tr_side, const X32Strip &xs, int64_t k,
+                                          float v) {
+  o[k] = v;
+  if (tr_side) o[d + (k % tr_side) * tr_side + k / tr_side] = v;
+  if (xs.W) {
+    const int64_t r = k / xs.cols, c = k - r * xs.cols, s = c / xs.W;
+    o[xs.off + s * xs.SP + r * xs.P + (c - s * xs.W)] = v;
+  }
+}
+
 struct FinArgs {
   int32_t mode;
   int32_t d;
@@ -58,6 +79,7 @@ struct FinArgs {
   double *x_out;             // [d] (may alias anchor)
   float *x32_out;            // optional [d]: fp32 copy of x_out (gathered by the CSR pass)
   int32_t tr_side;           // > 0: x32_out is [2d] and x32_out[d + tr(k)] holds the transposed copy
+  X32Strip xs;               // K4t strip copies in x32_out (xs.W > 0)
   double *v_scratch;         // [d]
   double *block_norm;        // [gridDim.x]
   const double *center;      // [d] or null
@@ -189,10 +211,7 @@ __global__ void __launch_bounds__(256) k_finalize(const FinArgs a) {
       xo = v * scale;
     }
     a.x_out[k] = xo;
-    if (a.x32_out) {
-      a.x32_out[k] = (float)xo;
-      if (a.tr_side) a.x32_out[a.d + (k % a.tr_side) * a.tr_side + k / a.tr_side] = (float)xo;
-    }
+    if (a.x32_out) x32_store(a.x32_out, a.d, a.tr_side, a.xs, k, (float)xo);
   }
   if (tid == 0) {
     SolveState *s = a.state;
@@ -212,13 +231,12 @@ __global__ void __launch_bounds__(256) k_finalize(const FinArgs a) {
 // ||v - c||² from the block partials of k_finalize in the same fixed order
 // (identical bits in every block), then scales its slice of v into x_out.
 // Replaces the single-block tail, which serialised d/256 dependent loads.
-__global__ void k_to_f32(const double *x, int64_t d, int32_t tr_side, float *out) {
+__global__ void k_to_f32(const double *x, int64_t d, int32_t tr_side, const X32Strip xs, float *out) {
   pdl_wait();
   pdl_trigger();
   for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < d;
        k += (int64_t)gridDim.x * blockDim.x) {
-    out[k] = (float)x[k];
-    if (tr_side) out[d + (k % tr_side) * tr_side + k / tr_side] = (float)x[k];
+    x32_store(out, d, tr_side, xs, k, (float)x[k]);
   }
 }
 
@@ -249,10 +267,7 @@ __global__ void __launch_bounds__(256) k_fin_apply(const FinArgs a) {
       xo = v * scale;
     }
     a.x_out[k] = xo;
-    if (a.x32_out) {
-      a.x32_out[k] = (float)xo;
-      if (a.tr_side) a.x32_out[a.d + (k % a.tr_side) * a.tr_side + k / a.tr_side] = (float)xo;
-    }
+    if (a.x32_out) x32_store(a.x32_out, a.d, a.tr_side, a.xs, k, (float)xo);
   }
   if (blockIdx.x == 0 && tid == 0) {
     SolveState *s = a.state;

@@ -258,6 +258,7 @@ struct poly_handle {
   float *rbuf = nullptr;               // [n_local] residuals between K4f and K4b
   float *xa32 = nullptr, *xh32 = nullptr, *xin32 = nullptr;  // CSR: fp32 copies of xa, xh, a caller's x
   int tr_side = 0;                     // CSR, d = s²: fp32 copies also hold x transposed at [d, 2d)
+  X32Strip xs{};                       // K4t: fp32 copies also hold the forward's strips
   int64_t tr_slices = 0;               // K4f slices that gather from the transposed copy
   bool sell16 = false;                 // both SELL copies in the 6-byte delta form
   bool dsell = false;                  // fp32: both copies in the dictionary-staged 5-byte form (dsell.cuh)
@@ -435,7 +436,7 @@ int enqueue_pass(poly_handle *h, const double *x, bool loss) {
     const float *x32 = x == h->xa ? h->xa32 : (x == h->xh ? h->xh32 : nullptr);
     if (!x32) {
       TRY(launch(h, (const void *)&k_to_f32, dim3((unsigned)std::min<int64_t>(1024, (p.d + 255) / 256)),
-                 dim3(256), 0, true, x, (int64_t)p.d, (int32_t)h->tr_side, h->xin32));
+                 dim3(256), 0, true, x, (int64_t)p.d, (int32_t)h->tr_side, h->xs, h->xin32));
       x32 = h->xin32;
     }
     CsrFwdArgs a{};
@@ -462,7 +463,7 @@ int enqueue_pass(poly_handle *h, const double *x, bool loss) {
   const float *x32 = x == h->xa ? h->xa32 : (x == h->xh ? h->xh32 : nullptr);
   if (!x32) {
     TRY(launch(h, (const void *)&k_to_f32, dim3((unsigned)std::min<int64_t>(1024, (p.d + 255) / 256)),
-               dim3(256), 0, true, x, (int64_t)p.d, (int32_t)h->tr_side, h->xin32));
+               dim3(256), 0, true, x, (int64_t)p.d, (int32_t)h->tr_side, h->xs, h->xin32));
     x32 = h->xin32;
   }
   a.x = x32;
@@ -542,6 +543,7 @@ FinArgs fin_base(poly_handle *h, int mode) {
   f.center = h->center;
   f.R = h->p.R;
   f.state = h->state;
+  f.xs = h->xs;
   return f;
 }
 
@@ -1665,8 +1667,8 @@ int build_tiled(poly_handle *h) {
   for (int32_t v : htc) lmax = std::max(lmax, v);
   const int32_t lcap = (std::max(1, lmax) + 3) & ~3;
   const size_t bwd_smem = (size_t)kBwdStages * kBwdCG * 2 * npw * kRecBytes + (size_t)lcap * 4 + 2 * kBwdStages * 8;
-  const size_t fwd_smem = (((size_t)m.rows_img * m.P * 4 + 127) & ~(size_t)127) + (size_t)kFwdStages * kFwdStageBytes +
-                          2 * kFwdStages * 8 + kFwdStages * 16;
+  const size_t fwd_smem = (((((size_t)m.rows_img * m.P + 3) & ~(size_t)3) * 4 + 127) & ~(size_t)127) +
+                          (size_t)kFwdStages * kFwdStageBytes + 2 * kFwdStages * 8 + kFwdStages * 16 + 8;
   if (bwd_smem + 2048 > 227 * 1024 || fwd_smem > 227 * 1024) {
     if (btime) fprintf(stderr, "[tiled build] unsupported: smem fwd %zu bwd %zu\n", fwd_smem, bwd_smem);
     return done(POLY_EUNSUPPORTED);
@@ -1794,6 +1796,27 @@ int build_tiled(poly_handle *h) {
       }
       h->k4_grid = h->pass_grid;  // loss partials: one per CTA
     }
+  }
+  {
+    // the fp32 iterate copies also hold the strips in the forward's layout
+    // (one bulk copy per CTA instead of per-element staging); padding zero
+    const int64_t SP = ((int64_t)m.rows_img * m.P + 3) & ~(int64_t)3, off = (d + 3) & ~(int64_t)3;
+    const size_t n32 = (size_t)(off + (int64_t)m.NS * SP);
+    float *b32[3] = {nullptr, nullptr, nullptr};
+    for (int q = 0; q < 3; ++q) {
+      if ((rc = dev_alloc(h, &b32[q], n32))) {
+        for (int u = 0; u < q; ++u) dev_release(h, b32[u]);
+        return done(rc);
+      }
+      cudaMemsetAsync(b32[q], 0, n32 * 4, st);
+    }
+    dev_release(h, h->xa32);
+    dev_release(h, h->xh32);
+    dev_release(h, h->xin32);
+    h->xa32 = b32[0], h->xh32 = b32[1], h->xin32 = b32[2];
+    h->xs = X32Strip{m.W, m.P, m.rows_img, m.cols_img, (int32_t)SP, off};
+    h->tfwd.xs_off = off;
+    h->tfwd.SP = (int32_t)SP;
   }
   h->tiled = true;
   h->tr_side = 0;  // the forward stages x itself: no transposed copy

@@ -98,6 +98,8 @@ struct StripFwd {
   double *pz;                // [NS][n] partial z (rows a strip does not touch stay 0)
   int64_t n;
   int32_t NS, rows_img, cols_img, W, P;
+  int64_t xs_off;            // the fp32 iterate's strip copies: strip s at x[xs_off + s * SP] (finalize.cuh X32Strip)
+  int32_t SP;                // floats per strip copy (rows_img * P rounded up to 4)
 };
 
 struct TileBwd {
@@ -240,11 +242,11 @@ __global__ void __launch_bounds__((kFwdWarps + 1) * 32, 1) k_strip_forward(const
                                                                            const float *__restrict__ x) {
   extern __shared__ __align__(128) uint8_t smem[];
   float *sx = (float *)smem;
-  const int nst = f.rows_img * f.P;
-  uint8_t *stg = smem + ((nst * 4 + 127) & ~127);
+  uint8_t *stg = smem + ((f.SP * 4 + 127) & ~127);
   uint64_t *full = (uint64_t *)(stg + kFwdStages * kFwdStageBytes);
   uint64_t *empty = full + kFwdStages;
   int4 *desc = (int4 *)(empty + kFwdStages);
+  uint64_t *xbar = (uint64_t *)(desc + kFwdStages);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int strip = blockIdx.x % f.NS;
   const int u0 = f.unit_start[strip], nu = f.unit_start[strip + 1] - u0;
@@ -253,6 +255,7 @@ __global__ void __launch_bounds__((kFwdWarps + 1) * 32, 1) k_strip_forward(const
       mbar_init(full + s, 1);
       mbar_init(empty + s, kFwdWarps);
     }
+    mbar_init(xbar, 1);
     fence_mbar_init();
   }
   __syncthreads();
@@ -262,7 +265,11 @@ __global__ void __launch_bounds__((kFwdWarps + 1) * 32, 1) k_strip_forward(const
       const uint64_t pol = l2_evict_first_policy();
       // (starting the ring before the wait — records are static — measured
       // slower in the graph: 126 vs 118 us per C4 step)
-      pdl_wait();  // the counter is reset by the previous link kernel
+      pdl_wait();  // the counter is reset by the previous link kernel, x written by the step kernel
+      // the strip's iterate: one bulk copy of its strip-layout fp32 copy (the
+      // strip's other CTAs read the same bytes: kept in L2)
+      mbar_arrive_expect_tx(xbar, (uint32_t)f.SP * 4);
+      bulk_g2s(sx, x + f.xs_off + (int64_t)strip * f.SP, (uint32_t)f.SP * 4, xbar, l2_evict_last_policy());
       int it = 0, st = 0;
       uint32_t eph = 0;  // stage index and the ring's pass parity (incremental: no division)
       int u = atomicAdd(f.ctr + strip, 1);
@@ -303,20 +310,8 @@ __global__ void __launch_bounds__((kFwdWarps + 1) * 32, 1) k_strip_forward(const
     }
     return;
   }
-  // consumers: stage the strip (rows_img x P floats, columns >= ws zero)
-  const int c0 = strip * f.W;
-  const int ws = min(f.W, f.cols_img - c0);
-  pdl_wait();  // x is written by the previous step kernel
-  for (int r = warp; r < f.rows_img; r += kFwdWarps) {
-    const float *xr = x + (int64_t)r * f.cols_img + c0;
-    float *sr = sx + r * f.P;
-    for (int c = lane; c < f.P; c += 32) {
-      if (c < ws) cp_async4(sr + c, xr + c);
-      else sr[c] = 0.f;
-    }
-  }
-  cp_async_wait_all();
-  named_bar(1, kFwdWarps * 32);
+  // consumers: the strip (rows_img x P floats, columns >= W zero) arrives on xbar
+  mbar_wait(xbar, 0);
   pdl_trigger();
   int idx = 0, row = -1;
   double a0 = 0.0, a1 = 0.0;
