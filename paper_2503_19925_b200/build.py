@@ -22,7 +22,7 @@ COMMON = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC,-O2", "-shared"
 
 # lib -> (sources, headers, extra nvcc flags, link libs)
 TARGETS = {
-    "libpoly.so": (["poly.cu"], ["common.cuh", "dense.cuh", "finalize.cuh", "csr.cuh", "aux.cuh", "tv.cuh", "small.cuh", "ctproj.cuh", "p2p.cuh", "nvls.cuh", "dsell.cuh", "tiled.cuh", "pass.cuh"],
+    "libpoly.so": (["poly.cu"], ["common.cuh", "dense.cuh", "finalize.cuh", "csr.cuh", "aux.cuh", "tv.cuh", "small.cuh", "ctproj.cuh", "p2p.cuh", "nvls.cuh", "dsell.cuh", "tiled.cuh"],
                    [], ["-ldl"]),
     "libpolysynth.so": (["synth.cu"], [], ["-fmad=false"], []),
 }

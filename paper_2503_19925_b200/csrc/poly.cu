@@ -48,7 +48,6 @@
 #include "nvls.cuh"
 #include "dsell.cuh"
 #include "tiled.cuh"
-#include "pass.cuh"
 
 using namespace poly;
 
@@ -279,10 +278,6 @@ struct poly_handle {
   size_t tf_smem = 0, tb_smem = 0;
   bool tile_epi = false;               // every warp of K4tb covers one k_finalize block
   int32_t tb_lcap = 0;                 // K4tb ray-list capacity (floats, multiple of 4)
-  int persist = 0;                     // K4p (pass.cuh): 1 link + backward persistent, 2 the whole pass
-  PassSync psync{};
-  int pass_grid = 0;
-  size_t pass_smem = 0;
   double mu_step = 0.0;                // != 0: μ is an arithmetic progression (geometric bins in K4tl)
   int64_t tf_groups = 0, tb_groups = 0;
   StepEpi epi{};                        // K4b's step epilogue for the next pass (on = 0: write g)
@@ -472,19 +467,6 @@ int enqueue_pass(poly_handle *h, const double *x, bool loss) {
   a.mode = p.mode;
   a.loss_partials = h->loss_partials;
   a.mu_step = h->mu_step;
-  if (h->tiled && h->persist) {
-    PassSync ps = h->psync;
-    ps.err = &h->state->comm_err;
-    if (h->persist == 2)
-      return launch(h, loss ? (const void *)&k_ct_pass<true> : (const void *)&k_ct_pass<false>, dim3(h->pass_grid),
-                    dim3(kPassWarps * 32), h->pass_smem, true, h->tfwd, h->tbwd, a, x32, h->partials, (int32_t)p.d,
-                    h->epi, ps);
-    TRY(launch(h, (const void *)&k_strip_forward, dim3(h->tf_grid), dim3((kFwdWarps + 1) * 32), h->tf_smem, true,
-               h->tfwd, x32));
-    return launch(h, loss ? (const void *)&k_ct_linkbwd<true> : (const void *)&k_ct_linkbwd<false>,
-                  dim3(h->pass_grid), dim3(kPassWarps * 32), h->pass_smem, true, h->tfwd, h->tbwd, a, h->partials,
-                  (int32_t)p.d, h->epi, ps);
-  }
   if (h->tiled) {
     TRY(launch(h, (const void *)&k_strip_forward, dim3(h->tf_grid), dim3((kFwdWarps + 1) * 32), h->tf_smem, true,
                h->tfwd, x32));
@@ -1652,10 +1634,9 @@ int build_tiled(poly_handle *h) {
   void *ts4 = nullptr;
   if ((rc = talloc(std::max(tb4, tb5), &ts4))) return done(rc);
   cub::DeviceScan::InclusiveSum(ts4, tb4, flag, pidx, (int)nnz, st);
-  // pair starts per tile (unpadded) and list offsets (each list padded to a multiple of 4: 16-byte copies)
+  // first chunk of every tile: the chunk tables' offsets
   k_widen<<<(int)std::min<int64_t>(4096, (ntiles + 256) / 256), 256, 0, st>>>(tcnt, ntiles, tcnt64);
   cub::DeviceScan::ExclusiveSum(ts4, tb5, tcnt64, pstart, (int)ntiles + 1, st);
-  k_round4<<<(int)std::min<int64_t>(4096, (ntiles + 256) / 256), 256, 0, st>>>(tcnt64, ntiles);
   cub::DeviceScan::ExclusiveSum(ts4, tb5, tcnt64, loff, (int)ntiles + 1, st);
   int64_t nlist = 0;
   cudaMemcpyAsync(&nlist, loff + ntiles, 8, cudaMemcpyDeviceToHost, st);
@@ -1663,9 +1644,10 @@ int build_tiled(poly_handle *h) {
   cudaMemcpyAsync(htc.data(), tcnt, ntiles * 4, cudaMemcpyDeviceToHost, st);
   if (cudaStreamSynchronize(st) != cudaSuccess)
     return done(fail(POLY_ECUDA, "tiled build: %s", cudaGetErrorString(cudaGetLastError())));
-  int32_t lmax = 0;
+  int32_t lmax = 0;  // most r chunks of a tile
   for (int32_t v : htc) lmax = std::max(lmax, v);
-  const int32_t lcap = (std::max(1, lmax) + 3) & ~3;
+  lmax *= 4;         // floats
+  const int32_t lcap = std::max(4, lmax);
   const size_t bwd_smem = (size_t)kBwdStages * kBwdCG * 2 * npw * kRecBytes + (size_t)lcap * 4 + 2 * kBwdStages * 8;
   const size_t fwd_smem = (((((size_t)m.rows_img * m.P + 3) & ~(size_t)3) * 4 + 127) & ~(size_t)127) +
                           (size_t)kFwdStages * kFwdStageBytes + 2 * kFwdStages * 8 + kFwdStages * 16 + 8;
@@ -1748,55 +1730,6 @@ int build_tiled(poly_handle *h) {
   // row per thread (two CTAs per SM, each thread looping over rows, measured
   // slower: 127.9 vs 117.9 us per C4 step)
   h->k4_grid = (int)std::min<int64_t>((n + 255) / 256, (int64_t)h->sms * 8);
-  // K4p (pass.cuh, opt-in): the link and the backward as one persistent
-  // kernel after the strip forward (POLY_PERSIST=linkbwd), or the whole pass
-  // as one (POLY_PERSIST=full); one CTA per SM, grid barrier(s).  Measured
-  // slower than the three kernels at C4 (68.1 / 71.7 vs 62.9 us per pass: the
-  // link on 15 warps per SM and the grid barriers cost more than the kernel
-  // boundaries they remove)
-  const char *pm = getenv("POLY_PERSIST");
-  if (2 * npw <= 14 && pm && (!strcmp(pm, "full") || !strcmp(pm, "linkbwd"))) {
-    const int mode = !strcmp(pm, "full") ? 2 : 1;
-    const int sb = kBwdCG * 2 * npw * kRecBytes;
-    const size_t lists = ((size_t)2 * lcap * 4 + 127) & ~(size_t)127;
-    const size_t bars = (size_t)(2 * kPassFwdStages + 2 * kPassMaxBwdStages) * 8 + kPassFwdStages * 16;
-    size_t abytes, psm;
-    int nstb;
-    if (mode == 2) {
-      const size_t ringB = (size_t)kPassFwdStages * kFwdStageBytes;
-      abytes = std::max<size_t>(((size_t)m.rows_img * m.P * 4 + 127) & ~(size_t)127, lists);
-      psm = abytes + ringB + bars;
-      nstb = (int)std::min<size_t>(kPassMaxBwdStages, ringB / sb);
-    } else {
-      abytes = lists;
-      nstb = (int)std::min<size_t>(kPassMaxBwdStages, (212 * 1024 - lists - bars) / sb);
-      psm = abytes + (size_t)nstb * sb + bars;
-    }
-    const void *f0 = mode == 2 ? (const void *)&k_ct_pass<false> : (const void *)&k_ct_linkbwd<false>;
-    const void *f1 = mode == 2 ? (const void *)&k_ct_pass<true> : (const void *)&k_ct_linkbwd<true>;
-    int occ = 0;
-    uint32_t *gbar = nullptr;
-    bool ok = psm <= 220 * 1024 && nstb >= 2;
-    if (ok)
-      ok = cudaFuncSetAttribute(f0, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)psm) == cudaSuccess &&
-           cudaFuncSetAttribute(f1, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)psm) == cudaSuccess &&
-           cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, f0, kPassWarps * 32, psm) == cudaSuccess && occ >= 1;
-    cudaGetLastError();
-    if (ok && (rc = palloc(8, (void **)&gbar)) == POLY_OK) {
-      cudaMemsetAsync(gbar, 0, 8, st);
-      h->persist = mode;
-      h->pass_grid = h->sms;  // one CTA per SM: every CTA resident for the grid barriers
-      h->pass_smem = psm;
-      h->psync = PassSync{gbar, nullptr, nstb, (int32_t)abytes, lcap};
-      if (h->pass_grid > h->nrslices) {
-        double *lp = nullptr;
-        if ((rc = dev_alloc(h, &lp, (size_t)h->pass_grid))) return done(rc);
-        dev_release(h, h->loss_partials);
-        h->loss_partials = lp;
-      }
-      h->k4_grid = h->pass_grid;  // loss partials: one per CTA
-    }
-  }
   {
     // the fp32 iterate copies also hold the strips in the forward's layout
     // (one bulk copy per CTA instead of per-element staging); padding zero
@@ -2466,7 +2399,9 @@ int poly_init(const poly_problem *pin, poly_handle **out) {
       }
     }
     if ((rc = dev_alloc(h, &h->loss_partials, (size_t)h->k4_grid)) != POLY_OK) return bail(rc);
-    if ((rc = dev_alloc(h, &h->rbuf, (size_t)std::max<int64_t>(1, p.n_local))) != POLY_OK) return bail(rc);
+    // r padded to whole float4s: K4tb copies aligned 4-row chunks of it
+    if ((rc = dev_alloc(h, &h->rbuf, (size_t)((std::max<int64_t>(1, p.n_local) + 3) & ~(int64_t)3))) != POLY_OK)
+      return bail(rc);
     {  // a square d may be an image: the fp32 copies get room for x transposed
       const int64_t s = (int64_t)llround(std::sqrt((double)p.d));
       if (s * s == p.d && s > 1) h->tr_side = (int)s;
@@ -2475,7 +2410,7 @@ int poly_init(const poly_problem *pin, poly_handle **out) {
     if ((rc = dev_alloc(h, &h->xa32, n32)) != POLY_OK) return bail(rc);
     if ((rc = dev_alloc(h, &h->xh32, n32)) != POLY_OK) return bail(rc);
     if ((rc = dev_alloc(h, &h->xin32, n32)) != POLY_OK) return bail(rc);
-    if (cudaMemsetAsync(h->rbuf, 0, std::max<int64_t>(1, p.n_local) * 4, h->work) != cudaSuccess)
+    if (cudaMemsetAsync(h->rbuf, 0, ((std::max<int64_t>(1, p.n_local) + 3) & ~(int64_t)3) * 4, h->work) != cudaSuccess)
       return bail(fail(POLY_ECUDA, "memset failed"));
   }
   h->fin_grid = (int)((p.d + 31) / 32);

@@ -49,6 +49,7 @@
 namespace poly {
 
 constexpr int kTileSlots = 256;      // pixels per backward tile (32 x 8)
+constexpr int kChunkRegs = 8;        // r chunks per backward thread held in registers across the wait
 constexpr int kMaxStrips = 64;
 constexpr int kRecBytes = 640;       // one warp-group: 32 x 4 B deltas + 32 x 16 B values
 #ifndef POLY_FWD_WARPS
@@ -107,7 +108,8 @@ struct TileBwd {
                              // ((tile_off[t] + k) * 2 * npw + w); zero records pad the shorter halves
   const int64_t *tile_off;   // [ntiles + 1] first group-row of each tile
   const uint16_t *base;      // [ntiles * 256][2] list position before each half's first entry
-  const int32_t *list;       // concatenated ray lists (rows ascending), each starting at a multiple of 4
+  const int32_t *list;       // per tile, the aligned float4 chunks of r its rays touch (r's float4 index,
+                             // ascending); an entry's position = 4 * chunk + (row & 3)
   const int64_t *list_off;   // [ntiles + 1]
   const int32_t *tcol;       // [ntiles * 256] column of each slot, -1: none
   int32_t ntiles;
@@ -379,7 +381,6 @@ __global__ void __launch_bounds__((kBwdWarps + 1) * 32, 1)
   const int sbytes = kBwdCG * ncw * kRecBytes;     // one stage
   uint8_t *stg = smem;
   float *sr = (float *)(smem + kBwdStages * sbytes);
-  int32_t *sl = (int32_t *)sr;
   uint64_t *full = (uint64_t *)(sr + lcap);
   uint64_t *empty = full + kBwdStages;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -414,17 +415,31 @@ __global__ void __launch_bounds__((kBwdWarps + 1) * 32, 1)
     return;
   }
   const int pw = warp % t.npw, h = warp / t.npw;
-  const int64_t L0 = t.list_off[tile];
-  const int L = (int)(t.list_off[tile + 1] - L0);
-  for (int i = 4 * tid; i < L; i += 4 * ncw * 32) cp_async16(sl + i, t.list + L0 + i);  // static
+  // r of the tile's rays, staged as whole aligned float4 chunks of r (the
+  // rays through a tile are runs of consecutive rows, one per view): the
+  // chunk table is static, read before the wait; after it one 16-byte load
+  // and store per chunk (per-element cp.async gathers cost 8 LSU cycles each)
+  const int nthr = ncw * 32;
+  const int64_t C0 = t.list_off[tile];
+  const int nc = (int)(t.list_off[tile + 1] - C0);
+  int32_t csrc[kChunkRegs];
+#pragma unroll
+  for (int q = 0; q < kChunkRegs; ++q) {
+    const int c = tid + q * nthr;
+    csrc[q] = c < nc ? t.list[C0 + c] : 0;
+  }
   const int slot = tile * kTileSlots + pw * 32 + lane;
   int idx = (int)t.base[(int64_t)slot * 2 + h];
-  cp_async_wait_all();
-  named_bar(1, ncw * 32);
   pdl_wait();  // r is written by the link kernel
-  for (int i = tid; i < L; i += ncw * 32) cp_async4(sr + i, r + sl[i]);  // in place, own slots only
-  cp_async_wait_all();
-  named_bar(1, ncw * 32);
+  const float4 *r4 = (const float4 *)r;
+  float4 *sr4 = (float4 *)sr;
+#pragma unroll
+  for (int q = 0; q < kChunkRegs; ++q) {
+    const int c = tid + q * nthr;
+    if (c < nc) sr4[c] = __ldcg(r4 + csrc[q]);
+  }
+  for (int c = tid + kChunkRegs * nthr; c < nc; c += nthr) sr4[c] = __ldcg(r4 + t.list[C0 + c]);
+  named_bar(1, nthr);
   double a0 = 0.0, a1 = 0.0;
   const int nst = (int)(ng / kBwdCG);
   int st = 0;
@@ -605,10 +620,12 @@ __global__ void k_tb_keys(const int32_t *rows, const int32_t *col, int64_t nnz, 
   }
 }
 
-// first entry of every (tile, row) pair; pairs per tile
+// first entry of every (tile, r chunk) pair — a chunk = 4 rows i with the
+// same i >> 2 (one aligned float4 of r); chunks per tile
 __global__ void k_tb_pairs(const uint64_t *ks, int64_t nnz, TiledGeom m, int32_t *flag, int32_t *tcnt) {
   for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < nnz; k += (int64_t)gridDim.x * blockDim.x) {
-    const bool f = k == 0 || (ks[k - 1] >> 8) != (ks[k] >> 8);
+    const int sh = 8 + min(2, m.rb);  // (tile, row >> 2)
+    const bool f = k == 0 || (ks[k - 1] >> sh) != (ks[k] >> sh);
     flag[k] = f ? 1 : 0;
     // one atomic per (warp, tile): sorted neighbours share the tile
     const int64_t t = (int64_t)(ks[k] >> (m.rb + 8));
@@ -619,22 +636,19 @@ __global__ void k_tb_pairs(const uint64_t *ks, int64_t nnz, TiledGeom m, int32_t
   }
 }
 
-// ray lists and the second sort's keys (tile*256 + slot | list position)
+// chunk tables (r's float4 index of each chunk a tile's rays touch, ascending)
+// and the second sort's keys (tile*256 + slot | position of the row in the
+// tile's staged r: 4 * chunk + (row & 3))
 __global__ void k_tb_list(const uint64_t *ks, const int32_t *pidx, const int32_t *flag, const int64_t *pstart,
                           const int64_t *list_off, int64_t nnz, TiledGeom m, int32_t *list, uint64_t *key2) {
   for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < nnz; k += (int64_t)gridDim.x * blockDim.x) {
     const uint64_t q = ks[k];
     const int64_t t = (int64_t)(q >> (m.rb + 8));
-    const int64_t pos = (int64_t)pidx[k] - 1 - pstart[t];  // inclusive scan of flag
-    if (flag[k]) list[list_off[t] + pos] = (int32_t)((q >> 8) & ((1ull << m.rb) - 1));
-    key2[k] = ((uint64_t)(t * kTileSlots + (int64_t)(q & 0xffu)) << m.pb) | (uint64_t)pos;
+    const int64_t ci = (int64_t)pidx[k] - 1 - pstart[t];  // inclusive scan of flag: chunk within the tile
+    const int32_t row = (int32_t)((q >> 8) & ((1ull << m.rb) - 1));
+    if (flag[k]) list[list_off[t] + ci] = row >> 2;
+    key2[k] = ((uint64_t)(t * kTileSlots + (int64_t)(q & 0xffu)) << m.pb) | (uint64_t)(4 * ci + (row & 3));
   }
-}
-
-// counts rounded up to a multiple of 4
-__global__ void k_round4(int64_t *c, int64_t n) {
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
-    c[i] = (c[i] + 3) & ~(int64_t)3;
 }
 
 // entries and first position per (tile, slot)

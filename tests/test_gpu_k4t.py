@@ -189,31 +189,3 @@ def test_k4t_falls_back_on_wide_gaps():
     rp = np.cumsum(rp)
     val = r.uniform(0.0, 0.05, cols.shape[0]).astype(np.float32)
     _parity(rp, cols, val, d, 11, expect_layout=1)
-
-
-@pytest.mark.parametrize("mode", ["linkbwd", "full"])
-def test_c4_k4p_persistent_matches(c4, monkeypatch, mode):
-    """The opt-in persistent forms of the K4t pass (pass.cuh: link + backward
-    as one kernel with a grid barrier, or the whole pass as one kernel) walk
-    the same records in the same order: the gradient bits equal the three
-    kernels'; the objective's partials are grouped per CTA, so ℓ agrees to
-    rounding; a 10-iteration solve with the step epilogue agrees to 1e-12."""
-    wg, wo = c4
-    W = _W()
-    x = 0.7 * wo["x_star"]
-    g0, l0 = _grad(W.make_poly(wg), x)
-    monkeypatch.setenv("POLY_PERSIST", mode)
-    p = W.make_poly(wg)
-    g1, l1 = _grad(p, x)
-    assert np.array_equal(g0, g1)
-    assert abs(l0 - l1) <= 1e-12 * abs(l0)
-    gam = 1.0 / (4.0 * G.C4.I_bar * 4e-5 * float(np.dot(wo["s"], wo["mu"])))
-    xs = []
-    for q in (p, None):
-        if q is None:
-            monkeypatch.delenv("POLY_PERSIST")
-            q = W.make_poly(wg)
-        xx = torch.zeros(G.C4.d, dtype=torch.float64, device="cuda")
-        q.solve(xx, 10, gam)
-        xs.append(xx.cpu().numpy())
-    assert rel(xs[0], xs[1]) <= 1e-12
