@@ -157,11 +157,12 @@ def _parity(row_ptr, col, val, d, seed, expect_layout=None, W=8):
     p.close()
 
 
-@pytest.mark.parametrize("n,d,width", [(3000, 5000, 60), (777, 70000, 200), (64, 300, 40)])
+@pytest.mark.parametrize("n,d,width", [(3000, 5000, 60), (777, 70000, 200), (64, 300, 40), (2, 300, 40), (3, 257, 50)])
 def test_k4t_generic_banded(n, d, width):
     """A non-square d (one image row of d pixels: strips and tiles of
     consecutive columns), ragged rows, empty rows, ragged last tile, d larger
-    than one strip (70000 columns: several strips): K4t, oracle parity."""
+    than one strip (70000 columns: several strips), two or three rows (the
+    sort key's row field narrower than the r-chunk shift): K4t, oracle parity."""
     rp, col, val = _banded(n, d, n + d, width, empty_rows=(3, n // 2))
     _parity(rp, col, val, d, n, expect_layout=3)
 
