@@ -31,6 +31,20 @@ namespace poly {
 #define POLY_K1_LINK_SPLIT 1  // WPR > 1: the row group's warps split the link's bins
 #endif
 
+#ifndef POLY_K1_FFMA2
+#define POLY_K1_FFMA2 1   // fp32 dot/axpy as packed fma.rn.f32x2 (sm_100): half the FMA issue slots
+#endif
+
+// g[0..3] += r * c[0..3] as two packed FMAs (each lane of f32x2 is an IEEE fma: same bits as four scalar FMAs)
+__device__ __forceinline__ void axpy4_f32x2(float (&g)[4], float r, const float (&c)[4]) {
+  const float2 rr = make_float2(r, r);
+  const float2 g0 = __ffma2_rn(rr, make_float2(c[0], c[1]), make_float2(g[0], g[1]));
+  const float2 g1 = __ffma2_rn(rr, make_float2(c[2], c[3]), make_float2(g[2], g[3]));
+  g[0] = g0.x, g[1] = g0.y, g[2] = g1.x, g[3] = g1.y;
+}
+
+constexpr double kK1KeepMB = 64.0;  // MB of A read with L2 evict-last (POLY_K1_KEEP_MB overrides)
+
 struct DenseArgs {
   const void *A;
   int64_t lda;           // row pitch, elements
@@ -50,6 +64,7 @@ struct DenseArgs {
   int32_t stages;
   int32_t side_stride;   // bytes of side data per stage
   int32_t mode;          // POLY_MODE_*
+  int32_t keep_stages;   // each CTA's first stages read with L2 evict-last (kept across passes), the rest evict-first
 };
 
 // Link + per-row scalar for one row (warp-uniform z).  Lanes take bins
@@ -274,6 +289,7 @@ __global__ void __launch_bounds__(32 * (NW + 1), 1) k_dense_loss_grad(const Dens
   // rows handled in pairs (one butterfly for two dots, one link pass for two
   // rows when W <= 32)
   constexpr bool PAIR = (RG % 2 == 0);
+  constexpr bool kF2 = POLY_K1_FFMA2 && std::is_same<T, float>::value && VEC == 4;
   using VT = typename Vec16<T>::type;
 
   extern __shared__ __align__(128) unsigned char smem[];
@@ -309,7 +325,7 @@ __global__ void __launch_bounds__(32 * (NW + 1), 1) k_dense_loss_grad(const Dens
     // ------------------------------------------------------------ producer
     // A is immutable, so streaming may start before the previous kernel
     // (programmatic dependent launch) has finished.
-    const uint64_t pol = l2_evict_first_policy();
+    const uint64_t pol_first = l2_evict_first_policy(), pol_last = l2_evict_last_policy();
     const int ysz = a.ytype == 2 ? 8 : 4;
     int slot = 0;
     uint32_t eph = 1;  // toggled to 0 when the ring first wraps: wait for phase 0
@@ -321,7 +337,7 @@ __global__ void __launch_bounds__(32 * (NW + 1), 1) k_dense_loss_grad(const Dens
         const uint32_t bytes = (uint32_t)((size_t)rows * lda * sizeof(T));
         mbar_arrive_expect_tx(&full[slot], bytes);
         bulk_g2s(ring + (size_t)slot * stage_elems, (const T *)a.A + r0 * lda, bytes, &full[slot],
-                 pol);
+                 st < a.keep_stages ? pol_last : pol_first);
       }
       unsigned char *sd = side + (size_t)slot * a.side_stride;
       const unsigned char *yg = (const unsigned char *)a.y + r0 * ysz;
@@ -393,6 +409,8 @@ __global__ void __launch_bounds__(32 * (NW + 1), 1) k_dense_loss_grad(const Dens
       if (lr < rows) {
         const T *rowp = tile + (size_t)lr * lda + lane_off;
         T pp[(V + 1) / 2];
+        float2 pp2 = make_float2(0.0f, 0.0f);
+        (void)pp2;
 #pragma unroll
         for (int v = 0; v < V; ++v) {
           T ch[VEC];
@@ -400,10 +418,20 @@ __global__ void __launch_bounds__(32 * (NW + 1), 1) k_dense_loss_grad(const Dens
             unpack<T>(*reinterpret_cast<const VT *>(rowp + v * 32 * VEC), ch);
           else
             load_chunk<T>(rowp - lane_off, lane_off + v * 32 * VEC, a.d, ch);
-          T pv = (v & 1) ? pp[v >> 1] : (T)0;
+          if constexpr (kF2) {
+            // even and odd elements in the two lanes of a packed FMA chain; the lanes are added after
+            // the pair of chunks
+            float2 p2 = (v & 1) ? pp2 : make_float2(0.0f, 0.0f);
+            p2 = __ffma2_rn(make_float2(ch[0], ch[1]), make_float2(xr[v][0], xr[v][1]), p2);
+            p2 = __ffma2_rn(make_float2(ch[2], ch[3]), make_float2(xr[v][2], xr[v][3]), p2);
+            pp2 = p2;
+            if ((v & 1) || v == V - 1) pp[v >> 1] = p2.x + p2.y;
+          } else {
+            T pv = (v & 1) ? pp[v >> 1] : (T)0;
 #pragma unroll
-          for (int e = 0; e < VEC; ++e) pv = fma(ch[e], xr[v][e], pv);
-          pp[v >> 1] = pv;
+            for (int e = 0; e < VEC; ++e) pv = fma(ch[e], xr[v][e], pv);
+            pp[v >> 1] = pv;
+          }
           if (KEEP) {
 #pragma unroll
             for (int e = 0; e < VEC; ++e) av[KEEP ? q : 0][v][e] = ch[e];
@@ -535,8 +563,12 @@ __global__ void __launch_bounds__(32 * (NW + 1), 1) k_dense_loss_grad(const Dens
               } else {
                 load_chunk<T>(rowp - lane_off, lane_off + v * 32 * VEC, a.d, ch);
               }
+              if constexpr (kF2) {
+                axpy4_f32x2(gacc[v], r2[u], ch);
+              } else {
 #pragma unroll
-              for (int e = 0; e < VEC; ++e) gacc[v][e] = fma(r2[u], ch[e], gacc[v][e]);
+                for (int e = 0; e < VEC; ++e) gacc[v][e] = fma(r2[u], ch[e], gacc[v][e]);
+              }
             }
           }
         }
@@ -567,8 +599,12 @@ __global__ void __launch_bounds__(32 * (NW + 1), 1) k_dense_loss_grad(const Dens
           } else {
             load_chunk<T>(rowp - lane_off, lane_off + v * 32 * VEC, a.d, ch);
           }
+          if constexpr (kF2) {
+            axpy4_f32x2(gacc[v], rt, ch);
+          } else {
 #pragma unroll
-          for (int e = 0; e < VEC; ++e) gacc[v][e] = fma(rt, ch[e], gacc[v][e]);
+            for (int e = 0; e < VEC; ++e) gacc[v][e] = fma(rt, ch[e], gacc[v][e]);
+          }
         }
       }
     }

@@ -244,7 +244,7 @@ struct poly_handle {
   // K1
   const DenseVariant *dv = nullptr;
   int full = 0;
-  int k1_grid = 0, k1_threads = 0, k1_stages = 0, k1_side = 0;
+  int k1_grid = 0, k1_threads = 0, k1_stages = 0, k1_side = 0, k1_keep = 0;
   size_t k1_smem = 0;
   int k4_grid = 0;                     // K4f blocks (= loss partials)
   int nrslices = 0;                    // 32-row SELL slices of A
@@ -412,6 +412,7 @@ int enqueue_pass(poly_handle *h, const double *x, bool loss) {
     a.stages = h->k1_stages;
     a.mode = p.mode;
     a.side_stride = h->k1_side;
+    a.keep_stages = h->k1_keep;
     return launch(h, h->dv->fn[h->full][loss ? 1 : 0], dim3(h->k1_grid), dim3(h->k1_threads), h->k1_smem,
                   true, a);
   }
@@ -1074,6 +1075,12 @@ int setup_dense(poly_handle *h) {
   const int64_t tiles = (p.n_local + dv->RPS - 1) / dv->RPS;
   h->k1_grid = (int)std::max<int64_t>(1, std::min<int64_t>(h->sms, tiles));
   h->G = h->k1_grid;
+  {
+    // each CTA's first stages kept in L2 across passes (evict-last); POLY_K1_KEEP_MB overrides
+    double keep_mb = kK1KeepMB;
+    if (const char *e = getenv("POLY_K1_KEEP_MB")) keep_mb = atof(e);
+    h->k1_keep = (int)(keep_mb * 1e6 / ((double)stage * h->k1_grid));
+  }
   return POLY_OK;
 }
 
@@ -1720,6 +1727,17 @@ int build_tiled(poly_handle *h) {
   }
   h->tfwd = StripFwd{frec, fhdr, uoff, d_ustart, d_ctr, pz, n, m.NS, m.rows_img, m.cols_img, m.W, m.P};
   h->tbwd = TileBwd{brec, toff, bbase, list, loff, tcol, (int32_t)ntiles, npw, inter};
+  {
+    // part of the records kept in L2 across passes (evict-last); the rest streams evict-first
+    double keep_f = kTiledKeepFwdMB, keep_b = kTiledKeepBwdMB;
+    if (const char *e = getenv("POLY_L2_KEEP_MB")) {
+      keep_f = keep_b = 0.0;
+      sscanf(e, "%lf,%lf", &keep_f, &keep_b);
+    }
+    const double fmb = (double)frows * kFwdWarps * kRecBytes / 1e6, bmb = (double)brows * 2 * npw * kRecBytes / 1e6;
+    h->tfwd.keep = fmb > 0 ? (int32_t)std::min(1024.0, std::max(0.0, keep_f / fmb * 1024.0)) : 0;
+    h->tbwd.keep = bmb > 0 ? (int32_t)std::min(1024.0, std::max(0.0, keep_b / bmb * 1024.0)) : 0;
+  }
   h->tf_grid = (int)std::max<int64_t>(m.NS, (int64_t)h->sms / m.NS * m.NS);
   h->tb_grid = (int)ntiles;
   h->tf_groups = frows * kFwdWarps;

@@ -78,6 +78,8 @@ constexpr int kFwdCG = POLY_FWD_CG;        // group-rows per forward stage (unit
 #ifndef POLY_STRIP_KB
 #define POLY_STRIP_KB 100              // largest iterate strip (shared memory), KB
 #endif
+constexpr double kTiledKeepFwdMB = 0.0;  // records read with L2 evict-last (POLY_L2_KEEP_MB="fwd,bwd" overrides)
+constexpr double kTiledKeepBwdMB = 32.0;
 constexpr int kFwdStages = POLY_FWD_STAGES;
 constexpr int kFwdHdr = kFwdWarps * 32 * 6;  // per unit: uint16 base[256], then int32 row[256]
 constexpr int kFwdStageBytes = kFwdHdr + kFwdCG * kFwdWarps * kRecBytes;
@@ -101,6 +103,8 @@ struct StripFwd {
   int32_t NS, rows_img, cols_img, W, P;
   int64_t xs_off;            // the fp32 iterate's strip copies: strip s at x[xs_off + s * SP] (finalize.cuh X32Strip)
   int32_t SP;                // floats per strip copy (rows_img * P rounded up to 4)
+  int32_t keep;              // of every 1024 units of a strip, the first `keep` are read with L2 evict-last
+                             // (they stay in L2 across passes: the solver re-reads the same A every pass)
 };
 
 struct TileBwd {
@@ -116,6 +120,7 @@ struct TileBwd {
   int32_t npw;               // pixel warps per tile (TW * TH / 32); 2 * npw consumer warps
   int32_t interleave;        // 1: stage k of every tile stored together ([k][tile]: the CTAs' bulk
                              // copies walk one contiguous region), 0: tile-major
+  int32_t keep;              // of every 1024 stages of a tile, the first `keep` are read with L2 evict-last
 };
 
 // byte offset of stage k of tile t (first group-row G0 in the tile-major form)
@@ -264,7 +269,7 @@ __global__ void __launch_bounds__((kFwdWarps + 1) * 32, 1) k_strip_forward(const
   if (warp == kFwdWarps) {
     // producer: units off the strip's counter, their header + records into the ring
     if (lane == 0) {
-      const uint64_t pol = l2_evict_first_policy();
+      const uint64_t pol_first = l2_evict_first_policy(), pol_last = l2_evict_last_policy();
       // (starting the ring before the wait — records are static — measured
       // slower in the graph: 126 vs 118 us per C4 step)
       pdl_wait();  // the counter is reset by the previous link kernel, x written by the step kernel
@@ -288,6 +293,7 @@ __global__ void __launch_bounds__((kFwdWarps + 1) * 32, 1) k_strip_forward(const
         const int un = done ? nu : atomicAdd(f.ctr + strip, 1);  // the next unit, prefetched while this one streams
         const int64_t U = (int64_t)u0 + u;
         const int64_t g0 = done ? 0 : f.unit_off[U], ng = done ? 1 : f.unit_off[U + 1] - g0;
+        const uint64_t pol = (int64_t)u * 1024 < (int64_t)f.keep * nu ? pol_last : pol_first;
         for (int64_t k = 0; k < ng; k += kFwdCG) {
           if (k == kFwdCG) prefetch_unit(un);
           if (it >= kFwdStages) mbar_wait(empty + st, eph ^ 1);
@@ -397,8 +403,9 @@ __global__ void __launch_bounds__((kBwdWarps + 1) * 32, 1)
   if (warp == ncw) {
     // producer: the tile's records are static — streaming starts before the wait
     if (lane == 0) {
-      const uint64_t pol = l2_evict_first_policy();
+      const uint64_t pol_first = l2_evict_first_policy(), pol_last = l2_evict_last_policy();
       const int64_t ns = ng / kBwdCG;
+      const int64_t nkeep = (ns * t.keep + 1023) >> 10;
       if (POLY_BWD_PF > kBwdStages && ns > kBwdStages)
         for (int64_t q = kBwdStages; q < min(ns, (int64_t)POLY_BWD_PF); ++q)
           bulk_prefetch_l2(t.rec + bwd_stage_off(t, tile, G0, q), sbytes);
@@ -409,7 +416,8 @@ __global__ void __launch_bounds__((kBwdWarps + 1) * 32, 1)
           bulk_prefetch_l2(t.rec + bwd_stage_off(t, tile, G0, k + POLY_BWD_PF), sbytes);
         if (k >= kBwdStages) mbar_wait(empty + st, eph ^ 1);
         mbar_arrive_expect_tx(full + st, sbytes);
-        bulk_g2s(stg + st * sbytes, t.rec + bwd_stage_off(t, tile, G0, k), sbytes, full + st, pol);
+        bulk_g2s(stg + st * sbytes, t.rec + bwd_stage_off(t, tile, G0, k), sbytes, full + st,
+                 k < nkeep ? pol_last : pol_first);
       }
     }
     return;
