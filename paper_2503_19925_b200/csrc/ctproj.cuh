@@ -59,6 +59,33 @@ __device__ __forceinline__ float chord(float dd, float plateau, float kd, float 
   return fminf(plateau, fmaxf(0.0f, fmaf(-dd, kd, kp)));
 }
 
+#ifndef POLY_PB_MAGIC
+#define POLY_PB_MAGIC 1   // floor/ceil through fp32 adds instead of F2I/I2F conversions (same results)
+#endif
+// floor(u) for |u| < 2^22 as a float and an int: u + 1.5·2^23 rounded towards -inf has unit ulp, so its
+// mantissa holds floor(u) — two adds on the fp32 pipe instead of F2I + I2F
+__device__ __forceinline__ void floor_fi(float u, float &kf, int &ki) {
+#if POLY_PB_MAGIC
+  const float t = __fadd_rd(u, 12582912.0f);
+  kf = t - 12582912.0f;
+  ki = __float_as_int(t) - 0x4B400000;
+#else
+  ki = __float2int_rd(u);
+  kf = (float)ki;
+#endif
+}
+// ceil(fr - w) for fr in [0, 1), w in (0, 1): 1 when fr > w, else 0 (fr - w > -1 and is never rounded to zero)
+__device__ __forceinline__ void ceil01_fi(float fr, float w, float &jf, int &ji) {
+#if POLY_PB_MAGIC
+  const bool up = fr > w;
+  jf = up ? 1.0f : 0.0f;
+  ji = up ? 1 : 0;
+#else
+  ji = __float2int_ru(fr - w);
+  jf = (float)ji;
+#endif
+}
+
 #ifndef POLY_PB_ROWS
 #define POLY_PB_ROWS 32
 #endif
@@ -187,21 +214,36 @@ __global__ void __launch_bounds__(512) k_pb_forward(const PbGeom g, const float 
         }
       } else {
         const int ra = max(0, r_lo - r0), rz = min(nr, r_hi - r0);
+        // EXACT01: w < 1, so ceil(fr - w) is 0 or 1 (a comparison); the 45-degree view (w = 1, where
+        // fr = 0 gives -1) keeps the conversions.  Uniform per block.
+        auto rows = [&](auto EXACT01) {
 #pragma unroll 4
-        for (int rr = ra; rr < rz; ++rr) {
-          const float u = fmaf(-(float)rr, tn, fr0);
-          const int ki = __float2int_rd(u);
-          const float fr = u - (float)ki;
-          // the footprint [c* - w, c* + w] (w <= 1) holds at most two pixel
-          // centres with a nonzero chord: cc0 = ceil(c* - w) and cc0 + 1
-          const int j_lo = __float2int_ru(fr - w);
-          const int cc0 = min(max(ci0 + ki + j_lo, -2), N);
-          const float sd0 = fr - (float)j_lo;  // c* - cc0 (unclamped), in (w - 1, w]
-          const float *xr = xsb + rr * NP + kPbPad + cc0;
-          // |sd0 - 1| = 1 - sd0: the second chord's argument folds into one FMA
-          zf = fmaf(chord(fabsf(sd0), inv_a, kd, kp), xr[0], zf);
-          zf = fmaf(fminf(inv_a, fmaxf(0.0f, fmaf(sd0, kd, kp1))), xr[1], zf);
-        }
+          for (int rr = ra; rr < rz; ++rr) {
+            const float u = fmaf(-(float)rr, tn, fr0);
+            int ki, j_lo;
+            float kf, jf;
+            floor_fi(u, kf, ki);
+            const float fr = u - kf;
+            // the footprint [c* - w, c* + w] (w <= 1) holds at most two pixel
+            // centres with a nonzero chord: cc0 = ceil(c* - w) and cc0 + 1
+            if (decltype(EXACT01)::value) {
+              ceil01_fi(fr, w, jf, j_lo);
+            } else {
+              j_lo = __float2int_ru(fr - w);
+              jf = (float)j_lo;
+            }
+            const int cc0 = min(max(ci0 + ki + j_lo, -2), N);
+            const float sd0 = fr - jf;  // c* - cc0 (unclamped), in (w - 1, w]
+            const float *xr = xsb + rr * NP + kPbPad + cc0;
+            // |sd0 - 1| = 1 - sd0: the second chord's argument folds into one FMA
+            zf = fmaf(chord(fabsf(sd0), inv_a, kd, kp), xr[0], zf);
+            zf = fmaf(fminf(inv_a, fmaxf(0.0f, fmaf(sd0, kd, kp1))), xr[1], zf);
+          }
+        };
+        if (w < 1.0f)
+          rows(std::true_type{});
+        else
+          rows(std::false_type{});
       }
       z += (double)zf;  // fp32 partial per chunk, fp64 across chunks
       zf = 0.0f;
@@ -352,10 +394,12 @@ __global__ void __launch_bounds__(kPbTile * kPbTile / kPbPx) k_pb_backward(const
 #pragma unroll
         for (int q = 0; q < kPbPx; ++q) {
           const float u = fmaf((float)q, v.cs, u0);
-          const int ki = __float2int_rd(u);
-          const float fr = u - (float)ki;
-          const int j_lo = __float2int_ru(fr - v.wb);
-          const float sd0 = fr - (float)j_lo;  // b* - (bin ki + j_lo)
+          int ki, j_lo;
+          float kf, jf;
+          floor_fi(u, kf, ki);
+          const float fr = u - kf;
+          ceil01_fi(fr, v.wb, jf, j_lo);
+          const float sd0 = fr - jf;  // b* - (bin ki + j_lo)
           const float *rb = rv + ki + j_lo;
           // sd0 <= wb < 1, so |sd0 - 1| = 1 - sd0 folds into one FMA
           accf[q] = fmaf(chord(fabsf(sd0), v.inv_max, v.kd, v.kp), rb[0], accf[q]);
