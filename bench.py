@@ -313,6 +313,10 @@ def run_ours(args):
             "read_ceiling_k8": read_ceiling,
             "frac_of_read_ceiling": (achieved / read_ceiling) if achieved and read_ceiling else None}
     desc = poly.describe()
+    # part of A the kernels read with L2 evict-last: it stays in L2 from pass to pass, so the DRAM bytes of
+    # a pass in the timed loop are below the algorithmic bytes by up to this much (`traffic` is ncu's
+    # cold-cache figure); `achieved` stays algorithmic bytes / time
+    roof["l2_keep_bytes"] = desc.get("l2_keep_bytes", 0)
     launches = launches_per_step(w, cfg, world) * args.steps  # (before e2e releases the device copy of A)
 
     cpu = None

@@ -297,7 +297,9 @@ int poly_kernel_times(poly_handle *h, double *out, int32_t nout);
  * every local index delta fits 8 bits; then out[0] forward CTAs, out[1] its
  * threads, out[2] column strips, out[3] backward tiles, out[4] forward smem),
  * 1 SELL16, 2 DSELL, 0 the 8-byte SELL; -1 for dense / matrix-free handles.
- * nout <= 13. */
+ * out[13] bytes of A (dense) or of its K4t copies that every pass reads with
+ * the L2 evict-last policy, so that they stay in L2 from one pass to the next
+ * (the rest streams evict-first); 0 otherwise.  nout <= 14. */
 int poly_describe(poly_handle *h, int64_t *out, int32_t nout);
 
 /* Write a fresh 128-byte ncclUniqueId into out (host).  Call on rank 0 and

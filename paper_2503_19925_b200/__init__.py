@@ -194,10 +194,10 @@ def poly_kernel_times(h: int):
 
 
 def poly_describe(h: int):
-    out = (C.c_int64 * 13)()
-    _check(_lib.poly_describe(h, out, 13))
+    out = (C.c_int64 * 14)()
+    _check(_lib.poly_describe(h, out, 14))
     return dict(zip(["grid", "threads", "rows_per_stage", "stages", "smem", "sms", "V", "WPR", "NW",
-                     "full", "comm_ranks", "k9", "csr_layout"], list(out)))
+                     "full", "comm_ranks", "k9", "csr_layout", "l2_keep_bytes"], list(out)))
 
 
 def poly_nccl_unique_id() -> bytes:

@@ -245,6 +245,7 @@ struct poly_handle {
   const DenseVariant *dv = nullptr;
   int full = 0;
   int k1_grid = 0, k1_threads = 0, k1_stages = 0, k1_side = 0, k1_keep = 0;
+  int64_t keep_bytes = 0;        // bytes of A (or its K4t copies) read with L2 evict-last per pass
   size_t k1_smem = 0;
   int k4_grid = 0;                     // K4f blocks (= loss partials)
   int nrslices = 0;                    // 32-row SELL slices of A
@@ -1080,6 +1081,8 @@ int setup_dense(poly_handle *h) {
     double keep_mb = kK1KeepMB;
     if (const char *e = getenv("POLY_K1_KEEP_MB")) keep_mb = atof(e);
     h->k1_keep = (int)(keep_mb * 1e6 / ((double)stage * h->k1_grid));
+    h->keep_bytes = std::min<int64_t>((int64_t)h->k1_keep * (int64_t)stage * h->k1_grid,
+                                      (int64_t)p.n_local * p.lda * (int64_t)h->elsize);
   }
   return POLY_OK;
 }
@@ -1737,6 +1740,7 @@ int build_tiled(poly_handle *h) {
     const double fmb = (double)frows * kFwdWarps * kRecBytes / 1e6, bmb = (double)brows * 2 * npw * kRecBytes / 1e6;
     h->tfwd.keep = fmb > 0 ? (int32_t)std::min(1024.0, std::max(0.0, keep_f / fmb * 1024.0)) : 0;
     h->tbwd.keep = bmb > 0 ? (int32_t)std::min(1024.0, std::max(0.0, keep_b / bmb * 1024.0)) : 0;
+    h->keep_bytes = (int64_t)((h->tfwd.keep * fmb + h->tbwd.keep * bmb) / 1024.0 * 1e6);
   }
   h->tf_grid = (int)std::max<int64_t>(m.NS, (int64_t)h->sms / m.NS * m.NS);
   h->tb_grid = (int)ntiles;
@@ -2967,8 +2971,8 @@ int poly_kernel_times(poly_handle *h, double *out, int32_t nout) {
 }
 
 int poly_describe(poly_handle *h, int64_t *out, int32_t nout) {
-  if (!h || !out || nout < 0 || nout > 13) return fail(POLY_EINVAL, "bad arguments");
-  int64_t v[13] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+  if (!h || !out || nout < 0 || nout > 14) return fail(POLY_EINVAL, "bad arguments");
+  int64_t v[14] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
   if (h->nccl) {
     int c = 0;
     if (nccl_api()->count(h->nccl, &c) == ncclSuccess) v[10] = c;
@@ -3000,6 +3004,7 @@ int poly_describe(poly_handle *h, int64_t *out, int32_t nout) {
   // CSR layout: 0 wide SELL-32, 1 compact SELL16, 2 DSELL, 3 K4t (tiled.cuh); -1 dense / matrix-free
   v[12] = h->p.layout != POLY_CSR ? -1 : (h->tiled ? 3 : (h->dsell ? 2 : (h->sell16 ? 1 : 0)));
   v[5] = h->sms;
+  v[13] = (h->p.layout == POLY_DENSE || h->tiled) ? h->keep_bytes : 0;
   for (int i = 0; i < nout; ++i) out[i] = v[i];
   return POLY_OK;
 }
