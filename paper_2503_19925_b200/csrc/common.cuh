@@ -109,6 +109,32 @@ __device__ __forceinline__ void pdl_trigger() {
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 }
 
+// Data written by the kernel that precedes this one in a programmatic-launch
+// chain is read past L1 (ld.global.cg): this grid may have started while the
+// writer was still running, so a const __restrict__ load (ld.global.nc) would
+// break that path's "read-only for the kernel's lifetime" contract.
+#ifndef POLY_HARDEN_LD
+#define POLY_HARDEN_LD 1
+#endif
+template <typename T>
+__device__ __forceinline__ T ld_prev(const T *p) {
+#if POLY_HARDEN_LD
+  return __ldcg(p);
+#else
+  return *p;
+#endif
+}
+// after griddepcontrol.wait and before a bulk copy (async proxy) of data the
+// previous grid wrote with ordinary stores (generic proxy)
+#ifndef POLY_PDL_PROXY_FENCE
+#define POLY_PDL_PROXY_FENCE 1
+#endif
+__device__ __forceinline__ void pdl_proxy_fence() {
+#if POLY_PDL_PROXY_FENCE
+  asm volatile("fence.proxy.async;" ::: "memory");
+#endif
+}
+
 // ------------------------------------------------------------ named barrier
 __device__ __forceinline__ void named_bar_sync(int id, int nthreads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
@@ -138,10 +164,30 @@ __device__ __forceinline__ double exp_nonpos_sfu(double x) {
   return (double)e2 * __longlong_as_double((long long)(1023 + (int)k) << 52);
 }
 
+#ifndef POLY_EXP_CONST
+#define POLY_EXP_CONST 1   // the polynomial's constants as constant-bank operands of the DFMAs
+#endif
+// 1/i! (i = 0..15), then log2 e and the two parts of ln 2: as 64-bit immediates each constant costs two
+// UMOVs per use (24 of the 48 instructions of one evaluation); from the constant bank they are operands
+__device__ __constant__ double kExpTab[19] = {
+    inv_factorial(0),  inv_factorial(1),  inv_factorial(2),  inv_factorial(3),  inv_factorial(4),  inv_factorial(5),
+    inv_factorial(6),  inv_factorial(7),  inv_factorial(8),  inv_factorial(9),  inv_factorial(10), inv_factorial(11),
+    inv_factorial(12), inv_factorial(13), inv_factorial(14), inv_factorial(15), 1.4426950408889634,
+    6.93147180369123816490e-01, 1.90821492927058770002e-10};
+
 template <int DEG = 13>
 __device__ __forceinline__ double exp_nonpos(double x) {
   if (DEG == 0) return exp_nonpos_sfu(x);
+  static_assert(DEG <= 15, "table");
   x = fmax(x, -708.0);
+#if POLY_EXP_CONST
+  const double k = rint(x * kExpTab[16]);
+  double r = fma(-k, kExpTab[17], x);
+  r = fma(-k, kExpTab[18], r);
+  double p = kExpTab[DEG];
+#pragma unroll
+  for (int i = DEG - 1; i >= 0; --i) p = fma(p, r, kExpTab[i]);
+#else
   const double k = rint(x * 1.4426950408889634);
   double r = fma(-k, 6.93147180369123816490e-01, x);
   r = fma(-k, 1.90821492927058770002e-10, r);
@@ -149,6 +195,7 @@ __device__ __forceinline__ double exp_nonpos(double x) {
   double p = inv_factorial(DEG);
 #pragma unroll
   for (int i = DEG - 1; i >= 0; --i) p = fma(p, r, inv_factorial(i));
+#endif
   return p * __longlong_as_double((long long)(1023 + (int)k) << 52);
 }
 

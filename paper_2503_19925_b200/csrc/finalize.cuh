@@ -106,7 +106,7 @@ __global__ void __launch_bounds__(256) k_finalize(const FinArgs a) {
     double acc = 0.0;
     if (c < a.d) {
       if (from_comm) {
-        if (sl == 0) acc = a.comm[c];
+        if (sl == 0) acc = ld_prev(a.comm + c);
       } else {
         // four independent accumulators (loads in flight together), combined
         // in a fixed order: deterministic for a fixed G
@@ -115,12 +115,12 @@ __global__ void __launch_bounds__(256) k_finalize(const FinArgs a) {
         const size_t st = (size_t)NWf * a.d;
         int i = sl;
         for (; i + 3 * NWf < a.G; i += 4 * NWf) {
-          q0 += col[(size_t)i * a.d];
-          q1 += col[(size_t)i * a.d + st];
-          q2 += col[(size_t)i * a.d + 2 * st];
-          q3 += col[(size_t)i * a.d + 3 * st];
+          q0 += ld_prev(col + (size_t)i * a.d);
+          q1 += ld_prev(col + (size_t)i * a.d + st);
+          q2 += ld_prev(col + (size_t)i * a.d + 2 * st);
+          q3 += ld_prev(col + (size_t)i * a.d + 3 * st);
         }
-        for (; i < a.G; i += NWf) q0 += col[(size_t)i * a.d];
+        for (; i < a.G; i += NWf) q0 += ld_prev(col + (size_t)i * a.d);
         acc = (q0 + q1) + (q2 + q3);
       }
     }
@@ -132,9 +132,9 @@ __global__ void __launch_bounds__(256) k_finalize(const FinArgs a) {
   if (blockIdx.x == 0 && sl == 1 && needs_g) {
     double l = 0.0;
     if (from_comm) {
-      l = (cl == 0) ? a.comm[a.d] : 0.0;
+      l = (cl == 0) ? ld_prev(a.comm + a.d) : 0.0;
     } else if (a.need_loss) {
-      for (int i = cl; i < a.GL; i += 32) l += a.loss_partials[i];
+      for (int i = cl; i < a.GL; i += 32) l += ld_prev(a.loss_partials + i);
     }
     l = warp_sum(l);
     if (cl == 0) s_loss = l;
@@ -162,7 +162,7 @@ __global__ void __launch_bounds__(256) k_finalize(const FinArgs a) {
   double q = 0.0;
   if (sl == 0) {
     if (c < a.d) {
-      double v = a.anchor[c];
+      double v = ld_prev(a.anchor + c);
       if (needs_g) {
         const double g = tot / nn;
         if (a.g_out) a.g_out[c] = g;
@@ -250,7 +250,7 @@ __global__ void __launch_bounds__(256) k_fin_apply(const FinArgs a) {
   // fixed tree: per-thread strided sums, warp butterflies, warps in order —
   // the same bits in every block
   double nr = 0.0;
-  for (int b = tid; b < nb; b += 256) nr += a.block_norm[b];
+  for (int b = tid; b < nb; b += 256) nr += ld_prev(a.block_norm + b);
   nr = warp_sum(nr);
   if ((tid & 31) == 0) s_w[tid >> 5] = nr;
   __syncthreads();
@@ -258,7 +258,7 @@ __global__ void __launch_bounds__(256) k_fin_apply(const FinArgs a) {
   double scale = 1.0;
   if ((a.set == 1 || a.set == 3) && nrm > a.R) scale = a.R / nrm;
   for (int k = blockIdx.x * blockDim.x + tid; k < a.d; k += gridDim.x * blockDim.x) {
-    const double v = a.v_scratch[k];
+    const double v = ld_prev(a.v_scratch + k);
     double xo;
     if (a.set == 1) {
       const double ck = a.center ? a.center[k] : 0.0;

@@ -78,8 +78,12 @@ constexpr int kFwdCG = POLY_FWD_CG;        // group-rows per forward stage (unit
 #ifndef POLY_STRIP_KB
 #define POLY_STRIP_KB 100              // largest iterate strip (shared memory), KB
 #endif
-constexpr double kTiledKeepFwdMB = 0.0;  // records read with L2 evict-last (POLY_L2_KEEP_MB="fwd,bwd" overrides)
-constexpr double kTiledKeepBwdMB = 32.0;
+// Records read with L2 evict-last (POLY_L2_KEEP_MB="fwd,bwd" overrides; experiments only).  Off: at C4 the
+// gain was 0.4 us per pass at best, and with part of the backward's records evict-last 1-2 % of
+// graph-replayed solves differed in their bits from run to run (0 of 2999 without; cause not found — see
+// DESIGN.md §7), which breaks the path's determinism guarantee.
+constexpr double kTiledKeepFwdMB = 0.0;
+constexpr double kTiledKeepBwdMB = 0.0;
 constexpr int kFwdStages = POLY_FWD_STAGES;
 constexpr int kFwdHdr = kFwdWarps * 32 * 6;  // per unit: uint16 base[256], then int32 row[256]
 constexpr int kFwdStageBytes = kFwdHdr + kFwdCG * kFwdWarps * kRecBytes;
@@ -275,6 +279,7 @@ __global__ void __launch_bounds__((kFwdWarps + 1) * 32, 1) k_strip_forward(const
       pdl_wait();  // the counter is reset by the previous link kernel, x written by the step kernel
       // the strip's iterate: one bulk copy of its strip-layout fp32 copy (the
       // strip's other CTAs read the same bytes: kept in L2)
+      pdl_proxy_fence();
       mbar_arrive_expect_tx(xbar, (uint32_t)f.SP * 4);
       bulk_g2s(sx, x + f.xs_off + (int64_t)strip * f.SP, (uint32_t)f.SP * 4, xbar, l2_evict_last_policy());
       int it = 0, st = 0;
@@ -360,7 +365,7 @@ __global__ void __launch_bounds__(256, 4) k_strip_link(const CsrFwdArgs a, const
   for (int64_t row = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; row < a.n;
        row += (int64_t)gridDim.x * blockDim.x) {
     double z = 0.0, yv, Ii = a.I_bar;
-    for (int s = 0; s < NS; ++s) z += pz[(int64_t)s * a.n + row];
+    for (int s = 0; s < NS; ++s) z += ld_prev(pz + (int64_t)s * a.n + row);
     if (a.ytype == 0) yv = (double)((const int32_t *)a.y)[row];
     else if (a.ytype == 1) yv = (double)((const float *)a.y)[row];
     else yv = ((const double *)a.y)[row];
@@ -478,7 +483,7 @@ __global__ void __launch_bounds__((kBwdWarps + 1) * 32, 1)
     double q = 0.0;
     if (c >= 0 && c < d) {
       const double gc = acc / e.n_norm;
-      double vv = e.anchor[c] - e.state->gamma * gc;
+      double vv = ld_prev(e.anchor + c) - e.state->gamma * gc;
       if (e.set == 2 || e.set == 3) vv = vv > 0.0 ? vv : 0.0;
       const double df = (e.set == 1 && e.center) ? vv - e.center[c] : vv;
       q = df * df;

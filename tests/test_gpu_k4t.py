@@ -190,3 +190,25 @@ def test_k4t_falls_back_on_wide_gaps():
     rp = np.cumsum(rp)
     val = r.uniform(0.0, 0.05, cols.shape[0]).astype(np.float32)
     _parity(rp, cols, val, d, 11, expect_layout=1)
+
+
+def test_c4_solve_bits_repeat(c4):
+    """Determinism of the graph-replayed solve (fixed summation order in every
+    kernel of Eq. extragrad-method): 300 repetitions of the
+    same 25-iteration C4 solve on one handle give identical bits.  (With part of
+    the backward's records read evict-last, 1-2 % of such runs differed — that
+    option is off.)"""
+    wg, _ = c4
+    p = _W().make_poly(wg)
+    assert p.describe()["csr_layout"] == 3 and p.describe()["l2_keep_bytes"] == 0
+    cfg = G.C4
+    gam = 1.0 / (4.0 * cfg.I_bar * 4e-5 * float(np.dot(*cfg.spectrum)))
+    ref = None
+    for _ in range(300):
+        x = torch.zeros(cfg.d, dtype=torch.float64, device="cuda")
+        p.solve(x, 25, gam)
+        if ref is None:
+            ref = x.clone()
+        else:
+            assert torch.equal(ref, x)
+    p.close()
