@@ -149,8 +149,9 @@ def _fd_worker(rank, world, port, name, path, q):
         import paper_2503_19925_b200 as P
         fd = os.open(path, os.O_RDONLY) if rank == 0 else -1
         got = P.poly_share_fd(rank, world, name, fd, timeout_s=30.0)
-        os.lseek(got, 0, os.SEEK_SET)
-        data = os.read(got, 64)
+        # the ranks' descriptors share one open file description (SCM_RIGHTS), hence one file
+        # offset: a positioned read, not lseek + read, which races between ranks
+        data = os.pread(got, 64, 0)
         if rank != 0:
             os.close(got)
         dist.barrier()
