@@ -409,6 +409,9 @@ __global__ void __launch_bounds__((kBwdWarps + 1) * 32, 1)
     // producer: the tile's records are static — streaming starts before the wait
     if (lane == 0) {
       const uint64_t pol_first = l2_evict_first_policy(), pol_last = l2_evict_last_policy();
+#ifdef POLY_BWD_LATE
+      pdl_wait();  // (experiment) no streaming before the link kernel has completed
+#endif
       const int64_t ns = ng / kBwdCG;
       const int64_t nkeep = (ns * t.keep + 1023) >> 10;
       if (POLY_BWD_PF > kBwdStages && ns > kBwdStages)
