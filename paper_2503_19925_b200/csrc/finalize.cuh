@@ -243,7 +243,9 @@ __global__ void k_to_f32(const double *x, int64_t d, int32_t tr_side, const X32S
 __global__ void __launch_bounds__(256) k_fin_apply(const FinArgs a) {
   __shared__ double s_w[8];
   pdl_wait();
+#ifndef POLY_FIN_LATE
   pdl_trigger();
+#endif
   const int tid = threadIdx.x;
   const int nb = (a.d + 31) / 32;  // k_finalize blocks
   // all 256 threads read the block norms (loads in flight together), then a

@@ -360,7 +360,13 @@ __global__ void __launch_bounds__(256, 4) k_strip_link(const CsrFwdArgs a, const
   __syncthreads();
   pdl_wait();  // the forward's partials
   if (blockIdx.x == 0 && threadIdx.x < NS) ctr[threadIdx.x] = 0;  // for the next forward
+  // The backward is launched when this kernel's CTAs exit, not earlier: with the trigger here (so that the
+  // backward's prologue and ring fill overlap the link, ~0.8 us per pass) 1-2 % of graph-replayed solves
+  // differed in their bits once the backward's first stages came from L2 (POLY_L2_KEEP_MB), and none in
+  // 1499 without the overlap; -DPOLY_LINK_EARLY=1 restores the early trigger.
+#if defined(POLY_LINK_EARLY) && POLY_LINK_EARLY
   pdl_trigger();
+#endif
   double lacc = 0.0;
   for (int64_t row = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; row < a.n;
        row += (int64_t)gridDim.x * blockDim.x) {
